@@ -1,0 +1,166 @@
+/*
+ * cks.h -- C ABI of libcks.so: the C-K-S zero-skipping convolution operators
+ * of arXiv 2306.15951 ("Reduce Computational Complexity for Convolutional
+ * Layers by Skipping Zeros") on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:<line> = the paper text (reference PAPER.md), section/eq/alg.
+ *
+ * Problem statement (Table I, Eqs (1)-(3) P:134-140):
+ *   X  in R^{N x I_H x I_W x I_C}   input feature maps, NHWC (C fastest)
+ *   W  in R^{O_C x F_H x F_W x I_C} filters, OHWI
+ *   Y  in R^{N x O_H x O_W x O_C}   output feature maps, NHWC
+ *   O_H = floor((I_H + 2 ph - F_H)/sh) + 1, O_W likewise.
+ *   (1) Y  = conv2D(X, W)              -- ConvV2, filter trimming (Alg. 1)
+ *   (2) dX = deconv2D(dY, W^rot180)    -- KS-deconv-V2 (Alg. 2/2B)
+ *   (3) dW = dilated_conv2D(X, dY)     -- Sk-dilated-V2 (Alg. 3/3B)
+ *
+ * Conventions (all entry points):
+ *   - Every device buffer is owned by the caller.  The library never
+ *     allocates device memory on the compute path; scratch space is queried
+ *     with cks_workspace_size() and passed in (ws, ws_bytes).
+ *   - Device pointers must be 16-byte aligned; tensors are dense (no strides).
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) with no implicit synchronisation.  Outputs are
+ *     OVERWRITTEN, never accumulated.  The cross-GPU allreduce of dW is the
+ *     caller's job.
+ *   - Validation errors are returned synchronously before anything is
+ *     launched.  Asynchronous CUDA faults surface at the caller's next
+ *     synchronisation (or as CKS_ERR_CUDA from the launch check).
+ *   - dtype CKS_BF16: X, W, dY are bfloat16 (raw 16-bit storage); the tensor
+ *     cores multiply bf16 and accumulate fp32.  CKS_TF32: X, W, dY are fp32
+ *     and multiplied as TF32 (hardware truncation).  Y, dX, dW are always
+ *     fp32.  Geometry is (N,C,H,W,OC,FH,FW,sh,sw,ph,pw,dh,dw); dh = dw = 1 is
+ *     required (the paper's "dilate" is the conv stride; there is no
+ *     forward filter dilation), else CKS_ERR_UNSUPPORTED.
+ *   - Validity (reading c16): sh,sw >= 1, 0 <= ph < F_H, 0 <= pw < F_W,
+ *     O_H, O_W >= 1, all extents >= 1, else CKS_ERR_GEOMETRY.
+ *   - Channel counts whose rows are not a 16-byte multiple (I_C or O_C not a
+ *     multiple of 8 for bf16 / 4 for tf32) are staged through zero-padded
+ *     copies inside the workspace ("last dimensions ... implicitly
+ *     padded"); padded-channel products are not counted as zero-free work.
+ *   - Supported extents: every spatial row count used by a kernel (O_H, O_W
+ *     for the forward; I_H, I_W for the deconvolution) is <= CKS_MAX_ROWS,
+ *     F_H, F_W <= 32, sh, sw <= 8, else CKS_ERR_UNSUPPORTED.
+ */
+#ifndef CKS_H
+#define CKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKS_MAX_ROWS 256
+
+typedef struct cks_geom {
+    int64_t N, C, H, W, OC, FH, FW; /* C = I_C; H, W = I_H, I_W (the X side) */
+    int32_t sh, sw, ph, pw, dh, dw;
+} cks_geom;
+
+typedef enum { CKS_TF32 = 0, CKS_BF16 = 1 } cks_dtype;
+
+typedef enum {
+    CKS_OK = 0,
+    CKS_ERR_NULL = 1,        /* a required pointer argument is NULL          */
+    CKS_ERR_GEOMETRY = 2,    /* invalid Table-I geometry (see above)         */
+    CKS_ERR_UNSUPPORTED = 3, /* valid but outside what this build supports   */
+    CKS_ERR_ALIGNMENT = 4,   /* device pointer not 16-byte aligned           */
+    CKS_ERR_WORKSPACE = 5,   /* ws too small / NULL while ws bytes needed     */
+    CKS_ERR_CUDA = 6,        /* a CUDA runtime/driver call failed            */
+    CKS_ERR_CAPACITY = 7     /* host output array too small (tables)          */
+} cks_status;
+
+typedef enum { CKS_OP_FWD = 0, CKS_OP_DECONV = 1, CKS_OP_WGRAD = 2 } cks_op;
+
+/* Output extent (Table I shape rule, floor rounding).  Host only. */
+cks_status cks_output_shape(const cks_geom* g, int64_t* OH, int64_t* OW);
+
+/* Bytes of scratch the op needs (0 if none).  `gz` is the Sk-dilated G_Z
+ * segment count for CKS_OP_WGRAD (0 = the library's choice);
+ * ignored for the other ops.  For CKS_OP_DECONV the size assumes the caller
+ * passes W (Stage1 runs into the workspace); pass c_packed to skip it. */
+cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz, size_t* bytes);
+
+/* The G_Z the library would use for this geometry with gz = 0 (P:212:
+ * "G_Z can be positive related to (N_a + N_b)/N_g ... the upper-bound can be
+ * decided by the number of streaming multi-processors").  Host only. */
+cks_status cks_choose_gz(const cks_geom* g, cks_dtype dt, int* gz);
+
+/* Eq (1) via ConvV2 (Alg. 1): Y[n,oh,ow,oc] = sum over the TRIMMED
+ * window fh in [fh_s, fh_e), fw in [fw_s, fw_e), ic of
+ * X[n, oh*sh-ph+fh, ow*sw-pw+fw, ic] * W[oc,fh,fw,ic]; padded zeros are never
+ * loaded or multiplied.  x: N*H*W*C (dtype), w: OC*FH*FW*C (dtype),
+ * y: N*OH*OW*OC fp32 (overwritten). */
+cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* Bytes of the packed KS-deconv sub-filter tensor for this geometry. */
+cks_status cks_ks_split_size(const cks_geom* g, cks_dtype dt, size_t* bytes);
+
+/* KS-deconv Stage1 (Alg. 2 Stage1 P:443, Fig. 5): rotate W by 180
+ * degrees and split it into sh*sw dense sub-filters, one per output phase
+ * (y, x): C_{y,x}[oc,ch,cw,ic] = W[oc, y+(oph_y-ch)*sh, x+(opw_x-cw)*sw, ic],
+ * oph_y = ceil((F_H-y)/sh)-1.  Stored packed and K-major for the tensor cores:
+ * c_packed[p = y*sw+x][ic][ch*CWm + cw][ocp], CHm = ceil(F_H/sh),
+ * CWm = ceil(F_W/sw), ocp < OCp = O_C rounded up to 16 bytes; slots outside a
+ * phase's CH_y x CW_x extent and channels >= O_C are zero.  Cacheable across
+ * calls while W is unchanged. */
+cks_status cks_ks_split(const cks_geom* g, cks_dtype dt, const void* w, void* c_packed, void* stream);
+
+/* Eq (2) via KS-deconv-V2 (Alg. 2 Stage2&3 + 2B): per phase (y, x)
+ * a unit-stride, filter-trimmed convolution of dY with C_{y,x}, its results
+ * scattered to dX rows ih = u*sh + ih_s(y) (fused Stage2&3).  No zero
+ * is inserted.  Exactly one of w (then Stage1 runs into ws) or c_packed (from
+ * cks_ks_split) must be non-NULL.  dy: N*OH*OW*OC (dtype), dx: N*H*W*C fp32
+ * (overwritten; rows no output reaches are written as 0, reading c10/c11). */
+cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w,
+                        const void* c_packed, float* dx, void* ws, size_t ws_bytes, void* stream);
+
+/* Eq (3) via Sk-dilated-V2 (Alg. 3/3B P:445): dW[oc,fh,fw,ic] = sum over
+ * n and the TRIMMED (oh, ow) range [oh_s, oh_e) x [ow_s, ow_e) of
+ * X[n, oh*sh+fh-ph, ow*sw+fw-pw, ic] * dY[n,oh,ow,oc]: leaping access into X
+ * with step = stride, no zero-inserted dY.  The G_K = N*O_H*O_W reduction is
+ * split into gz segments computed concurrently and aggregated in a fixed
+ * order (map-reduce).  x: N*H*W*C (dtype), dy: N*OH*OW*OC (dtype),
+ * dw: OC*FH*FW*C fp32 (overwritten).  gz = 0: library choice. */
+cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
+                             int gz, void* ws, size_t ws_bytes, void* stream);
+
+/* Per-axis integer tables the kernels consume (host only; bit-exact parity
+ * with the oracle's brute-force enumeration).  For one axis (I, F, s, p):
+ *   table 1 (T1, ConvV2 trim, Alg. 1): O rows of (o, ih_s, f_s, f_e)
+ *   table 2 (T2, KS phases, Alg. 2):   s phase records
+ *            (y, CH_y, oph_y, ih_s, U_y, a_y) each followed by U_y rows
+ *            (u, ih, oh_s, ch_s, ch_e); empty phases (CH_y = 0) have
+ *            a_y = oh_s = ch_s = ch_e = 0, and a_y = 0 when U_y = 0;
+ *            an empty trimmed window is written ch_s = ch_e = 0
+ *   table 3 (T3, Sk taps, Alg. 3B):   F rows of (f, ih_s, oh_s, oh_e)
+ *   table 4 (T4, trim classes):       runs (o_start, o_end, f_s, f_e)
+ * flattened into `out` (int64).  *len receives the element count; if it
+ * exceeds cap, nothing is written and CKS_ERR_CAPACITY is returned. */
+cks_status cks_axis_table(int64_t I, int64_t F, int32_t s, int32_t p, int table,
+                          int64_t* out, size_t cap, size_t* len);
+
+/* Operation counts (host only), out[0..7]:
+ *   0 zero-free MACs N*I_C*O_C*V_H*V_W (identical for all three operators)
+ *   1 V_H, 2 V_W (valid (o, f) pairs per axis)
+ *   3 T_Conv, 4 T_Deconv, 5 T_Dilated (with N, reading c9) -- Table III
+ *     nominal FLOPs
+ *   6 MACs issued by the forward kernel incl. padded channels
+ *   7 number of tensor-core tiles of the forward kernel */
+cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]);
+
+/* Number of kernel launches the op issues for this geometry/options (for
+ * the bench's gpu_launches claim).  c_packed_given: deconv skips Stage1. */
+cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, int c_packed_given,
+                            int* launches);
+
+const char* cks_status_string(cks_status s);
+int cks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKS_H */

@@ -1,0 +1,156 @@
+"""ctypes binding of libcks.so (include/cks.h) -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls and takes
+plain integers / pointers.  All compute runs in the CUDA kernels behind the C
+ABI; there is no CPU fallback: if the library is missing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcks.so")
+
+CKS_TF32, CKS_BF16 = 0, 1
+CKS_OP_FWD, CKS_OP_DECONV, CKS_OP_WGRAD = 0, 1, 2
+STATUS = {0: "CKS_OK", 1: "CKS_ERR_NULL", 2: "CKS_ERR_GEOMETRY", 3: "CKS_ERR_UNSUPPORTED",
+          4: "CKS_ERR_ALIGNMENT", 5: "CKS_ERR_WORKSPACE", 6: "CKS_ERR_CUDA", 7: "CKS_ERR_CAPACITY"}
+
+# Every symbol include/cks.h declares (tests check the .so exports all of them).
+EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2d_fwd", "cks_ks_split_size",
+           "cks_ks_split", "cks_deconv2d", "cks_dilated_wgrad", "cks_axis_table", "cks_op_counts",
+           "cks_launch_count", "cks_status_string", "cks_version")
+
+
+class CksError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)} ({_string(status)})")
+
+
+class cks_geom(C.Structure):
+    _fields_ = [("N", C.c_int64), ("C", C.c_int64), ("H", C.c_int64), ("W", C.c_int64), ("OC", C.c_int64),
+                ("FH", C.c_int64), ("FW", C.c_int64), ("sh", C.c_int32), ("sw", C.c_int32), ("ph", C.c_int32),
+                ("pw", C.c_int32), ("dh", C.c_int32), ("dw", C.c_int32)]
+
+
+def make_geom(N, C_, H, W, OC, FH, FW, sh, sw, ph, pw, dh=1, dw=1) -> cks_geom:
+    return cks_geom(N, C_, H, W, OC, FH, FW, sh, sw, ph, pw, dh, dw)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libcks.so not built ({LIB_PATH}); run python -m paper_2306_15951_b200.build "
+                               "or __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        G = C.POINTER(cks_geom)
+        vp, sz = C.c_void_p, C.c_size_t
+        sig = {
+            "cks_output_shape": (C.c_int, [G, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+            "cks_workspace_size": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.POINTER(sz)]),
+            "cks_choose_gz": (C.c_int, [G, C.c_int, C.POINTER(C.c_int)]),
+            "cks_conv2d_fwd": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_ks_split_size": (C.c_int, [G, C.c_int, C.POINTER(sz)]),
+            "cks_ks_split": (C.c_int, [G, C.c_int, vp, vp, vp]),
+            "cks_deconv2d": (C.c_int, [G, C.c_int, vp, vp, vp, vp, vp, sz, vp]),
+            "cks_dilated_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, C.c_int, vp, sz, vp]),
+            "cks_axis_table": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int,
+                                         C.POINTER(C.c_int64), sz, C.POINTER(sz)]),
+            "cks_op_counts": (C.c_int, [G, C.c_int, C.POINTER(C.c_int64)]),
+            "cks_launch_count": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+            "cks_status_string": (C.c_char_p, [C.c_int]),
+            "cks_version": (C.c_int, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _string(status: int) -> str:
+    try:
+        return lib().cks_status_string(status).decode()
+    except Exception:  # pragma: no cover
+        return "?"
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise CksError(st, where)
+
+
+# ------------------------------------------------------------ thin wrappers
+def cks_version() -> int:
+    return lib().cks_version()
+
+
+def cks_output_shape(g: cks_geom):
+    oh, ow = C.c_int64(), C.c_int64()
+    _check(lib().cks_output_shape(C.byref(g), C.byref(oh), C.byref(ow)), "cks_output_shape")
+    return oh.value, ow.value
+
+
+def cks_workspace_size(g: cks_geom, dtype: int, op: int, gz: int = 0) -> int:
+    b = C.c_size_t()
+    _check(lib().cks_workspace_size(C.byref(g), dtype, op, gz, C.byref(b)), "cks_workspace_size")
+    return b.value
+
+
+def cks_choose_gz(g: cks_geom, dtype: int) -> int:
+    v = C.c_int()
+    _check(lib().cks_choose_gz(C.byref(g), dtype, C.byref(v)), "cks_choose_gz")
+    return v.value
+
+
+def cks_ks_split_size(g: cks_geom, dtype: int) -> int:
+    b = C.c_size_t()
+    _check(lib().cks_ks_split_size(C.byref(g), dtype, C.byref(b)), "cks_ks_split_size")
+    return b.value
+
+
+def cks_conv2d_fwd(g, dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_conv2d_fwd(C.byref(g), dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream), "cks_conv2d_fwd")
+
+
+def cks_ks_split(g, dtype, w_ptr, c_ptr, stream):
+    _check(lib().cks_ks_split(C.byref(g), dtype, w_ptr, c_ptr, stream), "cks_ks_split")
+
+
+def cks_deconv2d(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_deconv2d(C.byref(g), dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream),
+           "cks_deconv2d")
+
+
+def cks_dilated_wgrad(g, dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_dilated_wgrad(C.byref(g), dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, stream),
+           "cks_dilated_wgrad")
+
+
+def cks_axis_table(I: int, F: int, s: int, p: int, table: int) -> list:
+    n = C.c_size_t()
+    st = lib().cks_axis_table(I, F, s, p, table, None, 0, C.byref(n))
+    if st not in (0, 7):
+        _check(st, "cks_axis_table")
+    buf = (C.c_int64 * max(n.value, 1))()
+    _check(lib().cks_axis_table(I, F, s, p, table, buf, n.value, C.byref(n)), "cks_axis_table")
+    return list(buf[:n.value])
+
+
+def cks_op_counts(g: cks_geom, dtype: int = CKS_BF16) -> dict:
+    out = (C.c_int64 * 8)()
+    _check(lib().cks_op_counts(C.byref(g), dtype, out), "cks_op_counts")
+    keys = ("zero_free_macs", "VH", "VW", "T_conv", "T_deconv", "T_dilated", "issued_macs_fwd", "tiles_fwd")
+    return dict(zip(keys, list(out)))
+
+
+def cks_launch_count(g: cks_geom, dtype: int, op: int, gz: int = 0, c_packed_given: bool = False) -> int:
+    v = C.c_int()
+    _check(lib().cks_launch_count(C.byref(g), dtype, op, gz, int(c_packed_given), C.byref(v)), "cks_launch_count")
+    return v.value

@@ -1,0 +1,518 @@
+// cks_api.cu -- the C ABI of libcks.so (include/cks.h): validation,
+// workspace carving, TMA descriptor encoding and kernel launches (layer L3).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/cks.h"
+#include "cks_plan.h"
+#include "kernels/aux.cuh"
+#include "kernels/igemm.cuh"
+#include "kernels/wgrad.cuh"
+
+using namespace cks;
+
+namespace {
+
+constexpr int kPlanSMs = 148;  // B200: plan decisions are device-independent
+
+// ------------------------------------------------------------------ driver entry
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+int device_sms() {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return kPlanSMs;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) return kPlanSMs;
+    return sms;
+}
+
+// rank-4 tiled tensor map, 128B swizzle, zero OOB fill
+bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
+                const uint32_t box[4]) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+    cuuint64_t gs[3] = {strides_b[0], strides_b[1], strides_b[2]};
+    cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                     const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cks_status last_cuda() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "[cks] CUDA error: %s\n", cudaGetErrorString(e));
+        return CKS_ERR_CUDA;
+    }
+    return CKS_OK;
+}
+
+template <typename K>
+cks_status set_smem(K kernel, int bytes) {
+    // cudaFuncSetAttribute per call is cheap; keep it stateless (multi-device safe)
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+        last_cuda();
+        return CKS_ERR_CUDA;
+    }
+    return CKS_OK;
+}
+
+void fill_axis(KAxis& k, const std::vector<KRow>& rows) {
+    memset(&k, 0, sizeof(k));
+    for (size_t i = 0; i < rows.size(); ++i) {
+        k.a0[i] = int16_t(rows[i].a0);
+        k.out[i] = int16_t(rows[i].out);
+        k.ts[i] = uint8_t(rows[i].ts);
+        k.te[i] = uint8_t(rows[i].te);
+        k.phase[i] = uint8_t(rows[i].phase);
+    }
+}
+
+bool rows_ok(const std::vector<KRow>& rows) {
+    if (rows.empty() || rows.size() > CKS_MAX_ROWS) return false;
+    for (auto& r : rows)
+        if (r.a0 < -32768 || r.a0 > 32767 || r.out > 32767 || r.ts < 0 || r.te > 255 || r.phase > 255) return false;
+    return true;
+}
+
+// ------------------------------------------------------------------ launchers
+template <int BN, bool TF>
+cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, cudaStream_t st) {
+    using S = IgemmShape<BN, TF>;
+    auto kern = igemm_kernel<BN, TF>;
+    if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
+    long long grid = std::min<long long>(p.num_tiles, device_sms());
+    if (grid < 1) grid = 1;
+    kern<<<unsigned(grid), 256, S::SMEM_BYTES, st>>>(a, b, p);
+    return last_cuda();
+}
+
+cks_status launch_igemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p,
+                        cudaStream_t st) {
+    if (tf32) {
+        switch (BN) {
+            case 32: return launch_igemm_t<32, true>(a, b, p, st);
+            case 64: return launch_igemm_t<64, true>(a, b, p, st);
+            case 128: return launch_igemm_t<128, true>(a, b, p, st);
+            case 256: return launch_igemm_t<256, true>(a, b, p, st);
+        }
+    } else {
+        switch (BN) {
+            case 32: return launch_igemm_t<32, false>(a, b, p, st);
+            case 64: return launch_igemm_t<64, false>(a, b, p, st);
+            case 128: return launch_igemm_t<128, false>(a, b, p, st);
+            case 256: return launch_igemm_t<256, false>(a, b, p, st);
+        }
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
+template <int BN>
+cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
+    using S = WgradShape<BN>;
+    auto kern = wgrad_kernel<BN>;
+    if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
+    long long grid = std::min<long long>(p.num_tiles, device_sms());
+    if (grid < 1) grid = 1;
+    kern<<<unsigned(grid), 256, S::SMEM_BYTES, st>>>(a, b, p);
+    return last_cuda();
+}
+
+cks_status launch_pad(cks_dtype dt, const void* src, void* dst, long long rows, int C, int Cp, cudaStream_t st) {
+    long long total = rows * Cp;
+    unsigned blocks = unsigned(std::min<long long>((total + 255) / 256, 148LL * 16));
+    if (dt == CKS_BF16)
+        pad_channels_kernel<uint16_t><<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(src),
+                                                              static_cast<uint16_t*>(dst), rows, C, Cp);
+    else
+        pad_channels_kernel<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(src),
+                                                              static_cast<uint32_t*>(dst), rows, C, Cp);
+    return last_cuda();
+}
+
+cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* out, cudaStream_t st) {
+    const int CHm = int(cdiv(g.FH, g.sh)), CWm = int(cdiv(g.FW, g.sw));
+    const int OCp = int(pad_ch(g.OC, dt));
+    dim3 grid(unsigned((OCp + 31) / 32), unsigned((g.C + 31) / 32), unsigned(g.sh * g.sw * CHm * CWm));
+    dim3 block(32, 8);
+    if (dt == CKS_BF16)
+        ks_split_kernel<uint16_t><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(w), static_cast<uint16_t*>(out),
+                                                          int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm,
+                                                          CWm, OCp);
+    else
+        ks_split_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(w), static_cast<uint32_t*>(out),
+                                                          int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm,
+                                                          CWm, OCp);
+    return last_cuda();
+}
+
+cks_status check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
+    if (L.total == 0) return CKS_OK;
+    if (!ws || ws_bytes < L.total) return CKS_ERR_WORKSPACE;
+    if (!aligned16(ws)) return CKS_ERR_ALIGNMENT;
+    return CKS_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int cks_version(void) { return 1; }
+
+const char* cks_status_string(cks_status s) {
+    switch (s) {
+        case CKS_OK: return "ok";
+        case CKS_ERR_NULL: return "null pointer argument";
+        case CKS_ERR_GEOMETRY: return "geometry error";
+        case CKS_ERR_UNSUPPORTED: return "unsupported configuration";
+        case CKS_ERR_ALIGNMENT: return "pointer not 16-byte aligned";
+        case CKS_ERR_WORKSPACE: return "workspace too small";
+        case CKS_ERR_CUDA: return "CUDA error";
+        case CKS_ERR_CAPACITY: return "output capacity too small";
+    }
+    return "unknown status";
+}
+
+cks_status cks_output_shape(const cks_geom* g, int64_t* OH, int64_t* OW) {
+    if (!g || !OH || !OW) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK && s != CKS_ERR_UNSUPPORTED) return s;
+    *OH = axis_h(*g).O;
+    *OW = axis_w(*g).O;
+    return CKS_OK;
+}
+
+cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz, size_t* bytes) {
+    if (!g || !bytes) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
+    *bytes = ws_layout(*g, dt, op, gz, false, kPlanSMs).total;
+    return CKS_OK;
+}
+
+cks_status cks_choose_gz(const cks_geom* g, cks_dtype dt, int* gz) {
+    (void)dt;
+    if (!g || !gz) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    *gz = wgrad_cfg(*g, 0, kPlanSMs).gz;
+    return CKS_OK;
+}
+
+cks_status cks_ks_split_size(const cks_geom* g, cks_dtype dt, size_t* bytes) {
+    if (!g || !bytes) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    *bytes = ks_split_bytes(*g, dt);
+    return CKS_OK;
+}
+
+cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y, void* ws,
+                          size_t ws_bytes, void* stream) {
+    if (!g || !x || !w || !y) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y)) return CKS_ERR_ALIGNMENT;
+    const Axis ah = axis_h(*g), aw = axis_w(*g);
+    auto rh = krows_fwd(ah), rw = krows_fwd(aw);
+    if (!rows_ok(rh) || !rows_ok(rw)) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout(*g, dt, CKS_OP_FWD, 0, false, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt);
+    const void* xs = x;
+    const void* wsrc = w;
+    if (Cp != g->C) {
+        void* xp = static_cast<uint8_t*>(ws) + L.x_pad;
+        void* wp = static_cast<uint8_t*>(ws) + L.w_pad;
+        if ((s = launch_pad(dt, x, xp, g->N * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        if ((s = launch_pad(dt, w, wp, g->OC * g->FH * g->FW, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        xs = xp;
+        wsrc = wp;
+    }
+    IgemmCfg cfg = igemm_cfg(ah.O, aw.O, g->N, g->OC, kPlanSMs);
+    const uint32_t BK = uint32_t(128 / eb);
+    CUtensorMap ta, tb;
+    {
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
+        uint32_t box[4] = {BK, 1, 1, 128};
+        if (!make_tmap4(&ta, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    {
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->FH * g->FW), uint64_t(g->OC), 1};
+        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->FH * g->FW * Cp * eb),
+                          uint64_t(g->OC * g->FH * g->FW * Cp * eb)};
+        uint32_t box[4] = {BK, 1, uint32_t(cfg.BN), 1};
+        if (!make_tmap4(&tb, dt, wsrc, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    IgemmParams p;
+    fill_axis(p.ah, rh);
+    fill_axis(p.aw, rw);
+    p.out = y;
+    p.rows_h = int(rh.size());
+    p.rows_w = int(rw.size());
+    p.nblk = cfg.nblk;
+    p.nbs = cfg.nbs;
+    p.kc_blocks = int((Cp + BK - 1) / BK);
+    p.slot_stride = int(g->FW);
+    p.phases_w = 1;
+    p.N = int(g->N);
+    p.out_H = int(ah.O);
+    p.out_W = int(aw.O);
+    p.out_C = int(g->OC);
+    p.num_tiles = cfg.tiles;
+    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, st);
+}
+
+cks_status cks_ks_split(const cks_geom* g, cks_dtype dt, const void* w, void* c_packed, void* stream) {
+    if (!g || !w || !c_packed) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (!aligned16(w) || !aligned16(c_packed)) return CKS_ERR_ALIGNMENT;
+    return launch_split(*g, dt, w, c_packed, static_cast<cudaStream_t>(stream));
+}
+
+cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w, const void* c_packed,
+                        float* dx, void* ws, size_t ws_bytes, void* stream) {
+    if (!g || !dy || !dx) return CKS_ERR_NULL;
+    if ((w == nullptr) == (c_packed == nullptr)) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (!aligned16(dy) || !aligned16(dx) || (w && !aligned16(w)) || (c_packed && !aligned16(c_packed)))
+        return CKS_ERR_ALIGNMENT;
+    const Axis ah = axis_h(*g), aw = axis_w(*g);
+    auto rh = krows_deconv(ah), rw = krows_deconv(aw);
+    if (!rows_ok(rh) || !rows_ok(rw)) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout(*g, dt, CKS_OP_DECONV, 0, c_packed != nullptr, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t eb = elem_bytes(dt), OCp = pad_ch(g->OC, dt);
+    const int64_t OH = ah.O, OW = aw.O;
+    const void* dys = dy;
+    if (OCp != g->OC) {
+        void* p = static_cast<uint8_t*>(ws) + L.dy_pad;
+        if ((s = launch_pad(dt, dy, p, g->N * OH * OW, int(g->OC), int(OCp), st)) != CKS_OK) return s;
+        dys = p;
+    }
+    const void* cp = c_packed;
+    if (!cp) {  // Stage1 into the workspace
+        void* p = static_cast<uint8_t*>(ws) + L.c_packed;
+        if ((s = launch_split(*g, dt, w, p, st)) != CKS_OK) return s;
+        cp = p;
+    }
+    const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
+    IgemmCfg cfg = igemm_cfg(ah.I, aw.I, g->N, g->C, kPlanSMs);
+    const uint32_t BK = uint32_t(128 / eb);
+    CUtensorMap ta, tb;
+    {
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(OW), uint64_t(OH), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(OW * OCp * eb), uint64_t(OH * OW * OCp * eb)};
+        uint32_t box[4] = {BK, 1, 1, 128};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    {
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(CHm * CWm), uint64_t(g->C), uint64_t(P)};
+        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(CHm * CWm * OCp * eb), uint64_t(g->C * CHm * CWm * OCp * eb)};
+        uint32_t box[4] = {BK, 1, uint32_t(cfg.BN), 1};
+        if (!make_tmap4(&tb, dt, cp, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    IgemmParams p;
+    fill_axis(p.ah, rh);
+    fill_axis(p.aw, rw);
+    p.out = dx;
+    p.rows_h = int(rh.size());
+    p.rows_w = int(rw.size());
+    p.nblk = cfg.nblk;
+    p.nbs = cfg.nbs;
+    p.kc_blocks = int((OCp + BK - 1) / BK);
+    p.slot_stride = int(CWm);
+    p.phases_w = g->sw;
+    p.N = int(g->N);
+    p.out_H = int(g->H);
+    p.out_W = int(g->W);
+    p.out_C = int(g->C);
+    p.num_tiles = cfg.tiles;
+    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, st);
+}
+
+cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
+                             void* ws, size_t ws_bytes, void* stream) {
+    if (!g || !x || !dy || !dw) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (dt != CKS_BF16) return CKS_ERR_UNSUPPORTED;  // MN-major TF32 operands: not in this build
+    if (gz < 0) return CKS_ERR_UNSUPPORTED;
+    if (!aligned16(x) || !aligned16(dy) || !aligned16(dw)) return CKS_ERR_ALIGNMENT;
+    if (g->OC > 65535 || g->C > 65535) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout(*g, dt, CKS_OP_WGRAD, gz, false, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Axis ah = axis_h(*g), aw = axis_w(*g);
+    const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt), OCp = pad_ch(g->OC, dt);
+    const void* xs = x;
+    const void* dys = dy;
+    if (Cp != g->C) {
+        void* p = static_cast<uint8_t*>(ws) + L.x_pad;
+        if ((s = launch_pad(dt, x, p, g->N * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        xs = p;
+    }
+    if (OCp != g->OC) {
+        void* p = static_cast<uint8_t*>(ws) + L.dy_pad;
+        if ((s = launch_pad(dt, dy, p, g->N * ah.O * aw.O, int(g->OC), int(OCp), st)) != CKS_OK) return s;
+        dys = p;
+    }
+    WgradCfg cfg = wgrad_cfg(*g, gz, kPlanSMs);
+    CUtensorMap ta, tb;
+    {
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ah.O), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ah.O * aw.O * OCp * eb)};
+        uint32_t box[4] = {64, 1, 1, 64};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    {
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
+        uint32_t box[4] = {64, 1, 1, 64};
+        if (!make_tmap4(&tb, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
+    }
+    WgradParams p;
+    memset(&p, 0, sizeof(p));
+    auto th = table_t3(ah), tw = table_t3(aw);
+    for (size_t i = 0; i < th.size(); ++i) {
+        p.oh_s[i] = int16_t(th[i].oh_s);
+        p.oh_e[i] = int16_t(th[i].oh_e);
+    }
+    for (size_t i = 0; i < tw.size(); ++i) {
+        p.ow_s[i] = int16_t(tw[i].oh_s);
+        p.ow_e[i] = int16_t(tw[i].oh_e);
+    }
+    p.out = cfg.gz > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    p.FH = int(g->FH);
+    p.FW = int(g->FW);
+    p.sh = g->sh;
+    p.sw = g->sw;
+    p.ph = g->ph;
+    p.pw = g->pw;
+    p.N = int(g->N);
+    p.OC = int(g->OC);
+    p.C = int(g->C);
+    p.mblocks = cfg.mblocks;
+    p.nbs = cfg.nbs;
+    p.gz = cfg.gz;
+    p.nblk64 = cfg.nblk64;
+    p.num_tiles = cfg.base_tiles * cfg.gz;
+    p.part_stride = g->OC * g->FH * g->FW * g->C;
+    switch (cfg.BN) {
+        case 64: s = launch_wgrad_t<64>(ta, tb, p, st); break;
+        case 128: s = launch_wgrad_t<128>(ta, tb, p, st); break;
+        case 256: s = launch_wgrad_t<256>(ta, tb, p, st); break;
+        default: return CKS_ERR_UNSUPPORTED;
+    }
+    if (s != CKS_OK) return s;
+    if (cfg.gz > 1) {
+        const long long n = p.part_stride;
+        unsigned blocks = unsigned(std::min<long long>((n / 4 + 255) / 256 + 1, 148LL * 8));
+        if (n % 4 == 0)
+            reduce_partials_kernel<<<blocks, 256, 0, st>>>(p.out, dw, n, cfg.gz);
+        else
+            reduce_partials_scalar_kernel<<<blocks, 256, 0, st>>>(p.out, dw, n, cfg.gz);
+        return last_cuda();
+    }
+    return CKS_OK;
+}
+
+cks_status cks_axis_table(int64_t I, int64_t F, int32_t s, int32_t p, int table, int64_t* out, size_t cap,
+                          size_t* len) {
+    if (!len) return CKS_ERR_NULL;
+    if (I < 1 || F < 1 || s < 1 || p < 0 || p >= F || I + 2 * p - F < 0) return CKS_ERR_GEOMETRY;
+    Axis a{I, F, s, p, out_extent(I, F, s, p)};
+    std::vector<int64_t> v;
+    switch (table) {
+        case 1:
+            for (auto& r : table_t1(a)) v.insert(v.end(), {r.o, r.ih_s, r.f_s, r.f_e});
+            break;
+        case 2:
+            for (auto& ph : table_t2(a)) {
+                v.insert(v.end(), {ph.y, ph.CH, ph.oph, ph.ih_s, ph.U, ph.a});
+                for (auto& r : ph.rows) v.insert(v.end(), {r.u, r.ih, r.oh_s, r.ch_s, r.ch_e});
+            }
+            break;
+        case 3:
+            for (auto& r : table_t3(a)) v.insert(v.end(), {r.f, r.ih_s, r.oh_s, r.oh_e});
+            break;
+        case 4:
+            for (auto& r : table_t4(a)) v.insert(v.end(), {r.o_start, r.o_end, r.f_s, r.f_e});
+            break;
+        default: return CKS_ERR_UNSUPPORTED;
+    }
+    *len = v.size();
+    if (v.size() > cap) return CKS_ERR_CAPACITY;
+    if (!v.empty()) {
+        if (!out) return CKS_ERR_NULL;
+        memcpy(out, v.data(), v.size() * sizeof(int64_t));
+    }
+    return CKS_OK;
+}
+
+cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]) {
+    if (!g || !out) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK && s != CKS_ERR_UNSUPPORTED) return s;
+    const Axis ah = axis_h(*g), aw = axis_w(*g);
+    const int64_t VH = axis_valid_pairs(ah), VW = axis_valid_pairs(aw);
+    const int64_t OHp = ah.O + (ah.O - 1) * (g->sh - 1), OWp = aw.O + (aw.O - 1) * (g->sw - 1);
+    out[0] = g->N * g->C * g->OC * VH * VW;
+    out[1] = VH;
+    out[2] = VW;
+    out[3] = 2 * (g->OC * g->N * ah.O * aw.O * g->FH * g->FW * g->C);
+    out[4] = 2 * (g->C * g->N * g->H * g->W * g->FH * g->FW * g->OC);
+    out[5] = 2 * (g->OC * g->FH * g->FW * g->C * OHp * OWp) * g->N;
+    IgemmCfg cfg = igemm_cfg(ah.O, aw.O, g->N, g->OC, kPlanSMs);
+    const int64_t Cp = pad_ch(g->C, dt), BK = 128 / elem_bytes(dt);
+    out[6] = int64_t(cfg.nblk) * 128 * int64_t(cfg.nbs) * cfg.BN * VH * VW * ((Cp + BK - 1) / BK * BK);
+    out[7] = cfg.tiles;
+    return CKS_OK;
+}
+
+cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, int c_packed_given, int* launches) {
+    if (!g || !launches) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    const bool cpad = pad_ch(g->C, dt) != g->C, ocpad = pad_ch(g->OC, dt) != g->OC;
+    int n = 1;
+    if (op == CKS_OP_FWD) n += cpad ? 2 : 0;
+    else if (op == CKS_OP_DECONV) n += (c_packed_given ? 0 : 1) + (ocpad ? 1 : 0);
+    else if (op == CKS_OP_WGRAD) n += (cpad ? 1 : 0) + (ocpad ? 1 : 0) + (wgrad_cfg(*g, gz, kPlanSMs).gz > 1 ? 1 : 0);
+    else return CKS_ERR_UNSUPPORTED;
+    *launches = n;
+    return CKS_OK;
+}
+
+}  // extern "C"

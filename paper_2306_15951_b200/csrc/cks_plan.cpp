@@ -1,0 +1,199 @@
+// cks_plan.cpp -- host-side geometry, closed-form index tables, tiling plan.
+// See cks_plan.h.  Citations: P:<line> = PAPER.md; readings c1-c16 =
+// SURVEY.md §8(c), listed in DESIGN.md.
+#include "cks_plan.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace cks {
+
+int64_t out_extent(int64_t I, int64_t F, int64_t s, int64_t p) {
+    return fdiv(I + 2 * p - F, s) + 1;  // Table I shape rule (reading c10)
+}
+
+cks_status validate(const cks_geom* g) {
+    if (!g) return CKS_ERR_NULL;
+    if (g->N < 1 || g->C < 1 || g->H < 1 || g->W < 1 || g->OC < 1 || g->FH < 1 || g->FW < 1)
+        return CKS_ERR_GEOMETRY;
+    if (g->sh < 1 || g->sw < 1 || g->ph < 0 || g->pw < 0) return CKS_ERR_GEOMETRY;
+    if (g->ph >= g->FH || g->pw >= g->FW) return CKS_ERR_GEOMETRY;  // reading c16
+    if (g->H + 2 * g->ph - g->FH < 0 || g->W + 2 * g->pw - g->FW < 0) return CKS_ERR_GEOMETRY;
+    if (g->dh != 1 || g->dw != 1) return CKS_ERR_UNSUPPORTED;        // dilate == stride
+    if (g->FH > 32 || g->FW > 32 || g->sh > 8 || g->sw > 8) return CKS_ERR_UNSUPPORTED;
+    if (g->N > (int64_t(1) << 30) || g->H > 65535 || g->W > 65535) return CKS_ERR_UNSUPPORTED;
+    return CKS_OK;
+}
+
+Axis axis_h(const cks_geom& g) { return {g.H, g.FH, g.sh, g.ph, out_extent(g.H, g.FH, g.sh, g.ph)}; }
+Axis axis_w(const cks_geom& g) { return {g.W, g.FW, g.sw, g.pw, out_extent(g.W, g.FW, g.sw, g.pw)}; }
+
+// T1 -- Alg. 1, reading c1: ih_s = o*s - p, [f_s, f_e) with
+// f_s = max(-ih_s, 0), f_e = min(I - ih_s, F)  ("ending at (fh_e-1, fw_e-1)").
+std::vector<T1Row> table_t1(const Axis& a) {
+    std::vector<T1Row> t;
+    for (int64_t o = 0; o < a.O; ++o) {
+        int64_t ih_s = o * a.s - a.p;
+        t.push_back({o, ih_s, std::max<int64_t>(-ih_s, 0), std::min(a.I - ih_s, a.F)});
+    }
+    return t;
+}
+
+// T2 -- Alg. 2 Stage1/Stage2&3 + 2B, readings c2 (C extent
+// ceil), c3 (rows while ih < I), c4 (trim end min(O - oh_s, CH_y)), c11
+// (empty phases), c12 (phase y writes ih = (y - p) mod s).
+std::vector<T2Phase> table_t2(const Axis& a) {
+    std::vector<T2Phase> out;
+    for (int64_t y = 0; y < a.s; ++y) {
+        T2Phase ph;
+        ph.y = y;
+        ph.CH = a.F > y ? cdiv(a.F - y, a.s) : 0;     // ceil((F_H - y)/sh)
+        ph.oph = ph.CH - 1;
+        int64_t ih_s = y - a.p;                         // Alg. 2: ih_s = y - ph
+        if (ih_s < 0) ih_s += cdiv(-ih_s, a.s) * a.s;  //  += ceil(-ih_s/sh)*sh
+        ph.ih_s = ih_s;
+        ph.U = ih_s < a.I ? cdiv(a.I - ih_s, a.s) : 0;
+        // oh_s(u) = (ih + ph - y)/sh - oph = u + a  (exact division)
+        ph.a = (ph.CH > 0 && ph.U > 0) ? fdiv(ih_s + a.p - y, a.s) - ph.oph : 0;  // 0 for empty phases
+        for (int64_t u = 0; u < ph.U; ++u) {
+            T2Row r{u, u * a.s + ih_s, 0, 0, 0};
+            if (ph.CH > 0) {
+                r.oh_s = u + ph.a;
+                int64_t cs = std::max<int64_t>(-r.oh_s, 0);
+                int64_t ce = std::min(a.O - r.oh_s, ph.CH);
+                if (ce > cs) { r.ch_s = cs; r.ch_e = ce; }
+            }
+            ph.rows.push_back(r);
+        }
+        out.push_back(std::move(ph));
+    }
+    return out;
+}
+
+// T3 -- Alg. 3B, reading c5: ih_s = f - p,
+// oh_s = max(ceil(-ih_s/s), 0), oh_e = min(O, ceil((I - ih_s)/s)); empty -> (0,0).
+std::vector<T3Row> table_t3(const Axis& a) {
+    std::vector<T3Row> t;
+    for (int64_t f = 0; f < a.F; ++f) {
+        int64_t ih_s = f - a.p;
+        int64_t os = std::max<int64_t>(cdiv(-ih_s, a.s), 0);
+        int64_t oe = std::min(a.O, cdiv(a.I - ih_s, a.s));
+        if (oe <= os) os = oe = 0;
+        t.push_back({f, ih_s, os, oe});
+    }
+    return t;
+}
+
+std::vector<T4Run> table_t4(const Axis& a) {
+    std::vector<T4Run> runs;
+    for (const auto& r : table_t1(a)) {
+        if (!runs.empty() && runs.back().f_s == r.f_s && runs.back().f_e == r.f_e && runs.back().o_end == r.o)
+            runs.back().o_end = r.o + 1;
+        else
+            runs.push_back({r.o, r.o + 1, r.f_s, r.f_e});
+    }
+    return runs;
+}
+
+int64_t axis_valid_pairs(const Axis& a) {
+    int64_t v = 0;
+    for (const auto& r : table_t1(a)) v += std::max<int64_t>(r.f_e - r.f_s, 0);
+    return v;
+}
+
+std::vector<KRow> krows_fwd(const Axis& a) {
+    std::vector<KRow> r;
+    for (const auto& t : table_t1(a)) r.push_back({t.ih_s, t.f_s, t.f_e, t.o, 0});
+    return r;
+}
+
+std::vector<KRow> krows_deconv(const Axis& a) {
+    std::vector<KRow> r;
+    for (const auto& ph : table_t2(a))
+        for (const auto& row : ph.rows) r.push_back({row.oh_s, row.ch_s, row.ch_e, row.ih, ph.y});
+    return r;
+}
+
+IgemmCfg igemm_cfg(int64_t rows_h, int64_t rows_w, int64_t N, int64_t nout, int num_sms) {
+    IgemmCfg c;
+    c.nblk = int((N + 127) / 128);
+    int64_t pix = rows_h * rows_w * c.nblk;
+    if (nout <= 32) c.BN = 32;
+    else if (nout <= 64) c.BN = 64;
+    else if (nout <= 128) c.BN = 128;
+    else c.BN = 256;
+    // more, narrower tiles when the grid would not fill the SMs
+    if (c.BN == 256 && pix * ((nout + 255) / 256) < num_sms) c.BN = 128;
+    c.nbs = int((nout + c.BN - 1) / c.BN);
+    c.tiles = pix * c.nbs;
+    return c;
+}
+
+// G_Z choice: the paper makes G_Z grow with (N_a + N_b)/N_g and
+// bounds it above by the SM count.  Here: enough segments that the
+// taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
+// with at least 4 K-blocks (256 images*positions) per segment.
+WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms) {
+    WgradCfg c;
+    c.mblocks = int((g.OC + 127) / 128);
+    c.BN = g.C <= 64 ? 64 : (g.C <= 128 ? 128 : 256);
+    c.nbs = int((g.C + c.BN - 1) / c.BN);
+    c.nblk64 = int((g.N + 63) / 64);
+    Axis ah = axis_h(g), aw = axis_w(g);
+    auto th = table_t3(ah), tw = table_t3(aw);
+    int64_t lmin = INT64_MAX, ntaps = 0;
+    for (auto& a : th)
+        for (auto& b : tw) {
+            int64_t L = (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
+            if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
+        }
+    if (ntaps == 0) lmin = 1;
+    c.base_tiles = int64_t(g.FH) * g.FW * c.mblocks * c.nbs;
+    if (gz_req > 0) {
+        c.gz = gz_req;
+    } else {
+        int64_t want = (num_sms + c.base_tiles / 2) / std::max<int64_t>(c.base_tiles, 1);
+        int64_t cap = std::max<int64_t>(lmin / 4, 1);
+        c.gz = int(std::max<int64_t>(1, std::min<int64_t>({want, cap, 64})));
+    }
+    return c;
+}
+
+size_t ks_split_bytes(const cks_geom& g, cks_dtype dt) {
+    int64_t chm = cdiv(g.FH, g.sh), cwm = cdiv(g.FW, g.sw);
+    return size_t(g.sh) * g.sw * g.C * chm * cwm * pad_ch(g.OC, dt) * elem_bytes(dt);
+}
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms) {
+    WsLayout L;
+    const int64_t eb = elem_bytes(dt);
+    const int64_t Cp = pad_ch(g.C, dt), OCp = pad_ch(g.OC, dt);
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph), OW = out_extent(g.W, g.FW, g.sw, g.pw);
+    size_t off = 0;
+    auto take = [&](size_t bytes, size_t& at, size_t& sz) {
+        if (!bytes) return;
+        at = off;
+        sz = bytes;
+        off += align256(bytes);
+    };
+    if (op == CKS_OP_FWD || op == CKS_OP_WGRAD) {
+        if (Cp != g.C) take(size_t(g.N) * g.H * g.W * Cp * eb, L.x_pad, L.x_pad_bytes);
+    }
+    if (op == CKS_OP_FWD) {
+        if (Cp != g.C) take(size_t(g.OC) * g.FH * g.FW * Cp * eb, L.w_pad, L.w_pad_bytes);
+    }
+    if (op == CKS_OP_DECONV || op == CKS_OP_WGRAD) {
+        if (OCp != g.OC) take(size_t(g.N) * OH * OW * OCp * eb, L.dy_pad, L.dy_pad_bytes);
+    }
+    if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
+    if (op == CKS_OP_WGRAD) {
+        WgradCfg c = wgrad_cfg(g, gz, num_sms);
+        if (c.gz > 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+    }
+    L.total = off;
+    return L;
+}
+
+}  // namespace cks

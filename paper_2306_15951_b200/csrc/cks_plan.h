@@ -1,0 +1,87 @@
+// cks_plan.h -- host-side geometry, index tables and tiling plan (layer L1).
+//
+// Closed-form versions of the per-axis tables of the C-K-S algorithms
+// (PAPER.md Appendix, Alg. 1 / 2 / 2B / 3B) under the readings of
+// SURVEY.md §8(c) (c1-c16).  The kernels consume exactly these tables; the
+// CPU test suite checks them bit-exactly against the oracle's brute-force
+// enumeration (tests/test_plan_abi.py).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/cks.h"
+
+namespace cks {
+
+// Mathematical floor / ceil division (correct for negative numerators; C++
+// '/' truncates toward zero, and oh_s can be -1 -- SURVEY.md §7 hard part 6).
+inline int64_t fdiv(int64_t a, int64_t b) {
+    int64_t q = a / b, r = a % b;
+    return (r != 0 && ((r < 0) != (b < 0))) ? q - 1 : q;
+}
+inline int64_t cdiv(int64_t a, int64_t b) { return -fdiv(-a, b); }
+inline int64_t fmod_pos(int64_t a, int64_t b) { return a - fdiv(a, b) * b; }
+
+struct Axis {
+    int64_t I, F, s, p, O;
+};
+
+struct T1Row { int64_t o, ih_s, f_s, f_e; };
+struct T2Row { int64_t u, ih, oh_s, ch_s, ch_e; };
+struct T2Phase {
+    int64_t y, CH, oph, ih_s, U, a;
+    std::vector<T2Row> rows;
+};
+struct T3Row { int64_t f, ih_s, oh_s, oh_e; };
+struct T4Run { int64_t o_start, o_end, f_s, f_e; };
+
+cks_status validate(const cks_geom* g);
+Axis axis_h(const cks_geom& g);
+Axis axis_w(const cks_geom& g);
+int64_t out_extent(int64_t I, int64_t F, int64_t s, int64_t p);
+
+std::vector<T1Row> table_t1(const Axis& a);      // Alg. 1 trim
+std::vector<T2Phase> table_t2(const Axis& a);    // Alg. 2 / 2B phases
+std::vector<T3Row> table_t3(const Axis& a);      // Alg. 3B taps
+std::vector<T4Run> table_t4(const Axis& a);      // trim classes
+int64_t axis_valid_pairs(const Axis& a);         // V
+
+// Per-axis row list consumed by the implicit-GEMM kernel (fwd / deconv).
+// Row r: A-operand coordinate of tap 0 (a0), trimmed tap window [ts, te),
+// output coordinate, phase index.  Fwd: one row per output o (T1).  Deconv:
+// the T2 rows of all phases in phase order.
+struct KRow { int64_t a0, ts, te, out, phase; };
+std::vector<KRow> krows_fwd(const Axis& a);
+std::vector<KRow> krows_deconv(const Axis& a);
+
+// channel padding to 16-byte rows
+inline int64_t pad_ch(int64_t c, cks_dtype dt) {
+    int64_t q = dt == CKS_BF16 ? 8 : 4;
+    return (c + q - 1) / q * q;
+}
+inline int64_t elem_bytes(cks_dtype dt) { return dt == CKS_BF16 ? 2 : 4; }
+
+// Kernel configuration decisions (shared by workspace query and launch).
+struct IgemmCfg {
+    int BN;        // output-channel tile
+    int nbs;       // number of BN tiles
+    int nblk;      // ceil(N / 128)
+    int64_t tiles;
+};
+IgemmCfg igemm_cfg(int64_t rows_h, int64_t rows_w, int64_t N, int64_t nout, int num_sms);
+
+struct WgradCfg {
+    int BN, nbs, mblocks, nblk64, gz;
+    int64_t base_tiles;
+};
+WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms);
+
+// Workspace layout (byte offsets, 256-aligned) for one op.
+struct WsLayout {
+    size_t x_pad = 0, w_pad = 0, dy_pad = 0, c_packed = 0, partial = 0, total = 0;
+    size_t x_pad_bytes = 0, w_pad_bytes = 0, dy_pad_bytes = 0, c_packed_bytes = 0, partial_bytes = 0;
+};
+WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms);
+size_t ks_split_bytes(const cks_geom& g, cks_dtype dt);
+
+}  // namespace cks

@@ -1,0 +1,226 @@
+// wgrad.cuh -- KB-WGRAD: Sk-dilated-V2 weight gradient (Alg. 3/3B)
+// on tcgen05 tensor cores with the G_Z map-reduce of P:210.
+//
+// Per filter tap (fh, fw) the weight gradient is a GEMM
+//   dW[oc][ic] (tap) = sum_k dY[k][oc] * X[gather(k)][ic],
+//   k = (oh, ow, n) over the TRIMMED range [oh_s, oh_e) x [ow_s, ow_e) x N
+// (T3, reading c5) -- the filter dY is read densely (no inserted zeros) and
+// X with LEAPING access ih = oh*sh + fh - ph, iw = ow*sw + fw - pw (P:196-206,
+// Fig. 7).  In NHWC both operands have the reduction axis strided and the
+// channel axis contiguous, so both are MN-major: a k-block is 64 images at
+// one (oh, ow), loaded by TMA 4-D boxes (64 ch, 1, 1, 64 images) into the
+// 128B-swizzled MN-major canonical layout (64-channel atoms, LBO = 8 KB
+// between atoms, SBO = 1 KB between 8-row K groups).
+//
+// Tile = (tap, OC block of 128, IC block of BN, segment z of G_Z).  Segment z
+// covers k-blocks [z*L/G_Z, (z+1)*L/G_Z) of the tap's L k-blocks; with G_Z > 1
+// each segment writes fp32 partials that KB-REDUCE sums in a fixed order
+// ("the results obtained from each segment are aggregated").
+#pragma once
+#include "ptx.cuh"
+
+namespace cks {
+
+struct WgradParams {
+    int16_t oh_s[32], oh_e[32], ow_s[32], ow_e[32];  // T3 per tap row / column
+    float* out;             // dW (gz == 1) or partials [gz][OC][FH*FW][C]
+    int FH, FW, sh, sw, ph, pw;
+    int N, OC, C;
+    int mblocks, nbs, gz, nblk64;
+    long long num_tiles;
+    long long part_stride;  // OC*FH*FW*C
+};
+
+template <int BN>
+struct WgradShape {
+    static constexpr int A_BYTES = 2 * 8192;        // 128 OC x 64 images (bf16)
+    static constexpr int B_BYTES = (BN / 64) * 8192;  // BN IC x 64 images
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+};
+
+struct WTile {
+    int nb, mb, z, fh, fw;
+    int kb0, kb1;  // k-block range of this segment
+    int wn;        // ow extent
+    int ohs, ows;
+};
+
+__device__ __forceinline__ WTile wdecode(long long t, const WgradParams& p) {
+    WTile c;
+    c.nb = int(t % p.nbs);
+    t /= p.nbs;
+    c.mb = int(t % p.mblocks);
+    t /= p.mblocks;
+    c.z = int(t % p.gz);
+    t /= p.gz;
+    const int tap = int(t);
+    c.fh = tap / p.FW;
+    c.fw = tap % p.FW;
+    c.ohs = p.oh_s[c.fh];
+    c.ows = p.ow_s[c.fw];
+    const int hn = p.oh_e[c.fh] - c.ohs, wn = p.ow_e[c.fw] - c.ows;
+    c.wn = wn;
+    const long long L = static_cast<long long>(hn) * wn * p.nblk64;
+    c.kb0 = int(L * c.z / p.gz);
+    c.kb1 = int(L * (c.z + 1) / p.gz);
+    return c;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
+                 const __grid_constant__ WgradParams p) {
+    using S = WgradShape<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
+    uint64_t* empty = full + S::STAGES;
+    uint64_t* tfull = empty + S::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmDY);
+        ptx::prefetch_tmap(&tmX);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int i = 0; i < S::STAGES; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 128);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, S::TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                const WTile c = wdecode(t, p);
+                for (int kb = c.kb0; kb < c.kb1; ++kb) {
+                    const int n64 = kb % p.nblk64;
+                    const int pos = kb / p.nblk64;
+                    const int oh = c.ohs + pos / c.wn, ow = c.ows + pos % c.wn;
+                    const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
+                    const int iw = ow * p.sw + c.fw - p.pw;
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+                    uint8_t* sa = smem + stage * S::STAGE_BYTES;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * 64, ow, oh, n64 * 64);
+#pragma unroll
+                    for (int j = 0; j < BN / 64; ++j)
+                        ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * 64, iw, ih,
+                                         n64 * 64);
+                    if (++stage == S::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, true, true);
+            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                const WTile c = wdecode(t, p);
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = c.kb0; kb < c.kb1; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + S::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {  // 64 images = 4 x K16
+                        const uint64_t ad = ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024);
+                        const uint64_t bd = ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024);
+                        ptx::mma_ss<false>(d, ad, bd, idesc, ((kb - c.kb0) | kk) != 0);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == S::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        const uint32_t sub = warp & 3;
+        const int row = int(sub * 32 + lane);
+        const int taps = p.FH * p.FW;
+        const bool vec4 = (p.C % 4) == 0;
+        uint32_t acc = 0, acc_phase = 0;
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const WTile c = wdecode(t, p);
+            const bool zero = c.kb1 <= c.kb0;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int oc = c.mb * 128 + row;
+            const int cbase = c.nb * BN;
+            const int cvalid = min(BN, p.C - cbase);
+            float* dst = nullptr;
+            if (oc < p.OC)
+                dst = p.out + c.z * p.part_stride + (static_cast<long long>(oc) * taps + c.fh * p.FW + c.fw) * p.C +
+                      cbase;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * BN + c0, r);
+                ptx::tmem_ld_wait();
+                if (dst != nullptr && c0 < cvalid) {
+                    if (zero) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = 0u;
+                    }
+                    if (vec4 && c0 + 32 <= cvalid) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<float4*>(dst + c0 + j) =
+                                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < cvalid) dst[c0 + j] = __uint_as_float(r[j]);
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, S::TMEM_COLS);
+    }
+}
+
+}  // namespace cks

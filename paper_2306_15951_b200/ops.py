@@ -1,0 +1,146 @@
+"""Torch-facing helpers over the C ABI (argument marshalling only).
+
+PyTorch provides device memory, streams and process groups; every step of the
+C-K-S path runs in libcks.so's CUDA kernels.  Tensors are NHWC (activations)
+and OHWI (filters), bfloat16 (CKS_BF16) or float32 (CKS_TF32); outputs fp32.
+There is no CPU fallback: non-CUDA tensors raise.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+from ._lib import CKS_BF16, CKS_TF32, make_geom
+
+_WS: dict = {}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return CKS_BF16
+    if t.dtype == torch.float32:
+        return CKS_TF32
+    raise TypeError(f"unsupported dtype {t.dtype} (bfloat16 or float32)")
+
+
+def _check_dev(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise RuntimeError("C-K-S ops run on CUDA tensors only (no CPU fallback)")
+        if not t.is_contiguous():
+            raise RuntimeError("C-K-S ops take dense contiguous tensors")
+
+
+def _stream_ptr(stream) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def workspace(nbytes: int, device, stream=None) -> torch.Tensor | None:
+    """Reusable per-(device, stream) scratch buffer (grown on demand)."""
+    if nbytes == 0:
+        return None
+    key = (torch.device(device).index, _stream_ptr(stream))
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def _ws_args(ws):
+    return (0, 0) if ws is None else (ws.data_ptr(), ws.numel())
+
+
+def _pair(v):
+    return (v, v) if isinstance(v, int) else tuple(v)
+
+
+def geom_of(x_shape, w_shape, stride, padding):
+    N, H, W, C = x_shape
+    OC, FH, FW, C2 = w_shape
+    if C != C2:
+        raise ValueError(f"channel mismatch X {C} vs W {C2}")
+    sh, sw = _pair(stride)
+    ph, pw = _pair(padding)
+    return make_geom(N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+
+
+def conv2d_fwd(x, w, stride=1, padding=0, out=None, stream=None):
+    """Y = conv2D(X, W) by ConvV2 (Eq (1), Alg. 1)."""
+    _check_dev(x, w, out)
+    dt = _dtype_code(x)
+    g = geom_of(tuple(x.shape), tuple(w.shape), stride, padding)
+    OH, OW = L.cks_output_shape(g)
+    if out is None:
+        out = torch.empty((g.N, OH, OW, g.OC), dtype=torch.float32, device=x.device)
+    ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_FWD), x.device, stream)
+    L.cks_conv2d_fwd(g, dt, x.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out
+
+
+def ks_split(w, stride, x_hw=None, out=None, stream=None):
+    """KS-deconv Stage1 (Alg. 2 Stage1): packed per-phase sub-filters."""
+    _check_dev(w, out)
+    dt = _dtype_code(w)
+    OC, FH, FW, C = w.shape
+    sh, sw = _pair(stride)
+    H, W = x_hw if x_hw is not None else (FH, FW)
+    g = make_geom(1, C, max(H, FH), max(W, FW), OC, FH, FW, sh, sw, 0, 0)
+    nbytes = L.cks_ks_split_size(g, dt)
+    if out is None:
+        out = torch.empty(nbytes // w.element_size(), dtype=w.dtype, device=w.device)
+    L.cks_ks_split(g, dt, w.data_ptr(), out.data_ptr(), _stream_ptr(stream))
+    return out
+
+
+def deconv2d(dy, w, x_hw, stride=1, padding=0, c_packed=None, in_channels=None, out=None, stream=None):
+    """dX = deconv2D(dY, W^rot180) by KS-deconv-V2 (Eq (2), Alg. 2/2B).
+    ``x_hw`` = (I_H, I_W) of the forward input (output padding, reading c10).
+    Pass ``c_packed`` (from ks_split) to skip Stage1; then ``w`` may be a
+    shape-only tensor and is not read."""
+    _check_dev(dy, c_packed, out)
+    dt = _dtype_code(dy)
+    N, OH_, OW_, OC = dy.shape
+    OC2, FH, FW, C = w.shape
+    if OC != OC2:
+        raise ValueError("dY channels != W out-channels")
+    H, W = x_hw
+    sh, sw = _pair(stride)
+    ph, pw = _pair(padding)
+    g = make_geom(N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+    if L.cks_output_shape(g) != (OH_, OW_):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = torch.empty((N, H, W, C), dtype=torch.float32, device=dy.device)
+    if c_packed is None:
+        _check_dev(w)
+        ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
+        wp, cp = w.data_ptr(), 0
+    else:
+        ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
+        wp, cp = 0, c_packed.data_ptr()
+    L.cks_deconv2d(g, dt, dy.data_ptr(), wp or None, cp or None, out.data_ptr(), *_ws_args(ws),
+                   _stream_ptr(stream))
+    return out
+
+
+def dilated_wgrad(x, dy, filter_hw, stride=1, padding=0, gz=0, out=None, stream=None):
+    """dW = dilated_conv2D(X, dY) by Sk-dilated-V2 (Eq (3), Alg. 3/3B)."""
+    _check_dev(x, dy, out)
+    dt = _dtype_code(x)
+    N, H, W, C = x.shape
+    OC = dy.shape[3]
+    FH, FW = filter_hw
+    sh, sw = _pair(stride)
+    ph, pw = _pair(padding)
+    g = make_geom(N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+    if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = torch.empty((OC, FH, FW, C), dtype=torch.float32, device=x.device)
+    ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_WGRAD, gz), x.device, stream)
+    L.cks_dilated_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), gz, *_ws_args(ws), _stream_ptr(stream))
+    return out

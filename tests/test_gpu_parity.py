@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C ABI of libcks.so) against the
+fp64 CPU oracle on identical seeded inputs.
+
+Tolerance: the contract (BASELINE.json north_star) is a normwise relative
+error <= 2e-2 for BF16 and <= 5e-3 for TF32 (fp32 accumulation).  Because the
+oracle receives exactly the bf16 values the GPU multiplies, the only BF16
+error source is fp32 accumulation order, so the tests also enforce a much
+tighter bound (tight_bf16) to catch a dropped or
+duplicated boundary tap that a 2e-2 normwise bound could hide on large maps.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from cks_synth import Layer, bf16_bits, get_config, make_layer_inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": 2e-2, "tf32": 5e-3}
+U32 = 2.0 ** -24  # fp32 unit roundoff
+
+
+def tight_bf16(k: int) -> float:
+    """Tight bound for bf16-exact inputs: fp32 accumulation of k terms has a
+    typical relative error ~ u*sqrt(k); 8x margin."""
+    return max(1e-6, 8.0 * U32 * np.sqrt(k))
+
+
+def red_len(lay, op):
+    OH, OW = lay.out_hw()
+    return {"fwd": lay.FH * lay.FW * lay.C, "deconv": lay.FH * lay.FW * lay.OC, "wgrad": lay.N * OH * OW}[op]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    from paper_2306_15951_b200 import build
+    build.build()
+    return torch
+
+
+def dev(torch, a, dtype):
+    """numpy float32 (bf16-representable for 'bf16') -> CUDA tensor."""
+    if dtype == "bf16":
+        bits = torch.from_numpy(bf16_bits(a).view(np.int16))
+        return bits.view(torch.bfloat16).cuda()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def nrm_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.linalg.norm(ref)
+    return np.linalg.norm(got - ref) / (den if den > 0 else 1.0)
+
+
+def check(got, ref, dtype, what, k=1):
+    e = nrm_err(got, ref)
+    assert e <= TOL[dtype], f"{what}: normwise error {e:.3e} > {TOL[dtype]}"
+    if dtype == "bf16":
+        assert e <= tight_bf16(k), f"{what}: normwise error {e:.3e} > tight bound {tight_bf16(k):.2e}"
+    return e
+
+
+def run_all(torch, lay: Layer, dtype="bf16", config=0, idx=0, ops=("fwd", "deconv", "wgrad"), gz=0,
+            via_split=False):
+    from paper_2306_15951_b200 import ops as K
+    a = make_layer_inputs(lay, config, idx, dtype)
+    X, W, G = dev(torch, a["X"], dtype), dev(torch, a["W"], dtype), dev(torch, a["dY"], dtype)
+    out = {}
+    s, p = (lay.sh, lay.sw), (lay.ph, lay.pw)
+    if "fwd" in ops:
+        out["fwd"] = K.conv2d_fwd(X, W, s, p)
+    if "deconv" in ops:
+        if via_split:
+            cp = K.ks_split(W, s)
+            out["deconv"] = K.deconv2d(G, W, (lay.H, lay.W), s, p, c_packed=cp)
+        else:
+            out["deconv"] = K.deconv2d(G, W, (lay.H, lay.W), s, p)
+    if "wgrad" in ops:
+        out["wgrad"] = K.dilated_wgrad(X, G, (lay.FH, lay.FW), s, p, gz=gz)
+    torch.cuda.synchronize()
+    return a, {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def check_full(torch, lay, dtype="bf16", **kw):
+    a, got = run_all(torch, lay, dtype, **kw)
+    s = (lay.sh, lay.sw, lay.ph, lay.pw)
+    if "fwd" in got:
+        check(got["fwd"], O.conv_ref(a["X"], a["W"], *s), dtype, f"{lay} fwd", red_len(lay, "fwd"))
+    if "deconv" in got:
+        check(got["deconv"], O.deconv_ref(a["dY"], a["W"], lay.H, lay.W, *s), dtype, f"{lay} deconv",
+              red_len(lay, "deconv"))
+    if "wgrad" in got:
+        check(got["wgrad"], O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, *s), dtype, f"{lay} wgrad",
+              red_len(lay, "wgrad"))
+    return got
+
+
+# ------------------------------------------------------------------ C1
+@pytest.mark.parametrize("dtype", ["bf16"])
+def test_c1_all_ops(torch_cuda, dtype):
+    lay = get_config(0)[1][0]
+    got = check_full(torch_cuda, lay, dtype)
+    # brute-force scalar loops too (C1 is tiny)
+    a = make_layer_inputs(lay, 0, 0, dtype)
+    s = (lay.sh, lay.sw, lay.ph, lay.pw)
+    assert nrm_err(got["fwd"], O.brute_conv(a["X"], a["W"], *s)) < tight_bf16(red_len(lay, "fwd"))
+    assert nrm_err(got["deconv"], O.brute_deconv(a["dY"], a["W"], lay.H, lay.W, *s)) < tight_bf16(red_len(lay, "deconv"))
+    assert nrm_err(got["wgrad"], O.brute_wgrad(a["X"], a["dY"], lay.FH, lay.FW, *s)) < tight_bf16(red_len(lay, "wgrad"))
+
+
+def test_c1_tf32_fwd_deconv(torch_cuda):
+    lay = get_config(0)[1][0]
+    check_full(torch_cuda, lay, "tf32", ops=("fwd", "deconv"))
+
+
+# ------------------------------------------------------- random geometries
+def _rand_layers(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        FH, FW = int(rng.choice([1, 2, 3, 4, 5, 7])), int(rng.choice([1, 3, 4, 5]))
+        sh, sw = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        ph, pw = int(rng.integers(0, FH)), int(rng.integers(0, FW))
+        H, W = int(rng.integers(max(1, FH - 2 * ph), 20)), int(rng.integers(max(1, FW - 2 * pw), 20))
+        C = int(rng.choice([3, 8, 16, 24, 64, 72, 136]))
+        OC = int(rng.choice([5, 8, 32, 64, 96, 200, 264]))
+        N = int(rng.choice([1, 3, 130]))
+        lay = Layer(f"rand{len(out)}", N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+        try:
+            O.geom(**lay.geom())
+        except O.GeometryError:
+            continue
+        if N * H * W * max(C, OC) > 3e6:
+            continue
+        out.append(lay)
+    return out
+
+
+@pytest.mark.parametrize("lay", _rand_layers(24, 11), ids=lambda l: f"{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
+def test_random_geometries(torch_cuda, lay):
+    check_full(torch_cuda, lay, "bf16", config=9, idx=int(lay.name[4:]))
+
+
+def test_empty_phase_and_unread_rows(torch_cuda):
+    # 1x1 s2 downsample: KS phase y=1 has CH=0 -> odd rows of dX must be 0 (c11);
+    # I=6, F=3, s=2, p=0: row 5 of X is never read -> dX row 5 = 0 (c10).
+    for lay in (Layer("ds", 4, 64, 8, 8, 128, 1, 1, 2, 2, 0, 0), Layer("tail", 3, 16, 6, 7, 24, 3, 3, 2, 2, 0, 0)):
+        got = check_full(torch_cuda, lay)
+        if lay.name == "ds":
+            assert np.all(got["deconv"][:, 1::2, :, :] == 0) and np.all(got["deconv"][:, :, 1::2, :] == 0)
+        else:
+            assert np.all(got["deconv"][:, 5, :, :] == 0)
+
+
+def test_ks_split_exact_and_cached_path(torch_cuda):
+    torch = torch_cuda
+    from paper_2306_15951_b200 import ops as K
+    lay = Layer("g", 5, 24, 8, 8, 40, 4, 4, 2, 2, 1, 1)
+    a = make_layer_inputs(lay, 7, 0)
+    W = dev(torch, a["W"], "bf16")
+    cp = K.ks_split(W, (2, 2)).float().cpu().numpy()
+    Ck, CH, CW = O.ks_split_alg(a["W"], 2, 2)          # [y, x, oc, ch, cw, ic]
+    OCp = (lay.OC + 7) // 8 * 8
+    CHm, CWm = Ck.shape[3], Ck.shape[4]
+    cp = cp.reshape(2 * 2, lay.C, CHm * CWm, OCp)
+    for y in range(2):
+        for x in range(2):
+            for ch in range(CHm):
+                for cw in range(CWm):
+                    np.testing.assert_array_equal(cp[y * 2 + x, :, ch * CWm + cw, :lay.OC], Ck[y, x, :, ch, cw, :].T)
+    assert np.all(cp[..., lay.OC:] == 0)
+    g1 = run_all(torch, lay, config=7, ops=("deconv",))[1]["deconv"]
+    g2 = run_all(torch, lay, config=7, ops=("deconv",), via_split=True)[1]["deconv"]
+    np.testing.assert_array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("gz", [1, 2, 3, 7])
+def test_wgrad_gz_segments_deterministic(torch_cuda, gz):
+    lay = Layer("w", 130, 64, 9, 9, 128, 3, 3, 2, 2, 1, 1)
+    got = check_full(torch_cuda, lay, ops=("wgrad",), gz=gz)
+    again = run_all(torch_cuda, lay, ops=("wgrad",), gz=gz)[1]["wgrad"]
+    np.testing.assert_array_equal(got["wgrad"], again)
+
+
+# ------------------------------------------- config layers, reduced batch
+def _config_layers():
+    out = []
+    for cfg in (1, 2, 3):
+        for i, lay in enumerate(get_config(cfg)[1]):
+            if lay.name.startswith(("l1_", "l2_", "l3_", "l4_")) and not lay.name.endswith("_0"):
+                continue  # repeated shapes
+            out.append((cfg, i, lay))
+    return out
+
+
+@pytest.mark.parametrize("cfg,i,lay", _config_layers(), ids=lambda v: v.name if isinstance(v, Layer) else str(v))
+def test_config_layers_reduced_batch(torch_cuda, cfg, i, lay):
+    """Each config layer at N=130 when the full layer is small enough for the
+    oracle (spans 2 batch tiles + a ragged tail), else N=3."""
+    big = lay.H * lay.W * max(lay.C, lay.OC) * lay.FH * lay.FW * lay.OC * lay.C
+    n = 130 if big < 4e9 else 3
+    check_full(torch_cuda, lay.with_batch(n), "bf16", config=cfg, idx=i, ops=lay.ops)
+
+
+# ------------------------------------------ full size, sampled outputs
+@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3)][::3],
+                         ids=lambda v: v.name if isinstance(v, Layer) else str(v))
+def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
+    """Full BASELINE batch, the bench's launch configuration; the oracle
+    computes sampled outputs one by one (rows for fwd/deconv, taps for wgrad)."""
+    a, got = run_all(torch_cuda, lay, "bf16", config=cfg, idx=i, ops=lay.ops)
+    rng = np.random.default_rng(cfg * 100 + i)
+    s = (lay.sh, lay.sw, lay.ph, lay.pw)
+    OH, OW = lay.out_hw()
+    if "fwd" in got:
+        smp = [(int(rng.integers(lay.N)), int(rng.integers(OH)), int(rng.integers(OW))) for _ in range(24)]
+        smp += [(lay.N - 1, 0, 0), (0, OH - 1, OW - 1)]
+        ref = O.conv_ref_rows(a["X"], a["W"], *s, smp)
+        check(np.stack([got["fwd"][t] for t in smp]), ref, "bf16", f"{lay.name} fwd sampled", red_len(lay, "fwd"))
+    if "deconv" in got:
+        smp = [(int(rng.integers(lay.N)), int(rng.integers(lay.H)), int(rng.integers(lay.W))) for _ in range(24)]
+        smp += [(lay.N - 1, lay.H - 1, lay.W - 1), (0, 0, 0)]
+        ref = O.deconv_ref_rows(a["dY"], a["W"], lay.H, lay.W, *s, smp)
+        check(np.stack([got["deconv"][t] for t in smp]), ref, "bf16", f"{lay.name} deconv sampled",
+              red_len(lay, "deconv"))
+    if "wgrad" in got:
+        taps = [(0, 0), (lay.FH - 1, lay.FW - 1), (lay.FH // 2, lay.FW // 2)]
+        ref = O.wgrad_ref_taps(a["X"], a["dY"], lay.FH, lay.FW, *s, taps)
+        check(np.stack([got["wgrad"][:, fh, fw, :] for fh, fw in taps]), ref, "bf16", f"{lay.name} wgrad sampled",
+              red_len(lay, "wgrad"))

@@ -1,0 +1,122 @@
+"""CPU-side checks of the C ABI (libcks.so): the library loads and exports
+every symbol include/cks.h declares; the integer plan tables the kernels
+consume are bit-exact against the oracle's brute-force enumeration; op
+counts, validation and error codes.  No compute call is made (no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+from paper_2306_15951_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2306_15951_b200 import build
+    build.build()
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "cks.h")).read()
+    declared = set(re.findall(r"^\s*(?:cks_status|const char\*|int)\s+(cks_\w+)\s*\(", hdr, re.M))
+    assert declared == set(L.EXPORTS), declared ^ set(L.EXPORTS)
+    lib = ctypes.CDLL(L.LIB_PATH)
+    for name in declared:
+        assert getattr(lib, name) is not None
+    assert L.cks_version() >= 1
+
+
+def _grid():
+    for I in range(1, 14):
+        for F in range(1, 8):
+            for s in range(1, 5):
+                for p in range(0, F):
+                    if I + 2 * p - F >= 0:
+                        yield I, F, s, p
+
+
+def _flat_t2(phases):
+    out = []
+    for ph in phases:
+        out += [ph["y"], ph["CH"], ph["oph"], ph["ih_s"], ph["U"], ph["a"]]
+        for r in ph["rows"]:
+            out += list(r)
+    return out
+
+
+def test_axis_tables_bit_exact_vs_oracle_grid():
+    n = 0
+    for I, F, s, p in _grid():
+        assert L.cks_axis_table(I, F, s, p, 1) == [v for r in O.table_T1(I, F, s, p) for v in r], (I, F, s, p)
+        assert L.cks_axis_table(I, F, s, p, 2) == _flat_t2(O.table_T2(I, F, s, p)), (I, F, s, p)
+        assert L.cks_axis_table(I, F, s, p, 3) == [v for r in O.table_T3(I, F, s, p) for v in r], (I, F, s, p)
+        assert L.cks_axis_table(I, F, s, p, 4) == [v for r in O.table_T4(I, F, s, p) for v in r], (I, F, s, p)
+        n += 1
+    assert n >= 1320
+
+
+@pytest.mark.parametrize("I,F,s,p", [(224, 7, 2, 3), (56, 3, 2, 1), (56, 1, 2, 0), (64, 4, 2, 1), (7, 3, 1, 1),
+                                     (4, 3, 2, 1), (255, 5, 3, 2)])
+def test_axis_tables_config_sizes(I, F, s, p):
+    assert L.cks_axis_table(I, F, s, p, 1) == [v for r in O.table_T1(I, F, s, p) for v in r]
+    assert L.cks_axis_table(I, F, s, p, 2) == _flat_t2(O.table_T2(I, F, s, p))
+    assert L.cks_axis_table(I, F, s, p, 3) == [v for r in O.table_T3(I, F, s, p) for v in r]
+
+
+def test_op_counts_vs_oracle():
+    from cks_synth import get_config
+    for cfg in (0, 1, 2, 3):
+        for lay in get_config(cfg)[1]:
+            g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+            got = L.cks_op_counts(g)
+            ref = O.op_counts(O.geom(**lay.geom()))
+            for k in ("zero_free_macs", "VH", "VW"):
+                assert got[k] == ref[k], (lay.name, k)
+            assert got["T_conv"] == ref["T_conv"] and got["T_deconv"] == ref["T_deconv"]
+            assert got["T_dilated"] == ref["T_dilated"]
+            assert L.cks_output_shape(g) == lay.out_hw()
+
+
+def test_validation_errors():
+    bad = [L.make_geom(1, 4, 1, 8, 8, 3, 3, 1, 1, 0, 0),   # F > padded I
+           L.make_geom(1, 4, 8, 8, 8, 3, 3, 1, 1, 3, 1),   # p >= F
+           L.make_geom(1, 4, 8, 8, 8, 3, 3, 0, 1, 1, 1),   # stride 0
+           L.make_geom(0, 4, 8, 8, 8, 3, 3, 1, 1, 1, 1)]   # N = 0
+    for g in bad:
+        with pytest.raises(L.CksError) as e:
+            L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD)
+        assert e.value.status == 2
+    g = L.make_geom(1, 4, 8, 8, 8, 3, 3, 1, 1, 1, 1, dh=2, dw=1)
+    with pytest.raises(L.CksError) as e:
+        L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD)
+    assert e.value.status == 3
+    # NULL / misaligned pointers are rejected before any CUDA call
+    g = L.make_geom(2, 8, 8, 8, 8, 3, 3, 2, 2, 1, 1)
+    lib = L.lib()
+    assert lib.cks_conv2d_fwd(ctypes.byref(g), 1, None, None, None, None, 0, None) == 1
+    assert lib.cks_conv2d_fwd(ctypes.byref(g), 1, 16, 17, 32, None, 0, None) == 4
+    assert lib.cks_deconv2d(ctypes.byref(g), 1, 16, 16, 16, 16, None, 0, None) == 1   # both w and c_packed
+    assert lib.cks_dilated_wgrad(ctypes.byref(g), 1, 16, 16, 16, -1, None, 0, None) == 3
+    # capacity error for tables
+    n = ctypes.c_size_t()
+    buf = (ctypes.c_int64 * 2)()
+    assert lib.cks_axis_table(8, 3, 2, 1, 1, buf, 2, ctypes.byref(n)) == 7 and n.value == 16
+
+
+def test_workspace_and_launch_counts():
+    g = L.make_geom(128, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)   # I_C = 3 -> padded staging
+    assert L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) >= 128 * 32 * 32 * 8 * 2
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 3
+    g = L.make_geom(128, 64, 32, 32, 64, 3, 3, 2, 2, 1, 1)
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV) == 2
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True) == 1
+    gz = L.cks_choose_gz(g, L.CKS_BF16)
+    assert 1 <= gz <= 64
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + (gz > 1)
+    ws = L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=4)
+    assert ws >= 4 * 64 * 9 * 64 * 4
+    assert L.cks_ks_split_size(g, L.CKS_BF16) == 4 * 64 * 2 * 2 * 64 * 2
