@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""bench.py -- one JSON line: zero-free TFLOP/s and ms per op (fwd / deconv /
+wgrad) of the C-K-S hot path on B200 (BASELINE.json metric).
+
+A "step" is one pass of the whole hot path over one batch of the workload:
+for every layer of the workload, ConvV2 forward, KS-deconv-V2 (Stage1 split
++ fused Stage2&3) and Sk-dilated-V2 weight gradient (+ G_Z reduce), as in a
+conv-layer training step.  Default workload: configs[1], the
+Cifar10 VGG-16 layer sweep, N = 128 per GPU (weak scaling; the global batch
+is 128 x n_gpus).  Under torchrun (N > 1 GPUs) every rank runs its batch
+shard and the per-layer dW are summed with one NCCL all_reduce per step.
+
+Timing: inputs resident in HBM; the step is one CUDA graph (the C-ABI calls
+captured once) replayed K times after W warm-ups; L2 is flushed (256 MB
+write) before every timed step, outside the timed events; per-op durations
+come from event nodes inside the graph (device clock); the step time is the
+max over ranks.  ``e2e`` repeats the step through the public Python API
+without graphs, with the step's inputs copied host->device from pinned
+memory and the results copied back inside the timed region.
+``--impl reference`` times the fp64 CPU oracle (oracle/) on a bounded
+sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "zero-free TFLOP/s and ms per op (fwd/deconv/wgrad) at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("cks", "reference"), default="cks")
+    ap.add_argument("--config", type=int, default=1, help="BASELINE configs index (default 1: C2 VGG sweep)")
+    ap.add_argument("--batch", type=int, default=None, help="override per-GPU batch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--layers", action="store_true", help="per-layer breakdown on stderr")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------------------- oracle
+def oracle_sample(layers, config, n_sub, budget_s=None):
+    """Run the fp64 oracle (as it stands) over every layer of the workload with
+    n_sub images; returns (seconds, zero-free flops, passes)."""
+    import oracle as O
+    from cks_synth import make_layer_inputs
+    samples = []
+    for i, lay in enumerate(layers):
+        l1 = lay.with_batch(n_sub)
+        samples.append((l1, make_layer_inputs(l1, config, i, "bf16")))
+    flops_pass = 0
+    for l1, _ in samples:
+        f = O.op_counts(O.geom(**l1.geom()))["zero_free_flops"]
+        flops_pass += f * len(l1.ops)
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        for l1, a in samples:
+            s = (l1.sh, l1.sw, l1.ph, l1.pw)
+            if "fwd" in l1.ops:
+                O.conv_ref(a["X"], a["W"], *s)
+            if "deconv" in l1.ops:
+                O.deconv_ref(a["dY"], a["W"], l1.H, l1.W, *s)
+            if "wgrad" in l1.ops:
+                O.wgrad_ref(a["X"], a["dY"], l1.FH, l1.FW, *s)
+        passes += 1
+        el = time.perf_counter() - t0
+        if budget_s is None or el >= budget_s:
+            return el, flops_pass * passes, passes
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((d.get("num_threads", 1) for d in threadpool_info()), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from cks_synth import get_config
+    desc, layers = get_config(args.config, args.batch)
+    n_sub = 1
+    for _ in range(args.warmup):
+        oracle_sample(layers, args.config, n_sub)
+    times, flops = [], 0
+    for _ in range(args.steps):
+        el, f, _ = oracle_sample(layers, args.config, n_sub)
+        times.append(el)
+        flops = f
+    ms = 1e3 * statistics.mean(times)
+    value = flops / (ms / 1e3) / 1e12
+    cores = blas_threads()
+    sample = f"all {len(layers)} layers x ops of '{desc}' at N={n_sub} image per step (oracle cost is linear in N)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "per_gpu_batch": layers[0].N, "sample_batch": n_sub,
+                   "parallelism": "host cores (oracle)"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- GPU arm
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm": float(d["hbm_gbs"]), "bf16": float(d["bf16_tflops"]),
+                "bf16_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "src": "measured"}
+    except Exception:
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
+
+
+def load_traffic(kernel):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class LayerBufs:
+    """Device buffers + the C-ABI calls of one layer (argument marshalling only)."""
+
+    def __init__(self, torch, lay, config, idx, rank, device):
+        import numpy as np
+        from cks_synth import bf16_bits, make_layer_inputs
+        from paper_2306_15951_b200 import _lib as L
+        self.lay, self.L = lay, L
+        a = make_layer_inputs(lay, config + 100 * rank, idx, "bf16")
+
+        def dev(x):
+            return torch.from_numpy(bf16_bits(x).view(np.int16)).view(torch.bfloat16).to(device)
+        self.host = {k: v for k, v in a.items()}
+        self.X, self.W, self.G = dev(a["X"]), dev(a["W"]), dev(a["dY"])
+        OH, OW = lay.out_hw()
+        f32 = dict(dtype=torch.float32, device=device)
+        self.Y = torch.empty((lay.N, OH, OW, lay.OC), **f32)
+        self.dX = torch.empty((lay.N, lay.H, lay.W, lay.C), **f32)
+        self.dW = None  # view into the flat allreduce buffer, set by the caller
+        g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+        self.g = g
+        cnt = L.cks_op_counts(g)
+        self.flops = 2 * cnt["zero_free_macs"]
+        self.cp = torch.empty(L.cks_ks_split_size(g, L.CKS_BF16) // 2, dtype=torch.bfloat16, device=device)
+        self.ws = {}
+        for op, code in (("fwd", L.CKS_OP_FWD), ("deconv", L.CKS_OP_DECONV), ("wgrad", L.CKS_OP_WGRAD)):
+            n = L.cks_workspace_size(g, L.CKS_BF16, code)
+            self.ws[op] = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+        self.launches = {
+            "fwd": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD),
+            "deconv": 1 + L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True),
+            "wgrad": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD),
+        }
+
+    def run(self, op, stream_ptr):
+        L, g = self.L, self.g
+        ws = self.ws[op]
+        if op == "fwd":
+            L.cks_conv2d_fwd(g, L.CKS_BF16, self.X.data_ptr(), self.W.data_ptr(), self.Y.data_ptr(), ws.data_ptr(),
+                             ws.numel(), stream_ptr)
+        elif op == "deconv":  # Stage1 (W changes every training step) + fused Stage2&3
+            L.cks_ks_split(g, L.CKS_BF16, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+            L.cks_deconv2d(g, L.CKS_BF16, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),
+                           ws.data_ptr(), ws.numel(), stream_ptr)
+        else:
+            L.cks_dilated_wgrad(g, L.CKS_BF16, self.X.data_ptr(), self.G.data_ptr(), self.dW.data_ptr(), 0,
+                                ws.data_ptr(), ws.numel(), stream_ptr)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    from cks_synth import get_config
+    from paper_2306_15951_b200 import build
+
+    ws_, rank, local = dist_env()
+    if args.gpus != ws_ and ws_ > 1:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE {ws_}", file=sys.stderr)
+    n_gpus = ws_
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if n_gpus > 1:
+        dist.init_process_group("nccl", device_id=device)
+    build.build()
+    desc, layers = get_config(args.config, args.batch)
+    bufs = [LayerBufs(torch, lay, args.config, i, rank, device) for i, lay in enumerate(layers)]
+    # flat dW buffer: one NCCL all_reduce per step for all layers
+    sizes = [b.lay.OC * b.lay.FH * b.lay.FW * b.lay.C for b in bufs]
+    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
+    off = 0
+    for b, s in zip(bufs, sizes):
+        b.dW = flat[off:off + s].view(b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C)
+        off += s
+    ops_seq = [(i, op) for i, b in enumerate(bufs) for op in ("fwd", "deconv", "wgrad") if op in b.lay.ops]
+    flops_step = sum(bufs[i].flops for i, _ in ops_seq)
+    launches_step = sum(bufs[i].launches[op] for i, op in ops_seq)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MB > 126 MB L2
+
+    # ---- capture the step as one CUDA graph with event nodes between ops
+    stream = torch.cuda.Stream(device)
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(ops_seq) + 1)]
+    with torch.cuda.stream(stream):
+        for i, op in ops_seq:  # eager warm-up (sets smem attributes, checks errors)
+            bufs[i].run(op, stream.cuda_stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        sp = torch.cuda.current_stream().cuda_stream
+        for k, (i, op) in enumerate(ops_seq):
+            evs[k].record()
+            bufs[i].run(op, sp)
+        evs[-1].record()
+
+    def step(sync_read=True):
+        graph.replay()
+        if n_gpus > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(flat)
+        if sync_read:
+            stream.synchronize()
+            return [evs[k].elapsed_time(evs[k + 1]) for k in range(len(ops_seq))]
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            flush.fill_(1.0)
+            step()
+    # ---- timed region
+    if n_gpus > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per_op_ms = [0.0] * len(ops_seq)
+    step_ms = []
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.fill_(float(_))
+            t_start.record(stream)
+            ms = step()
+            if n_gpus > 1:
+                t_end.record(stream)
+                stream.synchronize()
+                step_ms.append(t_start.elapsed_time(t_end))
+            else:
+                step_ms.append(sum(ms))
+            for k, v in enumerate(ms):
+                per_op_ms[k] += v
+    torch.cuda.synchronize()
+    # same step without the per-op event nodes (overhead check of the breakdown)
+    graph2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph2, stream=stream):
+        sp = torch.cuda.current_stream().cuda_stream
+        for i, op in ops_seq:
+            bufs[i].run(op, sp)
+    noev = []
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.steps // 2)):
+            flush.fill_(2.0)
+            t_start.record(stream)
+            graph2.replay()
+            t_end.record(stream)
+            stream.synchronize()
+            noev.append(t_start.elapsed_time(t_end))
+    if n_gpus > 1:
+        dist.barrier()
+    total_ms = sum(step_ms)
+    if n_gpus > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = flops_step * n_gpus / (ms_per_step / 1e3) / 1e12
+
+    # ---- per-op breakdown and roofline of the dominant kernel
+    fam = {"fwd": [0.0, 0], "deconv": [0.0, 0], "wgrad": [0.0, 0]}
+    for k, (i, op) in enumerate(ops_seq):
+        fam[op][0] += per_op_ms[k] / args.steps
+        fam[op][1] += bufs[i].flops
+    per_op = {op: {"ms": round(v[0], 5), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 2) if v[0] else None}
+              for op, v in fam.items() if v[1]}
+    igemm_ms, igemm_fl = fam["fwd"][0] + fam["deconv"][0], fam["fwd"][1] + fam["deconv"][1]
+    if igemm_ms >= fam["wgrad"][0]:
+        kname, kms, kfl, nl = "igemm_kernel", igemm_ms, igemm_fl, sum(1 for _, op in ops_seq if op != "wgrad")
+    else:
+        kname, kms, kfl, nl = "wgrad_kernel", fam["wgrad"][0], fam["wgrad"][1], sum(1 for _, op in ops_seq if op == "wgrad")
+    peaks = load_peaks()
+    achieved = kfl / (kms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 2), "peak": peaks["bf16"],
+                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4), "traffic": load_traffic(kname),
+                "launches_per_step": nl, "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)",
+                "timing": "op-level CUDA event nodes inside the step graph (kernel + its staging kernels)"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[-1,1) X/dY, kaiming-uniform W)",
+        "config": {"workload": desc, "layers": len(layers), "per_gpu_batch": layers[0].N,
+                   "global_batch": layers[0].N * n_gpus, "ops_per_step": len(ops_seq),
+                   "zero_free_gflop_per_gpu_step": round(flops_step / 1e9, 3),
+                   "l2": "flushed (256 MB write) before every timed step, outside the timed events",
+                   "parallelism": f"dp{n_gpus}",
+                   "step_ms_graph_without_event_nodes": round(statistics.mean(noev[1:] or noev), 5)},
+        "per_op": per_op, "roofline": roofline, "gpu_launches": launches_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    # ---- e2e through the public API with host buffers
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, max(2, min(args.steps, 10)), device)
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
+        el, f, passes = oracle_sample(layers, args.config, 1, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": f / el / 1e12, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "oracle",
+                                "sample": f"{passes} passes over all {len(layers)} layers x ops at N=1 image "
+                                          f"({el:.1f} s; oracle cost is linear in N)"}
+    if args.layers and rank == 0:
+        for k, (i, op) in enumerate(ops_seq):
+            ms = per_op_ms[k] / args.steps
+            print(f"  {bufs[i].lay.name:22s} {op:6s} {ms * 1e3:9.2f} us  {bufs[i].flops / ms / 1e9:9.1f} TFLOP/s",
+                  file=sys.stderr)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if n_gpus > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, steps, device):
+    """The same step through the public torch API (paper_2306_15951_b200.ops):
+    pinned host inputs -> device, the three operators, results -> host."""
+    from paper_2306_15951_b200 import ops as K
+    host_in, host_out = [], []
+    for b in bufs:
+        host_in.append({k: getattr(b, k).cpu().pin_memory() for k in ("X", "W", "G")})
+        host_out.append({k: torch.empty(getattr(b, k).shape, dtype=torch.float32).pin_memory()
+                         for k in ("Y", "dX", "dW")})
+    h2d = sum(t.numel() * t.element_size() for d in host_in for t in d.values())
+    d2h = 0
+    for b, d in zip(bufs, host_out):
+        for k in ("Y", "dX", "dW"):
+            opname = {"Y": "fwd", "dX": "deconv", "dW": "wgrad"}[k]
+            if opname in b.lay.ops:
+                d2h += d[k].numel() * 4
+    s = torch.cuda.Stream(device)
+
+    def one():
+        outs = []
+        for b, hi, ho in zip(bufs, host_in, host_out):
+            lay = b.lay
+            X = hi["X"].to(device, non_blocking=True)
+            W = hi["W"].to(device, non_blocking=True)
+            G = hi["G"].to(device, non_blocking=True)
+            st, pd = (lay.sh, lay.sw), (lay.ph, lay.pw)
+            if "fwd" in lay.ops:
+                ho["Y"].copy_(K.conv2d_fwd(X, W, st, pd), non_blocking=True)
+            if "deconv" in lay.ops:
+                ho["dX"].copy_(K.deconv2d(G, W, (lay.H, lay.W), st, pd), non_blocking=True)
+            if "wgrad" in lay.ops:
+                dW = K.dilated_wgrad(X, G, (lay.FH, lay.FW), st, pd)
+                if n_gpus > 1:
+                    dist.all_reduce(dW)
+                ho["dW"].copy_(dW, non_blocking=True)
+        return outs
+
+    with torch.cuda.stream(s):
+        one()
+        torch.cuda.synchronize()
+        if n_gpus > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(steps):
+            one()
+        e1.record(s)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if n_gpus > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(flops_step * n_gpus / (ms / 1e3) / 1e12, 3), "unit": "TFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 4), "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -5,8 +5,10 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 
 #include "../../include/cks.h"
 #include "cks_plan.h"
@@ -60,12 +62,42 @@ bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t d
     return r == CUDA_SUCCESS;
 }
 
+int debug_flags() {
+    static int f = [] {
+        const char* e = getenv("CKS_DEBUG_FLAGS");  // experiments only; unset in production
+        return e ? atoi(e) : 0;
+    }();
+    return f;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 cks_status last_cuda() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "[cks] CUDA error: %s\n", cudaGetErrorString(e));
+        return CKS_ERR_CUDA;
+    }
+    return CKS_OK;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; every kernel calls griddepcontrol.wait before
+// touching global memory, so stream order semantics are preserved.
+template <typename... KArgs, typename... Args>
+cks_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) != cudaSuccess) {
+        last_cuda();
         return CKS_ERR_CUDA;
     }
     return CKS_OK;
@@ -101,34 +133,92 @@ bool rows_ok(const std::vector<KRow>& rows) {
 
 // ------------------------------------------------------------------ launchers
 template <int BN, bool TF>
-cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, cudaStream_t st) {
-    using S = IgemmShape<BN, TF>;
+cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
+                          cudaStream_t st) {
     auto kern = igemm_kernel<BN, TF>;
-    if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
+    if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
-    kern<<<unsigned(grid), 256, S::SMEM_BYTES, st>>>(a, b, p);
-    return last_cuda();
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, a, b, p);
 }
 
-cks_status launch_igemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p,
+cks_status launch_igemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
                         cudaStream_t st) {
     if (tf32) {
         switch (BN) {
-            case 32: return launch_igemm_t<32, true>(a, b, p, st);
-            case 64: return launch_igemm_t<64, true>(a, b, p, st);
-            case 128: return launch_igemm_t<128, true>(a, b, p, st);
-            case 256: return launch_igemm_t<256, true>(a, b, p, st);
+            case 32: return launch_igemm_t<32, true>(a, b, p, smem, st);
+            case 64: return launch_igemm_t<64, true>(a, b, p, smem, st);
+            case 128: return launch_igemm_t<128, true>(a, b, p, smem, st);
         }
     } else {
         switch (BN) {
-            case 32: return launch_igemm_t<32, false>(a, b, p, st);
-            case 64: return launch_igemm_t<64, false>(a, b, p, st);
-            case 128: return launch_igemm_t<128, false>(a, b, p, st);
-            case 256: return launch_igemm_t<256, false>(a, b, p, st);
+            case 32: return launch_igemm_t<32, false>(a, b, p, smem, st);
+            case 64: return launch_igemm_t<64, false>(a, b, p, smem, st);
+            case 128: return launch_igemm_t<128, false>(a, b, p, smem, st);
         }
     }
     return CKS_ERR_UNSUPPORTED;
+}
+
+// Fill IgemmParams from the plan and launch (fwd and deconv share this).
+cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRow>& rh, const std::vector<KRow>& rw,
+                     const CUtensorMap& ta, const CUtensorMap& tb, float* out, int out_H, int out_W, int out_C,
+                     int N, int slot_stride, int phases_w, const WsLayout& L, void* ws, cudaStream_t st) {
+    IgemmCfg cfg = cfg_in;
+    if (debug_flags() & 16) {  // experiment: no split-K
+        cfg.Z = 1;
+        cfg.tiles = cfg.out_tiles;
+    }
+    IgemmParams p;
+    memset(&p, 0, sizeof(p));
+    fill_axis(p.ah, rh);
+    fill_axis(p.aw, rw);
+    p.out = out;
+    p.rows_h = int(rh.size());
+    p.nph_w = int(cfg.wph_cnt.size());
+    if (p.nph_w > 8) return CKS_ERR_UNSUPPORTED;
+    int off = 0, cum = 0;
+    for (int x = 0; x < p.nph_w; ++x) {
+        p.wph_off[x] = int16_t(off);
+        p.wph_cnt[x] = int16_t(cfg.wph_cnt[x]);
+        p.wb_cum[x] = int16_t(cum);
+        off += int(cfg.wph_cnt[x]);
+        cum += int((cfg.wph_cnt[x] + cfg.pbw - 1) / cfg.pbw);
+    }
+    p.wb_cum[p.nph_w] = int16_t(cum);
+    p.wblocks = cfg.wblocks;
+    p.pbw = cfg.pbw;
+    p.acc_stages = cfg.acc_stages;
+    p.nblk = cfg.nblk;
+    p.nbs = cfg.nbs;
+    p.kc_blocks = cfg.kc_blocks;
+    p.slot_stride = slot_stride;
+    p.phases_w = phases_w;
+    p.N = N;
+    p.out_H = out_H;
+    p.out_W = out_W;
+    p.out_C = out_C;
+    p.zsplit = cfg.Z;
+    p.num_tiles = cfg.tiles;
+    p.dbg = debug_flags();
+    if (const char* tp = getenv("CKS_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(strtoull(tp, nullptr, 0));
+    // shared memory: A-position ring (16 KB slots) + B-row ring (all taps of a filter row)
+    p.a_stages = cfg.a_stages;
+    p.b_stages = cfg.stages;
+    p.b_stage_bytes = cfg.stage_bytes;
+    p.ntap = cfg.ntap;
+    p.apos = cfg.apos;
+    p.unit_step = cfg.unit_step;
+    p.a0_step = cfg.a0_step;
+    if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
+    const int smem = 1024 + p.a_stages * p.apos * 16384 + p.b_stages * p.b_stage_bytes + 512;
+    if (cfg.Z > 1) {
+        if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
+        p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
+        p.sem = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + L.sem);
+        if (cudaMemsetAsync(p.sem, 0, L.sem_bytes, st) != cudaSuccess) return last_cuda();
+    }
+    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, smem, st);
 }
 
 template <int BN>
@@ -138,20 +228,17 @@ cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const Wgra
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
-    kern<<<unsigned(grid), 256, S::SMEM_BYTES, st>>>(a, b, p);
-    return last_cuda();
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), S::SMEM_BYTES, st, a, b, p);
 }
 
 cks_status launch_pad(cks_dtype dt, const void* src, void* dst, long long rows, int C, int Cp, cudaStream_t st) {
     long long total = rows * Cp;
     unsigned blocks = unsigned(std::min<long long>((total + 255) / 256, 148LL * 16));
     if (dt == CKS_BF16)
-        pad_channels_kernel<uint16_t><<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(src),
-                                                              static_cast<uint16_t*>(dst), rows, C, Cp);
-    else
-        pad_channels_kernel<uint32_t><<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(src),
-                                                              static_cast<uint32_t*>(dst), rows, C, Cp);
-    return last_cuda();
+        return launch_pdl(pad_channels_kernel<uint16_t>, dim3(blocks), dim3(256), 0, st,
+                          static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), rows, C, Cp);
+    return launch_pdl(pad_channels_kernel<uint32_t>, dim3(blocks), dim3(256), 0, st, static_cast<const uint32_t*>(src),
+                      static_cast<uint32_t*>(dst), rows, C, Cp);
 }
 
 cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* out, cudaStream_t st) {
@@ -160,14 +247,12 @@ cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* ou
     dim3 grid(unsigned((OCp + 31) / 32), unsigned((g.C + 31) / 32), unsigned(g.sh * g.sw * CHm * CWm));
     dim3 block(32, 8);
     if (dt == CKS_BF16)
-        ks_split_kernel<uint16_t><<<grid, block, 0, st>>>(static_cast<const uint16_t*>(w), static_cast<uint16_t*>(out),
-                                                          int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm,
-                                                          CWm, OCp);
-    else
-        ks_split_kernel<uint32_t><<<grid, block, 0, st>>>(static_cast<const uint32_t*>(w), static_cast<uint32_t*>(out),
-                                                          int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm,
-                                                          CWm, OCp);
-    return last_cuda();
+        return launch_pdl(ks_split_kernel<uint16_t>, grid, block, 0, st, static_cast<const uint16_t*>(w),
+                          static_cast<uint16_t*>(out), int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm, CWm,
+                          OCp);
+    return launch_pdl(ks_split_kernel<uint32_t>, grid, block, 0, st, static_cast<const uint32_t*>(w),
+                      static_cast<uint32_t*>(out), int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm, CWm,
+                      OCp);
 }
 
 cks_status check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
@@ -256,39 +341,23 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
         xs = xp;
         wsrc = wp;
     }
-    IgemmCfg cfg = igemm_cfg(ah.O, aw.O, g->N, g->OC, kPlanSMs);
+    IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
     const uint32_t BK = uint32_t(128 / eb);
     CUtensorMap ta, tb;
-    {
-        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
-        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
-        uint32_t box[4] = {BK, 1, 1, 128};
+    {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->H)};
+        uint64_t sb[3] = {uint64_t(g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
+        uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
         if (!make_tmap4(&ta, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
     }
-    {
-        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->FH * g->FW), uint64_t(g->OC), 1};
-        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->FH * g->FW * Cp * eb),
-                          uint64_t(g->OC * g->FH * g->FW * Cp * eb)};
-        uint32_t box[4] = {BK, 1, uint32_t(cfg.BN), 1};
+    {   // W viewed as (C, OC, FH*FW, 1): one box = the FW taps of a filter row x BN filters
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->OC), uint64_t(g->FH * g->FW), 1};
+        uint64_t sb[3] = {uint64_t(g->FH * g->FW * Cp * eb), uint64_t(Cp * eb), uint64_t(g->OC * g->FH * g->FW * Cp * eb)};
+        uint32_t box[4] = {BK, uint32_t(cfg.BN), uint32_t(g->FW), 1};
         if (!make_tmap4(&tb, dt, wsrc, d, sb, box)) return CKS_ERR_CUDA;
     }
-    IgemmParams p;
-    fill_axis(p.ah, rh);
-    fill_axis(p.aw, rw);
-    p.out = y;
-    p.rows_h = int(rh.size());
-    p.rows_w = int(rw.size());
-    p.nblk = cfg.nblk;
-    p.nbs = cfg.nbs;
-    p.kc_blocks = int((Cp + BK - 1) / BK);
-    p.slot_stride = int(g->FW);
-    p.phases_w = 1;
-    p.N = int(g->N);
-    p.out_H = int(ah.O);
-    p.out_W = int(aw.O);
-    p.out_C = int(g->OC);
-    p.num_tiles = cfg.tiles;
-    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, st);
+    return run_igemm(cfg, dt, rh, rw, ta, tb, y, int(ah.O), int(aw.O), int(g->OC), int(g->N), int(g->FW), 1, L, ws,
+                     st);
 }
 
 cks_status cks_ks_split(const cks_geom* g, cks_dtype dt, const void* w, void* c_packed, void* stream) {
@@ -328,38 +397,23 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
         cp = p;
     }
     const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
-    IgemmCfg cfg = igemm_cfg(ah.I, aw.I, g->N, g->C, kPlanSMs);
+    IgemmCfg cfg = igemm_cfg_deconv(*g, dt, kPlanSMs);
     const uint32_t BK = uint32_t(128 / eb);
     CUtensorMap ta, tb;
-    {
-        uint64_t d[4] = {uint64_t(OCp), uint64_t(OW), uint64_t(OH), uint64_t(g->N)};
-        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(OW * OCp * eb), uint64_t(OH * OW * OCp * eb)};
-        uint32_t box[4] = {BK, 1, 1, 128};
+    {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
+        uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
+        uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
         if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
     }
-    {
-        uint64_t d[4] = {uint64_t(OCp), uint64_t(CHm * CWm), uint64_t(g->C), uint64_t(P)};
-        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(CHm * CWm * OCp * eb), uint64_t(g->C * CHm * CWm * OCp * eb)};
-        uint32_t box[4] = {BK, 1, uint32_t(cfg.BN), 1};
+    {   // packed C_{y,x} viewed as (OCp, C, CHm*CWm, P): one box = the CWm taps of sub-filter row ch
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(g->C), uint64_t(CHm * CWm), uint64_t(P)};
+        uint64_t sb[3] = {uint64_t(CHm * CWm * OCp * eb), uint64_t(OCp * eb), uint64_t(g->C * CHm * CWm * OCp * eb)};
+        uint32_t box[4] = {BK, uint32_t(cfg.BN), uint32_t(CWm), 1};
         if (!make_tmap4(&tb, dt, cp, d, sb, box)) return CKS_ERR_CUDA;
     }
-    IgemmParams p;
-    fill_axis(p.ah, rh);
-    fill_axis(p.aw, rw);
-    p.out = dx;
-    p.rows_h = int(rh.size());
-    p.rows_w = int(rw.size());
-    p.nblk = cfg.nblk;
-    p.nbs = cfg.nbs;
-    p.kc_blocks = int((OCp + BK - 1) / BK);
-    p.slot_stride = int(CWm);
-    p.phases_w = g->sw;
-    p.N = int(g->N);
-    p.out_H = int(g->H);
-    p.out_W = int(g->W);
-    p.out_C = int(g->C);
-    p.num_tiles = cfg.tiles;
-    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, st);
+    return run_igemm(cfg, dt, rh, rw, ta, tb, dx, int(g->H), int(g->W), int(g->C), int(g->N), int(CWm), g->sw, L, ws,
+                     st);
 }
 
 cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
@@ -440,10 +494,10 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         const long long n = p.part_stride;
         unsigned blocks = unsigned(std::min<long long>((n / 4 + 255) / 256 + 1, 148LL * 8));
         if (n % 4 == 0)
-            reduce_partials_kernel<<<blocks, 256, 0, st>>>(p.out, dw, n, cfg.gz);
-        else
-            reduce_partials_scalar_kernel<<<blocks, 256, 0, st>>>(p.out, dw, n, cfg.gz);
-        return last_cuda();
+            return launch_pdl(reduce_partials_kernel, dim3(blocks), dim3(256), 0, st, (const float*)p.out, dw, n,
+                              cfg.gz);
+        return launch_pdl(reduce_partials_scalar_kernel, dim3(blocks), dim3(256), 0, st, (const float*)p.out, dw, n,
+                          cfg.gz);
     }
     return CKS_OK;
 }
@@ -494,7 +548,7 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]) {
     out[3] = 2 * (g->OC * g->N * ah.O * aw.O * g->FH * g->FW * g->C);
     out[4] = 2 * (g->C * g->N * g->H * g->W * g->FH * g->FW * g->OC);
     out[5] = 2 * (g->OC * g->FH * g->FW * g->C * OHp * OWp) * g->N;
-    IgemmCfg cfg = igemm_cfg(ah.O, aw.O, g->N, g->OC, kPlanSMs);
+    IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
     const int64_t Cp = pad_ch(g->C, dt), BK = 128 / elem_bytes(dt);
     out[6] = int64_t(cfg.nblk) * 128 * int64_t(cfg.nbs) * cfg.BN * VH * VW * ((Cp + BK - 1) / BK * BK);
     out[7] = cfg.tiles;

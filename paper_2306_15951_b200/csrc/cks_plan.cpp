@@ -4,6 +4,8 @@
 #include "cks_plan.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace cks {
@@ -114,19 +116,97 @@ std::vector<KRow> krows_deconv(const Axis& a) {
     return r;
 }
 
-IgemmCfg igemm_cfg(int64_t rows_h, int64_t rows_w, int64_t N, int64_t nout, int num_sms) {
+// experiments only: CKS_IGEMM_CFG="BN,PBW,Z" overrides the heuristic
+static bool cfg_override(int& bn, int& pbw, int& z) {
+    const char* e = getenv("CKS_IGEMM_CFG");
+    if (!e) return false;
+    return sscanf(e, "%d,%d,%d", &bn, &pbw, &z) == 3;
+}
+
+IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
+                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
     IgemmCfg c;
+    c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
-    int64_t pix = rows_h * rows_w * c.nblk;
-    if (nout <= 32) c.BN = 32;
-    else if (nout <= 64) c.BN = 64;
-    else if (nout <= 128) c.BN = 128;
-    else c.BN = 256;
-    // more, narrower tiles when the grid would not fill the SMs
-    if (c.BN == 256 && pix * ((nout + 255) / 256) < num_sms) c.BN = 128;
+    c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);
+    int ov_bn = 0, ov_pbw = 0, ov_z = 0;
+    const bool ov = cfg_override(ov_bn, ov_pbw, ov_z);
+    if (ov && ov_bn > 0) c.BN = ov_bn;
+    if (ov && ov_pbw > 0) force_pbw = ov_pbw;
     c.nbs = int((nout + c.BN - 1) / c.BN);
-    c.tiles = pix * c.nbs;
+    c.kc_blocks = int((kchan + (128 / eb) - 1) / (128 / eb));
+    c.ntap = int(ntap);
+    int64_t maxrow = 1;
+    for (auto v : wph_cnt) maxrow = std::max(maxrow, v);
+    auto tiles_for = [&](int bn, int pb) {
+        int64_t wb = 0;
+        for (auto v : wph_cnt) wb += (v + pb - 1) / pb;
+        return rows_h * wb * c.nblk * ((nout + bn - 1) / bn);
+    };
+    // Heuristic (tools/sweep_cfg.sh on B200): the largest pixel block (reuse of
+    // B rows and activation columns) that still gives >= 120 tiles; if even one
+    // pixel per tile leaves < 64 tiles, narrower BN; split-K (Z = 2) only for
+    // long K loops (>= 16 row steps) on grids of < 100 tiles.
+    int pbw = int(std::min<int64_t>({256 / c.BN, 8, maxrow}));
+    while (pbw > 1 && tiles_for(c.BN, pbw) < 120) --pbw;
+    if (tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0)) {
+        c.BN = 64;
+        pbw = 1;
+    }
+    c.nbs = int((nout + c.BN - 1) / c.BN);
+    if (force_pbw > 0) pbw = std::min<int>(force_pbw, int(std::min<int64_t>(256 / c.BN, 8)));
+    // smem: ring of B rows (ntap x BN x 128 B) and ring of A slots holding all
+    // pa activation columns of a row step (one TMA box, one barrier)
+    for (; pbw >= 1; --pbw) {
+        c.pa = int((pbw - 1) * a0_step + ntap);
+        c.stage_bytes = int(ntap * c.BN * 128);
+        if (2 * (int64_t(c.pa) * 16384 + c.stage_bytes) <= kSmemBudget && c.pa <= 256) break;
+    }
+    if (pbw < 1) pbw = 1;
+    c.pbw = pbw;
+    c.pa = int((pbw - 1) * a0_step + ntap);
+    c.stage_bytes = int(ntap * c.BN * 128);
+    c.unit_step = a0_step == 1;
+    c.a0_step = int(a0_step);
+    // A slot: as many of the pa columns as fit with >= 2 A slots and 2 B rows
+    c.stages = 2;
+    c.apos = c.pa;
+    while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * 16384 > kSmemBudget) --c.apos;
+    if (2 * c.stage_bytes + 2 * int64_t(c.apos) * 16384 > kSmemBudget) c.stages = 1;
+    c.a_stages = int(std::min<int64_t>(8, (kSmemBudget - c.stages * c.stage_bytes) / (int64_t(c.apos) * 16384)));
+    c.acc_stages = 2;
+    c.wblocks = 0;
+    for (auto v : wph_cnt) c.wblocks += int((v + c.pbw - 1) / c.pbw);
+    c.out_tiles = rows_h * c.wblocks * c.nblk * c.nbs;
+    // split-K to fill the SMs (one wave); at least 2 row steps per segment
+    const int64_t rs_full = std::max<int64_t>(max_taps_h * c.kc_blocks, 1);
+    c.Z = 1;
+    if (c.out_tiles < 100 && rs_full >= 16) c.Z = 2;
+    (void)num_sms;
+    if (ov && ov_z > 0) c.Z = ov_z;
+    c.tiles = c.out_tiles * c.Z;
     return c;
+}
+
+static int64_t max_window(const std::vector<KRow>& rows) {
+    int64_t m = 0;
+    for (auto& r : rows) m = std::max(m, r.te - r.ts);
+    return m;
+}
+
+IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms) {
+    Axis ah = axis_h(g), aw = axis_w(g);
+    auto rh = krows_fwd(ah);
+    return igemm_cfg(ah.O, {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt), max_window(rh), g.FW, g.sw, num_sms);
+}
+
+IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
+    Axis ah = axis_h(g), aw = axis_w(g);
+    auto rh = krows_deconv(ah);
+    std::vector<int64_t> cnt;
+    for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
+    return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
+                     num_sms);
 }
 
 // G_Z choice: the paper makes G_Z grow with (N_a + N_b)/N_g and
@@ -188,6 +268,13 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
         if (OCp != g.OC) take(size_t(g.N) * OH * OW * OCp * eb, L.dy_pad, L.dy_pad_bytes);
     }
     if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
+    if (op == CKS_OP_FWD || op == CKS_OP_DECONV) {
+        IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
+        if (c.Z > 1) {
+            take(size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4, L.partial, L.partial_bytes);
+            take(size_t(c.out_tiles) * 4, L.sem, L.sem_bytes);
+        }
+    }
     if (op == CKS_OP_WGRAD) {
         WgradCfg c = wgrad_cfg(g, gz, num_sms);
         if (c.gz > 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);

@@ -62,13 +62,33 @@ inline int64_t pad_ch(int64_t c, cks_dtype dt) {
 inline int64_t elem_bytes(cks_dtype dt) { return dt == CKS_BF16 ? 2 : 4; }
 
 // Kernel configuration decisions (shared by workspace query and launch).
+// The implicit GEMM tiles PBW consecutive pixels of one output row x 128
+// images x BN channels; under-filled grids split the row steps into Z
+// segments (deterministic in-kernel split-K).
 struct IgemmCfg {
-    int BN;        // output-channel tile
-    int nbs;       // number of BN tiles
-    int nblk;      // ceil(N / 128)
-    int64_t tiles;
+    int BN = 128;       // output-channel tile (32, 64, 128)
+    int pbw = 1;        // pixels per tile along w
+    int acc_stages = 2; // TMEM accumulator buffers
+    int nbs = 1;        // number of BN tiles
+    int nblk = 1;       // ceil(N / 128)
+    int wblocks = 1;
+    int Z = 1;          // split-K segments
+    int kc_blocks = 1;
+    int ntap = 1;       // taps per filter row (B box)
+    int pa = 1;         // activation positions per row step (A box)
+    int stage_bytes = 0, stages = 2;  // B-row ring: bytes per row, rows in flight
+    int a_stages = 8;                 // A ring (slots of apos x 16 KB)
+    int apos = 2;                     // activation columns per A slot
+    int unit_step = 1;                // consecutive pixels' tap-0 columns differ by 1
+    int a0_step = 1;                  // tap-0 column step between consecutive pixels
+    int64_t out_tiles = 0, tiles = 0;
+    std::vector<int64_t> wph_cnt;  // rows per w phase
 };
-IgemmCfg igemm_cfg(int64_t rows_h, int64_t rows_w, int64_t N, int64_t nout, int num_sms);
+IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
+                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512;  // minus alignment and barriers
+IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
+IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
 
 struct WgradCfg {
     int BN, nbs, mblocks, nblk64, gz;
@@ -78,8 +98,8 @@ WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms);
 
 // Workspace layout (byte offsets, 256-aligned) for one op.
 struct WsLayout {
-    size_t x_pad = 0, w_pad = 0, dy_pad = 0, c_packed = 0, partial = 0, total = 0;
-    size_t x_pad_bytes = 0, w_pad_bytes = 0, dy_pad_bytes = 0, c_packed_bytes = 0, partial_bytes = 0;
+    size_t x_pad = 0, w_pad = 0, dy_pad = 0, c_packed = 0, partial = 0, sem = 0, total = 0;
+    size_t x_pad_bytes = 0, w_pad_bytes = 0, dy_pad_bytes = 0, c_packed_bytes = 0, partial_bytes = 0, sem_bytes = 0;
 };
 WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms);
 size_t ks_split_bytes(const cks_geom& g, cks_dtype dt);

@@ -6,6 +6,8 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace cks {
 
 // Stage1: rotate W by 180 degrees and split it into sh*sw sub-filters,
@@ -18,6 +20,8 @@ template <typename T>
 __global__ void ks_split_kernel(const T* __restrict__ W, T* __restrict__ out, int OC, int FH, int FW, int C, int sh,
                                 int sw, int CHm, int CWm, int OCp) {
     __shared__ T tile[32][33];
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
     const int slots = CHm * CWm;
     const int ps = blockIdx.z;  // (phase, slot)
     const int pidx = ps / slots, slot = ps % slots;
@@ -48,6 +52,8 @@ __global__ void ks_split_kernel(const T* __restrict__ W, T* __restrict__ out, in
 // dst[r][0:Cp] = src[r][0:C] with zeros in [C, Cp).
 template <typename T>
 __global__ void pad_channels_kernel(const T* __restrict__ src, T* __restrict__ dst, long long rows, int C, int Cp) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
     const long long total = rows * Cp;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -59,6 +65,8 @@ __global__ void pad_channels_kernel(const T* __restrict__ src, T* __restrict__ d
 
 // out[i] = sum_{z = 0..gz-1} part[z][i], fixed order z = 0, 1, ... (deterministic).
 __global__ void reduce_partials_kernel(const float* __restrict__ part, float* __restrict__ out, long long n, int gz) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
     const long long n4 = n / 4;
     const float4* p4 = reinterpret_cast<const float4*>(part);
     float4* o4 = reinterpret_cast<float4*>(out);
@@ -79,6 +87,8 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, float* __
 
 __global__ void reduce_partials_scalar_kernel(const float* __restrict__ part, float* __restrict__ out, long long n,
                                               int gz) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         float a = part[i];

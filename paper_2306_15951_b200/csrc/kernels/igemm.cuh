@@ -2,33 +2,49 @@
 // tcgen05 tensor cores, shared by ConvV2 (Alg. 1) and the fused
 // Stage2&3 of KS-deconv-V2 (Alg. 2/2B).
 //
-// One tile = 128 batch images x BN output channels at ONE output pixel
-// (row rh, row rw of the per-axis plan tables).  All 128 GEMM rows of a tile
-// therefore share one trimmed filter window [ts_h, te_h) x [ts_w, te_w) --
-// the B200 analogue of P:156 "all threads in the same block have the same
-// trimmed-filters ... no warp-divergence": padded zeros are never loaded or
-// multiplied, and no bounds check exists in the K loop.
+// GEMM rows are BATCH IMAGES: an accumulator holds 128 images x BN output
+// channels of ONE output pixel, so all its rows share one trimmed filter
+// window [ts_h, te_h) x [ts_w, te_w) -- the B200 analogue of P:156 ("all
+// threads in the same block have the same trimmed-filters ... no warp-
+// divergence"): padded zeros are never loaded or multiplied and the K loop
+// has no bounds checks.
 //
-// GEMM view per tile: M = 128 images, N = BN channels, K = window taps x Ka
-// channels, both operands K-major:
-//   A[m][k] = act[n0+m, a0_h+ch, a0_w+cw, kc]   (TMA 4-D box (BK,1,1,128))
-//   B[j][k] = filt[phase][nb*BN+j][ch*slot_stride+cw][kc]  (box (BK,1,BN,1))
-//   out[n0+m, out_h, out_w, nb*BN+j] = D[m][j]  (fp32, overwritten)
-// For ConvV2 act = X, filt = W (slot = fh*FW+fw), a0 = o*s - p (T1).  For
-// KS-deconv act = dY, filt = the packed sub-filters C_{y,x} (Stage1), a0 =
-// oh_s = u + a_y and out = u*sh + ih_s (T2): the epilogue IS Stage3's
-// phase-strided composition ("Stage2 and Stage3 are fused").
+// A tile is PBW consecutive pixels of one output row (same h window, same
+// phase), 128 images, BN channels: PBW accumulators in TMEM.  Its K loop
+// runs over "row steps" (filter row ch in the h window) x (channel block
+// kc); per row step the producer loads
+//   * the B row: the filter taps cw in the union of the pixels' w windows,
+//     one (BK x BN) K-major tile each, once for all PBW pixels, and
+//   * the A positions: one (128 images x BK) K-major tile per activation
+//     column iw in the union of the pixels' windows, each loaded ONCE and
+//     multiplied into every (pixel j, tap cw = iw - a0w_j) it serves
+// (halo reuse: for unit stride a position feeds up to FW pixels).  Compared
+// with one pixel per tile this cuts the L2->SM bytes per MAC by ~1.7x, which
+// is what bounds this kernel (TMA ingress ~64 B/clk/SM).
+//
+//   fwd (ConvV2): act = X, filt = W [OC][FH*FW][C] (slot fh*FW+fw),
+//                 a0 = o*s - p, out = o (T1)
+//   KS-deconv:    act = dY, filt = packed C_{y,x} [P][C][CHm*CWm][OCp]
+//                 (Stage1), a0 = oh_s = u + a_y, out = u*sh + ih_s (T2): the
+//                 epilogue is Stage3's phase-strided composition.
+//
+// Under-filled grids split the row steps into Z segments (split-K); each
+// segment writes fp32 partials and the LAST arriving CTA of an output tile
+// sums the Z partials in fixed order z = 0..Z-1 (deterministic, no extra
+// launch, no inter-CTA waiting).
 //
 // Warp roles (256 threads, 1 CTA/SM, persistent over tiles):
-//   warp 0 lane 0  TMA producer  (smem ring of STAGES {A,B} slots, mbarriers)
-//   warp 1 lane 0  MMA issuer    (tcgen05.mma into a double-buffered TMEM acc)
+//   warp 0 lane 0  TMA producer (B-row ring + A-position ring, mbarriers)
+//   warp 1 lane 0  MMA issuer   (tcgen05.mma, kind::f16 or kind::tf32)
 //   warp 2         TMEM allocator
-//   warps 4..7     epilogue      (tcgen05.ld -> fp32 global stores)
+//   warps 4..7     epilogue     (tcgen05.ld -> fp32 stores / split-K reduce)
 #pragma once
 #include "ptx.cuh"
 #include "../../../include/cks.h"
 
 namespace cks {
+
+constexpr int kMaxPBW = 8;
 
 struct KAxis {
     int16_t a0[CKS_MAX_ROWS];   // A coordinate of tap 0
@@ -41,41 +57,135 @@ struct KAxis {
 struct IgemmParams {
     KAxis ah, aw;
     float* out;
-    int rows_h, rows_w;
-    int nblk, nbs;
-    int kc_blocks;    // ceil(Ka / BK)
-    int slot_stride;  // tap slot = ch * slot_stride + cw
-    int phases_w;     // phase = phase_h * phases_w + phase_w
-    int N;
-    int out_H, out_W, out_C;
-    long long num_tiles;
+    float* part;  // split-K partials [out_tiles][Z][PBW*BN/4][128 rows][4] (coalesced per warp)
+    int* sem;     // split-K arrival counters [out_tiles] (zero on entry, left zero)
+    int rows_h;
+    int nph_w;                 // w phases
+    int16_t wph_off[9], wph_cnt[9], wb_cum[9];
+    int wblocks;               // pixel blocks along w
+    int pbw, acc_stages;       // pixels per tile, TMEM accumulator buffers
+    int nblk, nbs, kc_blocks;  // image blocks, BN blocks, BK channel blocks
+    int slot_stride;           // filter tap slot = ch * slot_stride + cw
+    int phases_w;              // phase = phase_h * phases_w + phase_w
+    int N, out_H, out_W, out_C;
+    int a_stages, b_stages;    // smem rings: A positions (16 KB each), B rows
+    int b_stage_bytes;         // ntap * BN * 128
+    int ntap;                  // filter taps per B row (one TMA box)
+    int apos;                  // activation positions per A slot (one TMA box)
+    int unit_step;             // consecutive pixels' tap-0 columns differ by 1 (N-merged MMAs)
+    int a0_step;               // a0 of pixel j = a0 of pixel 0 + j * a0_step (T1: stride, T2: 1)
+    int zsplit;
+    long long num_tiles;  // output tiles x zsplit
+    int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
+    unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// debug: per-CTA global-timer milestones -> trace[4*1024*5 + cta*8 + k]
+__device__ __forceinline__ void trace_gt(const IgemmParams& p, int k) {
+    if (p.trace != nullptr && blockIdx.x < 148) p.trace[4 * 1024 * 5 + blockIdx.x * 8 + k] = gtimer();
+}
+
+// debug timeline: entry = (code << 56) | clock64
+__device__ __forceinline__ void trace_ev(const IgemmParams& p, int role, int& idx, unsigned code) {
+    if (p.trace != nullptr && blockIdx.x < 4 && idx < 1024) {
+        const unsigned long long t = clock64();
+        p.trace[(blockIdx.x * 5 + role) * 1024 + idx] = (static_cast<unsigned long long>(code) << 56) | (t & 0x00FFFFFFFFFFFFFFull);
+        ++idx;
+    }
+}
 
 template <int BN, bool kTF32>
 struct IgemmShape {
     static constexpr int EB = kTF32 ? 4 : 2;
-    static constexpr int BK = 128 / EB;   // one 128-byte swizzle row of K
-    static constexpr int UK = 32 / EB;    // K per tcgen05.mma
+    static constexpr int BK = 128 / EB;  // one 128-byte swizzle row of K
+    static constexpr int UK = 32 / EB;   // K per tcgen05.mma
     static constexpr int A_BYTES = 128 * 128;
-    static constexpr int B_BYTES = BN * 128;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int TILE_B = BN * 128;
+    static constexpr int SMEM_MAX = 227 * 1024;
 };
 
-struct TileCoord {
-    int nb, nblk, rh, rw;
+// Per-tile decode shared by the three roles.  Per-pixel data lives in fixed
+// size arrays that are only indexed inside fully unrolled loops (registers).
+struct Tile {
+    int z, nb, nblk, rh, j0, len, ph;
+    int rs0, rs1;         // row-step range [rs0, rs1) of this split
+    int rot;              // per-CTA rotation of the row-step order (spreads weight reads over L2)
+    int chs;              // first filter row of the h window
+    int cwlo, cwhi;       // union of the pixels' w windows
+    int pos_lo, pos_hi;   // union of A columns
+    int a0[kMaxPBW], ts[kMaxPBW], te[kMaxPBW];
+    long long out_tile;
 };
-__device__ __forceinline__ TileCoord decode_tile(long long t, const IgemmParams& p) {
-    TileCoord c;
+
+__device__ __forceinline__ Tile decode_tile(long long t, const IgemmParams& p) {
+    Tile c;
+    c.z = int(t % p.zsplit);
+    t /= p.zsplit;
+    c.out_tile = t;
     c.nb = int(t % p.nbs);
     t /= p.nbs;
     c.nblk = int(t % p.nblk);
     t /= p.nblk;
-    c.rw = int(t % p.rows_w);
-    c.rh = int(t / p.rows_w);
+    const int wb = int(t % p.wblocks);
+    c.rh = int(t / p.wblocks);
+    int x = 0;
+    while (x + 1 < p.nph_w && p.wb_cum[x + 1] <= wb) ++x;
+    c.j0 = p.wph_off[x] + (wb - p.wb_cum[x]) * p.pbw;
+    c.len = min(p.pbw, p.wph_off[x] + p.wph_cnt[x] - c.j0);
+    c.ph = p.ah.phase[c.rh] * p.phases_w + p.aw.phase[c.j0];
+    const int chs = p.ah.ts[c.rh], che = p.ah.te[c.rh];
+    c.chs = chs;
+    int lo = 1 << 20, hi = -(1 << 20), plo = 1 << 20, phi = -(1 << 20);
+#pragma unroll
+    for (int j = 0; j < kMaxPBW; ++j) {
+        c.a0[j] = 0;
+        c.ts[j] = 0;
+        c.te[j] = 0;
+        if (j < c.len) {
+            c.a0[j] = p.aw.a0[c.j0 + j];
+            c.ts[j] = p.aw.ts[c.j0 + j];
+            c.te[j] = p.aw.te[c.j0 + j];
+            if (c.te[j] > c.ts[j]) {
+                lo = min(lo, c.ts[j]);
+                hi = max(hi, c.te[j]);
+                plo = min(plo, c.a0[j] + c.ts[j]);
+                phi = max(phi, c.a0[j] + c.te[j]);
+            }
+        }
+    }
+    const bool empty = (hi <= lo) || (che <= chs);
+    c.cwlo = empty ? 0 : lo;
+    c.cwhi = empty ? 0 : hi;
+    c.pos_lo = empty ? 0 : plo;
+    c.pos_hi = empty ? 0 : phi;
+    const int rs = empty ? 0 : (che - chs) * p.kc_blocks;
+    c.rs0 = int((long long)rs * c.z / p.zsplit);
+    c.rs1 = int((long long)rs * (c.z + 1) / p.zsplit);
+    c.rot = c.rs1 > c.rs0 ? int(blockIdx.x % unsigned(c.rs1 - c.rs0)) : 0;
     return c;
+}
+
+// i-th row step of tile c (rotated start; every role uses the same order)
+__device__ __forceinline__ int row_step(const Tile& c, int i) {
+    int r = i + c.rot;
+    if (r >= c.rs1) r -= c.rs1 - c.rs0;
+    return r;
+}
+
+// bitmask of pixels j of the tile that use activation column iw
+__device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxPBW; ++j) {
+        const int cw = iw - c.a0[j];
+        if (cw >= c.ts[j] && cw < c.te[j]) m |= 1u << j;
+    }
+    return m;
 }
 
 template <int BN, bool kTF32>
@@ -84,22 +194,37 @@ __global__ void __launch_bounds__(256, 1)
                  const __grid_constant__ IgemmParams p) {
     using S = IgemmShape<BN, kTF32>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
-    uint64_t* empty = full + S::STAGES;
-    uint64_t* tfull = empty + S::STAGES;
+    // 1 KB alignment by offset arithmetic (keeps the shared address space visible to the compiler)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t a_slot = uint32_t(p.apos) * S::A_BYTES;
+    uint8_t* abuf = smem;                                    // a_stages x apos x 16 KB
+    uint8_t* bbuf = smem + p.a_stages * a_slot;              // b_stages x b_stage_bytes
+    uint64_t* bars = reinterpret_cast<uint64_t*>(bbuf + p.b_stages * p.b_stage_bytes);
+    uint64_t* afull = bars;
+    uint64_t* aempty = afull + p.a_stages;
+    uint64_t* bfull = aempty + p.a_stages;
+    uint64_t* bempty = bfull + p.b_stages;
+    uint64_t* tfull = bempty + p.b_stages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    const uint32_t tmem_cols = 512;
 
+    if (threadIdx.x == 0) trace_gt(p, 0);
+    ptx::pdl_launch_dependents();
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
     }
     if (warp == 1 && lane == 0) {
-        for (int i = 0; i < S::STAGES; ++i) {
-            ptx::mbar_init(&full[i], 1);
-            ptx::mbar_init(&empty[i], 1);
+        for (int i = 0; i < p.a_stages; ++i) {
+            ptx::mbar_init(&afull[i], 1);
+            ptx::mbar_init(&aempty[i], 1);
+        }
+        for (int i = 0; i < p.b_stages; ++i) {
+            ptx::mbar_init(&bfull[i], 1);
+            ptx::mbar_init(&bempty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -107,128 +232,273 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, S::TMEM_COLS);
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) trace_gt(p, 1);
+    ptx::pdl_wait();  // inputs of this op may come from the previous kernel
+    if (threadIdx.x == 0) trace_gt(p, 2);
 
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer
-            uint32_t stage = 0, phase = 0;
-            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const TileCoord c = decode_tile(t, p);
-                const int chs = p.ah.ts[c.rh], che = p.ah.te[c.rh];
-                const int cws = p.aw.ts[c.rw], cwe = p.aw.te[c.rw];
-                const int a0h = p.ah.a0[c.rh], a0w = p.aw.a0[c.rw];
-                const int ph = p.ah.phase[c.rh] * p.phases_w + p.aw.phase[c.rw];
-                for (int ch = chs; ch < che; ++ch)
-                    for (int cw = cws; cw < cwe; ++cw)
-                        for (int kc = 0; kc < p.kc_blocks; ++kc) {
-                            ptx::mbar_wait(&empty[stage], phase ^ 1);
-                            ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-                            uint8_t* sa = smem + stage * S::STAGE_BYTES;
-                            ptx::tma_load_4d(sa, &tmA, &full[stage], kc * S::BK, a0w + cw, a0h + ch, c.nblk * 128);
-                            ptx::tma_load_4d(sa + S::A_BYTES, &tmB, &full[stage], kc * S::BK,
-                                             ch * p.slot_stride + cw, c.nb * BN, ph);
-                            if (++stage == S::STAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
-                        }
+    if (warp == 0 || warp == 3) {
+        // ---------------- TMA producers.  The whole warp walks the (uniform)
+        // schedule and one elected lane issues: warp 0 loads the A slots (apos
+        // consecutive activation columns x 128 images, one box), warp 3 the B
+        // rows (all taps of one filter row, one box).
+        const bool is_b = warp == 3;
+        uint32_t aq = 0, bq = 0;  // A / B sequence numbers
+        int ti = 0;
+        const int trole = warp == 0 ? 0 : 4;
+        if (lane == 0) trace_ev(p, trole, ti, 0);
+        const uint32_t btx = uint32_t(p.ntap * S::TILE_B);
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const Tile c = decode_tile(t, p);
+            const int a0h = p.ah.a0[c.rh];
+            for (int ri = c.rs0; ri < c.rs1; ++ri) {
+                const int r = row_step(c, ri);
+                const int ch = c.chs + r / p.kc_blocks, kc = r % p.kc_blocks;
+                if (is_b) {
+                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
+                    ptx::mbar_wait(&bempty[bs], bph ^ 1);
+                    if (ptx::elect_one()) {
+                        ptx::mbar_arrive_expect_tx(&bfull[bs], btx);
+                        ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, &bfull[bs], kc * S::BK, c.nb * BN,
+                                         ch * p.slot_stride, c.ph);
+                    }
+                    __syncwarp();
+                    if (lane == 0) trace_ev(p, trole, ti, 1);
+                    ++bq;
+                    continue;
+                }
+                for (int iw0 = c.pos_lo; iw0 < c.pos_hi; iw0 += p.apos) {
+                    const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
+                    ++aq;
+                    ptx::mbar_wait(&aempty[as], aph ^ 1);
+                    if (ptx::elect_one()) {
+                        ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
+                        ptx::tma_load_4d(abuf + as * a_slot, &tmA, &afull[as], kc * S::BK, c.nblk * 128, iw0,
+                                         a0h + ch);
+                    }
+                    __syncwarp();
+                    if (lane == 0) trace_ev(p, trole, ti, 2);
+                }
             }
         }
-        __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
             // ---------------- MMA issuer (single thread)
-            constexpr uint32_t idesc = ptx::instr_desc(128, BN, kTF32, false, false);
-            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+            // K-major SW128 descriptor without the start address: LBO 16 B, SBO 1 KB
+            const uint64_t dconst = ptx::smem_desc_sw128(0, 16, 1024);
+            uint32_t aq = 0, bq = 0, acc = 0, acc_ph = 0;
+            int ti = 0;
+            if (lane == 0) trace_ev(p, 1, ti, 0);
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const TileCoord c = decode_tile(t, p);
-                const int nsteps = (p.ah.te[c.rh] - p.ah.ts[c.rh]) * (p.aw.te[c.rw] - p.aw.ts[c.rw]) * p.kc_blocks;
-                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                const Tile c = decode_tile(t, p);
+                ptx::mbar_wait(&tempty[acc], acc_ph ^ 1);
+                if (lane == 0) trace_ev(p, 1, ti, 3);
                 ptx::tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int k = 0; k < nsteps; ++k) {
-                    ptx::mbar_wait(&full[stage], phase);
-                    ptx::tc_fence_after();
-                    const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
-                    const uint32_t b_addr = a_addr + S::A_BYTES;
+                const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BN);
+                uint32_t started = 0;
+                for (int ri = c.rs0; ri < c.rs1; ++ri) {
+                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
+                    ptx::mbar_wait(&bfull[bs], bph);
+                    if (lane == 0) trace_ev(p, 1, ti, 1);
+                    if (lane == 0 && ri == c.rs0 && t == blockIdx.x) trace_gt(p, 3);
+                    const uint32_t b_addr = ptx::smem_u32(bbuf + bs * p.b_stage_bytes);
+                    for (int iw0 = c.pos_lo; iw0 < c.pos_hi; iw0 += p.apos) {
+                        const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
+                        ++aq;
+                        ptx::mbar_wait(&afull[as], aph);
+                        if (lane == 0) trace_ev(p, 1, ti, 2);
+                        ptx::tc_fence_after();
+                        for (int qq = 0; qq < p.apos; ++qq) {
+                            const int iw = iw0 + qq;
+                            uint32_t m = pos_mask(c, iw);
+                            if (!m) continue;  // padding / unused column: never multiplied
+                            const uint64_t adesc =
+                                dconst | uint64_t((ptx::smem_u32(abuf + as * a_slot) + uint32_t(qq) * S::A_BYTES) >> 4);
+                            // groups of consecutive pixels with the same accumulate state; with a
+                            // unit tap-0 step, pixels jlo..jhi use taps cw_jlo, cw_jlo-1, ... which are
+                            // consecutive B tiles, and their accumulators (reversed TMEM order) are
+                            // consecutive columns: one MMA of N = cnt*BN covers the group
+                            while (m) {
+                                const int jlo = __ffs(m) - 1;
+                                const uint32_t st0 = (started >> jlo) & 1u;
+                                int cnt = 1;
+                                if (p.unit_step) {
+                                    while (jlo + cnt < kMaxPBW && ((m >> (jlo + cnt)) & 1u) &&
+                                           (((started >> (jlo + cnt)) & 1u) == st0) && (cnt + 1) * BN <= 256)
+                                        ++cnt;
+                                }
+                                const int jhi = jlo + cnt - 1;
+                                const uint32_t d = dbase + uint32_t((p.pbw - 1 - jhi) * BN);
+                                const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);  // smallest tap of the group
+                                const uint64_t bdesc = dconst | uint64_t((b_addr + uint32_t(cw_lo * S::TILE_B)) >> 4);
+                                const uint32_t idesc = ptx::instr_desc(128, uint32_t(cnt * BN), kTF32, false, false);
+                                if (!(p.dbg & 2) && ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < S::BK / S::UK; ++kk) {
-                        const uint64_t ad = ptx::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
-                        ptx::mma_ss<kTF32>(d, ad, bd, idesc, (k | kk) != 0);
+                                    for (int kk = 0; kk < S::BK / S::UK; ++kk)
+                                        ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
+                                                           kk ? 1u : st0);
+                                }
+                                __syncwarp();
+                                const uint32_t gm = ((1u << cnt) - 1u) << jlo;
+                                started |= gm;
+                                m &= ~gm;
+                            }
+                        }
+                        if (ptx::elect_one()) ptx::mma_commit(&aempty[as]);  // A slot free when these MMAs finish
+                        __syncwarp();
+                        if (lane == 0) trace_ev(p, 1, ti, 4);
                     }
-                    ptx::mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
-                    if (++stage == S::STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                    if (ptx::elect_one()) ptx::mma_commit(&bempty[bs]);  // B row free
+                    __syncwarp();
+                    ++bq;
                 }
-                ptx::mma_commit(&tfull[acc]);  // accumulator ready (immediately if nsteps == 0)
-                if (++acc == 2) {
+                if (lane == 0) trace_gt(p, 4);
+                if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);  // accumulators ready (immediately if no MMA)
+                __syncwarp();
+                if (++acc == uint32_t(p.acc_stages)) {
                     acc = 0;
-                    acc_phase ^= 1;
+                    acc_ph ^= 1;
                 }
             }
         }
         __syncwarp();
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> fp32 stores
-        const uint32_t sub = warp & 3;  // TMEM sub-partition = lanes [32*sub, 32*sub+32)
+        // (thread = accumulator row = one image; 16-byte vector stores)
+        const uint32_t sub = warp & 3;  // TMEM sub-partition: lanes [32*sub, 32*sub+32)
         const int row = int(sub * 32 + lane);
-        uint32_t acc = 0, acc_phase = 0;
+        const int et = threadIdx.x - 128;  // 0..127
+        uint32_t acc = 0, acc_ph = 0;
+        const int pw_cols = p.pbw * BN;
+        const bool split = p.zsplit > 1;
         const bool vec4 = (p.out_C % 4) == 0;
+        int ti = 0;
+        if (et == 0) trace_ev(p, 2, ti, 0);
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const TileCoord c = decode_tile(t, p);
-            const bool empty_win = (p.ah.te[c.rh] <= p.ah.ts[c.rh]) || (p.aw.te[c.rw] <= p.aw.ts[c.rw]);
-            ptx::mbar_wait(&tfull[acc], acc_phase);
+            const Tile c = decode_tile(t, p);
+            ptx::mbar_wait(&tfull[acc], acc_ph);
+            if (et == 0) trace_ev(p, 2, ti, 1);
             ptx::tc_fence_after();
-            const int n = c.nblk * 128 + row;
+            const int nrow0 = c.nblk * 128 + int(sub) * 32;  // image of lane 0
+            const int n = nrow0 + int(lane);
             const int cbase = c.nb * BN;
             const int cvalid = min(BN, p.out_C - cbase);
-            float* dst = nullptr;
-            if (n < p.N)
-                dst = p.out + ((static_cast<long long>(n) * p.out_H + p.ah.out[c.rh]) * p.out_W + p.aw.out[c.rw]) *
-                                  p.out_C + cbase;
+            const bool any = c.rs1 > c.rs0;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t r[32];
-                ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * BN + c0, r);
-                ptx::tmem_ld_wait();
-                if (dst != nullptr && c0 < cvalid) {
-                    if (empty_win) {
+            for (int j = 0; j < c.len; ++j) {
+                const bool live = any && (p.aw.te[c.j0 + j] > p.aw.ts[c.j0 + j]);
+                float* dst = nullptr;
+                if (split)  // column group q = (j*BN + c)/4 of row `row`
+                    dst = p.part + ((c.out_tile * p.zsplit + c.z) * (pw_cols / 4) + j * (BN / 4)) * 512LL + row * 4;
+                else if (n < p.N)
+                    dst = p.out + ((static_cast<long long>(n) * p.out_H + p.ah.out[c.rh]) * p.out_W +
+                                   p.aw.out[c.j0 + j]) * p.out_C + cbase;
+                const int lim = split ? BN : cvalid;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN + c0,
+                                   r);
+                    ptx::tmem_ld_wait();
+                    if (dst == nullptr || c0 >= lim || (p.dbg & 1)) continue;
+                    if (!live) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) r[j] = 0u;
+                        for (int q = 0; q < 32; ++q) r[q] = 0u;
                     }
-                    if (vec4 && c0 + 32 <= cvalid) {
+                    if (split) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<float4*>(dst + c0 + j) =
-                                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                        for (int q = 0; q < 32; q += 4)
+                            *reinterpret_cast<float4*>(dst + (c0 + q) / 4 * 512) =
+                                make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]),
+                                            __uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
+                    } else if (vec4 && c0 + 32 <= lim) {
+#pragma unroll
+                        for (int q = 0; q < 32; q += 4)
+                            *reinterpret_cast<float4*>(dst + c0 + q) =
+                                make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]),
+                                            __uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (c0 + j < cvalid) dst[c0 + j] = __uint_as_float(r[j]);
+                        for (int q = 0; q < 32; ++q)
+                            if (c0 + q < lim) dst[c0 + q] = __uint_as_float(r[q]);
                     }
                 }
             }
+            // TMEM drained: release the accumulator buffer before the split-K reduce
+            if (et == 0) trace_ev(p, 2, ti, 2);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
-            if (++acc == 2) {
+            if (++acc == uint32_t(p.acc_stages)) {
                 acc = 0;
-                acc_phase ^= 1;
+                acc_ph ^= 1;
+            }
+            if (split) {
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (et == 0) {
+                    const int old = atomicAdd(&p.sem[c.out_tile], 1);
+                    const int last = old == p.zsplit - 1;
+                    if (last) p.sem[c.out_tile] = 0;  // leave the counter zeroed for the next call
+                    *red_flag = last;
+                    __threadfence();
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (et == 0) trace_ev(p, 2, ti, 3);
+                if (*red_flag && n < p.N) {
+                    // last segment: sum the Z partials in order z = 0..Z-1; thread = row,
+                    // 8 column groups x Z vector loads in flight, coalesced 512 B per warp load
+                    const float4* base = reinterpret_cast<const float4*>(p.part) +
+                                         (c.out_tile * p.zsplit) * (pw_cols / 4) * 128LL + row;
+                    const long long zs = (pw_cols / 4) * 128LL;
+                    for (int j = 0; j < c.len; ++j) {
+                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + p.ah.out[c.rh]) * p.out_W +
+                                               p.aw.out[c.j0 + j]) * p.out_C + cbase;
+                        for (int c0 = 0; c0 < cvalid; c0 += 32) {
+                            const float4* src = base + (j * BN + c0) / 4 * 128LL;
+                            float4 v[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) v[q] = __ldcg(src + q * 128);
+                            for (int z = 1; z < p.zsplit; ++z) {
+                                float4 w[8];
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) w[q] = __ldcg(src + z * zs + q * 128);
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    v[q].x += w[q].x;
+                                    v[q].y += w[q].y;
+                                    v[q].z += w[q].z;
+                                    v[q].w += w[q].w;
+                                }
+                            }
+                            if (vec4 && c0 + 32 <= cvalid) {
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) *reinterpret_cast<float4*>(orow + c0 + 4 * q) = v[q];
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 8; ++q) {
+                                    const float e[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u)
+                                        if (c0 + 4 * q + u < cvalid) orow[c0 + 4 * q + u] = e[u];
+                                }
+                            }
+                        }
+                    }
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // red_flag reuse guard
+                if (et == 0) trace_ev(p, 2, ti, 4);
             }
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) trace_gt(p, 5);
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, S::TMEM_COLS);
+        ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
 }
 

@@ -75,13 +75,14 @@ __global__ void __launch_bounds__(256, 1)
                  const __grid_constant__ WgradParams p) {
     using S = WgradShape<BN>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
     uint64_t* empty = full + S::STAGES;
     uint64_t* tfull = empty + S::STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
+    ptx::pdl_launch_dependents();
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmDY);
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < S::STAGES; ++i) {
-            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&full[i], 2);  // A producer + B producer
             ptx::mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -103,70 +104,81 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    ptx::pdl_wait();  // inputs of this op may come from the previous kernel
 
-    if (warp == 0) {
-        if (lane == 0) {
-            uint32_t stage = 0, phase = 0;
-            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const WTile c = wdecode(t, p);
-                for (int kb = c.kb0; kb < c.kb1; ++kb) {
-                    const int n64 = kb % p.nblk64;
-                    const int pos = kb / p.nblk64;
-                    const int oh = c.ohs + pos / c.wn, ow = c.ows + pos % c.wn;
-                    const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
-                    const int iw = ow * p.sw + c.fw - p.pw;
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-                    uint8_t* sa = smem + stage * S::STAGE_BYTES;
+    if (warp == 0 || warp == 3) {
+        // ---------------- TMA producers (whole warp walks the uniform schedule,
+        // one elected lane issues): warp 0 loads dY (A, 2 OC chunks), warp 3
+        // loads X (B, BN/64 IC chunks) with the leaping row ih = oh*sh + fh - ph
+        const bool is_b = warp == 3;
+        uint32_t stage = 0, phase = 0;
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const WTile c = wdecode(t, p);
+            for (int kb = c.kb0; kb < c.kb1; ++kb) {
+                const int n64 = kb % p.nblk64;
+                const int pos = kb / p.nblk64;
+                const int oh = c.ohs + pos / c.wn, ow = c.ows + pos % c.wn;
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * S::STAGE_BYTES;
+                if (ptx::elect_one()) {
+                    if (!is_b) {
+                        ptx::mbar_arrive_expect_tx(&full[stage], S::A_BYTES);
 #pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * 64, ow, oh, n64 * 64);
+                        for (int j = 0; j < 2; ++j)
+                            ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * 64, ow, oh, n64 * 64);
+                    } else {
+                        const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
+                        const int iw = ow * p.sw + c.fw - p.pw;
+                        ptx::mbar_arrive_expect_tx(&full[stage], S::B_BYTES);
 #pragma unroll
-                    for (int j = 0; j < BN / 64; ++j)
-                        ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * 64, iw, ih,
-                                         n64 * 64);
-                    if (++stage == S::STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                        for (int j = 0; j < BN / 64; ++j)
+                            ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * 64, iw,
+                                             ih, n64 * 64);
                     }
+                }
+                __syncwarp();
+                if (++stage == S::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
-        __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, true, true);
-            uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const WTile c = wdecode(t, p);
-                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        // ---------------- MMA issuer (whole warp, elected lane issues)
+        constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, true, true);
+        const uint64_t dconst = ptx::smem_desc_sw128(0, 8192, 1024);  // MN-major: LBO 8 KB, SBO 1 KB
+        uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            const WTile c = wdecode(t, p);
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d = tmem_base + acc * BN;
+            for (int kb = c.kb0; kb < c.kb1; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
-                const uint32_t d = tmem_base + acc * BN;
-                for (int kb = c.kb0; kb < c.kb1; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
-                    ptx::tc_fence_after();
-                    const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
-                    const uint32_t b_addr = a_addr + S::A_BYTES;
+                const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
+                const uint64_t ad = dconst | uint64_t(a_addr >> 4);
+                const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES) >> 4);
+                if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {  // 64 images = 4 x K16
-                        const uint64_t ad = ptx::smem_desc_sw128(a_addr + kk * 2048, 8192, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(b_addr + kk * 2048, 8192, 1024);
-                        ptx::mma_ss<false>(d, ad, bd, idesc, ((kb - c.kb0) | kk) != 0);
-                    }
+                    for (int kk = 0; kk < 4; ++kk)  // 64 images = 4 x K16 (+2 KB per K16 step)
+                        ptx::mma_ss<false>(d, ad + uint64_t(kk * 128), bd + uint64_t(kk * 128), idesc,
+                                           ((kb - c.kb0) | kk) != 0);
                     ptx::mma_commit(&empty[stage]);
-                    if (++stage == S::STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
-                ptx::mma_commit(&tfull[acc]);
-                if (++acc == 2) {
-                    acc = 0;
-                    acc_phase ^= 1;
+                __syncwarp();
+                if (++stage == S::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
+            if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
         }
-        __syncwarp();
     } else if (warp >= 4) {
         const uint32_t sub = warp & 3;
         const int row = int(sub * 32 + lane);
