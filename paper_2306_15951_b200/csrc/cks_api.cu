@@ -49,7 +49,7 @@ int device_sms() {
 
 // rank-4 tiled tensor map, 128B swizzle, zero OOB fill
 bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
-                const uint32_t box[4]) {
+                const uint32_t box[4], int row_bytes = 128) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
@@ -58,7 +58,9 @@ bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t d
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                      const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                      : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -132,32 +134,37 @@ bool rows_ok(const std::vector<KRow>& rows) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <int BN, bool TF>
+template <int BN, bool TF, int KB>
 cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
                           cudaStream_t st) {
-    auto kern = igemm_kernel<BN, TF>;
+    auto kern = igemm_kernel<BN, TF, KB>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
     return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, a, b, p);
 }
 
-cks_status launch_igemm(int BN, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
-                        cudaStream_t st) {
-    if (tf32) {
-        switch (BN) {
-            case 32: return launch_igemm_t<32, true>(a, b, p, smem, st);
-            case 64: return launch_igemm_t<64, true>(a, b, p, smem, st);
-            case 128: return launch_igemm_t<128, true>(a, b, p, smem, st);
-        }
-    } else {
-        switch (BN) {
-            case 32: return launch_igemm_t<32, false>(a, b, p, smem, st);
-            case 64: return launch_igemm_t<64, false>(a, b, p, smem, st);
-            case 128: return launch_igemm_t<128, false>(a, b, p, smem, st);
-        }
+template <bool TF, int KB>
+cks_status launch_igemm_kb(int BN, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
+                           cudaStream_t st) {
+    switch (BN) {
+        case 32: return launch_igemm_t<32, TF, KB>(a, b, p, smem, st);
+        case 64: return launch_igemm_t<64, TF, KB>(a, b, p, smem, st);
+        case 128: return launch_igemm_t<128, TF, KB>(a, b, p, smem, st);
     }
     return CKS_ERR_UNSUPPORTED;
+}
+
+cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p,
+                        int smem, cudaStream_t st) {
+    if (tf32) {
+        if (KB == 32) return launch_igemm_kb<true, 32>(BN, a, b, p, smem, st);
+        if (KB == 64) return launch_igemm_kb<true, 64>(BN, a, b, p, smem, st);
+        return launch_igemm_kb<true, 128>(BN, a, b, p, smem, st);
+    }
+    if (KB == 32) return launch_igemm_kb<false, 32>(BN, a, b, p, smem, st);
+    if (KB == 64) return launch_igemm_kb<false, 64>(BN, a, b, p, smem, st);
+    return launch_igemm_kb<false, 128>(BN, a, b, p, smem, st);
 }
 
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
@@ -211,14 +218,14 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.unit_step = cfg.unit_step;
     p.a0_step = cfg.a0_step;
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
-    const int smem = 1024 + p.a_stages * p.apos * 16384 + p.b_stages * p.b_stage_bytes + 512;
+    const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512;
     if (cfg.Z > 1) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
         p.sem = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + L.sem);
         if (cudaMemsetAsync(p.sem, 0, L.sem_bytes, st) != cudaSuccess) return last_cuda();
     }
-    return launch_igemm(cfg.BN, dt == CKS_TF32, ta, tb, p, smem, st);
+    return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, p, smem, st);
 }
 
 template <int BN>
@@ -342,19 +349,19 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
         wsrc = wp;
     }
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
-    const uint32_t BK = uint32_t(128 / eb);
+    const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->H)};
         uint64_t sb[3] = {uint64_t(g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
         uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
-        if (!make_tmap4(&ta, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
+        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     {   // W viewed as (C, OC, FH*FW, 1): one box = the FW taps of a filter row x BN filters
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->OC), uint64_t(g->FH * g->FW), 1};
         uint64_t sb[3] = {uint64_t(g->FH * g->FW * Cp * eb), uint64_t(Cp * eb), uint64_t(g->OC * g->FH * g->FW * Cp * eb)};
         uint32_t box[4] = {BK, uint32_t(cfg.BN), uint32_t(g->FW), 1};
-        if (!make_tmap4(&tb, dt, wsrc, d, sb, box)) return CKS_ERR_CUDA;
+        if (!make_tmap4(&tb, dt, wsrc, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     return run_igemm(cfg, dt, rh, rw, ta, tb, y, int(ah.O), int(aw.O), int(g->OC), int(g->N), int(g->FW), 1, L, ws,
                      st);
@@ -398,19 +405,19 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
     }
     const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
     IgemmCfg cfg = igemm_cfg_deconv(*g, dt, kPlanSMs);
-    const uint32_t BK = uint32_t(128 / eb);
+    const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
         uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
         uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
         uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
-        if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
+        if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     {   // packed C_{y,x} viewed as (OCp, C, CHm*CWm, P): one box = the CWm taps of sub-filter row ch
         uint64_t d[4] = {uint64_t(OCp), uint64_t(g->C), uint64_t(CHm * CWm), uint64_t(P)};
         uint64_t sb[3] = {uint64_t(CHm * CWm * OCp * eb), uint64_t(OCp * eb), uint64_t(g->C * CHm * CWm * OCp * eb)};
         uint32_t box[4] = {BK, uint32_t(cfg.BN), uint32_t(CWm), 1};
-        if (!make_tmap4(&tb, dt, cp, d, sb, box)) return CKS_ERR_CUDA;
+        if (!make_tmap4(&tb, dt, cp, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     return run_igemm(cfg, dt, rh, rw, ta, tb, dx, int(g->H), int(g->W), int(g->C), int(g->N), int(CWm), g->sw, L, ws,
                      st);
@@ -549,7 +556,7 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]) {
     out[4] = 2 * (g->C * g->N * g->H * g->W * g->FH * g->FW * g->OC);
     out[5] = 2 * (g->OC * g->FH * g->FW * g->C * OHp * OWp) * g->N;
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
-    const int64_t Cp = pad_ch(g->C, dt), BK = 128 / elem_bytes(dt);
+    const int64_t Cp = pad_ch(g->C, dt), BK = cfg.KB / elem_bytes(dt);
     out[6] = int64_t(cfg.nblk) * 128 * int64_t(cfg.nbs) * cfg.BN * VH * VW * ((Cp + BK - 1) / BK * BK);
     out[7] = cfg.tiles;
     return CKS_OK;

@@ -134,7 +134,11 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     if (ov && ov_bn > 0) c.BN = ov_bn;
     if (ov && ov_pbw > 0) force_pbw = ov_pbw;
     c.nbs = int((nout + c.BN - 1) / c.BN);
-    c.kc_blocks = int((kchan + (128 / eb) - 1) / (128 / eb));
+    // K block: the narrowest swizzle row (32 / 64 / 128 B) holding all channels,
+    // else 128 B blocks
+    const int64_t kbytes = kchan * eb;
+    c.KB = kbytes <= 32 ? 32 : (kbytes <= 64 ? 64 : 128);
+    c.kc_blocks = int((kchan + (c.KB / eb) - 1) / (c.KB / eb));
     c.ntap = int(ntap);
     int64_t maxrow = 1;
     for (auto v : wph_cnt) maxrow = std::max(maxrow, v);
@@ -159,21 +163,22 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // pa activation columns of a row step (one TMA box, one barrier)
     for (; pbw >= 1; --pbw) {
         c.pa = int((pbw - 1) * a0_step + ntap);
-        c.stage_bytes = int(ntap * c.BN * 128);
-        if (2 * (int64_t(c.pa) * 16384 + c.stage_bytes) <= kSmemBudget && c.pa <= 256) break;
+        c.stage_bytes = int(ntap * c.BN * c.KB);
+        if (2 * (int64_t(c.pa) * 128 * c.KB + c.stage_bytes) <= kSmemBudget && c.pa <= 256) break;
     }
     if (pbw < 1) pbw = 1;
     c.pbw = pbw;
     c.pa = int((pbw - 1) * a0_step + ntap);
-    c.stage_bytes = int(ntap * c.BN * 128);
+    c.stage_bytes = int(ntap * c.BN * c.KB);
     c.unit_step = a0_step == 1;
     c.a0_step = int(a0_step);
     // A slot: as many of the pa columns as fit with >= 2 A slots and 2 B rows
     c.stages = 2;
     c.apos = c.pa;
-    while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * 16384 > kSmemBudget) --c.apos;
-    if (2 * c.stage_bytes + 2 * int64_t(c.apos) * 16384 > kSmemBudget) c.stages = 1;
-    c.a_stages = int(std::min<int64_t>(8, (kSmemBudget - c.stages * c.stage_bytes) / (int64_t(c.apos) * 16384)));
+    const int64_t col_bytes = 128 * c.KB;  // one activation column, 128 images
+    while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) --c.apos;
+    if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) c.stages = 1;
+    c.a_stages = int(std::min<int64_t>(8, (kSmemBudget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
     c.acc_stages = 2;
     c.wblocks = 0;
     for (auto v : wph_cnt) c.wblocks += int((v + c.pbw - 1) / c.pbw);

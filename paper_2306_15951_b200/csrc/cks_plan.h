@@ -74,6 +74,7 @@ struct IgemmCfg {
     int wblocks = 1;
     int Z = 1;          // split-K segments
     int kc_blocks = 1;
+    int KB = 128;       // bytes per K row: 32 / 64 / 128 (swizzle width)
     int ntap = 1;       // taps per filter row (B box)
     int pa = 1;         // activation positions per row step (A box)
     int stage_bytes = 0, stages = 2;  // B-row ring: bytes per row, rows in flight

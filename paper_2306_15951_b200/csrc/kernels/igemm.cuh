@@ -99,13 +99,16 @@ __device__ __forceinline__ void trace_ev(const IgemmParams& p, int role, int& id
     }
 }
 
-template <int BN, bool kTF32>
+// KB = bytes of one K row (32 / 64 / 128 -> SWIZZLE_32B / 64B / 128B): narrow
+// channel counts (e.g. I_C = 3 padded to 8) use a narrow K block instead of
+// multiplying TMA zero fill.
+template <int BN, bool kTF32, int KB = 128>
 struct IgemmShape {
     static constexpr int EB = kTF32 ? 4 : 2;
-    static constexpr int BK = 128 / EB;  // one 128-byte swizzle row of K
-    static constexpr int UK = 32 / EB;   // K per tcgen05.mma
-    static constexpr int A_BYTES = 128 * 128;
-    static constexpr int TILE_B = BN * 128;
+    static constexpr int BK = KB / EB;   // channels per K block
+    static constexpr int UK = 32 / EB;   // K per tcgen05.mma (32 bytes)
+    static constexpr int A_BYTES = 128 * KB;
+    static constexpr int TILE_B = BN * KB;
     static constexpr int SMEM_MAX = 227 * 1024;
 };
 
@@ -188,11 +191,11 @@ __device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
     return m;
 }
 
-template <int BN, bool kTF32>
+template <int BN, bool kTF32, int KB>
 __global__ void __launch_bounds__(256, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ IgemmParams p) {
-    using S = IgemmShape<BN, kTF32>;
+    using S = IgemmShape<BN, kTF32, KB>;
     extern __shared__ uint8_t smem_raw[];
     // 1 KB alignment by offset arithmetic (keeps the shared address space visible to the compiler)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -213,30 +216,40 @@ __global__ void __launch_bounds__(256, 1)
     if (threadIdx.x == 0) trace_gt(p, 0);
     ptx::pdl_launch_dependents();
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    if (warp == 0 && lane == 0) {
-        ptx::prefetch_tmap(&tmA);
-        ptx::prefetch_tmap(&tmB);
+    // Setup without a block-wide barrier so the producers issue their first
+    // loads while TMEM is being allocated: warp 0 initialises the mbarriers and
+    // releases warp 3 (named barrier 2); warps 1, 2, 4-7 wait on named barrier 3
+    // for both the barrier init (warp 0 arrives) and the TMEM allocation (warp 2).
+    if (warp == 0) {
+        if (lane == 0) {
+            ptx::prefetch_tmap(&tmA);
+            ptx::prefetch_tmap(&tmB);
+            for (int i = 0; i < p.a_stages; ++i) {
+                ptx::mbar_init(&afull[i], 1);
+                ptx::mbar_init(&aempty[i], 1);
+            }
+            for (int i = 0; i < p.b_stages; ++i) {
+                ptx::mbar_init(&bfull[i], 1);
+                ptx::mbar_init(&bempty[i], 1);
+            }
+            for (int i = 0; i < 2; ++i) {
+                ptx::mbar_init(&tfull[i], 1);
+                ptx::mbar_init(&tempty[i], 128);
+            }
+            ptx::fence_barrier_init();
+        }
+        __syncwarp();
+        asm volatile("bar.arrive 3, 224;" ::: "memory");
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+    } else if (warp == 3) {
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+    } else {
+        if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
+        ptx::tc_fence_before();
+        asm volatile("bar.sync 3, 224;" ::: "memory");
+        ptx::tc_fence_after();
     }
-    if (warp == 1 && lane == 0) {
-        for (int i = 0; i < p.a_stages; ++i) {
-            ptx::mbar_init(&afull[i], 1);
-            ptx::mbar_init(&aempty[i], 1);
-        }
-        for (int i = 0; i < p.b_stages; ++i) {
-            ptx::mbar_init(&bfull[i], 1);
-            ptx::mbar_init(&bempty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 128);
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base = (warp == 0 || warp == 3) ? 0u : *tmem_slot;
     if (threadIdx.x == 0) trace_gt(p, 1);
     ptx::pdl_wait();  // inputs of this op may come from the previous kernel
     if (threadIdx.x == 0) trace_gt(p, 2);
@@ -289,7 +302,7 @@ __global__ void __launch_bounds__(256, 1)
         {
             // ---------------- MMA issuer (single thread)
             // K-major SW128 descriptor without the start address: LBO 16 B, SBO 1 KB
-            const uint64_t dconst = ptx::smem_desc_sw128(0, 16, 1024);
+            const uint64_t dconst = ptx::smem_desc_kmajor(0, KB);
             uint32_t aq = 0, bq = 0, acc = 0, acc_ph = 0;
             int ti = 0;
             if (lane == 0) trace_ev(p, 1, ti, 0);

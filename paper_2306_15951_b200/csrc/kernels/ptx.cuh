@@ -151,6 +151,21 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
     return d;
 }
 
+// Same with a runtime/compile-time swizzle: row bytes 32 / 64 / 128 ->
+// layout type 6 / 4 / 2 (SWIZZLE_32B / 64B / 128B).
+__host__ __device__ constexpr uint32_t swizzle_layout_type(int row_bytes) {
+    return row_bytes == 128 ? 2u : (row_bytes == 64 ? 4u : 6u);
+}
+__device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t saddr, int row_bytes) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t(1) << 16;                             // LBO (unused for swizzled K-major)
+    d |= uint64_t(((8u * uint32_t(row_bytes)) >> 4) & 0x3FFFu) << 32;  // SBO: 8 rows
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(swizzle_layout_type(row_bytes)) << 61;
+    return d;
+}
+
 // Instruction descriptor (kind::f16 / kind::tf32): D fp32 [4,6)=1,
 // A fmt [7,10), B fmt [10,13) (BF16 = 1, TF32 = 2), A major [15], B major
 // [16] (0 = K, 1 = MN), N>>3 [17,23), M>>4 [24,29).
