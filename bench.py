@@ -130,50 +130,58 @@ def run_reference(args):
 
 # --------------------------------------------------------------------- clocks
 class ClockSampler:
-    """NVML samples of SM clock and throttle reasons during the timed region."""
+    """nvidia-smi sampling (every 50 ms) of SM clock and throttle reasons during
+    the timed region -- the profiling recipe's clocks line."""
 
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
-               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.01)
+        self.index = index
+        self.proc = None
+        self.out = None
 
     def __enter__(self):
-        if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        import subprocess
+        import tempfile
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.out,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        if self.nv:
-            self._stop.set()
-            self.t.join()
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
 
     def summary(self):
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            with open(self.out.name) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) < 6:
+                        continue
+                    try:
+                        sm.append(float(parts[0]))
+                        mx = float(parts[1])
+                    except ValueError:
+                        continue
+                    for nm, v in zip(names, parts[2:6]):
+                        if v.lower() in ("active", "1"):
+                            reasons.add(nm)
+            os.unlink(self.out.name)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
 
 
 # --------------------------------------------------------------------- GPU arm
@@ -222,6 +230,10 @@ class LayerBufs:
         self.g = g
         cnt = L.cks_op_counts(g)
         self.flops = 2 * cnt["zero_free_macs"]
+        # algorithmic bytes (read inputs once, write the fp32 output once)
+        xb, wb, gb = lay.N * lay.H * lay.W * lay.C * 2, lay.OC * lay.FH * lay.FW * lay.C * 2, lay.N * OH * OW * lay.OC * 2
+        self.algo_bytes = {"fwd": xb + wb + gb * 2, "deconv": gb + wb + xb * 2,
+                           "wgrad": xb + gb + wb * 2, "split": 2 * wb}
         self.cp = torch.empty(L.cks_ks_split_size(g, L.CKS_BF16) // 2, dtype=torch.bfloat16, device=device)
         self.ws = {}
         for op, code in (("fwd", L.CKS_OP_FWD), ("deconv", L.CKS_OP_DECONV), ("wgrad", L.CKS_OP_WGRAD)):
@@ -229,7 +241,8 @@ class LayerBufs:
             self.ws[op] = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
         self.launches = {
             "fwd": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD),
-            "deconv": 1 + L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True),
+            "split": 1,
+            "deconv": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True),
             "wgrad": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD),
         }
 
@@ -282,9 +295,16 @@ def run_gpu(args):
     for b, s in zip(bufs, sizes):
         b.dW = flat[off:off + s].view(b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C)
         off += s
-    ops_seq = [(i, op) for i, b in enumerate(bufs) for op in ("fwd", "deconv", "wgrad") if op in b.lay.ops]
-    flops_step = sum(bufs[i].flops for i, _ in ops_seq)
-    launches_step = sum(bufs[i].launches[op] for i, op in ops_seq)
+    ops_seq = []
+    for i, b in enumerate(bufs):
+        for op in ("fwd", "deconv", "wgrad"):
+            if op in b.lay.ops:
+                if op == "deconv":
+                    ops_seq.append((i, "split"))
+                ops_seq.append((i, "deconv_only" if op == "deconv" else op))
+    OPF = {"fwd": "fwd", "deconv_only": "deconv", "wgrad": "wgrad", "split": "split"}
+    flops_step = sum(bufs[i].flops for i, op in ops_seq if op != "split")
+    launches_step = sum(bufs[i].launches[OPF[op]] for i, op in ops_seq)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MB > 126 MB L2
 
     # ---- capture the step as one CUDA graph with event nodes between ops
@@ -292,14 +312,14 @@ def run_gpu(args):
     evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(ops_seq) + 1)]
     with torch.cuda.stream(stream):
         for i, op in ops_seq:  # eager warm-up (sets smem attributes, checks errors)
-            bufs[i].run(op, stream.cuda_stream)
+            bufs[i].run_split(stream.cuda_stream) if op == "split" else bufs[i].run(op, stream.cuda_stream)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         sp = torch.cuda.current_stream().cuda_stream
         for k, (i, op) in enumerate(ops_seq):
             evs[k].record()
-            bufs[i].run(op, sp)
+            bufs[i].run_split(sp) if op == "split" else bufs[i].run(op, sp)
         evs[-1].record()
 
     def step(sync_read=True):
@@ -403,22 +423,27 @@ def run_gpu(args):
     value = flops_step * n_gpus / (ms_per_step / 1e3) / 1e12
 
     # ---- per-op breakdown and roofline of the dominant kernel
-    fam = {"fwd": [0.0, 0], "deconv": [0.0, 0], "wgrad": [0.0, 0]}
+    fam = {"fwd": [0.0, 0], "split": [0.0, 0], "deconv": [0.0, 0], "wgrad": [0.0, 0]}
     for k, (i, op) in enumerate(ops_seq):
-        fam[op][0] += per_op_ms[k] / args.steps
-        fam[op][1] += bufs[i].flops
-    per_op = {op: {"ms": round(v[0], 5), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 2) if v[0] else None}
-              for op, v in fam.items() if v[1]}
+        f = OPF[op]
+        fam[f][0] += per_op_ms[k] / args.steps
+        fam[f][1] += bufs[i].flops if f != "split" else 0
+    per_op = {op: {"ms": round(v[0], 5), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 2) if v[1] else None}
+              for op, v in fam.items() if v[0]}
     igemm_ms, igemm_fl = fam["fwd"][0] + fam["deconv"][0], fam["fwd"][1] + fam["deconv"][1]
     if igemm_ms >= fam["wgrad"][0]:
-        kname, kms, kfl, nl = "igemm_kernel", igemm_ms, igemm_fl, sum(1 for _, op in ops_seq if op != "wgrad")
+        kname, kms, kfl, nl = "igemm_kernel", igemm_ms, igemm_fl, sum(1 for _, op in ops_seq if op in ("fwd", "deconv_only"))
     else:
         kname, kms, kfl, nl = "wgrad_kernel", fam["wgrad"][0], fam["wgrad"][1], sum(1 for _, op in ops_seq if op == "wgrad")
     peaks = load_peaks()
     achieved = kfl / (kms / 1e3) / 1e12
+    kops = ("fwd", "deconv_only") if kname == "igemm_kernel" else ("wgrad",)
+    algo_b = [bufs[i].algo_bytes[OPF[op]] for i, op in ops_seq if op in kops]
     roofline = {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 2), "peak": peaks["bf16"],
                 "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4), "traffic": load_traffic(kname),
                 "launches_per_step": nl, "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)",
+                "algorithmic_bytes_per_launch": round(sum(algo_b) / max(len(algo_b), 1)),
+                "traffic_src": "profiles/ncu_traffic.json: mean ncu dram__bytes_read+write per launch (cold-cache replay)",
                 "timing": "op-level CUDA event nodes inside the step graph (kernel + its staging kernels)"}
 
     line = {
@@ -447,7 +472,8 @@ def run_gpu(args):
     if args.layers and rank == 0:
         for k, (i, op) in enumerate(ops_seq):
             ms = per_op_ms[k] / args.steps
-            print(f"  {bufs[i].lay.name:22s} {op:6s} {ms * 1e3:9.2f} us  {bufs[i].flops / ms / 1e9:9.1f} TFLOP/s",
+            fl = bufs[i].flops if op != "split" else 0
+            print(f"  {bufs[i].lay.name:22s} {op:11s} {ms * 1e3:9.2f} us  {fl / ms / 1e9:9.1f} TFLOP/s",
                   file=sys.stderr)
     if rank == 0:
         print(json.dumps(line), flush=True)
