@@ -72,6 +72,20 @@ int debug_flags() {
     return f;
 }
 
+// fp32 output map (TMA store), 128B swizzle
+bool make_tmap4_f32(CUtensorMap* m, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
+                    const uint32_t box[4]) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+    cuuint64_t gs[3] = {strides_b[0], strides_b[1], strides_b[2]};
+    cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), gd, gs, bd, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 cks_status last_cuda() {
@@ -115,6 +129,16 @@ cks_status set_smem(K kernel, int bytes) {
     return CKS_OK;
 }
 
+FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    uint32_t l = 0;
+    while ((uint64_t(1) << l) < d) ++l;
+    f.sh = 31 + l;
+    f.m = uint32_t(((uint64_t(1) << f.sh) + d - 1) / d);
+    return f;
+}
+
 void fill_axis(KAxis& k, const std::vector<KRow>& rows) {
     memset(&k, 0, sizeof(k));
     for (size_t i = 0; i < rows.size(); ++i) {
@@ -135,36 +159,36 @@ bool rows_ok(const std::vector<KRow>& rows) {
 
 // ------------------------------------------------------------------ launchers
 template <int BN, bool TF, int KB>
-cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
-                          cudaStream_t st) {
+cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const IgemmParams& p,
+                          int smem, cudaStream_t st) {
     auto kern = igemm_kernel<BN, TF, KB>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
-    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, a, b, p);
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, a, b, y, p);
 }
 
 template <bool TF, int KB>
-cks_status launch_igemm_kb(int BN, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p, int smem,
-                           cudaStream_t st) {
+cks_status launch_igemm_kb(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y,
+                           const IgemmParams& p, int smem, cudaStream_t st) {
     switch (BN) {
-        case 32: return launch_igemm_t<32, TF, KB>(a, b, p, smem, st);
-        case 64: return launch_igemm_t<64, TF, KB>(a, b, p, smem, st);
-        case 128: return launch_igemm_t<128, TF, KB>(a, b, p, smem, st);
+        case 32: return launch_igemm_t<32, TF, KB>(a, b, y, p, smem, st);
+        case 64: return launch_igemm_t<64, TF, KB>(a, b, y, p, smem, st);
+        case 128: return launch_igemm_t<128, TF, KB>(a, b, y, p, smem, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
 
-cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const IgemmParams& p,
-                        int smem, cudaStream_t st) {
+cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y,
+                        const IgemmParams& p, int smem, cudaStream_t st) {
     if (tf32) {
-        if (KB == 32) return launch_igemm_kb<true, 32>(BN, a, b, p, smem, st);
-        if (KB == 64) return launch_igemm_kb<true, 64>(BN, a, b, p, smem, st);
-        return launch_igemm_kb<true, 128>(BN, a, b, p, smem, st);
+        if (KB == 32) return launch_igemm_kb<true, 32>(BN, a, b, y, p, smem, st);
+        if (KB == 64) return launch_igemm_kb<true, 64>(BN, a, b, y, p, smem, st);
+        return launch_igemm_kb<true, 128>(BN, a, b, y, p, smem, st);
     }
-    if (KB == 32) return launch_igemm_kb<false, 32>(BN, a, b, p, smem, st);
-    if (KB == 64) return launch_igemm_kb<false, 64>(BN, a, b, p, smem, st);
-    return launch_igemm_kb<false, 128>(BN, a, b, p, smem, st);
+    if (KB == 32) return launch_igemm_kb<false, 32>(BN, a, b, y, p, smem, st);
+    if (KB == 64) return launch_igemm_kb<false, 64>(BN, a, b, y, p, smem, st);
+    return launch_igemm_kb<false, 128>(BN, a, b, y, p, smem, st);
 }
 
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
@@ -206,6 +230,11 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.out_W = out_W;
     p.out_C = out_C;
     p.zsplit = cfg.Z;
+    p.fd_z = make_fastdiv(uint32_t(cfg.Z));
+    p.fd_nbs = make_fastdiv(uint32_t(cfg.nbs));
+    p.fd_nblk = make_fastdiv(uint32_t(cfg.nblk));
+    p.fd_wb = make_fastdiv(uint32_t(cfg.wblocks));
+    p.fd_kc = make_fastdiv(uint32_t(cfg.kc_blocks));
     p.num_tiles = cfg.tiles;
     p.dbg = debug_flags();
     if (const char* tp = getenv("CKS_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(strtoull(tp, nullptr, 0));
@@ -218,14 +247,27 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.unit_step = cfg.unit_step;
     p.a0_step = cfg.a0_step;
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
-    const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512;
+    const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 + int(2 * sizeof(KAxis)) + 2048;
     if (cfg.Z > 1) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
         p.sem = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + L.sem);
         if (cudaMemsetAsync(p.sem, 0, L.sem_bytes, st) != cudaSuccess) return last_cuda();
     }
-    return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, p, smem, st);
+    // output tensor map (fp32, 32 channels x 32 images boxes, 128B swizzle) for
+    // the last-tile TMA-store epilogue; needs 16-byte rows and staging room in
+    // the (then idle) A/B rings: 4 warps x PBW x BN/32 blocks of 4 KB
+    CUtensorMap ty;
+    memset(&ty, 0, sizeof(ty));
+    const int64_t stage_need = int64_t(4) * cfg.pbw * (cfg.BN / 32) * 4096;
+    const int64_t ring = int64_t(p.a_stages) * p.apos * 128 * cfg.KB + int64_t(p.b_stages) * p.b_stage_bytes;
+    if (cfg.Z == 1 && out_C % 4 == 0 && stage_need <= ring && !(debug_flags() & 32)) {
+        uint64_t d[4] = {uint64_t(out_C), uint64_t(out_W), uint64_t(out_H), uint64_t(N)};
+        uint64_t sb[3] = {uint64_t(out_C) * 4, uint64_t(out_W) * out_C * 4, uint64_t(out_H) * out_W * out_C * 4};
+        uint32_t box[4] = {32, 1, 1, 32};
+        if (make_tmap4_f32(&ty, out, d, sb, box)) p.tma_store = 1;
+    }
+    return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }
 
 template <int BN>

@@ -87,7 +87,7 @@ struct IgemmCfg {
 };
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 512;  // minus alignment and barriers
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 2048;  // minus alignment, barriers, tables, MMA programs
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
 

@@ -46,6 +46,16 @@ namespace cks {
 
 constexpr int kMaxPBW = 8;
 
+// Division by a launch constant d via a host-computed multiplier:
+// n / d = (n * m) >> sh with l = ceil(log2 d), sh = 31 + l, m = ceil(2^sh / d);
+// exact for n < 2^31 (error m*d - 2^sh < d <= 2^l, so (m*d - 2^sh) * n < 2^sh).
+struct FastDiv {
+    uint32_t m, sh, d;
+};
+__device__ __forceinline__ uint32_t fdivu(uint32_t n, const FastDiv& f) {
+    return uint32_t((uint64_t(n) * f.m) >> f.sh);
+}
+
 struct KAxis {
     int16_t a0[CKS_MAX_ROWS];   // A coordinate of tap 0
     int16_t out[CKS_MAX_ROWS];  // output coordinate
@@ -75,7 +85,9 @@ struct IgemmParams {
     int unit_step;             // consecutive pixels' tap-0 columns differ by 1 (N-merged MMAs)
     int a0_step;               // a0 of pixel j = a0 of pixel 0 + j * a0_step (T1: stride, T2: 1)
     int zsplit;
+    FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
+    int tma_store;        // last tile per CTA: stage in the idle rings, TMA-store the output
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
 };
@@ -125,23 +137,29 @@ struct Tile {
     long long out_tile;
 };
 
-__device__ __forceinline__ Tile decode_tile(long long t, const IgemmParams& p) {
+__device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p, const KAxis& ah, const KAxis& aw) {
+    // 32-bit decode (tile counts < 2^31; 64-bit div/mod is a slow software routine)
     Tile c;
-    c.z = int(t % p.zsplit);
-    t /= p.zsplit;
+    uint32_t t = uint32_t(t64);
+    uint32_t q = fdivu(t, p.fd_z);
+    c.z = int(t - q * uint32_t(p.zsplit));
+    t = q;
     c.out_tile = t;
-    c.nb = int(t % p.nbs);
-    t /= p.nbs;
-    c.nblk = int(t % p.nblk);
-    t /= p.nblk;
-    const int wb = int(t % p.wblocks);
-    c.rh = int(t / p.wblocks);
+    q = fdivu(t, p.fd_nbs);
+    c.nb = int(t - q * uint32_t(p.nbs));
+    t = q;
+    q = fdivu(t, p.fd_nblk);
+    c.nblk = int(t - q * uint32_t(p.nblk));
+    t = q;
+    q = fdivu(t, p.fd_wb);
+    const int wb = int(t - q * uint32_t(p.wblocks));
+    c.rh = int(q);
     int x = 0;
     while (x + 1 < p.nph_w && p.wb_cum[x + 1] <= wb) ++x;
     c.j0 = p.wph_off[x] + (wb - p.wb_cum[x]) * p.pbw;
     c.len = min(p.pbw, p.wph_off[x] + p.wph_cnt[x] - c.j0);
-    c.ph = p.ah.phase[c.rh] * p.phases_w + p.aw.phase[c.j0];
-    const int chs = p.ah.ts[c.rh], che = p.ah.te[c.rh];
+    c.ph = ah.phase[c.rh] * p.phases_w + aw.phase[c.j0];
+    const int chs = ah.ts[c.rh], che = ah.te[c.rh];
     c.chs = chs;
     int lo = 1 << 20, hi = -(1 << 20), plo = 1 << 20, phi = -(1 << 20);
 #pragma unroll
@@ -150,9 +168,9 @@ __device__ __forceinline__ Tile decode_tile(long long t, const IgemmParams& p) {
         c.ts[j] = 0;
         c.te[j] = 0;
         if (j < c.len) {
-            c.a0[j] = p.aw.a0[c.j0 + j];
-            c.ts[j] = p.aw.ts[c.j0 + j];
-            c.te[j] = p.aw.te[c.j0 + j];
+            c.a0[j] = aw.a0[c.j0 + j];
+            c.ts[j] = aw.ts[c.j0 + j];
+            c.te[j] = aw.te[c.j0 + j];
             if (c.te[j] > c.ts[j]) {
                 lo = min(lo, c.ts[j]);
                 hi = max(hi, c.te[j]);
@@ -167,8 +185,8 @@ __device__ __forceinline__ Tile decode_tile(long long t, const IgemmParams& p) {
     c.pos_lo = empty ? 0 : plo;
     c.pos_hi = empty ? 0 : phi;
     const int rs = empty ? 0 : (che - chs) * p.kc_blocks;
-    c.rs0 = int((long long)rs * c.z / p.zsplit);
-    c.rs1 = int((long long)rs * (c.z + 1) / p.zsplit);
+    c.rs0 = p.zsplit == 1 ? 0 : int(fdivu(uint32_t(rs) * uint32_t(c.z), p.fd_z));
+    c.rs1 = p.zsplit == 1 ? rs : int(fdivu(uint32_t(rs) * uint32_t(c.z + 1), p.fd_z));
     c.rot = c.rs1 > c.rs0 ? int(blockIdx.x % unsigned(c.rs1 - c.rs0)) : 0;
     return c;
 }
@@ -194,7 +212,7 @@ __device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
 template <int BN, bool kTF32, int KB>
 __global__ void __launch_bounds__(256, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ IgemmParams p) {
+                 const __grid_constant__ CUtensorMap tmY, const __grid_constant__ IgemmParams p) {
     using S = IgemmShape<BN, kTF32, KB>;
     extern __shared__ uint8_t smem_raw[];
     // 1 KB alignment by offset arithmetic (keeps the shared address space visible to the compiler)
@@ -212,44 +230,41 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
     const uint32_t tmem_cols = 512;
+    // per-axis plan tables copied to smem once (one parallel pass of independent
+    // constant loads instead of dependent cold loads in every role's decode)
+    KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
+    int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));  // 2 x 64 entries
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&p.ah);
+        uint4* dst = reinterpret_cast<uint4*>(tab);
+        for (int i = threadIdx.x; i < int(2 * sizeof(KAxis) / 16); i += blockDim.x) dst[i] = src[i];
+    }
 
     if (threadIdx.x == 0) trace_gt(p, 0);
     ptx::pdl_launch_dependents();
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-    // Setup without a block-wide barrier so the producers issue their first
-    // loads while TMEM is being allocated: warp 0 initialises the mbarriers and
-    // releases warp 3 (named barrier 2); warps 1, 2, 4-7 wait on named barrier 3
-    // for both the barrier init (warp 0 arrives) and the TMEM allocation (warp 2).
-    if (warp == 0) {
-        if (lane == 0) {
-            ptx::prefetch_tmap(&tmA);
-            ptx::prefetch_tmap(&tmB);
-            for (int i = 0; i < p.a_stages; ++i) {
-                ptx::mbar_init(&afull[i], 1);
-                ptx::mbar_init(&aempty[i], 1);
-            }
-            for (int i = 0; i < p.b_stages; ++i) {
-                ptx::mbar_init(&bfull[i], 1);
-                ptx::mbar_init(&bempty[i], 1);
-            }
-            for (int i = 0; i < 2; ++i) {
-                ptx::mbar_init(&tfull[i], 1);
-                ptx::mbar_init(&tempty[i], 128);
-            }
-            ptx::fence_barrier_init();
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int i = 0; i < p.a_stages; ++i) {
+            ptx::mbar_init(&afull[i], 1);
+            ptx::mbar_init(&aempty[i], 1);
         }
-        __syncwarp();
-        asm volatile("bar.arrive 3, 224;" ::: "memory");
-        asm volatile("bar.sync 2, 64;" ::: "memory");
-    } else if (warp == 3) {
-        asm volatile("bar.sync 2, 64;" ::: "memory");
-    } else {
-        if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
-        ptx::tc_fence_before();
-        asm volatile("bar.sync 3, 224;" ::: "memory");
-        ptx::tc_fence_after();
+        for (int i = 0; i < p.b_stages; ++i) {
+            ptx::mbar_init(&bfull[i], 1);
+            ptx::mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tfull[i], 1);
+            ptx::mbar_init(&tempty[i], 128);
+        }
+        ptx::fence_barrier_init();
     }
-    const uint32_t tmem_base = (warp == 0 || warp == 3) ? 0u : *tmem_slot;
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) trace_gt(p, 1);
     ptx::pdl_wait();  // inputs of this op may come from the previous kernel
     if (threadIdx.x == 0) trace_gt(p, 2);
@@ -266,11 +281,12 @@ __global__ void __launch_bounds__(256, 1)
         if (lane == 0) trace_ev(p, trole, ti, 0);
         const uint32_t btx = uint32_t(p.ntap * S::TILE_B);
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const Tile c = decode_tile(t, p);
-            const int a0h = p.ah.a0[c.rh];
+            const Tile c = decode_tile(t, p, tab[0], tab[1]);
+            const int a0h = tab[0].a0[c.rh];
             for (int ri = c.rs0; ri < c.rs1; ++ri) {
                 const int r = row_step(c, ri);
-                const int ch = c.chs + r / p.kc_blocks, kc = r % p.kc_blocks;
+                const int rq = int(fdivu(uint32_t(r), p.fd_kc));
+                const int ch = c.chs + rq, kc = r - rq * p.kc_blocks;
                 if (is_b) {
                     const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
                     ptx::mbar_wait(&bempty[bs], bph ^ 1);
@@ -307,34 +323,25 @@ __global__ void __launch_bounds__(256, 1)
             int ti = 0;
             if (lane == 0) trace_ev(p, 1, ti, 0);
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const Tile c = decode_tile(t, p);
+                const Tile c = decode_tile(t, p, tab[0], tab[1]);
                 ptx::mbar_wait(&tempty[acc], acc_ph ^ 1);
                 if (lane == 0) trace_ev(p, 1, ti, 3);
                 ptx::tc_fence_after();
                 const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BN);
-                uint32_t started = 0;
-                for (int ri = c.rs0; ri < c.rs1; ++ri) {
-                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
-                    ptx::mbar_wait(&bfull[bs], bph);
-                    if (lane == 0) trace_ev(p, 1, ti, 1);
-                    if (lane == 0 && ri == c.rs0 && t == blockIdx.x) trace_gt(p, 3);
-                    const uint32_t b_addr = ptx::smem_u32(bbuf + bs * p.b_stage_bytes);
-                    for (int iw0 = c.pos_lo; iw0 < c.pos_hi; iw0 += p.apos) {
-                        const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
-                        ++aq;
-                        ptx::mbar_wait(&afull[as], aph);
-                        if (lane == 0) trace_ev(p, 1, ti, 2);
-                        ptx::tc_fence_after();
-                        for (int qq = 0; qq < p.apos; ++qq) {
-                            const int iw = iw0 + qq;
+                // ---- MMA program of this tile, built once: entry = one MMA group
+                // (A slot, column in slot, first accumulator column, tap of the
+                // group's first B tile, N, accumulate flag).  List 0 serves the first
+                // row step (groups split by accumulate state), list 1 the others.
+                int np0 = 0, np1 = 0;
+                {
+                    uint32_t started = 0;
+#pragma unroll 1
+                    for (int li = 0; li < 2; ++li) {
+                        if (li == 1) started = 0xFFu;
+                        int n = 0;
+                        for (int qa = 0; c.pos_lo + qa < c.pos_hi; ++qa) {
+                            const int iw = c.pos_lo + qa;
                             uint32_t m = pos_mask(c, iw);
-                            if (!m) continue;  // padding / unused column: never multiplied
-                            const uint64_t adesc =
-                                dconst | uint64_t((ptx::smem_u32(abuf + as * a_slot) + uint32_t(qq) * S::A_BYTES) >> 4);
-                            // groups of consecutive pixels with the same accumulate state; with a
-                            // unit tap-0 step, pixels jlo..jhi use taps cw_jlo, cw_jlo-1, ... which are
-                            // consecutive B tiles, and their accumulators (reversed TMEM order) are
-                            // consecutive columns: one MMA of N = cnt*BN covers the group
                             while (m) {
                                 const int jlo = __ffs(m) - 1;
                                 const uint32_t st0 = (started >> jlo) & 1u;
@@ -345,21 +352,54 @@ __global__ void __launch_bounds__(256, 1)
                                         ++cnt;
                                 }
                                 const int jhi = jlo + cnt - 1;
-                                const uint32_t d = dbase + uint32_t((p.pbw - 1 - jhi) * BN);
-                                const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);  // smallest tap of the group
-                                const uint64_t bdesc = dconst | uint64_t((b_addr + uint32_t(cw_lo * S::TILE_B)) >> 4);
-                                const uint32_t idesc = ptx::instr_desc(128, uint32_t(cnt * BN), kTF32, false, false);
-                                if (!(p.dbg & 2) && ptx::elect_one()) {
-#pragma unroll
-                                    for (int kk = 0; kk < S::BK / S::UK; ++kk)
-                                        ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
-                                                           kk ? 1u : st0);
-                                }
-                                __syncwarp();
+                                const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);
+                                if (lane == 0)
+                                    prog[li * 64 + n] = make_int4(qa / p.apos, qa % p.apos, (p.pbw - 1 - jhi) * BN,
+                                                                  cw_lo | (cnt << 8) | (int(st0) << 16));
+                                ++n;
                                 const uint32_t gm = ((1u << cnt) - 1u) << jlo;
                                 started |= gm;
                                 m &= ~gm;
                             }
+                        }
+                        if (li == 0) np0 = n; else np1 = n;
+                    }
+                }
+                __syncwarp();
+                const uint32_t idesc0 = ptx::instr_desc(128, 0, kTF32, false, false);
+                bool first = true;
+                for (int ri = c.rs0; ri < c.rs1; ++ri) {
+                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
+                    ptx::mbar_wait(&bfull[bs], bph);
+                    if (lane == 0) trace_ev(p, 1, ti, 1);
+                    const uint64_t bdesc0 = dconst | uint64_t(ptx::smem_u32(bbuf + bs * p.b_stage_bytes) >> 4);
+                    const int4* pl = prog + (first ? 0 : 64);
+                    const int np = first ? np0 : np1;
+                    first = false;
+                    int e = 0;
+                    for (int k = 0; c.pos_lo + k * p.apos < c.pos_hi; ++k) {
+                        const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
+                        ++aq;
+                        ptx::mbar_wait(&afull[as], aph);
+                        if (lane == 0) trace_ev(p, 1, ti, 2);
+                        ptx::tc_fence_after();
+                        const uint64_t aslot = dconst | uint64_t(ptx::smem_u32(abuf + as * a_slot) >> 4);
+                        for (; e < np; ++e) {
+                            const int4 en = pl[e];
+                            if (en.x != k) break;
+                            const uint64_t adesc = aslot + uint64_t(uint32_t(en.y) * (S::A_BYTES >> 4));
+                            const uint64_t bdesc = bdesc0 + uint64_t(uint32_t(en.w & 0xFF) * (S::TILE_B >> 4));
+                            const uint32_t cnt = uint32_t(en.w >> 8) & 0xFFu;
+                            const uint32_t idesc = idesc0 | (((cnt * BN) >> 3) << 17);
+                            const uint32_t d = dbase + uint32_t(en.z);
+                            const uint32_t acc0 = uint32_t(en.w >> 16) & 1u;
+                            if (!(p.dbg & 2) && ptx::elect_one()) {
+#pragma unroll
+                                for (int kk = 0; kk < S::BK / S::UK; ++kk)
+                                    ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
+                                                       kk ? 1u : acc0);
+                            }
+                            __syncwarp();
                         }
                         if (ptx::elect_one()) ptx::mma_commit(&aempty[as]);  // A slot free when these MMAs finish
                         __syncwarp();
@@ -392,7 +432,7 @@ __global__ void __launch_bounds__(256, 1)
         int ti = 0;
         if (et == 0) trace_ev(p, 2, ti, 0);
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const Tile c = decode_tile(t, p);
+            const Tile c = decode_tile(t, p, tab[0], tab[1]);
             ptx::mbar_wait(&tfull[acc], acc_ph);
             if (et == 0) trace_ev(p, 2, ti, 1);
             ptx::tc_fence_after();
@@ -401,15 +441,57 @@ __global__ void __launch_bounds__(256, 1)
             const int cbase = c.nb * BN;
             const int cvalid = min(BN, p.out_C - cbase);
             const bool any = c.rs1 > c.rs0;
+            // the CTA's last tile: the smem rings are idle (all MMAs done), so stage
+            // 32x32 fp32 blocks there (128B swizzle) and write full lines by TMA store
+            if (p.tma_store && !split && t + gridDim.x >= p.num_tiles && !(p.dbg & 1)) {
+                uint8_t* stg = smem + sub * uint32_t(c.len * (BN / 32)) * 4096u;
+                int k = 0;
+#pragma unroll 1
+                for (int j = 0; j < c.len; ++j) {
+                    const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32, ++k) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
+                                           c0, r);
+                        ptx::tmem_ld_wait();
+                        if (c0 >= cvalid) continue;
+                        float* blk = reinterpret_cast<float*>(stg + k * 4096);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 v = live ? make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                                __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                            *reinterpret_cast<float4*>(blk + lane * 32 + ((q ^ (lane & 7)) << 2)) = v;
+                        }
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (ptx::elect_one()) {
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], tab[0].out[c.rh], nrow0);
+                            ptx::bulk_commit();
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (ptx::elect_one()) ptx::bulk_wait_read0();  // smem must outlive the TMA reads
+                __syncwarp();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+                if (++acc == uint32_t(p.acc_stages)) {
+                    acc = 0;
+                    acc_ph ^= 1;
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int j = 0; j < c.len; ++j) {
-                const bool live = any && (p.aw.te[c.j0 + j] > p.aw.ts[c.j0 + j]);
+                const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
                 float* dst = nullptr;
                 if (split)  // column group q = (j*BN + c)/4 of row `row`
                     dst = p.part + ((c.out_tile * p.zsplit + c.z) * (pw_cols / 4) + j * (BN / 4)) * 512LL + row * 4;
                 else if (n < p.N)
-                    dst = p.out + ((static_cast<long long>(n) * p.out_H + p.ah.out[c.rh]) * p.out_W +
-                                   p.aw.out[c.j0 + j]) * p.out_C + cbase;
+                    dst = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                                   tab[1].out[c.j0 + j]) * p.out_C + cbase;
                 const int lim = split ? BN : cvalid;
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -468,8 +550,8 @@ __global__ void __launch_bounds__(256, 1)
                                          (c.out_tile * p.zsplit) * (pw_cols / 4) * 128LL + row;
                     const long long zs = (pw_cols / 4) * 128LL;
                     for (int j = 0; j < c.len; ++j) {
-                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + p.ah.out[c.rh]) * p.out_W +
-                                               p.aw.out[c.j0 + j]) * p.out_C + cbase;
+                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                                               tab[1].out[c.j0 + j]) * p.out_C + cbase;
                         for (int c0 = 0; c0 < cvalid; c0 += 32) {
                             const float4* src = base + (j * BN + c0) / 4 * 128LL;
                             float4 v[8];

@@ -48,14 +48,15 @@ struct WTile {
     int ohs, ows;
 };
 
-__device__ __forceinline__ WTile wdecode(long long t, const WgradParams& p) {
+__device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     WTile c;
-    c.nb = int(t % p.nbs);
-    t /= p.nbs;
-    c.mb = int(t % p.mblocks);
-    t /= p.mblocks;
-    c.z = int(t % p.gz);
-    t /= p.gz;
+    uint32_t t = uint32_t(t64);  // 32-bit decode (64-bit div/mod is slow)
+    c.nb = int(t % uint32_t(p.nbs));
+    t /= uint32_t(p.nbs);
+    c.mb = int(t % uint32_t(p.mblocks));
+    t /= uint32_t(p.mblocks);
+    c.z = int(t % uint32_t(p.gz));
+    t /= uint32_t(p.gz);
     const int tap = int(t);
     c.fh = tap / p.FW;
     c.fw = tap % p.FW;
@@ -63,9 +64,9 @@ __device__ __forceinline__ WTile wdecode(long long t, const WgradParams& p) {
     c.ows = p.ow_s[c.fw];
     const int hn = p.oh_e[c.fh] - c.ohs, wn = p.ow_e[c.fw] - c.ows;
     c.wn = wn;
-    const long long L = static_cast<long long>(hn) * wn * p.nblk64;
-    c.kb0 = int(L * c.z / p.gz);
-    c.kb1 = int(L * (c.z + 1) / p.gz);
+    const uint32_t L = uint32_t(hn) * uint32_t(wn) * uint32_t(p.nblk64);
+    c.kb0 = int(uint64_t(L) * uint32_t(c.z) / uint32_t(p.gz));
+    c.kb1 = int(uint64_t(L) * uint32_t(c.z + 1) / uint32_t(p.gz));
     return c;
 }
 
