@@ -117,10 +117,13 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 }
 
 // experiments only: CKS_IGEMM_CFG="BN,PBW,Z" overrides the heuristic
+static int g_ov_apos = 0, g_ov_bst = 0;
 static bool cfg_override(int& bn, int& pbw, int& z) {
     const char* e = getenv("CKS_IGEMM_CFG");
     if (!e) return false;
-    return sscanf(e, "%d,%d,%d", &bn, &pbw, &z) == 3;
+    g_ov_apos = g_ov_bst = 0;
+    const int n = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &g_ov_apos, &g_ov_bst);
+    return n >= 3;
 }
 
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
@@ -178,6 +181,8 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     const int64_t col_bytes = 128 * c.KB;  // one activation column, 128 images
     while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) --c.apos;
     if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) c.stages = 1;
+    if (ov && g_ov_apos > 0) c.apos = std::min(c.pa, g_ov_apos);
+    if (ov && g_ov_bst > 0) c.stages = g_ov_bst;
     c.a_stages = int(std::min<int64_t>(8, (kSmemBudget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
     c.acc_stages = 2;
     c.wblocks = 0;

@@ -21,9 +21,10 @@ U32 = 2.0 ** -24  # fp32 unit roundoff
 
 
 def tight_bf16(k: int) -> float:
-    """Tight bound for bf16-exact inputs: fp32 accumulation of k terms has a
-    typical relative error ~ u*sqrt(k); 8x margin."""
-    return max(1e-6, 8.0 * U32 * np.sqrt(k))
+    """Tight bound for bf16-exact inputs: fp32 (tensor-core) accumulation of k
+    terms has a typical relative error ~ u*sqrt(k); 32x margin, measured worst
+    case 12x at k = 3.2M (ResNet stem wgrad) -- DESIGN.md "Tolerances"."""
+    return max(1e-6, 32.0 * U32 * np.sqrt(k))
 
 
 def red_len(lay, op):
@@ -145,6 +146,37 @@ def test_random_geometries(torch_cuda, lay):
     check_full(torch_cuda, lay, "bf16", config=9, idx=int(lay.name[4:]))
 
 
+@pytest.mark.parametrize("lay", _rand_layers(10, 23), ids=lambda l: f"tf32-{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
+def test_random_geometries_tf32(torch_cuda, lay):
+    """TF32 (fp32 storage, TF32 tensor-core multiply) forward and KS-deconv."""
+    check_full(torch_cuda, lay, "tf32", config=8, idx=int(lay.name[4:]), ops=("fwd", "deconv"))
+
+
+def test_sharded_step_single_gpu(torch_cuda):
+    """The batch-sharded arithmetic of dist.py on one GPU: two shards run
+    sequentially, partial dW summed on the host == full-batch oracle."""
+    torch = torch_cuda
+    from paper_2306_15951_b200.dist import FlatGrads, shard_range, sharded_layer_step
+    lay = Layer("sh", 131, 64, 9, 9, 96, 3, 3, 2, 2, 1, 1)
+    a = make_layer_inputs(lay, 5, 0)
+    X, W, G = dev(torch, a["X"], "bf16"), dev(torch, a["W"], "bf16"), dev(torch, a["dY"], "bf16")
+    fg = FlatGrads([(lay.OC, lay.FH, lay.FW, lay.C)], "cuda")
+    dW = np.zeros((lay.OC, lay.FH, lay.FW, lay.C))
+    Ys, dXs = [], []
+    for r in range(2):
+        lo, hi = shard_range(lay.N, 2, r)
+        y, dx = sharded_layer_step(X[lo:hi].contiguous(), W, G[lo:hi].contiguous(), (2, 2), (1, 1), fg.views[0])
+        torch.cuda.synchronize()
+        Ys.append(y.cpu().numpy())
+        dXs.append(dx.cpu().numpy())
+        dW += fg.views[0].cpu().numpy()
+    s = (lay.sh, lay.sw, lay.ph, lay.pw)
+    check(np.concatenate(Ys), O.conv_ref(a["X"], a["W"], *s), "bf16", "sharded fwd", red_len(lay, "fwd"))
+    check(np.concatenate(dXs), O.deconv_ref(a["dY"], a["W"], lay.H, lay.W, *s), "bf16", "sharded deconv",
+          red_len(lay, "deconv"))
+    check(dW, O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, *s), "bf16", "sharded wgrad", red_len(lay, "wgrad"))
+
+
 def test_empty_phase_and_unread_rows(torch_cuda):
     # 1x1 s2 downsample: KS phase y=1 has CH=0 -> odd rows of dX must be 0 (c11);
     # I=6, F=3, s=2, p=0: row 5 of X is never read -> dX row 5 = 0 (c10).
@@ -207,7 +239,8 @@ def test_config_layers_reduced_batch(torch_cuda, cfg, i, lay):
 
 
 # ------------------------------------------ full size, sampled outputs
-@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3)][::3],
+@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3)][::2] +
+                         [c for c in _config_layers() if c[0] == 2][::3],
                          ids=lambda v: v.name if isinstance(v, Layer) else str(v))
 def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
     """Full BASELINE batch, the bench's launch configuration; the oracle
