@@ -14,6 +14,7 @@
 #include "cks_plan.h"
 #include "kernels/aux.cuh"
 #include "kernels/igemm.cuh"
+#include "kernels/narrow.cuh"
 #include "kernels/wgrad.cuh"
 
 using namespace cks;
@@ -304,6 +305,125 @@ cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* ou
                       OCp);
 }
 
+// ------------------------------------------------------------------ narrow-channel row path
+// X viewed as (W*C elements, N, H, 1): a box (JB, imgs, FH, 1) is the
+// contiguous (fw, c) run of all FH filter rows for `imgs` images, element-
+// addressed at (ow*sw - pw)*C (negative / past-the-end = padding, zero fill).
+bool make_row_xmap(CUtensorMap* m, const void* x, const cks_geom& g, uint32_t JB, uint32_t imgs) {
+    uint64_t d[4] = {uint64_t(g.W * g.C), uint64_t(g.N), uint64_t(g.H), 1};
+    uint64_t sb[3] = {uint64_t(g.H * g.W * g.C * 2), uint64_t(g.W * g.C * 2), uint64_t(g.N * g.H * g.W * g.C * 2)};
+    uint32_t box[4] = {JB, imgs, uint32_t(g.FH), 1};
+    return make_tmap4(m, CKS_BF16, x, d, sb, box, int(JB * 2));
+}
+
+template <int JB, int BN>
+cks_status launch_fwd_row_t(const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem, int grid,
+                            cudaStream_t st) {
+    auto kern = fwd_row_kernel<JB, BN>;
+    if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, ty, p);
+}
+
+template <int JB>
+cks_status launch_fwd_row_jb(int BN, const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem,
+                             int grid, cudaStream_t st) {
+    switch (BN) {
+        case 32: return launch_fwd_row_t<JB, 32>(tx, ty, p, smem, grid, st);
+        case 64: return launch_fwd_row_t<JB, 64>(tx, ty, p, smem, grid, st);
+        case 128: return launch_fwd_row_t<JB, 128>(tx, ty, p, smem, grid, st);
+        case 256: return launch_fwd_row_t<JB, 256>(tx, ty, p, smem, grid, st);
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
+cks_status run_fwd_row(const cks_geom& g, const RowCfg& rc, const void* x, const void* w, float* y, cudaStream_t st) {
+    CUtensorMap tx, ty;
+    memset(&ty, 0, sizeof(ty));
+    if (!make_row_xmap(&tx, x, g, uint32_t(rc.JB), 128)) return CKS_ERR_CUDA;
+    RowFwdParams p;
+    memset(&p, 0, sizeof(p));
+    p.w = static_cast<const uint16_t*>(w);
+    p.y = y;
+    p.N = int(g.N), p.H = int(g.H), p.W = int(g.W), p.C = int(g.C), p.OC = int(g.OC);
+    p.FH = int(g.FH), p.FW = int(g.FW), p.sh = g.sh, p.sw = g.sw, p.ph = g.ph, p.pw = g.pw;
+    p.OH = int(axis_h(g).O), p.OW = int(axis_w(g).O);
+    p.nblk = rc.nblk;
+    p.P = rc.P;
+    for (int k = 0; k < 8; ++k) p.delta[k] = rc.delta[k];
+    p.stages = rc.stages;
+    if (g.OC % 32 == 0 && !(debug_flags() & 32)) {  // TMA-store epilogue: 32 channels x 32 images boxes
+        uint64_t d[4] = {uint64_t(g.OC), uint64_t(p.OW), uint64_t(p.OH), uint64_t(g.N)};
+        uint64_t sb[3] = {uint64_t(g.OC) * 4, uint64_t(p.OW) * g.OC * 4, uint64_t(p.OH) * p.OW * g.OC * 4};
+        uint32_t box[4] = {32, 1, 1, 32};
+        if (make_tmap4_f32(&ty, y, d, sb, box)) p.tma_store = 1;
+    }
+    switch (rc.JB) {
+        case 16: return launch_fwd_row_jb<16>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+        case 32: return launch_fwd_row_jb<32>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+        case 64: return launch_fwd_row_jb<64>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
+template <int JB, int BN>
+cks_status launch_wgrad_row_t(const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p, int smem,
+                              cudaStream_t st) {
+    auto kern = wgrad_row_kernel<JB, BN>;
+    if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
+    long long grid = std::max<long long>(1, std::min<long long>(p.num_tiles, device_sms()));
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, tdy, p);
+}
+
+template <int JB>
+cks_status launch_wgrad_row_jb(int BN, const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p,
+                               int smem, cudaStream_t st) {
+    switch (BN) {
+        case 64: return launch_wgrad_row_t<JB, 64>(tx, tdy, p, smem, st);
+        case 128: return launch_wgrad_row_t<JB, 128>(tx, tdy, p, smem, st);
+        case 256: return launch_wgrad_row_t<JB, 256>(tx, tdy, p, smem, st);
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
+// per-tap Sk-dilated-V2 kernel (KB-WGRAD)
+cks_status run_wgrad_taps(const cks_geom& g, const WgradCfg& cfg, const Axis& ah, const Axis& aw,
+                          const CUtensorMap& ta, const CUtensorMap& tb, float* wout, long long part_stride,
+                          cudaStream_t st) {
+    WgradParams p;
+    memset(&p, 0, sizeof(p));
+    auto th = table_t3(ah), tw = table_t3(aw);
+    for (size_t i = 0; i < th.size(); ++i) {
+        p.oh_s[i] = int16_t(th[i].oh_s);
+        p.oh_e[i] = int16_t(th[i].oh_e);
+    }
+    for (size_t i = 0; i < tw.size(); ++i) {
+        p.ow_s[i] = int16_t(tw[i].oh_s);
+        p.ow_e[i] = int16_t(tw[i].oh_e);
+    }
+    p.out = wout;
+    p.FH = int(g.FH);
+    p.FW = int(g.FW);
+    p.sh = g.sh;
+    p.sw = g.sw;
+    p.ph = g.ph;
+    p.pw = g.pw;
+    p.N = int(g.N);
+    p.OC = int(g.OC);
+    p.C = int(g.C);
+    p.mblocks = cfg.mblocks;
+    p.nbs = cfg.nbs;
+    p.gz = cfg.gz;
+    p.nblk64 = cfg.nblk64;
+    p.num_tiles = cfg.base_tiles * cfg.gz;
+    p.part_stride = part_stride;
+    switch (cfg.BN) {
+        case 64: return launch_wgrad_t<64>(ta, tb, p, st);
+        case 128: return launch_wgrad_t<128>(ta, tb, p, st);
+        case 256: return launch_wgrad_t<256>(ta, tb, p, st);
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
 cks_status check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
     if (L.total == 0) return CKS_OK;
     if (!ws || ws_bytes < L.total) return CKS_ERR_WORKSPACE;
@@ -379,6 +499,8 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
     WsLayout L = ws_layout(*g, dt, CKS_OP_FWD, 0, false, kPlanSMs);
     if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const RowCfg rc = row_cfg_fwd(*g, dt);
+    if (rc.ok) return run_fwd_row(*g, rc, x, w, y, st);  // narrow channels: filter-row K-blocks
     const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt);
     const void* xs = x;
     const void* wsrc = w;
@@ -481,7 +603,8 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt), OCp = pad_ch(g->OC, dt);
     const void* xs = x;
     const void* dys = dy;
-    if (Cp != g->C) {
+    WgradCfg cfg = wgrad_cfg(*g, gz, kPlanSMs);
+    if (Cp != g->C && !cfg.row) {
         void* p = static_cast<uint8_t*>(ws) + L.x_pad;
         if ((s = launch_pad(dt, x, p, g->N * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
         xs = p;
@@ -491,61 +614,62 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         if ((s = launch_pad(dt, dy, p, g->N * ah.O * aw.O, int(g->OC), int(OCp), st)) != CKS_OK) return s;
         dys = p;
     }
-    WgradCfg cfg = wgrad_cfg(*g, gz, kPlanSMs);
-    CUtensorMap ta, tb;
+    CUtensorMap ta;  // dY viewed as (OC, OW, OH, N): boxes of 64 channels x 64 images
     {
         uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ah.O), uint64_t(g->N)};
         uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ah.O * aw.O * OCp * eb)};
         uint32_t box[4] = {64, 1, 1, 64};
         if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
     }
-    {
-        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
-        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
-        uint32_t box[4] = {64, 1, 1, 64};
-        if (!make_tmap4(&tb, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
-    }
-    WgradParams p;
-    memset(&p, 0, sizeof(p));
-    auto th = table_t3(ah), tw = table_t3(aw);
-    for (size_t i = 0; i < th.size(); ++i) {
-        p.oh_s[i] = int16_t(th[i].oh_s);
-        p.oh_e[i] = int16_t(th[i].oh_e);
-    }
-    for (size_t i = 0; i < tw.size(); ++i) {
-        p.ow_s[i] = int16_t(tw[i].oh_s);
-        p.ow_e[i] = int16_t(tw[i].oh_e);
-    }
-    p.out = cfg.gz > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
-    p.FH = int(g->FH);
-    p.FW = int(g->FW);
-    p.sh = g->sh;
-    p.sw = g->sw;
-    p.ph = g->ph;
-    p.pw = g->pw;
-    p.N = int(g->N);
-    p.OC = int(g->OC);
-    p.C = int(g->C);
-    p.mblocks = cfg.mblocks;
-    p.nbs = cfg.nbs;
-    p.gz = cfg.gz;
-    p.nblk64 = cfg.nblk64;
-    p.num_tiles = cfg.base_tiles * cfg.gz;
-    p.part_stride = g->OC * g->FH * g->FW * g->C;
-    switch (cfg.BN) {
-        case 64: s = launch_wgrad_t<64>(ta, tb, p, st); break;
-        case 128: s = launch_wgrad_t<128>(ta, tb, p, st); break;
-        case 256: s = launch_wgrad_t<256>(ta, tb, p, st); break;
-        default: return CKS_ERR_UNSUPPORTED;
+    float* wout = cfg.gz > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    const long long part_stride = g->OC * g->FH * g->FW * g->C;
+    if (cfg.row) {  // narrow channels: (fh, fw, c) rows as the GEMM M dimension
+        const RowCfg rc = row_cfg_wgrad(*g, dt, gz, kPlanSMs);
+        CUtensorMap tx;
+        if (!make_row_xmap(&tx, x, *g, uint32_t(rc.JB), 64)) return CKS_ERR_CUDA;
+        RowWgradParams q;
+        memset(&q, 0, sizeof(q));
+        q.out = wout;
+        q.part_stride = part_stride;
+        q.N = int(g->N), q.H = int(g->H), q.W = int(g->W), q.C = int(g->C), q.OC = int(g->OC);
+        q.FH = int(g->FH), q.FW = int(g->FW), q.sh = g->sh, q.sw = g->sw, q.ph = g->ph, q.pw = g->pw;
+        q.OH = int(ah.O), q.OW = int(aw.O);
+        q.mb = rc.mb;
+        q.nbs = rc.nbs;
+        q.P = rc.P;
+        for (int k = 0; k < 8; ++k) q.delta[k] = rc.delta[k];
+        q.gzc = rc.gzc;
+        q.nblk64 = rc.nblk;
+        q.num_tiles = int(rc.tiles);
+        q.stages = rc.stages;
+        q.a_bytes = rc.mb * 16384;
+        switch (rc.JB) {
+            case 16: s = launch_wgrad_row_jb<16>(rc.BN, tx, ta, q, rc.smem, st); break;
+            case 32: s = launch_wgrad_row_jb<32>(rc.BN, tx, ta, q, rc.smem, st); break;
+            case 64: s = launch_wgrad_row_jb<64>(rc.BN, tx, ta, q, rc.smem, st); break;
+            default: return CKS_ERR_UNSUPPORTED;
+        }
+    } else {
+        CUtensorMap tb;  // X viewed as (C, W, H, N): leaping rows ih = oh*sh + fh - ph
+        {
+            uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
+            uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
+            uint32_t box[4] = {64, 1, 1, 64};
+            if (!make_tmap4(&tb, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
+        }
+        s = run_wgrad_taps(*g, cfg, ah, aw, ta, tb, wout, part_stride, st);
     }
     if (s != CKS_OK) return s;
-    if (cfg.gz > 1) {
-        const long long n = p.part_stride;
-        unsigned blocks = unsigned(std::min<long long>((n / 4 + 255) / 256 + 1, 148LL * 8));
-        if (n % 4 == 0)
-            return launch_pdl(reduce_partials_kernel, dim3(blocks), dim3(256), 0, st, (const float*)p.out, dw, n,
-                              cfg.gz);
-        return launch_pdl(reduce_partials_scalar_kernel, dim3(blocks), dim3(256), 0, st, (const float*)p.out, dw, n,
+    if (cfg.gz > 1) {  // fixed-order aggregation of the G_Z segments
+        const long long n = part_stride;
+        const bool v4 = n % 4 == 0;
+        const long long nv = v4 ? n / 4 : n;
+        const unsigned G = unsigned(std::min(16, cfg.gz));
+        const unsigned blocks = unsigned(std::min<long long>((nv + 31) / 32, 148LL * 16));
+        if (v4)
+            return launch_pdl(reduce_partials_kernel<float4>, dim3(blocks), dim3(32, G), 0, st,
+                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, cfg.gz);
+        return launch_pdl(reduce_partials_kernel<float>, dim3(blocks), dim3(32, G), 0, st, (const float*)wout, dw, nv,
                           cfg.gz);
     }
     return CKS_OK;
@@ -610,9 +734,12 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     if (s != CKS_OK) return s;
     const bool cpad = pad_ch(g->C, dt) != g->C, ocpad = pad_ch(g->OC, dt) != g->OC;
     int n = 1;
-    if (op == CKS_OP_FWD) n += cpad ? 2 : 0;
+    if (op == CKS_OP_FWD) n += (cpad && !row_cfg_fwd(*g, dt).ok) ? 2 : 0;
     else if (op == CKS_OP_DECONV) n += (c_packed_given ? 0 : 1) + (ocpad ? 1 : 0);
-    else if (op == CKS_OP_WGRAD) n += (cpad ? 1 : 0) + (ocpad ? 1 : 0) + (wgrad_cfg(*g, gz, kPlanSMs).gz > 1 ? 1 : 0);
+    else if (op == CKS_OP_WGRAD) {
+        const WgradCfg c = wgrad_cfg(*g, gz, kPlanSMs);
+        n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) + (c.gz > 1 ? 1 : 0);
+    }
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;
     return CKS_OK;

@@ -223,8 +223,97 @@ IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
 // bounds it above by the SM count.  Here: enough segments that the
 // taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
 // with at least 4 K-blocks (256 images*positions) per segment.
+// Column classes: the (fw, c) run of output column ow starts at element
+// (ow*sw - pw)*C; TMA needs 16-byte (8-element) aligned box origins, so the
+// box starts delta = start mod 8 elements early; delta has period
+// P = 8 / gcd(sw*C, 8) in ow.
+static void row_classes(const cks_geom& g, RowCfg& c) {
+    int64_t q = (int64_t(g.sw) * g.C) % 8, a = 8;
+    while (q) { int64_t t = a % q; a = q; q = t; }  // gcd(sw*C, 8)
+    c.P = int(8 / a);
+    for (int k = 0; k < c.P; ++k) c.delta[k] = int(fmod_pos((int64_t(k) * g.sw - g.pw) * g.C, 8));
+}
+
+static bool row_setup(const cks_geom& g, cks_dtype dt, RowCfg& c) {
+    if (dt != CKS_BF16 || g.C > 16) return false;
+    if ((g.W * g.C * 2) % 16 != 0) return false;  // TMA row pitch
+    row_classes(g, c);
+    int dmax = 0;
+    for (int k = 0; k < c.P; ++k) dmax = std::max(dmax, c.delta[k]);
+    const int64_t jn = g.FW * g.C + dmax;
+    c.JB = jn <= 16 ? 16 : (jn <= 32 ? 32 : (jn <= 64 ? 64 : 0));
+    return c.JB != 0;
+}
+
+// Narrow fwd: tile = output pixel x 128 images x all OC; W rows resident.
+RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
+    RowCfg c;
+    if (!row_setup(g, dt, c) || g.OC > 256) return c;
+    c.BN = 32;
+    while (c.BN < g.OC) c.BN *= 2;
+    const int wbytes = int((g.FH * c.BN * c.JB * 2 + 1023) / 1024 * 1024);
+    const int sbytes = int((g.FH * 128 * c.JB * 2 + 1023) / 1024 * 1024);
+    const int staging = 4 * 2 * 4096;
+    const int budget = 227 * 1024 - 1024 - 256;
+    c.stages = std::min(8, (budget - wbytes - staging) / sbytes);
+    if (c.stages < 2) return c;
+    c.smem = 1024 + wbytes + c.stages * sbytes + staging + 256;
+    c.nblk = int((g.N + 127) / 128);
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph), OW = out_extent(g.W, g.FW, g.sw, g.pw);
+    c.tiles = OH * OW * c.nblk;
+    const int64_t per_class = OH * ((OW + c.P - 1) / c.P) * c.nblk;
+    c.grid = int(c.P * std::max<int64_t>(1, std::min<int64_t>(148 / c.P, per_class)));
+    c.ok = true;
+    return c;
+}
+
+// Narrow wgrad: M = (fh, j) rows, 128/JB filter rows per M-block; N = OC
+// block; K = (oh, ow, 64 images) of one column class, split into segments;
+// all P * gzc segments are G_Z map-reduce partials.
+RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+    RowCfg c;
+    if (!row_setup(g, dt, c)) return c;
+    const int R = 128 / c.JB;
+    c.mb = int((g.FH + R - 1) / R);
+    if (c.mb > 4) return c;
+    const int cap = 256 / c.mb;  // TMEM: mb accumulators of BN columns
+    c.BN = 64;
+    while (c.BN < pad_ch(g.OC, dt) && c.BN * 2 <= cap) c.BN *= 2;
+    if (c.BN > cap) return c;
+    c.nbs = int((pad_ch(g.OC, dt) + c.BN - 1) / c.BN);
+    c.nblk = int((g.N + 63) / 64);
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph), OW = out_extent(g.W, g.FW, g.sw, g.pw);
+    const int64_t Lk = OH * ((OW + c.P - 1) / c.P) * c.nblk;  // k-blocks of the largest class
+    if (gz_req > 0) {
+        c.gzc = int((gz_req + c.P - 1) / c.P);
+    } else {
+        int64_t want = std::max<int64_t>(1, num_sms / (int64_t(c.nbs) * c.P));
+        c.gzc = int(std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(Lk / 8, 1))));
+    }
+    c.gz = c.P * c.gzc;
+    const int stage = c.mb * 16384 + c.BN * 128;
+    c.stages = std::min(8, (227 * 1024 - 2048) / stage);
+    if (c.stages < 2) return c;
+    c.smem = 1024 + c.stages * stage + 256;
+    c.tiles = int64_t(c.nbs) * c.gz;
+    c.grid = int(std::min<int64_t>(c.tiles, num_sms));
+    c.ok = true;
+    return c;
+}
+
 WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms) {
     WgradCfg c;
+    RowCfg rc = row_cfg_wgrad(g, CKS_BF16, gz_req, num_sms);
+    if (rc.ok) {
+        c.row = true;
+        c.BN = rc.BN;
+        c.nbs = rc.nbs;
+        c.mblocks = rc.mb;
+        c.nblk64 = rc.nblk;
+        c.gz = rc.gz;
+        c.base_tiles = rc.nbs;
+        return c;
+    }
     c.mblocks = int((g.OC + 127) / 128);
     c.BN = g.C <= 64 ? 64 : (g.C <= 128 ? 128 : 256);
     c.nbs = int((g.C + c.BN - 1) / c.BN);
@@ -268,17 +357,19 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
         sz = bytes;
         off += align256(bytes);
     };
-    if (op == CKS_OP_FWD || op == CKS_OP_WGRAD) {
+    const bool row = (op == CKS_OP_FWD && row_cfg_fwd(g, dt).ok) ||
+                     (op == CKS_OP_WGRAD && dt == CKS_BF16 && wgrad_cfg(g, gz, num_sms).row);
+    if ((op == CKS_OP_FWD || op == CKS_OP_WGRAD) && !row) {  // the row path reads X unpadded
         if (Cp != g.C) take(size_t(g.N) * g.H * g.W * Cp * eb, L.x_pad, L.x_pad_bytes);
     }
-    if (op == CKS_OP_FWD) {
+    if (op == CKS_OP_FWD && !row) {
         if (Cp != g.C) take(size_t(g.OC) * g.FH * g.FW * Cp * eb, L.w_pad, L.w_pad_bytes);
     }
     if (op == CKS_OP_DECONV || op == CKS_OP_WGRAD) {
         if (OCp != g.OC) take(size_t(g.N) * OH * OW * OCp * eb, L.dy_pad, L.dy_pad_bytes);
     }
     if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
-    if (op == CKS_OP_FWD || op == CKS_OP_DECONV) {
+    if ((op == CKS_OP_FWD && !row) || op == CKS_OP_DECONV) {
         IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
         if (c.Z > 1) {
             take(size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4, L.partial, L.partial_bytes);

@@ -91,9 +91,29 @@ constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 2048;  // minus ali
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
 
+// Narrow-channel row path (kernels/narrow.cuh): one filter row's contiguous
+// (fw, c) run is one K-block of JB elements.  Eligible for bf16 with
+// FW*C <= 64, C <= 16 and 16-byte X row pitch (W*C*2 % 16 == 0).
+struct RowCfg {
+    bool ok = false;
+    int JB = 0;          // K-block / M-atom width in elements: 16, 32, 64
+    int BN = 0;          // OC tile
+    int stages = 0;      // pipeline depth
+    int smem = 0;        // dynamic shared memory bytes
+    int mb = 1, nbs = 1, gz = 1, nblk = 1;  // wgrad: M-blocks, OC blocks, G_Z (total), 64-image blocks
+    int P = 1;           // column classes of equal run alignment delta
+    int delta[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int gzc = 1;         // wgrad: segments per class (gz = P * gzc)
+    int grid = 1;        // CTAs (a multiple of P for the fwd kernel)
+    int64_t tiles = 0;
+};
+RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt);
+RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
+
 struct WgradCfg {
     int BN, nbs, mblocks, nblk64, gz;
     int64_t base_tiles;
+    bool row = false;  // narrow-channel row kernel
 };
 WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms);
 

@@ -63,37 +63,45 @@ __global__ void pad_channels_kernel(const T* __restrict__ src, T* __restrict__ d
     }
 }
 
-// out[i] = sum_{z = 0..gz-1} part[z][i], fixed order z = 0, 1, ... (deterministic).
-__global__ void reduce_partials_kernel(const float* __restrict__ part, float* __restrict__ out, long long n, int gz) {
-    ptx::pdl_launch_dependents();
-    ptx::pdl_wait();
-    const long long n4 = n / 4;
-    const float4* p4 = reinterpret_cast<const float4*>(part);
-    float4* o4 = reinterpret_cast<float4*>(out);
-    const long long s4 = n / 4;  // partial stride in float4 (n % 4 == 0 on this path)
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float4 a = p4[i];
-        for (int z = 1; z < gz; ++z) {
-            const float4 b = p4[z * s4 + i];
-            a.x += b.x;
-            a.y += b.y;
-            a.z += b.z;
-            a.w += b.w;
-        }
-        o4[i] = a;
-    }
-}
+// out[i] = sum_{z = 0..gz-1} part[z][i] with a FIXED association
+// (deterministic): z-group g = threadIdx.y sums z = g, g+G, g+2G, ... in
+// increasing z, then the G group sums are added in order g = 0..G-1.
+// blockDim = (32, G); one block covers 32 vector elements.
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float vadd(float a, float b) { return a + b; }
+template <typename V>
+__device__ __forceinline__ V vzero();
+template <>
+__device__ __forceinline__ float4 vzero<float4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+template <>
+__device__ __forceinline__ float vzero<float>() { return 0.f; }
 
-__global__ void reduce_partials_scalar_kernel(const float* __restrict__ part, float* __restrict__ out, long long n,
-                                              int gz) {
+template <typename V>
+__global__ void reduce_partials_kernel(const V* __restrict__ part, V* __restrict__ out, long long nv, int gz) {
+    __shared__ V acc[16][32];
     ptx::pdl_launch_dependents();
     ptx::pdl_wait();
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float a = part[i];
-        for (int z = 1; z < gz; ++z) a += part[z * n + i];
-        out[i] = a;
+    const int G = int(blockDim.y), g = int(threadIdx.y), x = int(threadIdx.x);
+    for (long long i0 = blockIdx.x * 32LL; i0 < nv; i0 += gridDim.x * 32LL) {
+        const long long i = i0 + x;
+        V a = vzero<V>();
+        if (i < nv) {
+            int z = g;
+            for (; z + 3 * G < gz; z += 4 * G) {  // 4 independent loads in flight
+                const V v0 = part[z * nv + i], v1 = part[(z + G) * nv + i];
+                const V v2 = part[(z + 2 * G) * nv + i], v3 = part[(z + 3 * G) * nv + i];
+                a = vadd(vadd(vadd(vadd(a, v0), v1), v2), v3);
+            }
+            for (; z < gz; z += G) a = vadd(a, part[z * nv + i]);
+        }
+        acc[g][x] = a;
+        __syncthreads();
+        if (g == 0 && i < nv) {
+            V r = acc[0][x];
+            for (int q = 1; q < G; ++q) r = vadd(r, acc[q][x]);
+            out[i] = r;
+        }
+        __syncthreads();
     }
 }
 

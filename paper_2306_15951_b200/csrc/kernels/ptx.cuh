@@ -93,6 +93,7 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, const void* s
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -178,6 +179,26 @@ __device__ __forceinline__ uint64_t smem_desc_kmajor(uint32_t saddr, int row_byt
     d |= uint64_t(1) << 46;
     d |= uint64_t(swizzle_layout_type(row_bytes)) << 61;
     return d;
+}
+
+// MN-major swizzled operand: LBO = byte stride between swizzle atoms along
+// M/N (an atom spans row_bytes of the MN axis), SBO = byte stride between
+// 8-row groups along K.
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo, int row_bytes) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(swizzle_layout_type(row_bytes)) << 61;
+    return d;
+}
+
+// Byte offset of a 16-byte chunk under the TMA/UMMA swizzle of `row_bytes`
+// wide rows (Swizzle<B,4,3>: address bits [4,4+B) ^= bits [7,7+B)), for an
+// offset relative to a 1024-byte aligned base.
+__host__ __device__ constexpr uint32_t swz(uint32_t off, int row_bytes) {
+    return off ^ (((off >> 7) & (row_bytes == 128 ? 7u : (row_bytes == 64 ? 3u : 1u))) << 4);
 }
 
 // Instruction descriptor (kind::f16 / kind::tf32): D fp32 [4,6)=1,

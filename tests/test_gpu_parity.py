@@ -152,6 +152,53 @@ def test_random_geometries_tf32(torch_cuda, lay):
     check_full(torch_cuda, lay, "tf32", config=8, idx=int(lay.name[4:]), ops=("fwd", "deconv"))
 
 
+def _narrow_layers(n, seed):
+    """Narrow-channel layers (FW*C <= 64): the filter-row kernels
+    (kernels/narrow.cuh); a few have a row pitch W*C*2 that is not a multiple
+    of 16 bytes and take the padded per-tap path instead."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        C = int(rng.choice([1, 2, 3, 4, 8, 16]))
+        FW = int(rng.choice([f for f in (1, 2, 3, 4, 5, 7) if f * C <= 64]))
+        FH = int(rng.choice([1, 2, 3, 4, 5, 7]))
+        sh, sw = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        ph, pw = int(rng.integers(0, FH)), int(rng.integers(0, FW))
+        H = int(rng.integers(max(1, FH - 2 * ph), 24))
+        W = int(rng.integers(max(1, FW - 2 * pw), 24))
+        if rng.random() < 0.8:  # mostly 16-byte row pitch (row path)
+            q = 8 // np.gcd(8, C)
+            W = max(q, (W + q - 1) // q * q)
+        OC = int(rng.choice([5, 8, 32, 64, 96, 128, 200]))
+        N = int(rng.choice([1, 63, 130, 257]))
+        lay = Layer(f"narrow{len(out)}", N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+        try:
+            O.geom(**lay.geom())
+        except O.GeometryError:
+            continue
+        if N * H * W * max(C, OC) > 4e6:
+            continue
+        out.append(lay)
+    return out
+
+
+@pytest.mark.parametrize("lay", _narrow_layers(20, 5), ids=lambda l: f"{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
+def test_narrow_channel_geometries(torch_cuda, lay):
+    check_full(torch_cuda, lay, "bf16", config=7, idx=int(lay.name[6:]))
+
+
+@pytest.mark.parametrize("gz", [1, 3, 200])
+def test_narrow_wgrad_segments(torch_cuda, gz):
+    """Row-path Sk-dilated with explicit G_Z: same result for every
+    segment count, bit-identical on repeat."""
+    lay = Layer("nz", 70, 3, 20, 16, 64, 7, 7, 2, 2, 3, 3)
+    a, got = run_all(torch_cuda, lay, "bf16", config=7, idx=99, ops=("wgrad",), gz=gz)
+    _, got2 = run_all(torch_cuda, lay, "bf16", config=7, idx=99, ops=("wgrad",), gz=gz)
+    assert np.array_equal(got["wgrad"], got2["wgrad"])
+    ref = O.wgrad_ref(a["X"], a["dY"], 7, 7, 2, 2, 3, 3)
+    check(got["wgrad"], ref, "bf16", f"narrow wgrad gz={gz}", red_len(lay, "wgrad"))
+
+
 def test_sharded_step_single_gpu(torch_cuda):
     """The batch-sharded arithmetic of dist.py on one GPU: two shards run
     sequentially, partial dW summed on the host == full-batch oracle."""

@@ -108,9 +108,15 @@ def test_validation_errors():
 
 
 def test_workspace_and_launch_counts():
-    g = L.make_geom(128, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)   # I_C = 3 -> padded staging
-    assert L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) >= 128 * 32 * 32 * 8 * 2
+    g = L.make_geom(128, 3, 32, 33, 64, 3, 3, 1, 1, 1, 1)   # I_C = 3, odd row pitch -> padded staging
+    assert L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) >= 128 * 32 * 33 * 8 * 2
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 3
+    g = L.make_geom(128, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)   # narrow row path: X read unpadded
+    assert L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) == 0
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 1
+    assert L.cks_launch_count(g, L.CKS_TF32, L.CKS_OP_FWD) == 3   # TF32 keeps the per-tap path
+    gz = L.cks_choose_gz(g, L.CKS_BF16)
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + (gz > 1)
     g = L.make_geom(128, 64, 32, 32, 64, 3, 3, 2, 2, 1, 1)
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV) == 2
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True) == 1
