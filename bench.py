@@ -251,6 +251,9 @@ class LayerBufs:
 
     def run(self, op, stream_ptr):
         L, g = self.L, self.g
+        if op == "split":  # Stage1 alone
+            L.cks_ks_split(g, L.CKS_BF16, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+            return
         if op == "deconv_only":  # Stage2&3 from the already split sub-filters
             ws = self.ws["deconv"]
             L.cks_deconv2d(g, L.CKS_BF16, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),

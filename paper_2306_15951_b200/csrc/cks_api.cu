@@ -248,7 +248,9 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.unit_step = cfg.unit_step;
     p.a0_step = cfg.a0_step;
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
-    const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 + int(2 * sizeof(KAxis)) + 2048;
+    p.epi_stage = cfg.epi;
+    const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
+                     int(2 * sizeof(KAxis)) + 2048 + (cfg.epi ? kEpiStageBytes : 0);
     if (cfg.Z > 1) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
@@ -294,8 +296,8 @@ cks_status launch_pad(cks_dtype dt, const void* src, void* dst, long long rows, 
 cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* out, cudaStream_t st) {
     const int CHm = int(cdiv(g.FH, g.sh)), CWm = int(cdiv(g.FW, g.sw));
     const int OCp = int(pad_ch(g.OC, dt));
-    dim3 grid(unsigned((OCp + 31) / 32), unsigned((g.C + 31) / 32), unsigned(g.sh * g.sw * CHm * CWm));
-    dim3 block(32, 8);
+    dim3 grid(unsigned((OCp + 63) / 64), unsigned((g.C + 63) / 64), unsigned(g.sh * g.sw * CHm * CWm));
+    dim3 block(256);
     if (dt == CKS_BF16)
         return launch_pdl(ks_split_kernel<uint16_t>, grid, block, 0, st, static_cast<const uint16_t*>(w),
                           static_cast<uint16_t*>(out), int(g.OC), int(g.FH), int(g.FW), int(g.C), g.sh, g.sw, CHm, CWm,

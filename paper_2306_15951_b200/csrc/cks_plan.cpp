@@ -126,9 +126,17 @@ static bool cfg_override(int& bn, int& pbw, int& z) {
     return n >= 3;
 }
 
+bool epi_staging() {
+    const char* e = getenv("CKS_EPI_STAGE");  // experiments only
+    return !(e && atoi(e) == 0);
+}
+
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
     IgemmCfg c;
+    // coalesced-store epilogue staging only where the output rows allow 16 B vectors
+    c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
+    const int64_t budget = kSmemBudget - (c.epi ? kEpiStageBytes : 0);
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
     c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);
@@ -167,7 +175,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     for (; pbw >= 1; --pbw) {
         c.pa = int((pbw - 1) * a0_step + ntap);
         c.stage_bytes = int(ntap * c.BN * c.KB);
-        if (2 * (int64_t(c.pa) * 128 * c.KB + c.stage_bytes) <= kSmemBudget && c.pa <= 256) break;
+        if (2 * (int64_t(c.pa) * 128 * c.KB + c.stage_bytes) <= budget && c.pa <= 256) break;
     }
     if (pbw < 1) pbw = 1;
     c.pbw = pbw;
@@ -179,11 +187,11 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     c.stages = 2;
     c.apos = c.pa;
     const int64_t col_bytes = 128 * c.KB;  // one activation column, 128 images
-    while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) --c.apos;
-    if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > kSmemBudget) c.stages = 1;
+    while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > budget) --c.apos;
+    if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > budget) c.stages = 1;
     if (ov && g_ov_apos > 0) c.apos = std::min(c.pa, g_ov_apos);
     if (ov && g_ov_bst > 0) c.stages = g_ov_bst;
-    c.a_stages = int(std::min<int64_t>(8, (kSmemBudget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
+    c.a_stages = int(std::min<int64_t>(8, (budget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
     c.acc_stages = 2;
     c.wblocks = 0;
     for (auto v : wph_cnt) c.wblocks += int((v + c.pbw - 1) / c.pbw);
@@ -193,7 +201,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     c.Z = 1;
     if (c.out_tiles < 100 && rs_full >= 16) c.Z = 2;
     (void)num_sms;
-    if (ov && ov_z > 0) c.Z = ov_z;
+    if (ov && ov_z > 0) c.Z = int(std::min<int64_t>(ov_z, rs_full));
     c.tiles = c.out_tiles * c.Z;
     return c;
 }

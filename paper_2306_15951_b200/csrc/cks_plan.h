@@ -79,6 +79,7 @@ struct IgemmCfg {
     int pa = 1;         // activation positions per row step (A box)
     int stage_bytes = 0, stages = 2;  // B-row ring: bytes per row, rows in flight
     int a_stages = 8;                 // A ring (slots of apos x 16 KB)
+    int epi = 0;                      // epilogue staging buffers present
     int apos = 2;                     // activation columns per A slot
     int unit_step = 1;                // consecutive pixels' tap-0 columns differ by 1
     int a0_step = 1;                  // tap-0 column step between consecutive pixels
@@ -88,6 +89,8 @@ struct IgemmCfg {
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 2048;  // minus alignment, barriers, tables, MMA programs
+constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
+bool epi_staging();                       // coalesced-store epilogue (default on; CKS_EPI_STAGE=0 disables)
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
 

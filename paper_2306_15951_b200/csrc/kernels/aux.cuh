@@ -15,11 +15,13 @@ namespace cks {
 //   oph_y = ceil((F_H-y)/sh) - 1,
 // stored packed and K-major for the KS GEMM: out[p][ic][ch*CWm+cw][ocp].
 // Slots outside the phase extent and channels >= OC are written as zero.
-// Tile transpose through shared memory: 32 oc x 32 ic per block.
+// Per (phase, slot) this is a transpose of the (oc x ic) plane of one tap:
+// 64 x 64 tiles through shared memory, 16-byte global loads / stores when the
+// rows allow it (C % 8 == 0, OCp % 8 == 0; 2-byte element type).
 template <typename T>
-__global__ void ks_split_kernel(const T* __restrict__ W, T* __restrict__ out, int OC, int FH, int FW, int C, int sh,
-                                int sw, int CHm, int CWm, int OCp) {
-    __shared__ T tile[32][33];
+__global__ void __launch_bounds__(256) ks_split_kernel(const T* __restrict__ W, T* __restrict__ out, int OC, int FH,
+                                                       int FW, int C, int sh, int sw, int CHm, int CWm, int OCp) {
+    __shared__ T tile[64][66];
     ptx::pdl_launch_dependents();
     ptx::pdl_wait();
     const int slots = CHm * CWm;
@@ -32,20 +34,52 @@ __global__ void ks_split_kernel(const T* __restrict__ W, T* __restrict__ out, in
     const bool live = ch < CH && cw < CW;
     const int fh = y + (CH - 1 - ch) * sh;
     const int fw = x + (CW - 1 - cw) * sw;
-    const int oc0 = blockIdx.x * 32, ic0 = blockIdx.y * 32;
-    // load W[oc0+ty][fh][fw][ic0+tx] (coalesced over ic)
-    for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
-        const int oc = oc0 + ty, ic = ic0 + threadIdx.x;
-        T v = T(0);
-        if (live && oc < OC && ic < C) v = W[((static_cast<long long>(oc) * FH + fh) * FW + fw) * C + ic];
-        tile[ty][threadIdx.x] = v;
+    const int oc0 = blockIdx.x * 64, ic0 = blockIdx.y * 64;
+    const int t = threadIdx.x;
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+    const bool vec = (C % V) == 0 && (OCp % V) == 0 && sizeof(T) == 2;
+    // load W[oc0+r][fh][fw][ic0 .. ic0+63] -> tile[r][.]
+    if (vec) {
+        for (int q = t; q < 64 * (64 / V); q += 256) {
+            const int r = q / (64 / V), c = (q % (64 / V)) * V;
+            const int oc = oc0 + r, ic = ic0 + c;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (live && oc < OC && ic < C)
+                v = *reinterpret_cast<const uint4*>(W + ((static_cast<long long>(oc) * FH + fh) * FW + fw) * C + ic);
+            const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int k = 0; k < V; ++k) tile[r][c + k] = e[k];
+        }
+    } else {
+        for (int q = t; q < 64 * 64; q += 256) {
+            const int r = q / 64, c = q % 64;
+            const int oc = oc0 + r, ic = ic0 + c;
+            T v = T(0);
+            if (live && oc < OC && ic < C) v = W[((static_cast<long long>(oc) * FH + fh) * FW + fw) * C + ic];
+            tile[r][c] = v;
+        }
     }
     __syncthreads();
-    // store out[pidx][ic0+ty][slot][oc0+tx] (coalesced over oc)
-    for (int ty = threadIdx.y; ty < 32; ty += blockDim.y) {
-        const int ic = ic0 + ty, oc = oc0 + threadIdx.x;
-        if (ic < C && oc < OCp)
-            out[((static_cast<long long>(pidx) * C + ic) * slots + slot) * OCp + oc] = tile[threadIdx.x][ty];
+    // store out[pidx][ic0+r][slot][oc0 .. oc0+63] <- tile[.][r]
+    if (vec) {
+        for (int q = t; q < 64 * (64 / V); q += 256) {
+            const int r = q / (64 / V), c = (q % (64 / V)) * V;
+            const int ic = ic0 + r, oc = oc0 + c;
+            if (ic < C && oc < OCp) {
+                uint4 v;
+                T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+                for (int k = 0; k < V; ++k) e[k] = tile[c + k][r];
+                *reinterpret_cast<uint4*>(out + ((static_cast<long long>(pidx) * C + ic) * slots + slot) * OCp + oc) = v;
+            }
+        }
+    } else {
+        for (int q = t; q < 64 * 64; q += 256) {
+            const int r = q / 64, c = q % 64;
+            const int ic = ic0 + r, oc = oc0 + c;
+            if (ic < C && oc < OCp)
+                out[((static_cast<long long>(pidx) * C + ic) * slots + slot) * OCp + oc] = tile[c][r];
+        }
     }
 }
 

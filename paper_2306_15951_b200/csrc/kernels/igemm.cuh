@@ -88,6 +88,7 @@ struct IgemmParams {
     FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
     int tma_store;        // last tile per CTA: stage in the idle rings, TMA-store the output
+    int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
 };
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(256, 1)
     // constant loads instead of dependent cold loads in every role's decode)
     KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
     int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));  // 2 x 64 entries
+    float* epi = reinterpret_cast<float*>(prog + 2 * 64);  // epilogue staging (p.epi_stage): 4 x 4 KB
     {
         const uint4* src = reinterpret_cast<const uint4*>(&p.ah);
         uint4* dst = reinterpret_cast<uint4*>(tab);
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(256, 1)
         const int pw_cols = p.pbw * BN;
         const bool split = p.zsplit > 1;
         const bool vec4 = (p.out_C % 4) == 0;
+        const bool stage = !split && p.epi_stage && vec4;  // coalesced-store epilogue
         int ti = 0;
         if (et == 0) trace_ev(p, 2, ti, 0);
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -499,12 +502,35 @@ __global__ void __launch_bounds__(256, 1)
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN + c0,
                                    r);
                     ptx::tmem_ld_wait();
-                    if (dst == nullptr || c0 >= lim || (p.dbg & 1)) continue;
+                    if (c0 >= lim || (p.dbg & 1) || (dst == nullptr && !stage)) continue;  // stage: warp-uniform
                     if (!live) {
 #pragma unroll
                         for (int q = 0; q < 32; ++q) r[q] = 0u;
                     }
-                    if (split) {
+                    if (stage) {
+                        // transpose through a 128B-swizzled 32 x 32 block: 8 lanes write one
+                        // image's 32 channels (128 B, a full line) per store instruction
+                        float* blk = epi + sub * 1024;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            *reinterpret_cast<float4*>(blk + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                                make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                        __syncwarp();
+                        const int cq = int(lane & 7);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int rr = 4 * k + int(lane >> 3);
+                            const float4 v = *reinterpret_cast<const float4*>(blk + rr * 32 + ((cq ^ (rr & 7)) << 2));
+                            const int nn = nrow0 + rr;
+                            const int cc = c0 + 4 * cq;
+                            if (nn < p.N && cc < lim)
+                                *reinterpret_cast<float4*>(p.out + ((static_cast<long long>(nn) * p.out_H +
+                                                                     tab[0].out[c.rh]) * p.out_W +
+                                                                    tab[1].out[c.j0 + j]) * p.out_C + cbase + cc) = v;
+                        }
+                        __syncwarp();
+                    } else if (split) {
 #pragma unroll
                         for (int q = 0; q < 32; q += 4)
                             *reinterpret_cast<float4*>(dst + (c0 + q) / 4 * 512) =

@@ -17,7 +17,8 @@ def main():
     desc, layers = get_config(cfg)
     s = torch.cuda.current_stream()
     for idx, lay in enumerate(layers):
-        if names and lay.name not in names or op not in lay.ops:
+        base = "deconv" if op in ("split", "deconv_only") else op
+        if names and lay.name not in names or base not in lay.ops:
             continue
         b = LayerBufs(torch, lay, cfg, idx, 0, torch.device("cuda", 0))
         b.dW = torch.empty((lay.OC, lay.FH, lay.FW, lay.C), dtype=torch.float32, device="cuda")

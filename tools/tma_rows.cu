@@ -72,17 +72,23 @@ int main() {
     unsigned long long* cyc;
     cudaMalloc(&cyc, sms * 8);
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    printf("RB R T S nw  B/clk/SM\n");
-    for (int RB : {32, 64, 128})
-        for (int R : {64, 128, 256})
-            for (int T : {1, 4, 7})
-                for (int S : {4, 8, 16})
-                    for (int nw : {1, 2, 4}) {
+    printf("ctas contig RB R T S nw  B/clk/SM\n");
+    for (int ctas : {148, 64, 16})
+    for (int contig : {0, 1})
+    for (int RB : {64, 128})
+        for (int R : {128})
+            for (int T : {1, 4})
+                for (int S : {4, 8})
+                    for (int nw : {1, 2}) {
                         const int bytes = RB * R * T;
                         if (S * bytes + 1024 > 200 * 1024 || nw > S) continue;
                         CUtensorMap tm;
                         cuuint64_t dims[4] = {(cuuint64_t)W * C, (cuuint64_t)N, (cuuint64_t)H, 1};
                         cuuint64_t str[3] = {(cuuint64_t)H * W * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)N * H * W * C * 2};
+                        if (contig) {  // rows of one box contiguous: (W*C, N) with N stride = RB bytes... use a dense [H][N][RB] view
+                            dims[0] = RB / 2; dims[1] = N; dims[2] = H; dims[3] = 1;
+                            str[0] = RB; str[1] = (cuuint64_t)N * RB; str[2] = (cuuint64_t)N * H * RB;
+                        }
                         cuuint32_t box[4] = {(cuuint32_t)RB / 2, (cuuint32_t)R, (cuuint32_t)T, 1}, es[4] = {1, 1, 1, 1};
                         CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, d, dims, str, box, es,
                                          CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -91,14 +97,15 @@ int main() {
                         if (r != CUDA_SUCCESS) { printf("enc fail %d\n", r); continue; }
                         const int iters = 400000 / (S * bytes / 64) + 4;
                         const int smem = S * bytes + S * 8 + 64;
-                        bench<<<sms, 128, smem>>>(tm, bytes, S, nw, iters, W - 4, H - 8, cyc);
-                        bench<<<sms, 128, smem>>>(tm, bytes, S, nw, iters, W - 4, H - 8, cyc);
+                        const int wx = contig ? 1 : W - 4;
+                        bench<<<ctas, 128, smem>>>(tm, bytes, S, nw, iters, wx, H - 8, cyc);
+                        bench<<<ctas, 128, smem>>>(tm, bytes, S, nw, iters, wx, H - 8, cyc);
                         cudaDeviceSynchronize();
-                        std::vector<unsigned long long> h(sms);
-                        cudaMemcpy(h.data(), cyc, sms * 8, cudaMemcpyDeviceToHost);
+                        std::vector<unsigned long long> h(ctas);
+                        cudaMemcpy(h.data(), cyc, ctas * 8, cudaMemcpyDeviceToHost);
                         double mx = 0;
                         for (auto v : h) mx = v > mx ? v : mx;
-                        printf("%3d %3d %d %2d %d  %6.1f\n", RB, R, T, S, nw, (double)iters * S * bytes / mx);
+                        printf("%3d %d %3d %3d %d %2d %d  %6.1f\n", ctas, contig, RB, R, T, S, nw, (double)iters * S * bytes / mx);
                     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
