@@ -85,14 +85,19 @@ cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz
 
 /* The G_Z the library would use for this geometry with gz = 0 (P:212:
  * "G_Z can be positive related to (N_a + N_b)/N_g ... the upper-bound can be
- * decided by the number of streaming multi-processors").  Host only. */
+ * decided by the number of streaming multi-processors").  For narrow-channel
+ * bf16 layers (FW*C <= 64, C <= 16, W*C*2 a multiple of 16: the filter-row
+ * kernel) the segments are per column class and the returned G_Z, like a
+ * requested gz, is a multiple of the class count P = 8 / gcd(sw*C, 8)
+ * (a requested gz is rounded up).  Host only. */
 cks_status cks_choose_gz(const cks_geom* g, cks_dtype dt, int* gz);
 
 /* Eq (1) via ConvV2 (Alg. 1): Y[n,oh,ow,oc] = sum over the TRIMMED
  * window fh in [fh_s, fh_e), fw in [fw_s, fw_e), ic of
  * X[n, oh*sh-ph+fh, ow*sw-pw+fw, ic] * W[oc,fh,fw,ic]; padded zeros are never
- * loaded or multiplied.  x: N*H*W*C (dtype), w: OC*FH*FW*C (dtype),
- * y: N*OH*OW*OC fp32 (overwritten). */
+ * loaded or multiplied (narrow-channel bf16 layers, FW*C <= 64: trimmed in h,
+ * the w-direction padding of a filter-row run is TMA zero fill).
+ * x: N*H*W*C (dtype), w: OC*FH*FW*C (dtype), y: N*OH*OW*OC fp32 (overwritten). */
 cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y,
                           void* ws, size_t ws_bytes, void* stream);
 
