@@ -250,7 +250,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
     p.epi_stage = cfg.epi;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
-                     int(2 * sizeof(KAxis)) + 2048 + (cfg.epi ? kEpiStageBytes : 0);
+                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes : 0);
     if (cfg.Z > 1) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);

@@ -88,7 +88,7 @@ struct IgemmCfg {
 };
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 2048;  // minus alignment, barriers, tables, MMA programs
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 4160;  // minus alignment, barriers, tables, MMA programs
 constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
 bool epi_staging();                       // coalesced-store epilogue (default on; CKS_EPI_STAGE=0 disables)
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);

@@ -45,6 +45,7 @@
 namespace cks {
 
 constexpr int kMaxPBW = 8;
+constexpr int kProgSlot = 2 + 2 * 64;  // int4: header {np0, np1, rs0, rs1}, {pos_lo, pos_hi, -, -}, 2 lists
 
 // Division by a launch constant d via a host-computed multiplier:
 // n / d = (n * m) >> sh with l = ceil(log2 d), sh = 31 + l, m = ceil(2^sh / d);
@@ -228,14 +229,17 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* bempty = bfull + p.b_stages;
     uint64_t* tfull = bempty + p.b_stages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* pfull = tempty + 2;   // MMA programs built by warp 2 (double buffered)
+    uint64_t* pempty = pfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
     int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
     const uint32_t tmem_cols = 512;
     // per-axis plan tables copied to smem once (one parallel pass of independent
     // constant loads instead of dependent cold loads in every role's decode)
     KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
-    int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));  // 2 x 64 entries
-    float* epi = reinterpret_cast<float*>(prog + 2 * 64);  // epilogue staging (p.epi_stage): 4 x 4 KB
+    // 2 program slots x (2 header + 2 x 64 entries)
+    int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));
+    float* epi = reinterpret_cast<float*>(prog + 2 * kProgSlot);  // epilogue staging (p.epi_stage): 4 x 4 KB
     {
         const uint4* src = reinterpret_cast<const uint4*>(&p.ah);
         uint4* dst = reinterpret_cast<uint4*>(tab);
@@ -259,6 +263,8 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 128);
+            ptx::mbar_init(&pfull[i], 32);
+            ptx::mbar_init(&pempty[i], 32);
         }
         ptx::fence_barrier_init();
     }
@@ -293,9 +299,13 @@ __global__ void __launch_bounds__(256, 1)
                     const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
                     ptx::mbar_wait(&bempty[bs], bph ^ 1);
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&bfull[bs], btx);
-                        ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, &bfull[bs], kc * S::BK, c.nb * BN,
-                                         ch * p.slot_stride, c.ph);
+                        if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
+                            ptx::mbar_arrive(&bfull[bs]);  // experiment: B traffic removed (wrong results)
+                        } else {
+                            ptx::mbar_arrive_expect_tx(&bfull[bs], btx);
+                            ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, &bfull[bs], kc * S::BK, c.nb * BN,
+                                             ch * p.slot_stride, c.ph);
+                        }
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, trole, ti, 1);
@@ -307,9 +317,13 @@ __global__ void __launch_bounds__(256, 1)
                     ++aq;
                     ptx::mbar_wait(&aempty[as], aph ^ 1);
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
-                        ptx::tma_load_4d(abuf + as * a_slot, &tmA, &afull[as], kc * S::BK, c.nblk * 128, iw0,
-                                         a0h + ch);
+                        if ((p.dbg & 8) && aq > uint32_t(p.a_stages)) {
+                            ptx::mbar_arrive(&afull[as]);  // experiment: A traffic removed (wrong results)
+                        } else {
+                            ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
+                            ptx::tma_load_4d(abuf + as * a_slot, &tmA, &afull[as], kc * S::BK, c.nblk * 128, iw0,
+                                             a0h + ch);
+                        }
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, trole, ti, 2);
@@ -324,62 +338,30 @@ __global__ void __launch_bounds__(256, 1)
             uint32_t aq = 0, bq = 0, acc = 0, acc_ph = 0;
             int ti = 0;
             if (lane == 0) trace_ev(p, 1, ti, 0);
+            uint32_t ps = 0, pph = 0;
             for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const Tile c = decode_tile(t, p, tab[0], tab[1]);
+                ptx::mbar_wait(&pfull[ps], pph);  // program of this tile (warp 2)
+                const int4* pg = prog + ps * kProgSlot;
+                const int4 h0 = pg[0], h1 = pg[1];
+                const int np0 = h0.x, np1 = h0.y, rs0 = h0.z, rs1 = h0.w, pos_lo = h1.x, pos_hi = h1.y;
+                __syncwarp();
                 ptx::mbar_wait(&tempty[acc], acc_ph ^ 1);
                 if (lane == 0) trace_ev(p, 1, ti, 3);
                 ptx::tc_fence_after();
                 const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BN);
-                // ---- MMA program of this tile, built once: entry = one MMA group
-                // (A slot, column in slot, first accumulator column, tap of the
-                // group's first B tile, N, accumulate flag).  List 0 serves the first
-                // row step (groups split by accumulate state), list 1 the others.
-                int np0 = 0, np1 = 0;
-                {
-                    uint32_t started = 0;
-#pragma unroll 1
-                    for (int li = 0; li < 2; ++li) {
-                        if (li == 1) started = 0xFFu;
-                        int n = 0;
-                        for (int qa = 0; c.pos_lo + qa < c.pos_hi; ++qa) {
-                            const int iw = c.pos_lo + qa;
-                            uint32_t m = pos_mask(c, iw);
-                            while (m) {
-                                const int jlo = __ffs(m) - 1;
-                                const uint32_t st0 = (started >> jlo) & 1u;
-                                int cnt = 1;
-                                if (p.unit_step) {
-                                    while (jlo + cnt < kMaxPBW && ((m >> (jlo + cnt)) & 1u) &&
-                                           (((started >> (jlo + cnt)) & 1u) == st0) && (cnt + 1) * BN <= 256)
-                                        ++cnt;
-                                }
-                                const int jhi = jlo + cnt - 1;
-                                const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);
-                                if (lane == 0)
-                                    prog[li * 64 + n] = make_int4(qa / p.apos, qa % p.apos, (p.pbw - 1 - jhi) * BN,
-                                                                  cw_lo | (cnt << 8) | (int(st0) << 16));
-                                ++n;
-                                const uint32_t gm = ((1u << cnt) - 1u) << jlo;
-                                started |= gm;
-                                m &= ~gm;
-                            }
-                        }
-                        if (li == 0) np0 = n; else np1 = n;
-                    }
-                }
                 __syncwarp();
                 const uint32_t idesc0 = ptx::instr_desc(128, 0, kTF32, false, false);
                 bool first = true;
-                for (int ri = c.rs0; ri < c.rs1; ++ri) {
+                for (int ri = rs0; ri < rs1; ++ri) {
                     const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
                     ptx::mbar_wait(&bfull[bs], bph);
                     if (lane == 0) trace_ev(p, 1, ti, 1);
                     const uint64_t bdesc0 = dconst | uint64_t(ptx::smem_u32(bbuf + bs * p.b_stage_bytes) >> 4);
-                    const int4* pl = prog + (first ? 0 : 64);
+                    const int4* pl = pg + 2 + (first ? 0 : 64);
                     const int np = first ? np0 : np1;
                     first = false;
                     int e = 0;
-                    for (int k = 0; c.pos_lo + k * p.apos < c.pos_hi; ++k) {
+                    for (int k = 0; pos_lo + k * p.apos < pos_hi; ++k) {
                         const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
                         ++aq;
                         ptx::mbar_wait(&afull[as], aph);
@@ -411,12 +393,104 @@ __global__ void __launch_bounds__(256, 1)
                     __syncwarp();
                     ++bq;
                 }
+                ptx::mbar_arrive(&pempty[ps]);  // program slot consumed (all 32 lanes)
+                if (++ps == 2) {
+                    ps = 0;
+                    pph ^= 1;
+                }
                 if (lane == 0) trace_gt(p, 4);
                 if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);  // accumulators ready (immediately if no MMA)
                 __syncwarp();
                 if (++acc == uint32_t(p.acc_stages)) {
                     acc = 0;
                     acc_ph ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        // ---------------- MMA-program builder (runs ahead of the MMA warp by one tile)
+        {
+            uint32_t ps = 0, pph = 0;
+            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                const Tile c = decode_tile(t, p, tab[0], tab[1]);
+                ptx::mbar_wait(&pempty[ps], pph ^ 1);
+                int4* pg = prog + ps * kProgSlot;
+                // ---- MMA program of this tile, built by this warp ahead of the MMA warp: entry =
+                // one MMA group (A slot, column in slot, first accumulator column, tap
+                // of the group's first B tile, N, accumulate flag).  List 0 serves the
+                // first row step (groups split by accumulate state), list 1 the others.
+                // Lane = activation column; a pixel is "started" in list 0 once an
+                // earlier column used it (warp prefix-OR), entry offsets by warp scan.
+                int np0 = 0, np1 = 0;
+                {
+                    const int ncol = c.pos_hi - c.pos_lo;
+                    uint32_t carry = 0;
+#pragma unroll 1
+                    for (int base = 0; base < ncol; base += 32) {
+                        const int qa = base + int(lane);
+                        const int iw = c.pos_lo + qa;
+                        const uint32_t m = qa < ncol ? pos_mask(c, iw) : 0u;
+                        uint32_t incl = m;
+#pragma unroll
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+                            if (int(lane) >= off) incl |= v;
+                        }
+                        uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+                        if (lane == 0) excl = 0;
+                        excl |= carry;
+                        // groups of this column in list li (started state st)
+                        auto groups = [&](uint32_t started, int off, bool emit) -> int {
+                            uint32_t mm = m;
+                            int n = 0;
+                            while (mm) {
+                                const int jlo = __ffs(mm) - 1;
+                                const uint32_t st0 = (started >> jlo) & 1u;
+                                int cnt = 1;
+                                if (p.unit_step) {
+                                    while (jlo + cnt < kMaxPBW && ((mm >> (jlo + cnt)) & 1u) &&
+                                           (((started >> (jlo + cnt)) & 1u) == st0) && (cnt + 1) * BN <= 256)
+                                        ++cnt;
+                                }
+                                if (emit) {
+                                    const int jhi = jlo + cnt - 1;
+                                    const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);
+                                    pg[2 + off + n] = make_int4(qa / p.apos, qa % p.apos, (p.pbw - 1 - jhi) * BN,
+                                                              cw_lo | (cnt << 8) | (int(st0) << 16));
+                                }
+                                ++n;
+                                mm &= ~(((1u << cnt) - 1u) << jlo);
+                            }
+                            return n;
+                        };
+                        const int n0 = groups(excl, 0, false), n1 = groups(0xFFu, 0, false);
+                        int s0 = n0, s1 = n1;
+#pragma unroll
+                        for (int off = 1; off < 32; off <<= 1) {
+                            const int v0 = __shfl_up_sync(0xffffffffu, s0, off);
+                            const int v1 = __shfl_up_sync(0xffffffffu, s1, off);
+                            if (int(lane) >= off) {
+                                s0 += v0;
+                                s1 += v1;
+                            }
+                        }
+                        groups(excl, np0 + s0 - n0, true);
+                        groups(0xFFu, 64 + np1 + s1 - n1, true);
+                        np0 += __shfl_sync(0xffffffffu, s0, 31);
+                        np1 += __shfl_sync(0xffffffffu, s1, 31);
+                        carry |= __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                }
+                if (lane == 0) {
+                    pg[0] = make_int4(np0, np1, c.rs0, c.rs1);
+                    pg[1] = make_int4(c.pos_lo, c.pos_hi, 0, 0);
+                }
+                __syncwarp();
+                ptx::mbar_arrive(&pfull[ps]);  // all 32 lanes
+                if (++ps == 2) {
+                    ps = 0;
+                    pph ^= 1;
                 }
             }
         }

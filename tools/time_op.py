@@ -28,7 +28,8 @@ def main():
         with torch.cuda.graph(g):
             for _ in range(reps):
                 b.run(op, torch.cuda.current_stream().cuda_stream)
-        g.replay()
+        for _ in range(int(os.environ.get("TIME_OP_WARM", "1"))):  # clock ramp-up
+            g.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         g.replay()
