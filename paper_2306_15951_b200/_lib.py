@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcks.so")
+LIB_PATH = os.environ.get("CKS_LIB_VARIANT") or os.path.join(_PKG, "libcks.so")  # variant: experiments only
 
 CKS_TF32, CKS_BF16 = 0, 1
 CKS_OP_FWD, CKS_OP_DECONV, CKS_OP_WGRAD = 0, 1, 2

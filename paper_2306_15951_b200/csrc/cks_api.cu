@@ -50,7 +50,7 @@ int device_sms() {
 
 // rank-4 tiled tensor map, 128B swizzle, zero OOB fill
 bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
-                const uint32_t box[4], int row_bytes = 128) {
+                const uint32_t box[4], int row_bytes = 128, bool atom32 = false) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
@@ -59,8 +59,9 @@ bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t d
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                      const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                      : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
+                     atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B  // MN-major tf32 (SWIZZLE_128B_BASE32B)
+                            : (row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B)),
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -102,22 +103,32 @@ cks_status last_cuda() {
 // while its predecessor drains; every kernel calls griddepcontrol.wait before
 // touching global memory, so stream order semantics are preserved.
 template <typename... KArgs, typename... Args>
-cks_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t st, Args&&... args) {
+cks_status launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t st, int cluster,
+                              Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = size_t(smem);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = unsigned(cluster);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cluster > 1 ? 2 : 1;
     if (cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...) != cudaSuccess) {
         last_cuda();
         return CKS_ERR_CUDA;
     }
     return CKS_OK;
+}
+
+template <typename... KArgs, typename... Args>
+cks_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, int smem, cudaStream_t st, Args&&... args) {
+    return launch_pdl_cluster(kern, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
 template <typename K>
@@ -164,9 +175,12 @@ cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUte
                           int smem, cudaStream_t st) {
     auto kern = igemm_kernel<BN, TF, KB>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
-    long long grid = std::min<long long>(p.num_tiles, device_sms());
+    long long grid = std::min<long long>(p.num_tiles, device_sms() / p.cm * p.cm);  // whole clusters
     if (grid < 1) grid = 1;
-    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, a, b, y, p);
+    if (p.cm > 1 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return last_cuda();
+    return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(256), smem, st, p.cm, a, b, y, p);
 }
 
 template <bool TF, int KB>
@@ -249,6 +263,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.a0_step = cfg.a0_step;
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
     p.epi_stage = cfg.epi;
+    p.cm = cfg.cm;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
                      int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes : 0);
     if (cfg.Z > 1) {
@@ -273,10 +288,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }
 
-template <int BN>
+template <int BN, bool TF>
 cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
-    using S = WgradShape<BN>;
-    auto kern = wgrad_kernel<BN>;
+    using S = WgradShape<BN, TF>;
+    auto kern = wgrad_kernel<BN, TF>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
@@ -388,7 +403,7 @@ cks_status launch_wgrad_row_jb(int BN, const CUtensorMap& tx, const CUtensorMap&
 }
 
 // per-tap Sk-dilated-V2 kernel (KB-WGRAD)
-cks_status run_wgrad_taps(const cks_geom& g, const WgradCfg& cfg, const Axis& ah, const Axis& aw,
+cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, const Axis& ah, const Axis& aw,
                           const CUtensorMap& ta, const CUtensorMap& tb, float* wout, long long part_stride,
                           cudaStream_t st) {
     WgradParams p;
@@ -418,10 +433,11 @@ cks_status run_wgrad_taps(const cks_geom& g, const WgradCfg& cfg, const Axis& ah
     p.nblk64 = cfg.nblk64;
     p.num_tiles = cfg.base_tiles * cfg.gz;
     p.part_stride = part_stride;
+    const bool tf = dt == CKS_TF32;
     switch (cfg.BN) {
-        case 64: return launch_wgrad_t<64>(ta, tb, p, st);
-        case 128: return launch_wgrad_t<128>(ta, tb, p, st);
-        case 256: return launch_wgrad_t<256>(ta, tb, p, st);
+        case 64: return tf ? launch_wgrad_t<64, true>(ta, tb, p, st) : launch_wgrad_t<64, false>(ta, tb, p, st);
+        case 128: return tf ? launch_wgrad_t<128, true>(ta, tb, p, st) : launch_wgrad_t<128, false>(ta, tb, p, st);
+        case 256: return tf ? launch_wgrad_t<256, true>(ta, tb, p, st) : launch_wgrad_t<256, false>(ta, tb, p, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
@@ -473,11 +489,10 @@ cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz
 }
 
 cks_status cks_choose_gz(const cks_geom* g, cks_dtype dt, int* gz) {
-    (void)dt;
     if (!g || !gz) return CKS_ERR_NULL;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
-    *gz = wgrad_cfg(*g, 0, kPlanSMs).gz;
+    *gz = wgrad_cfg(*g, dt, 0, kPlanSMs).gz;
     return CKS_OK;
 }
 
@@ -520,7 +535,7 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
     {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->H)};
         uint64_t sb[3] = {uint64_t(g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
-        uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
+        uint32_t box[4] = {BK, 128u / uint32_t(cfg.cm), cfg.cm > 1 ? 1u : uint32_t(cfg.apos), 1};
         if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     {   // W viewed as (C, OC, FH*FW, 1): one box = the FW taps of a filter row x BN filters
@@ -576,7 +591,7 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
     {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
         uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
         uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
-        uint32_t box[4] = {BK, 128, uint32_t(cfg.apos), 1};
+        uint32_t box[4] = {BK, 128u / uint32_t(cfg.cm), cfg.cm > 1 ? 1u : uint32_t(cfg.apos), 1};
         if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     {   // packed C_{y,x} viewed as (OCp, C, CHm*CWm, P): one box = the CWm taps of sub-filter row ch
@@ -594,7 +609,6 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     if (!g || !x || !dy || !dw) return CKS_ERR_NULL;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
-    if (dt != CKS_BF16) return CKS_ERR_UNSUPPORTED;  // MN-major TF32 operands: not in this build
     if (gz < 0) return CKS_ERR_UNSUPPORTED;
     if (!aligned16(x) || !aligned16(dy) || !aligned16(dw)) return CKS_ERR_ALIGNMENT;
     if (g->OC > 65535 || g->C > 65535) return CKS_ERR_UNSUPPORTED;
@@ -605,7 +619,7 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt), OCp = pad_ch(g->OC, dt);
     const void* xs = x;
     const void* dys = dy;
-    WgradCfg cfg = wgrad_cfg(*g, gz, kPlanSMs);
+    WgradCfg cfg = wgrad_cfg(*g, dt, gz, kPlanSMs);
     if (Cp != g->C && !cfg.row) {
         void* p = static_cast<uint8_t*>(ws) + L.x_pad;
         if ((s = launch_pad(dt, x, p, g->N * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
@@ -620,8 +634,8 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     {
         uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ah.O), uint64_t(g->N)};
         uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ah.O * aw.O * OCp * eb)};
-        uint32_t box[4] = {64, 1, 1, 64};
-        if (!make_tmap4(&ta, dt, dys, d, sb, box)) return CKS_ERR_CUDA;
+        uint32_t box[4] = {uint32_t(128 / eb), 1, 1, 64};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
     float* wout = cfg.gz > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
@@ -656,10 +670,10 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         {
             uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
             uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
-            uint32_t box[4] = {64, 1, 1, 64};
-            if (!make_tmap4(&tb, dt, xs, d, sb, box)) return CKS_ERR_CUDA;
+            uint32_t box[4] = {uint32_t(128 / eb), 1, 1, 64};
+            if (!make_tmap4(&tb, dt, xs, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
         }
-        s = run_wgrad_taps(*g, cfg, ah, aw, ta, tb, wout, part_stride, st);
+        s = run_wgrad_taps(*g, dt, cfg, ah, aw, ta, tb, wout, part_stride, st);
     }
     if (s != CKS_OK) return s;
     if (cfg.gz > 1) {  // fixed-order aggregation of the G_Z segments
@@ -739,7 +753,7 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     if (op == CKS_OP_FWD) n += (cpad && !row_cfg_fwd(*g, dt).ok) ? 2 : 0;
     else if (op == CKS_OP_DECONV) n += (c_packed_given ? 0 : 1) + (ocpad ? 1 : 0);
     else if (op == CKS_OP_WGRAD) {
-        const WgradCfg c = wgrad_cfg(*g, gz, kPlanSMs);
+        const WgradCfg c = wgrad_cfg(*g, dt, gz, kPlanSMs);
         n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) + (c.gz > 1 ? 1 : 0);
     }
     else return CKS_ERR_UNSUPPORTED;

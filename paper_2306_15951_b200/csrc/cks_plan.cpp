@@ -203,6 +203,14 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     (void)num_sms;
     if (ov && ov_z > 0) c.Z = int(std::min<int64_t>(ov_z, rs_full));
     c.tiles = c.out_tiles * c.Z;
+    // A-tile multicast across the BN blocks of one pixel (thread-block cluster):
+    // every CTA loads 128/cm of the images of each activation column
+    c.cm = 1;
+    const char* mc = getenv("CKS_MCAST");  // experiments only (measured slower on B200: off by default)
+    if (c.Z == 1 && mc && atoi(mc) == 1) {
+        if (c.nbs % 4 == 0) c.cm = 4;
+        else if (c.nbs % 2 == 0) c.cm = 2;
+    }
     return c;
 }
 
@@ -309,9 +317,9 @@ RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     return c;
 }
 
-WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms) {
+WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     WgradCfg c;
-    RowCfg rc = row_cfg_wgrad(g, CKS_BF16, gz_req, num_sms);
+    RowCfg rc = row_cfg_wgrad(g, dt, gz_req, num_sms);
     if (rc.ok) {
         c.row = true;
         c.BN = rc.BN;
@@ -366,7 +374,7 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
         off += align256(bytes);
     };
     const bool row = (op == CKS_OP_FWD && row_cfg_fwd(g, dt).ok) ||
-                     (op == CKS_OP_WGRAD && dt == CKS_BF16 && wgrad_cfg(g, gz, num_sms).row);
+                     (op == CKS_OP_WGRAD && wgrad_cfg(g, dt, gz, num_sms).row);
     if ((op == CKS_OP_FWD || op == CKS_OP_WGRAD) && !row) {  // the row path reads X unpadded
         if (Cp != g.C) take(size_t(g.N) * g.H * g.W * Cp * eb, L.x_pad, L.x_pad_bytes);
     }
@@ -385,7 +393,7 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
         }
     }
     if (op == CKS_OP_WGRAD) {
-        WgradCfg c = wgrad_cfg(g, gz, num_sms);
+        WgradCfg c = wgrad_cfg(g, dt, gz, num_sms);
         if (c.gz > 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
     }
     L.total = off;

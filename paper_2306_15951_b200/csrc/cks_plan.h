@@ -80,6 +80,7 @@ struct IgemmCfg {
     int stage_bytes = 0, stages = 2;  // B-row ring: bytes per row, rows in flight
     int a_stages = 8;                 // A ring (slots of apos x 16 KB)
     int epi = 0;                      // epilogue staging buffers present
+    int cm = 1;                       // cluster size along the BN blocks (A-tile multicast)
     int apos = 2;                     // activation columns per A slot
     int unit_step = 1;                // consecutive pixels' tap-0 columns differ by 1
     int a0_step = 1;                  // tap-0 column step between consecutive pixels
@@ -118,7 +119,7 @@ struct WgradCfg {
     int64_t base_tiles;
     bool row = false;  // narrow-channel row kernel
 };
-WgradCfg wgrad_cfg(const cks_geom& g, int gz_req, int num_sms);
+WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 
 // Workspace layout (byte offsets, 256-aligned) for one op.
 struct WsLayout {

@@ -88,6 +88,7 @@ struct IgemmParams {
     int zsplit;
     FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
+    int cm;               // cluster size along the O_C blocks: the A tile of a pixel is multicast (1 = off)
     int tma_store;        // last tile per CTA: stage in the idle rings, TMA-store the output
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
@@ -189,7 +190,7 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
     const int rs = empty ? 0 : (che - chs) * p.kc_blocks;
     c.rs0 = p.zsplit == 1 ? 0 : int(fdivu(uint32_t(rs) * uint32_t(c.z), p.fd_z));
     c.rs1 = p.zsplit == 1 ? rs : int(fdivu(uint32_t(rs) * uint32_t(c.z + 1), p.fd_z));
-    c.rot = c.rs1 > c.rs0 ? int(blockIdx.x % unsigned(c.rs1 - c.rs0)) : 0;
+    c.rot = c.rs1 > c.rs0 ? int((blockIdx.x / unsigned(p.cm)) % unsigned(c.rs1 - c.rs0)) : 0;  // cluster-uniform
     return c;
 }
 
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::prefetch_tmap(&tmB);
         for (int i = 0; i < p.a_stages; ++i) {
             ptx::mbar_init(&afull[i], 1);
-            ptx::mbar_init(&aempty[i], 1);
+            ptx::mbar_init(&aempty[i], p.cm);  // every CTA of the cluster consumes the multicast slot
         }
         for (int i = 0; i < p.b_stages; ++i) {
             ptx::mbar_init(&bfull[i], 1);
@@ -271,8 +272,11 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
     ptx::tc_fence_before();
     __syncthreads();
+    if (p.cm > 1) ptx::cluster_sync();  // peers' barriers exist before the first multicast
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t crank = p.cm > 1 ? blockIdx.x % uint32_t(p.cm) : 0u;
+    const uint16_t cmask = uint16_t((1u << p.cm) - 1u);
     if (threadIdx.x == 0) trace_gt(p, 1);
     ptx::pdl_wait();  // inputs of this op may come from the previous kernel
     if (threadIdx.x == 0) trace_gt(p, 2);
@@ -319,6 +323,14 @@ __global__ void __launch_bounds__(256, 1)
                     if (ptx::elect_one()) {
                         if ((p.dbg & 8) && aq > uint32_t(p.a_stages)) {
                             ptx::mbar_arrive(&afull[as]);  // experiment: A traffic removed (wrong results)
+                        } else if (p.cm > 1) {
+                            // this CTA's 128/cm images of every column, multicast to the cluster
+                            ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
+                            const int rows = 128 / p.cm;
+                            for (int col = 0; col < p.apos; ++col)
+                                ptx::tma_load_4d_mc(abuf + as * a_slot + col * S::A_BYTES + crank * rows * KB, &tmA,
+                                                    &afull[as], kc * S::BK, c.nblk * 128 + int(crank) * rows,
+                                                    iw0 + col, a0h + ch, cmask);
                         } else {
                             ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
                             ptx::tma_load_4d(abuf + as * a_slot, &tmA, &afull[as], kc * S::BK, c.nblk * 128, iw0,
@@ -368,9 +380,11 @@ __global__ void __launch_bounds__(256, 1)
                         if (lane == 0) trace_ev(p, 1, ti, 2);
                         ptx::tc_fence_after();
                         const uint64_t aslot = dconst | uint64_t(ptx::smem_u32(abuf + as * a_slot) >> 4);
-                        for (; e < np; ++e) {
-                            const int4 en = pl[e];
-                            if (en.x != k) break;
+                        // entries of this A slot; the next entry is loaded while the
+                        // current one issues (hides the shared-memory load latency)
+                        int4 en = e < np ? pl[e] : make_int4(-1, 0, 0, 0);
+                        for (; en.x == k; ++e) {
+                            const int4 nx = e + 1 < np ? pl[e + 1] : make_int4(-1, 0, 0, 0);
                             const uint64_t adesc = aslot + uint64_t(uint32_t(en.y) * (S::A_BYTES >> 4));
                             const uint64_t bdesc = bdesc0 + uint64_t(uint32_t(en.w & 0xFF) * (S::TILE_B >> 4));
                             const uint32_t cnt = uint32_t(en.w >> 8) & 0xFFu;
@@ -384,8 +398,14 @@ __global__ void __launch_bounds__(256, 1)
                                                        kk ? 1u : acc0);
                             }
                             __syncwarp();
+                            en = nx;
                         }
-                        if (ptx::elect_one()) ptx::mma_commit(&aempty[as]);  // A slot free when these MMAs finish
+                        if (ptx::elect_one()) {  // A slot free (in every CTA that multicasts into it)
+                            if (p.cm > 1)
+                                ptx::mma_commit_mc(&aempty[as], cmask);
+                            else
+                                ptx::mma_commit(&aempty[as]);
+                        }
                         __syncwarp();
                         if (lane == 0) trace_ev(p, 1, ti, 4);
                     }
@@ -690,6 +710,7 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
     __syncthreads();
+    if (p.cm > 1) ptx::cluster_sync();  // no CTA leaves while peers may still signal it
     if (threadIdx.x == 0) trace_gt(p, 5);
     if (warp == 2) {
         ptx::tc_fence_after();

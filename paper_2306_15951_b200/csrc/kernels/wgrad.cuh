@@ -31,10 +31,18 @@ struct WgradParams {
     long long part_stride;  // OC*FH*FW*C
 };
 
-template <int BN>
+// One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
+// an MN-major swizzle atom column.  BF16: SWIZZLE_128B (16 B chunks, 8-row
+// K groups, SBO 1 KB).  TF32: SWIZZLE_128B_BASE32B (32 B chunks, 4-row K
+// groups, SBO 512 B) -- the MN-major layout tcgen05 kind::tf32 requires.
+template <int BN, bool kTF32 = false>
 struct WgradShape {
-    static constexpr int A_BYTES = 2 * 8192;        // 128 OC x 64 images (bf16)
-    static constexpr int B_BYTES = (BN / 64) * 8192;  // BN IC x 64 images
+    static constexpr int EB = kTF32 ? 4 : 2;
+    static constexpr int CH = 128 / EB;                 // channels per box
+    static constexpr int A_BYTES = (128 / CH) * 8192;   // 128 OC x 64 images
+    static constexpr int B_BYTES = (BN / CH) * 8192;    // BN IC x 64 images
+    static constexpr int UK = 32 / EB;                  // K (images) per MMA
+    static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
@@ -70,11 +78,11 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     return c;
 }
 
-template <int BN>
+template <int BN, bool kTF32 = false>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
-    using S = WgradShape<BN>;
+    using S = WgradShape<BN, kTF32>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
@@ -125,15 +133,16 @@ __global__ void __launch_bounds__(256, 1)
                     if (!is_b) {
                         ptx::mbar_arrive_expect_tx(&full[stage], S::A_BYTES);
 #pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * 64, ow, oh, n64 * 64);
+                        for (int j = 0; j < 128 / S::CH; ++j)
+                            ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow, oh,
+                                             n64 * 64);
                     } else {
                         const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
                         const int iw = ow * p.sw + c.fw - p.pw;
                         ptx::mbar_arrive_expect_tx(&full[stage], S::B_BYTES);
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * 64, iw,
+                        for (int j = 0; j < BN / S::CH; ++j)
+                            ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * S::CH, iw,
                                              ih, n64 * 64);
                     }
                 }
@@ -146,8 +155,9 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (whole warp, elected lane issues)
-        constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, true, true);
-        const uint64_t dconst = ptx::smem_desc_sw128(0, 8192, 1024);  // MN-major: LBO 8 KB, SBO 1 KB
+        constexpr uint32_t idesc = ptx::instr_desc(128, BN, kTF32, true, true);
+        // MN-major: LBO 8 KB between 128 B channel atoms, SBO = one K group (8 x / 4 x 128 B)
+        const uint64_t dconst = kTF32 ? ptx::smem_desc_mn_b32(0, 8192, 512) : ptx::smem_desc_sw128(0, 8192, 1024);
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const WTile c = wdecode(t, p);
@@ -162,9 +172,9 @@ __global__ void __launch_bounds__(256, 1)
                 const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES) >> 4);
                 if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)  // 64 images = 4 x K16 (+2 KB per K16 step)
-                        ptx::mma_ss<false>(d, ad + uint64_t(kk * 128), bd + uint64_t(kk * 128), idesc,
-                                           ((kb - c.kb0) | kk) != 0);
+                    for (int kk = 0; kk < 64 / S::UK; ++kk)  // 64 images = 4 x K16 (bf16) / 8 x K8 (tf32)
+                        ptx::mma_ss<kTF32>(d, ad + uint64_t(kk * (S::KSTEP >> 4)), bd + uint64_t(kk * (S::KSTEP >> 4)),
+                                           idesc, ((kb - c.kb0) | kk) != 0);
                     ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();

@@ -113,9 +113,9 @@ def test_c1_all_ops(torch_cuda, dtype):
     assert nrm_err(got["wgrad"], O.brute_wgrad(a["X"], a["dY"], lay.FH, lay.FW, *s)) < tight_bf16(red_len(lay, "wgrad"))
 
 
-def test_c1_tf32_fwd_deconv(torch_cuda):
+def test_c1_tf32_all_ops(torch_cuda):
     lay = get_config(0)[1][0]
-    check_full(torch_cuda, lay, "tf32", ops=("fwd", "deconv"))
+    check_full(torch_cuda, lay, "tf32")
 
 
 # ------------------------------------------------------- random geometries
@@ -148,8 +148,8 @@ def test_random_geometries(torch_cuda, lay):
 
 @pytest.mark.parametrize("lay", _rand_layers(10, 23), ids=lambda l: f"tf32-{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
 def test_random_geometries_tf32(torch_cuda, lay):
-    """TF32 (fp32 storage, TF32 tensor-core multiply) forward and KS-deconv."""
-    check_full(torch_cuda, lay, "tf32", config=8, idx=int(lay.name[4:]), ops=("fwd", "deconv"))
+    """TF32 (fp32 storage, TF32 tensor-core multiply): all three operators."""
+    check_full(torch_cuda, lay, "tf32", config=8, idx=int(lay.name[4:]))
 
 
 def _narrow_layers(n, seed):
@@ -283,6 +283,14 @@ def test_config_layers_reduced_batch(torch_cuda, cfg, i, lay):
     big = lay.H * lay.W * max(lay.C, lay.OC) * lay.FH * lay.FW * lay.OC * lay.C
     n = 130 if big < 4e9 else 3
     check_full(torch_cuda, lay.with_batch(n), "bf16", config=cfg, idx=i, ops=lay.ops)
+
+
+@pytest.mark.parametrize("cfg,i,lay", _config_layers()[::3], ids=lambda v: v.name if isinstance(v, Layer) else str(v))
+def test_config_layers_reduced_batch_tf32(torch_cuda, cfg, i, lay):
+    """Every third config layer in TF32 (fp32 storage), reduced batch as above."""
+    big = lay.H * lay.W * max(lay.C, lay.OC) * lay.FH * lay.FW * lay.OC * lay.C
+    n = 67 if big < 4e9 else 2
+    check_full(torch_cuda, lay.with_batch(n), "tf32", config=cfg, idx=i, ops=lay.ops)
 
 
 # ------------------------------------------ full size, sampled outputs
