@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
-FAMILY = [("igemm_kernel", "igemm_kernel (KB-CONV / KB-KS)"), ("wgrad_kernel", "wgrad_kernel (KB-WGRAD)"),
+FAMILY = [("igemm_kernel", "igemm_kernel (KB-CONV / KB-KS)"), ("wgrad_row_kernel", "wgrad_row_kernel (KB-WGRAD-ROW)"),
+          ("fwd_row_kernel", "fwd_row_kernel (KB-CONV-ROW)"), ("wgrad_kernel", "wgrad_kernel (KB-WGRAD)"),
           ("ks_split", "ks_split_kernel (KB-SPLIT)"), ("reduce_partials", "reduce_partials (KB-REDUCE)"),
           ("pad_channels", "pad_channels (KB-PAD)")]
 
