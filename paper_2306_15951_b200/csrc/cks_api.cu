@@ -264,6 +264,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     if (p.a_stages < 2 || p.b_stages < 1) return CKS_ERR_UNSUPPORTED;
     p.epi_stage = cfg.epi;
     p.cm = cfg.cm;
+    p.unified = cfg.unified;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
                      int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes : 0);
     if (cfg.Z > 1) {

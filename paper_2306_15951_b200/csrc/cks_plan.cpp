@@ -149,6 +149,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // else 128 B blocks
     const int64_t kbytes = kchan * eb;
     c.KB = kbytes <= 32 ? 32 : (kbytes <= 64 ? 64 : 128);
+    if (const char* kb = getenv("CKS_IGEMM_KB")) c.KB = std::min(c.KB, atoi(kb));  // experiments only
     c.kc_blocks = int((kchan + (c.KB / eb) - 1) / (c.KB / eb));
     c.ntap = int(ntap);
     int64_t maxrow = 1;
@@ -192,6 +193,16 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     if (ov && g_ov_apos > 0) c.apos = std::min(c.pa, g_ov_apos);
     if (ov && g_ov_bst > 0) c.stages = g_ov_bst;
     c.a_stages = int(std::min<int64_t>(8, (budget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
+    // one A slot per row step: A slot and B row form one stage (one barrier pair,
+    // one commit per row step); as many stages as fit
+    const char* un = getenv("CKS_UNIFIED");  // experiments only: 0 disables
+    if (c.apos == c.pa && !(un && atoi(un) == 0)) {
+        const int64_t st = std::min<int64_t>(8, budget / (int64_t(c.apos) * col_bytes + c.stage_bytes));
+        if (st >= 2) {
+            c.unified = 1;
+            c.stages = c.a_stages = int(st);
+        }
+    }
     c.acc_stages = 2;
     c.wblocks = 0;
     for (auto v : wph_cnt) c.wblocks += int((v + c.pbw - 1) / c.pbw);

@@ -81,6 +81,7 @@ struct IgemmCfg {
     int a_stages = 8;                 // A ring (slots of apos x 16 KB)
     int epi = 0;                      // epilogue staging buffers present
     int cm = 1;                       // cluster size along the BN blocks (A-tile multicast)
+    int unified = 0;                  // A slot + B row of a row step share one barrier pair
     int apos = 2;                     // activation columns per A slot
     int unit_step = 1;                // consecutive pixels' tap-0 columns differ by 1
     int a0_step = 1;                  // tap-0 column step between consecutive pixels

@@ -89,6 +89,7 @@ struct IgemmParams {
     FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
     int cm;               // cluster size along the O_C blocks: the A tile of a pixel is multicast (1 = off)
+    int unified;          // one A slot per row step: A slot + B row share one full/empty barrier pair
     int tma_store;        // last tile per CTA: stage in the idle rings, TMA-store the output
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         for (int i = 0; i < p.a_stages; ++i) {
-            ptx::mbar_init(&afull[i], 1);
+            ptx::mbar_init(&afull[i], p.unified ? 2 : 1);  // unified: A and B producers
             ptx::mbar_init(&aempty[i], p.cm);  // every CTA of the cluster consumes the multicast slot
         }
         for (int i = 0; i < p.b_stages; ++i) {
@@ -301,13 +302,14 @@ __global__ void __launch_bounds__(256, 1)
                 const int ch = c.chs + rq, kc = r - rq * p.kc_blocks;
                 if (is_b) {
                     const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
-                    ptx::mbar_wait(&bempty[bs], bph ^ 1);
+                    uint64_t* bf = p.unified ? &afull[bs] : &bfull[bs];
+                    ptx::mbar_wait(p.unified ? &aempty[bs] : &bempty[bs], bph ^ 1);
                     if (ptx::elect_one()) {
                         if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
-                            ptx::mbar_arrive(&bfull[bs]);  // experiment: B traffic removed (wrong results)
+                            ptx::mbar_arrive(bf);  // experiment: B traffic removed (wrong results)
                         } else {
-                            ptx::mbar_arrive_expect_tx(&bfull[bs], btx);
-                            ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, &bfull[bs], kc * S::BK, c.nb * BN,
+                            ptx::mbar_arrive_expect_tx(bf, btx);
+                            ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, bf, kc * S::BK, c.nb * BN,
                                              ch * p.slot_stride, c.ph);
                         }
                     }
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(256, 1)
                 bool first = true;
                 for (int ri = rs0; ri < rs1; ++ri) {
                     const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
-                    ptx::mbar_wait(&bfull[bs], bph);
+                    if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
                     if (lane == 0) trace_ev(p, 1, ti, 1);
                     const uint64_t bdesc0 = dconst | uint64_t(ptx::smem_u32(bbuf + bs * p.b_stage_bytes) >> 4);
                     const int4* pl = pg + 2 + (first ? 0 : 64);
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(256, 1)
                         __syncwarp();
                         if (lane == 0) trace_ev(p, 1, ti, 4);
                     }
-                    if (ptx::elect_one()) ptx::mma_commit(&bempty[bs]);  // B row free
+                    if (!p.unified && ptx::elect_one()) ptx::mma_commit(&bempty[bs]);  // B row free
                     __syncwarp();
                     ++bq;
                 }
