@@ -116,20 +116,37 @@ std::vector<KRow> krows_deconv(const Axis& a) {
     return r;
 }
 
-// experiments only: CKS_IGEMM_CFG="BN,PBW,Z" overrides the heuristic
+// Experiment knobs (tools/ sweeps only; all unset in production), read once
+// per process: CKS_IGEMM_CFG="BN,PBW,Z[,APOS,BSTAGES]" overrides the tile
+// heuristic, CKS_IGEMM_KB caps the K-block bytes, CKS_EPI_STAGE=0 /
+// CKS_UNIFIED=0 disable the coalesced epilogue / unified stage barriers,
+// CKS_MCAST=1 enables the (slower) cluster multicast of A.
+struct Knobs {
+    bool ov = false;
+    int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
+    int kb = 0, epi = 1, unified = 1, mcast = 0;
+    Knobs() {
+        if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
+        if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
+        if (const char* e = getenv("CKS_EPI_STAGE")) epi = atoi(e) != 0;
+        if (const char* e = getenv("CKS_UNIFIED")) unified = atoi(e) != 0;
+        if (const char* e = getenv("CKS_MCAST")) mcast = atoi(e) == 1;
+    }
+};
+static const Knobs& knobs() {
+    static const Knobs k;
+    return k;
+}
 static int g_ov_apos = 0, g_ov_bst = 0;
 static bool cfg_override(int& bn, int& pbw, int& z) {
-    const char* e = getenv("CKS_IGEMM_CFG");
-    if (!e) return false;
-    g_ov_apos = g_ov_bst = 0;
-    const int n = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &g_ov_apos, &g_ov_bst);
-    return n >= 3;
+    const Knobs& k = knobs();
+    if (!k.ov) return false;
+    bn = k.bn, pbw = k.pbw, z = k.z;
+    g_ov_apos = k.apos, g_ov_bst = k.bst;
+    return true;
 }
 
-bool epi_staging() {
-    const char* e = getenv("CKS_EPI_STAGE");  // experiments only
-    return !(e && atoi(e) == 0);
-}
+bool epi_staging() { return knobs().epi != 0; }
 
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
@@ -149,7 +166,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // else 128 B blocks
     const int64_t kbytes = kchan * eb;
     c.KB = kbytes <= 32 ? 32 : (kbytes <= 64 ? 64 : 128);
-    if (const char* kb = getenv("CKS_IGEMM_KB")) c.KB = std::min(c.KB, atoi(kb));  // experiments only
+    if (knobs().kb > 0) c.KB = std::min(c.KB, knobs().kb);
     c.kc_blocks = int((kchan + (c.KB / eb) - 1) / (c.KB / eb));
     c.ntap = int(ntap);
     int64_t maxrow = 1;
@@ -195,8 +212,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     c.a_stages = int(std::min<int64_t>(8, (budget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
     // one A slot per row step: A slot and B row form one stage (one barrier pair,
     // one commit per row step); as many stages as fit
-    const char* un = getenv("CKS_UNIFIED");  // experiments only: 0 disables
-    if (c.apos == c.pa && !(un && atoi(un) == 0)) {
+    if (c.apos == c.pa && knobs().unified) {
         const int64_t st = std::min<int64_t>(8, budget / (int64_t(c.apos) * col_bytes + c.stage_bytes));
         if (st >= 2) {
             c.unified = 1;
@@ -217,8 +233,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // A-tile multicast across the BN blocks of one pixel (thread-block cluster):
     // every CTA loads 128/cm of the images of each activation column
     c.cm = 1;
-    const char* mc = getenv("CKS_MCAST");  // experiments only (measured slower on B200: off by default)
-    if (c.Z == 1 && mc && atoi(mc) == 1) {
+    if (c.Z == 1 && knobs().mcast) {  // measured slower on B200: off by default
         if (c.nbs % 4 == 0) c.cm = 4;
         else if (c.nbs % 2 == 0) c.cm = 2;
     }

@@ -126,3 +126,28 @@ def test_workspace_and_launch_counts():
     ws = L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=4)
     assert ws >= 4 * 64 * 9 * 64 * 4
     assert L.cks_ks_split_size(g, L.CKS_BF16) == 4 * 64 * 2 * 2 * 64 * 2
+
+
+def test_narrow_row_path_plan():
+    """Narrow-channel bf16 layers (FW*C <= 64, C <= 16, W*C*2 % 16 == 0) take the
+    filter-row kernels: no channel padding pass, and the Sk-dilated G_Z is a
+    multiple of the column-class count P = 8 / gcd(sw*C, 8) (include/cks.h)."""
+    from math import gcd
+    for (C, W, FW, sw, OC) in [(3, 224, 7, 2, 64), (3, 32, 3, 1, 64), (3, 64, 4, 2, 128), (1, 16, 5, 1, 8),
+                               (2, 24, 7, 3, 32), (4, 8, 3, 2, 8), (8, 16, 3, 1, 16), (16, 8, 3, 2, 40)]:
+        g = L.make_geom(70, C, W, W, OC, FW, FW, sw, sw, FW // 2, FW // 2)
+        P = 8 // gcd(sw * C, 8)
+        gz = L.cks_choose_gz(g, L.CKS_BF16)
+        assert gz % P == 0 and gz >= P, (C, W, FW, sw, gz, P)
+        assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 1          # no X/W padding pass
+        ocpad = OC % 8 != 0
+        assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + ocpad + (gz > 1)
+        # a requested gz is rounded up to a multiple of P
+        ws = L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=P + 1)
+        assert ws >= 2 * P * OC * FW * FW * C * 4
+        # TF32 keeps the per-tap path (channel padding to 4)
+        cpad = C % 4 != 0
+        assert L.cks_launch_count(g, L.CKS_TF32, L.CKS_OP_FWD) == 1 + 2 * cpad
+    # row pitch not a multiple of 16 bytes -> padded per-tap path
+    g = L.make_geom(70, 3, 33, 33, 64, 3, 3, 1, 1, 1, 1)
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 3
