@@ -373,7 +373,7 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     if (gz_req > 0) {
         c.gz = gz_req;
     } else {
-        int64_t want = (num_sms + c.base_tiles / 2) / std::max<int64_t>(c.base_tiles, 1);
+        int64_t want = std::max<int64_t>(1, num_sms / std::max<int64_t>(c.base_tiles, 1));  // one wave
         int64_t cap = std::max<int64_t>(lmin / 4, 1);
         c.gz = int(std::max<int64_t>(1, std::min<int64_t>({want, cap, 64})));
     }
