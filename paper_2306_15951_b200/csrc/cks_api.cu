@@ -289,10 +289,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }
 
-template <int BN, bool TF>
+template <int BN, bool TF, int KIMG>
 cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
-    using S = WgradShape<BN, TF>;
-    auto kern = wgrad_kernel<BN, TF>;
+    using S = WgradShape<BN, TF, KIMG>;
+    auto kern = wgrad_kernel<BN, TF, KIMG>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
@@ -435,11 +435,16 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.num_tiles = cfg.base_tiles * cfg.gz;
     p.part_stride = part_stride;
     const bool tf = dt == CKS_TF32;
+    const bool k128 = cfg.kimg == 128;
+#define CKS_WG(BN_)                                                                                   \
+    (tf ? (k128 ? launch_wgrad_t<BN_, true, 128>(ta, tb, p, st) : launch_wgrad_t<BN_, true, 64>(ta, tb, p, st)) \
+        : (k128 ? launch_wgrad_t<BN_, false, 128>(ta, tb, p, st) : launch_wgrad_t<BN_, false, 64>(ta, tb, p, st)))
     switch (cfg.BN) {
-        case 64: return tf ? launch_wgrad_t<64, true>(ta, tb, p, st) : launch_wgrad_t<64, false>(ta, tb, p, st);
-        case 128: return tf ? launch_wgrad_t<128, true>(ta, tb, p, st) : launch_wgrad_t<128, false>(ta, tb, p, st);
-        case 256: return tf ? launch_wgrad_t<256, true>(ta, tb, p, st) : launch_wgrad_t<256, false>(ta, tb, p, st);
+        case 64: return CKS_WG(64);
+        case 128: return CKS_WG(128);
+        case 256: return CKS_WG(256);
     }
+#undef CKS_WG
     return CKS_ERR_UNSUPPORTED;
 }
 
@@ -631,11 +636,11 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         if ((s = launch_pad(dt, dy, p, g->N * ah.O * aw.O, int(g->OC), int(OCp), st)) != CKS_OK) return s;
         dys = p;
     }
-    CUtensorMap ta;  // dY viewed as (OC, OW, OH, N): boxes of 64 channels x 64 images
+    CUtensorMap ta;  // dY viewed as (OC, OW, OH, N): boxes of 128 B of channels x 64 / 128 images
     {
         uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ah.O), uint64_t(g->N)};
         uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ah.O * aw.O * OCp * eb)};
-        uint32_t box[4] = {uint32_t(128 / eb), 1, 1, 64};
+        uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.row ? 64 : cfg.kimg)};
         if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
     float* wout = cfg.gz > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
@@ -671,7 +676,7 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         {
             uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
             uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
-            uint32_t box[4] = {uint32_t(128 / eb), 1, 1, 64};
+            uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.kimg)};
             if (!make_tmap4(&tb, dt, xs, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
         }
         s = run_wgrad_taps(*g, dt, cfg, ah, aw, ta, tb, wout, part_stride, st);

@@ -124,13 +124,14 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
         if (const char* e = getenv("CKS_EPI_STAGE")) epi = atoi(e) != 0;
         if (const char* e = getenv("CKS_UNIFIED")) unified = atoi(e) != 0;
         if (const char* e = getenv("CKS_MCAST")) mcast = atoi(e) == 1;
+        if (const char* e = getenv("CKS_WGRAD_KIMG")) kimg128 = atoi(e) == 128;
     }
 };
 static const Knobs& knobs() {
@@ -359,7 +360,10 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     c.mblocks = int((g.OC + 127) / 128);
     c.BN = g.C <= 64 ? 64 : (g.C <= 128 ? 128 : 256);
     c.nbs = int((g.C + c.BN - 1) / c.BN);
-    c.nblk64 = int((g.N + 63) / 64);
+    // 128-image k-blocks (half the barrier round trips) where the stage stays
+    // small enough for a 4-deep ring (BN = 64); measured slower for BN >= 128
+    c.kimg = (g.N >= 128 && c.BN == 64 && knobs().kimg128) ? 128 : 64;
+    c.nblk64 = int((g.N + c.kimg - 1) / c.kimg);
     Axis ah = axis_h(g), aw = axis_w(g);
     auto th = table_t3(ah), tw = table_t3(aw);
     int64_t lmin = INT64_MAX, ntaps = 0;

@@ -119,6 +119,7 @@ struct WgradCfg {
     int BN, nbs, mblocks, nblk64, gz;
     int64_t base_tiles;
     bool row = false;  // narrow-channel row kernel
+    int kimg = 64;     // images per k-block (64 or 128)
 };
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 

@@ -26,7 +26,7 @@ struct WgradParams {
     float* out;             // dW (gz == 1) or partials [gz][OC][FH*FW][C]
     int FH, FW, sh, sw, ph, pw;
     int N, OC, C;
-    int mblocks, nbs, gz, nblk64;
+    int mblocks, nbs, gz, nblk64;  // nblk64: image blocks of KIMG (64 or 128) images
     long long num_tiles;
     long long part_stride;  // OC*FH*FW*C
 };
@@ -35,12 +35,13 @@ struct WgradParams {
 // an MN-major swizzle atom column.  BF16: SWIZZLE_128B (16 B chunks, 8-row
 // K groups, SBO 1 KB).  TF32: SWIZZLE_128B_BASE32B (32 B chunks, 4-row K
 // groups, SBO 512 B) -- the MN-major layout tcgen05 kind::tf32 requires.
-template <int BN, bool kTF32 = false>
+template <int BN, bool kTF32 = false, int KIMG = 64>
 struct WgradShape {
     static constexpr int EB = kTF32 ? 4 : 2;
     static constexpr int CH = 128 / EB;                 // channels per box
-    static constexpr int A_BYTES = (128 / CH) * 8192;   // 128 OC x 64 images
-    static constexpr int B_BYTES = (BN / CH) * 8192;    // BN IC x 64 images
+    static constexpr int ATOM = KIMG * 128;             // one box: 128 B of channels x KIMG images
+    static constexpr int A_BYTES = (128 / CH) * ATOM;   // 128 OC x KIMG images
+    static constexpr int B_BYTES = (BN / CH) * ATOM;    // BN IC x KIMG images
     static constexpr int UK = 32 / EB;                  // K (images) per MMA
     static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -78,11 +79,11 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     return c;
 }
 
-template <int BN, bool kTF32 = false>
+template <int BN, bool kTF32 = false, int KIMG = 64>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
-    using S = WgradShape<BN, kTF32>;
+    using S = WgradShape<BN, kTF32, KIMG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
@@ -134,16 +135,16 @@ __global__ void __launch_bounds__(256, 1)
                         ptx::mbar_arrive_expect_tx(&full[stage], S::A_BYTES);
 #pragma unroll
                         for (int j = 0; j < 128 / S::CH; ++j)
-                            ptx::tma_load_4d(sa + j * 8192, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow, oh,
-                                             n64 * 64);
+                            ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow, oh,
+                                             n64 * KIMG);
                     } else {
                         const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
                         const int iw = ow * p.sw + c.fw - p.pw;
                         ptx::mbar_arrive_expect_tx(&full[stage], S::B_BYTES);
 #pragma unroll
                         for (int j = 0; j < BN / S::CH; ++j)
-                            ptx::tma_load_4d(sa + S::A_BYTES + j * 8192, &tmX, &full[stage], c.nb * BN + j * S::CH, iw,
-                                             ih, n64 * 64);
+                            ptx::tma_load_4d(sa + S::A_BYTES + j * S::ATOM, &tmX, &full[stage], c.nb * BN + j * S::CH,
+                                             iw, ih, n64 * KIMG);
                     }
                 }
                 __syncwarp();
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256, 1)
         // ---------------- MMA issuer (whole warp, elected lane issues)
         constexpr uint32_t idesc = ptx::instr_desc(128, BN, kTF32, true, true);
         // MN-major: LBO 8 KB between 128 B channel atoms, SBO = one K group (8 x / 4 x 128 B)
-        const uint64_t dconst = kTF32 ? ptx::smem_desc_mn_b32(0, 8192, 512) : ptx::smem_desc_sw128(0, 8192, 1024);
+        const uint64_t dconst = kTF32 ? ptx::smem_desc_mn_b32(0, S::ATOM, 512) : ptx::smem_desc_sw128(0, S::ATOM, 1024);
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const WTile c = wdecode(t, p);
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(256, 1)
                 const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES) >> 4);
                 if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 64 / S::UK; ++kk)  // 64 images = 4 x K16 (bf16) / 8 x K8 (tf32)
+                    for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
                         ptx::mma_ss<kTF32>(d, ad + uint64_t(kk * (S::KSTEP >> 4)), bd + uint64_t(kk * (S::KSTEP >> 4)),
                                            idesc, ((kb - c.kb0) | kk) != 0);
                     ptx::mma_commit(&empty[stage]);
