@@ -286,7 +286,10 @@ def run_gpu(args):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if n_gpus > 1:
+    # the data-parallel path (NCCL dW all_reduce) runs for N > 1; CKS_BENCH_DIST=1
+    # exercises it with a single rank under torchrun (testing on one GPU)
+    use_dist = n_gpus > 1 or (os.environ.get("CKS_BENCH_DIST") == "1" and "RANK" in os.environ)
+    if use_dist:
         dist.init_process_group("nccl", device_id=device)
     build.build()
     desc, layers = get_config(args.config, args.batch)
@@ -330,7 +333,7 @@ def run_gpu(args):
 
     def step(sync_read=True):
         graph.replay()
-        if n_gpus > 1:
+        if use_dist:
             with torch.cuda.stream(stream):
                 dist.all_reduce(flat)
         if sync_read:
@@ -342,7 +345,7 @@ def run_gpu(args):
             flush.fill_(1.0)
             step()
     # ---- timed region
-    if n_gpus > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     per_op_ms = [0.0] * len(ops_seq)
@@ -354,7 +357,7 @@ def run_gpu(args):
             flush.fill_(float(_))
             t_start.record(stream)
             ms = step()
-            if n_gpus > 1:
+            if use_dist:
                 t_end.record(stream)
                 stream.synchronize()
                 step_ms.append(t_start.elapsed_time(t_end))
@@ -368,60 +371,125 @@ def run_gpu(args):
     # splits on a side stream; then the backward chain in reverse layer order
     # (KS-deconv on the main stream) with each layer's Sk-dilated wgrad on a
     # second side stream, released when the layer above finished its deconv.
-    s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
-    graph2 = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph2, stream=stream):
-        main = torch.cuda.current_stream()
-        fork = torch.cuda.Event()
-        fork.record(main)
-        s1.wait_event(fork)
-        s2.wait_event(fork)
-        with torch.cuda.stream(s1):
+    s1, s2, s3 = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
+    # data-parallel: the flat dW is all-reduced in buckets of layers, each
+    # launched (on s3, NCCL) as soon as the bucket's wgrads are done, so the
+    # communication overlaps the rest of the backward chain.  The step graph is
+    # cut at the bucket boundaries; single-GPU runs use one graph.
+    order = list(reversed(range(len(bufs))))  # backward order
+    cuts = []  # index into `order` after which a bucket closes
+    nbuck = int(os.environ.get("CKS_BENCH_BUCKETS", "3"))
+    if use_dist and nbuck > 1:
+        tot, acc = sum(sizes), 0
+        for k, i in enumerate(order):
+            acc += sizes[i]
+            if acc >= tot / nbuck * (len(cuts) + 1) - 1 and k < len(order) - 1:
+                cuts.append(k)
+    cuts.append(len(order) - 1)
+    offs = [0]
+    for sz in sizes:
+        offs.append(offs[-1] + sz)
+    # one graph for the whole step; after the last wgrad of every bucket the
+    # bucket's NCCL all_reduce (captured on s3) overlaps the remaining backward
+    # (host-side external events for this measured ~25 us slower on C2)
+    bucket_of = {}
+    buckets, k0 = [], 0
+    for k1 in cuts:
+        layers_k = order[k0:k1 + 1]
+        buckets.append((offs[min(layers_k)], offs[max(layers_k) + 1]))
+        for i in layers_k:
+            bucket_of[i] = len(buckets) - 1
+        k0 = k1 + 1
+    last_of_bucket = {order[k1]: bi for bi, k1 in enumerate(cuts)}
+    ar_in_graph = os.environ.get("CKS_BENCH_AR_GRAPH", "1") == "1"
+    if use_dist and ar_in_graph:
+        s3.wait_stream(stream)
+        with torch.cuda.stream(s3):  # communicator warm-up on the capture-side stream
+            dist.all_reduce(flat)
+        stream.wait_stream(s3)
+        torch.cuda.synchronize()
+    def capture(ar_graph):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            main = torch.cuda.current_stream()
+            fork = torch.cuda.Event()
+            fork.record(main)
+            s1.wait_event(fork)
+            s2.wait_event(fork)
+            with torch.cuda.stream(s1):
+                for i, b in enumerate(bufs):
+                    if "deconv" in b.lay.ops:
+                        b.run_split(s1.cuda_stream)
+                split_done = torch.cuda.Event()
+                split_done.record(s1)
             for i, b in enumerate(bufs):
+                if "fwd" in b.lay.ops:
+                    b.run("fwd", main.cuda_stream)
+            main.wait_event(split_done)
+            for i in order:
+                b = bufs[i]
+                ev = torch.cuda.Event()
+                ev.record(main)
+                if "wgrad" in b.lay.ops:
+                    s2.wait_event(ev)
+                    with torch.cuda.stream(s2):
+                        b.run("wgrad", s2.cuda_stream)
+                if use_dist and ar_graph and i in last_of_bucket:
+                    # this bucket's dW is complete: NCCL all_reduce captured as graph nodes on s3
+                    done = torch.cuda.Event()
+                    done.record(s2)
+                    s3.wait_event(done)
+                    lo, hi = buckets[last_of_bucket[i]]
+                    with torch.cuda.stream(s3):
+                        dist.all_reduce(flat[lo:hi])
                 if "deconv" in b.lay.ops:
-                    b.run_split(s1.cuda_stream)
-            split_done = torch.cuda.Event()
-            split_done.record(s1)
-        for i, b in enumerate(bufs):
-            if "fwd" in b.lay.ops:
-                b.run("fwd", main.cuda_stream)
-        main.wait_event(split_done)
-        for i in reversed(range(len(bufs))):
-            b = bufs[i]
-            ev = torch.cuda.Event()
-            ev.record(main)
-            if "wgrad" in b.lay.ops:
-                s2.wait_event(ev)
-                with torch.cuda.stream(s2):
-                    b.run("wgrad", s2.cuda_stream)
-            if "deconv" in b.lay.ops:
-                b.run("deconv_only", main.cuda_stream)
-        join = torch.cuda.Event()
-        join.record(s2)
-        main.wait_event(join)
+                    b.run("deconv_only", main.cuda_stream)
+            join = torch.cuda.Event()
+            join.record(s2)
+            main.wait_event(join)
+            if use_dist and ar_graph:
+                join3 = torch.cuda.Event()
+                join3.record(s3)
+                main.wait_event(join3)
+        return g
+
+    try:
+        graph2 = capture(ar_in_graph)
+    except Exception as exc:  # NCCL capture unavailable: reduce after the graph instead
+        if not (use_dist and ar_in_graph):
+            raise
+        print(f"[bench] NCCL graph capture failed ({exc}); all_reduce after the step graph", file=sys.stderr)
+        torch.cuda.synchronize()
+        ar_in_graph = False
+        graph2 = capture(False)
+    skip_ar = os.environ.get("CKS_BENCH_NOAR") == "1"  # experiments: no collective at all
+
+    def replay_step():
+        graph2.replay()
+        if use_dist and not skip_ar and not ar_in_graph:  # fallback: one all_reduce after the step
+            dist.all_reduce(flat)
+
     noev = []
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             flush.fill_(2.0)
-            graph2.replay()
+            replay_step()
         torch.cuda.synchronize()
-        if n_gpus > 1:
+        if use_dist:
             dist.barrier()
         with ClockSampler(local) as clk:
             for k in range(args.steps):
                 flush.fill_(float(k))
                 t_start.record(stream)
-                graph2.replay()
-                if n_gpus > 1:
-                    dist.all_reduce(flat)
+                replay_step()
                 t_end.record(stream)
                 stream.synchronize()
                 noev.append(t_start.elapsed_time(t_end))
-    if n_gpus > 1:
+    if use_dist:
         dist.barrier()
     serial_ms = sum(step_ms) / args.steps
     total_ms = sum(noev)
-    if n_gpus > 1:
+    if use_dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -461,7 +529,10 @@ def run_gpu(args):
                    "zero_free_gflop_per_gpu_step": round(flops_step / 1e9, 3),
                    "l2": "flushed (256 MB write) before every timed step, outside the timed events",
                    "parallelism": f"dp{n_gpus}",
-                   "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad (CUDA graph)",
+                   "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad (CUDA graph)"
+                               + (("; dW all_reduce in %d buckets overlapping the backward (NCCL in the graph)"
+                                   % len(buckets) if ar_in_graph else "; dW all_reduce after the step graph")
+                                  if use_dist else ""),
                    "serialized_step_ms_with_op_events": round(serial_ms, 5)},
         "per_op": per_op, "roofline": roofline, "gpu_launches": launches_step * args.steps,
         "clocks": clk.summary(),
@@ -483,7 +554,7 @@ def run_gpu(args):
                   file=sys.stderr)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if n_gpus > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 
