@@ -177,10 +177,10 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
         for (auto v : wph_cnt) wb += (v + pb - 1) / pb;
         return rows_h * wb * c.nblk * ((nout + bn - 1) / bn);
     };
-    // Heuristic (tools/sweep_cfg.sh on B200): the largest pixel block (reuse of
-    // B rows and activation columns) that still gives >= 120 tiles; if even one
-    // pixel per tile leaves < 64 tiles, narrower BN; split-K (Z = 2) only for
-    // long K loops (>= 16 row steps) on grids of < 100 tiles.
+    // Heuristic (tools/sweep_cfg.sh, tools/sweep_z.sh on B200): the largest pixel
+    // block (reuse of B rows and activation columns) that still gives >= 120
+    // tiles; if even one pixel per tile leaves < 64 tiles, narrower BN; split-K
+    // (Z = 2) only for long K loops (>= 16 row steps) on grids of < 32 tiles.
     int pbw = int(std::min<int64_t>({256 / c.BN, 8, maxrow}));
     while (pbw > 1 && tiles_for(c.BN, pbw) < 120) --pbw;
     if (tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0)) {
@@ -227,7 +227,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // split-K to fill the SMs (one wave); at least 2 row steps per segment
     const int64_t rs_full = std::max<int64_t>(max_taps_h * c.kc_blocks, 1);
     c.Z = 1;
-    if (c.out_tiles < 100 && rs_full >= 16) c.Z = 2;
+    if (c.out_tiles < 32 && rs_full >= 16) c.Z = 2;  // only very under-filled grids (sweep: Z = 2 at < 100 tiles was slower)
     (void)num_sms;
     if (ov && ov_z > 0) c.Z = int(std::min<int64_t>(ov_z, rs_full));
     c.tiles = c.out_tiles * c.Z;

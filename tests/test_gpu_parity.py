@@ -199,6 +199,20 @@ def test_narrow_wgrad_segments(torch_cuda, gz):
     check(got["wgrad"], ref, "bf16", f"narrow wgrad gz={gz}", red_len(lay, "wgrad"))
 
 
+@pytest.mark.parametrize("lay", [Layer("sk0", 100, 512, 4, 4, 256, 3, 3, 2, 2, 1, 1),
+                                 Layer("sk1", 70, 256, 5, 5, 512, 3, 3, 2, 2, 1, 1),
+                                 Layer("sk2", 129, 384, 3, 3, 128, 3, 3, 1, 1, 1, 1)],
+                         ids=lambda l: l.name)
+def test_igemm_split_k_small_grid(torch_cuda, lay):
+    """Under-filled grids (< 32 output tiles, >= 16 row steps) take the in-kernel
+    deterministic split-K (Z = 2, last-arriving CTA sums the partials)."""
+    check_full(torch_cuda, lay, "bf16", config=6, idx=int(lay.name[2:]))
+    a, got = run_all(torch_cuda, lay, "bf16", config=6, idx=int(lay.name[2:]))
+    _, again = run_all(torch_cuda, lay, "bf16", config=6, idx=int(lay.name[2:]))
+    for op in got:
+        assert np.array_equal(got[op], again[op]), f"{op} not deterministic"
+
+
 def test_sharded_step_single_gpu(torch_cuda):
     """The batch-sharded arithmetic of dist.py on one GPU: two shards run
     sequentially, partial dW summed on the host == full-batch oracle."""
