@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--layers", action="store_true", help="per-layer breakdown on stderr")
+    ap.add_argument("--no-zins", action="store_true", help="skip the zero-inserted-formulation comparison")
     return ap.parse_args()
 
 
@@ -537,6 +538,10 @@ def run_gpu(args):
         "per_op": per_op, "roofline": roofline, "gpu_launches": launches_step * args.steps,
         "clocks": clk.summary(),
     }
+    # ---- the zero-inserted / zero-padded formulation on the same kernels
+    if not args.no_zins and n_gpus == 1:
+        fam_cks = {"fwd": fam["fwd"][0], "deconv": fam["deconv"][0] + fam["split"][0], "wgrad": fam["wgrad"][0]}
+        line["zins"] = run_zins(torch, bufs, max(3, min(args.steps, 20)), device, flush, fam_cks, args.layers)
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
         line["e2e"] = run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, max(2, min(args.steps, 10)), device)
@@ -557,6 +562,77 @@ def run_gpu(args):
     if use_dist:
         dist.destroy_process_group()
     return 0
+
+
+def run_zins(torch, bufs, steps, device, flush, cks_ms, per_layer):
+    """Time cks_zins_* (KB-ZINS: the operands materialised with every padded and
+    inserted zero, then the same tensor-core kernels with nothing left to
+    trim) exactly like the serialized C-K-S ops: one CUDA graph with event
+    nodes between the ops, L2 flushed before every replay.  Reports the time
+    ratio next to the nominal (Table III) / zero-free FLOP ratio."""
+    from paper_2306_15951_b200 import _lib as L
+    seq = []
+    for i, b in enumerate(bufs):
+        for op in ("fwd", "deconv", "wgrad"):
+            if op in b.lay.ops:
+                seq.append((i, op))
+    code = {"fwd": L.CKS_OP_FWD, "deconv": L.CKS_OP_DECONV, "wgrad": L.CKS_OP_WGRAD}
+    need = max(L.cks_zins_workspace_size(bufs[i].g, L.CKS_BF16, code[op]) for i, op in seq)
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+    dw = torch.empty(max(b.dW.numel() for b in bufs), dtype=torch.float32, device=device)
+
+    def run(i, op, sp):
+        b = bufs[i]
+        if op == "fwd":
+            L.cks_zins_conv2d_fwd(b.g, L.CKS_BF16, b.X.data_ptr(), b.W.data_ptr(), b.Y.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), sp)
+        elif op == "deconv":
+            L.cks_zins_deconv2d(b.g, L.CKS_BF16, b.G.data_ptr(), b.W.data_ptr(), b.dX.data_ptr(), ws.data_ptr(),
+                                ws.numel(), sp)
+        else:
+            L.cks_zins_wgrad(b.g, L.CKS_BF16, b.X.data_ptr(), b.G.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+                             ws.numel(), sp)
+
+    stream = torch.cuda.Stream(device)
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(seq) + 1)]
+    with torch.cuda.stream(stream):
+        for i, op in seq:
+            run(i, op, stream.cuda_stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        sp = torch.cuda.current_stream().cuda_stream
+        for k, (i, op) in enumerate(seq):
+            evs[k].record()
+            run(i, op, sp)
+        evs[-1].record()
+    acc = [0.0] * len(seq)
+    with torch.cuda.stream(stream):
+        for it in range(steps + 2):
+            flush.fill_(float(it))
+            graph.replay()
+            stream.synchronize()
+            if it >= 2:
+                for k in range(len(seq)):
+                    acc[k] += evs[k].elapsed_time(evs[k + 1]) / steps
+    ms = {"fwd": 0.0, "deconv": 0.0, "wgrad": 0.0}
+    nominal = {"fwd": 0, "deconv": 0, "wgrad": 0}
+    zf = {"fwd": 0, "deconv": 0, "wgrad": 0}
+    tkey = {"fwd": "T_conv", "deconv": "T_deconv", "wgrad": "T_dilated"}
+    for k, (i, op) in enumerate(seq):
+        ms[op] += acc[k]
+        cnt = L.cks_op_counts(bufs[i].g)
+        nominal[op] += cnt[tkey[op]]
+        zf[op] += bufs[i].flops
+        if per_layer:
+            print(f"  zins {bufs[i].lay.name:22s} {op:7s} {acc[k] * 1e3:9.2f} us", file=sys.stderr)
+    return {"what": "cks_zins_*: zero-padded (fwd) / zero-inserted (deconv, wgrad) operands materialised in HBM "
+                    "(P:114, Eqs (1)-(3) as written) + the same tcgen05 kernels; serialized graph, L2 flushed",
+            "ms": {k: round(v, 5) for k, v in ms.items() if v},
+            "cks_ms": {k: round(v, 5) for k, v in cks_ms.items() if v},
+            "time_ratio_zins_over_cks": {k: round(ms[k] / cks_ms[k], 3) for k in ms if ms[k] and cks_ms.get(k)},
+            "nominal_over_zero_free_flops": {k: round(nominal[k] / zf[k], 3) for k in ms if zf[k]},
+            "steps": steps}
 
 
 def run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, steps, device):

@@ -162,6 +162,37 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]);
 cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, int c_packed_given,
                             int* launches);
 
+/* ------------------------------------------------------------ KB-ZINS
+ * The formulation C-K-S removes, for measurement ("measured
+ * time of the zero-inserted formulation vs C-K-S"): each call materialises the
+ * operand of the textbook definition with all its structural zeros in the
+ * workspace and runs the same tensor-core kernels on it, which then have no
+ * zero to skip.  Results equal the C-K-S entry points (same sums, the extra
+ * terms are exact zeros); only the time differs.
+ *   cks_zins_conv2d_fwd  Eq (1) on Xpad = X zero-padded by (ph, pw) (Fig. 1
+ *                        P:47), convolved with stride (sh, sw) and no padding.
+ *   cks_zins_deconv2d    Eq (2) as P:114 states it: Z = dY with (sh-1, sw-1)
+ *                        zeros inserted between elements, padded by
+ *                        q = F-1-p before and q + r after (r = (I+2p-F) mod s,
+ *                        reading c10), convolved with stride 1 by W^rot180
+ *                        with I_C / O_C swapped (built by Stage1 at unit
+ *                        stride into the workspace).
+ *   cks_zins_wgrad       Eq (3): the zero-inserted dY (+ r trailing
+ *                        rows / columns) is the filter of a unit-stride
+ *                        convolution over X padded by (ph, pw).
+ * Arguments, layouts, dtypes and errors as for the C-K-S entry point of the
+ * same operator; ws must hold cks_zins_workspace_size(op) bytes (staged
+ * operand + rotated filter + the inner call's workspace) and is required.
+ * Errors of the inner geometry (e.g. a staged extent > CKS_MAX_ROWS rows)
+ * are returned as for the inner call. */
+cks_status cks_zins_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, size_t* bytes);
+cks_status cks_zins_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y,
+                               void* ws, size_t ws_bytes, void* stream);
+cks_status cks_zins_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w, float* dx,
+                             void* ws, size_t ws_bytes, void* stream);
+cks_status cks_zins_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
+                          void* ws, size_t ws_bytes, void* stream);
+
 const char* cks_status_string(cks_status s);
 int cks_version(void);
 

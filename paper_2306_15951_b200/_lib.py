@@ -20,7 +20,8 @@ STATUS = {0: "CKS_OK", 1: "CKS_ERR_NULL", 2: "CKS_ERR_GEOMETRY", 3: "CKS_ERR_UNS
 # Every symbol include/cks.h declares (tests check the .so exports all of them).
 EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2d_fwd", "cks_ks_split_size",
            "cks_ks_split", "cks_deconv2d", "cks_dilated_wgrad", "cks_axis_table", "cks_op_counts",
-           "cks_launch_count", "cks_status_string", "cks_version")
+           "cks_launch_count", "cks_status_string", "cks_version", "cks_zins_workspace_size",
+           "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad")
 
 
 class CksError(RuntimeError):
@@ -64,6 +65,10 @@ def lib():
                                          C.POINTER(C.c_int64), sz, C.POINTER(sz)]),
             "cks_op_counts": (C.c_int, [G, C.c_int, C.POINTER(C.c_int64)]),
             "cks_launch_count": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
+            "cks_zins_workspace_size": (C.c_int, [G, C.c_int, C.c_int, C.POINTER(sz)]),
+            "cks_zins_conv2d_fwd": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_zins_deconv2d": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_zins_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
             "cks_status_string": (C.c_char_p, [C.c_int]),
             "cks_version": (C.c_int, []),
         }
@@ -154,3 +159,25 @@ def cks_launch_count(g: cks_geom, dtype: int, op: int, gz: int = 0, c_packed_giv
     v = C.c_int()
     _check(lib().cks_launch_count(C.byref(g), dtype, op, gz, int(c_packed_given), C.byref(v)), "cks_launch_count")
     return v.value
+
+
+# ------------------------------------------------ KB-ZINS (measurement baseline)
+def cks_zins_workspace_size(g: cks_geom, dtype: int, op: int) -> int:
+    b = C.c_size_t()
+    _check(lib().cks_zins_workspace_size(C.byref(g), dtype, op, C.byref(b)), "cks_zins_workspace_size")
+    return b.value
+
+
+def cks_zins_conv2d_fwd(g, dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_zins_conv2d_fwd(C.byref(g), dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream),
+           "cks_zins_conv2d_fwd")
+
+
+def cks_zins_deconv2d(g, dtype, dy_ptr, w_ptr, dx_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_zins_deconv2d(C.byref(g), dtype, dy_ptr, w_ptr, dx_ptr, ws_ptr, ws_bytes, stream),
+           "cks_zins_deconv2d")
+
+
+def cks_zins_wgrad(g, dtype, x_ptr, dy_ptr, dw_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_zins_wgrad(C.byref(g), dtype, x_ptr, dy_ptr, dw_ptr, ws_ptr, ws_bytes, stream),
+           "cks_zins_wgrad")

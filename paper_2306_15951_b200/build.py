@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcks.so")
 SOURCES = [os.path.join(CSRC, "cks_api.cu"), os.path.join(CSRC, "cks_plan.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("cks_plan.h", "kernels/ptx.cuh", "kernels/igemm.cuh",
-                                                  "kernels/wgrad.cuh", "kernels/aux.cuh")] + \
+                                                  "kernels/wgrad.cuh", "kernels/aux.cuh", "kernels/narrow.cuh")] + \
     [os.path.join(os.path.dirname(PKG), "include", "cks.h")]
 
 

@@ -455,6 +455,95 @@ cks_status check_ws(const WsLayout& L, void* ws, size_t ws_bytes) {
     return CKS_OK;
 }
 
+
+// ---------------------------------------------------------------- KB-ZINS
+// The textbook (zero-inserting / zero-padding) formulation of Eqs (1)-(3),
+// run on the same tensor-core kernels so the measured difference is the
+// structural zeros alone (SURVEY §8(d) "measured time of the zero-inserted
+// formulation"): the staged operand holds every zero of the definition and
+// the inner call has nothing to trim.
+struct ZinsLayout {
+    cks_geom inner;   // geometry of the inner C-K-S call on the staged operand
+    cks_op inner_op;
+    int64_t Hs, Ws, Cs, Hd, Wd, Cd;  // staging: source / destination extents
+    int ish, isw, top, left;         // insertion strides and leading zeros
+    size_t stage = 0, filt = 0, inner_ws = 0, total = 0, inner_ws_bytes = 0;
+};
+
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+ZinsLayout zins_layout(const cks_geom& g, cks_dtype dt, cks_op op) {
+    ZinsLayout Z;
+    const Axis ah = axis_h(g), aw = axis_w(g);
+    const int64_t rh = g.H + 2 * g.ph - g.FH - (ah.O - 1) * g.sh;  // output padding r (reading c10)
+    const int64_t rw = g.W + 2 * g.pw - g.FW - (aw.O - 1) * g.sw;
+    Z.inner = g;
+    if (op == CKS_OP_FWD) {  // Eq (1): explicit Xpad, unpadded conv
+        Z.Hs = g.H, Z.Ws = g.W, Z.Cs = Z.Cd = g.C;
+        Z.ish = Z.isw = 1, Z.top = g.ph, Z.left = g.pw;
+        Z.Hd = g.H + 2 * g.ph, Z.Wd = g.W + 2 * g.pw;
+        Z.inner.H = Z.Hd, Z.inner.W = Z.Wd, Z.inner.ph = Z.inner.pw = 0;
+        Z.inner_op = CKS_OP_FWD;
+    } else if (op == CKS_OP_DECONV) {  // Eq (2): zero_insert(dY) padded q / q + r, conv with W^rot180
+        const int64_t qh = g.FH - 1 - g.ph, qw = g.FW - 1 - g.pw;
+        Z.Hs = ah.O, Z.Ws = aw.O, Z.Cs = g.OC, Z.Cd = pad_ch(g.OC, dt);
+        Z.ish = g.sh, Z.isw = g.sw, Z.top = int(qh), Z.left = int(qw);
+        Z.Hd = (ah.O - 1) * g.sh + 1 + 2 * qh + rh, Z.Wd = (aw.O - 1) * g.sw + 1 + 2 * qw + rw;
+        Z.inner = cks_geom{g.N, Z.Cd, Z.Hd, Z.Wd, g.C, g.FH, g.FW, 1, 1, 0, 0, 1, 1};
+        Z.inner_op = CKS_OP_FWD;
+    } else {  // Eq (3): the zero-inserted dY (+ r trailing rows) is the filter of a unit-stride conv
+        Z.Hs = ah.O, Z.Ws = aw.O, Z.Cs = Z.Cd = g.OC;
+        Z.ish = g.sh, Z.isw = g.sw, Z.top = Z.left = 0;
+        Z.Hd = (ah.O - 1) * g.sh + 1 + rh, Z.Wd = (aw.O - 1) * g.sw + 1 + rw;
+        Z.inner.sh = Z.inner.sw = 1;
+        Z.inner_op = CKS_OP_WGRAD;
+    }
+    const size_t eb = size_t(elem_bytes(dt));
+    size_t off = 0;
+    Z.stage = off;
+    off += al256(size_t(g.N) * Z.Hd * Z.Wd * Z.Cd * eb);
+    Z.filt = off;
+    if (op == CKS_OP_DECONV) {
+        cks_geom g1 = g;
+        g1.sh = g1.sw = 1;  // Stage1 with unit stride = rot180 with channels swapped: [IC][FH*FW][OCp] (OHWI)
+        off += al256(ks_split_bytes(g1, dt));
+    }
+    Z.inner_ws = off;
+    Z.inner_ws_bytes = validate(&Z.inner) == CKS_OK ? ws_layout(Z.inner, dt, Z.inner_op, 0, false, kPlanSMs).total : 0;
+    Z.total = off + Z.inner_ws_bytes;
+    return Z;
+}
+
+cks_status launch_zero_insert(const ZinsLayout& Z, cks_dtype dt, int64_t N, const void* src, void* dst,
+                              cudaStream_t st) {
+    const int64_t eb = elem_bytes(dt);
+    const long long rows = N * Z.Hd;
+    if (rows > 0x7fffffffLL) return CKS_ERR_UNSUPPORTED;
+    if ((Z.Cs * eb) % 16 == 0 && (Z.Cd * eb) % 16 == 0) {
+        const int v = int(16 / eb);
+        return launch_pdl(zero_insert_kernel<uint4>, dim3(unsigned(rows)), dim3(256), 0, st,
+                          static_cast<const uint4*>(src), static_cast<uint4*>(dst), int(Z.Hs), int(Z.Ws),
+                          int(Z.Cs / v), int(Z.Hd), int(Z.Wd), int(Z.Cd / v), Z.ish, Z.isw, Z.top, Z.left);
+    }
+    if (dt == CKS_BF16)
+        return launch_pdl(zero_insert_kernel<uint16_t>, dim3(unsigned(rows)), dim3(256), 0, st,
+                          static_cast<const uint16_t*>(src), static_cast<uint16_t*>(dst), int(Z.Hs), int(Z.Ws),
+                          int(Z.Cs), int(Z.Hd), int(Z.Wd), int(Z.Cd), Z.ish, Z.isw, Z.top, Z.left);
+    return launch_pdl(zero_insert_kernel<uint32_t>, dim3(unsigned(rows)), dim3(256), 0, st,
+                      static_cast<const uint32_t*>(src), static_cast<uint32_t*>(dst), int(Z.Hs), int(Z.Ws),
+                      int(Z.Cs), int(Z.Hd), int(Z.Wd), int(Z.Cd), Z.ish, Z.isw, Z.top, Z.left);
+}
+
+cks_status zins_prepare(const cks_geom* g, cks_dtype dt, cks_op op, void* ws, size_t ws_bytes, ZinsLayout* Z) {
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    *Z = zins_layout(*g, dt, op);
+    if ((s = validate(&Z->inner)) != CKS_OK) return s;
+    if (!ws || ws_bytes < Z->total) return CKS_ERR_WORKSPACE;
+    if (!aligned16(ws)) return CKS_ERR_ALIGNMENT;
+    return CKS_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -765,6 +854,60 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;
     return CKS_OK;
+}
+
+cks_status cks_zins_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, size_t* bytes) {
+    if (!g || !bytes) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
+    const ZinsLayout Z = zins_layout(*g, dt, op);
+    if ((s = validate(&Z.inner)) != CKS_OK) return s;
+    *bytes = Z.total;
+    return CKS_OK;
+}
+
+cks_status cks_zins_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y, void* ws,
+                               size_t ws_bytes, void* stream) {
+    if (!g || !x || !w || !y || !ws) return CKS_ERR_NULL;
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y)) return CKS_ERR_ALIGNMENT;
+    ZinsLayout Z;
+    cks_status s = zins_prepare(g, dt, CKS_OP_FWD, ws, ws_bytes, &Z);
+    if (s != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    if ((s = launch_zero_insert(Z, dt, g->N, x, base + Z.stage, st)) != CKS_OK) return s;
+    return cks_conv2d_fwd(&Z.inner, dt, base + Z.stage, w, y, base + Z.inner_ws, Z.inner_ws_bytes, stream);
+}
+
+cks_status cks_zins_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w, float* dx, void* ws,
+                             size_t ws_bytes, void* stream) {
+    if (!g || !dy || !w || !dx || !ws) return CKS_ERR_NULL;
+    if (!aligned16(dy) || !aligned16(w) || !aligned16(dx)) return CKS_ERR_ALIGNMENT;
+    ZinsLayout Z;
+    cks_status s = zins_prepare(g, dt, CKS_OP_DECONV, ws, ws_bytes, &Z);
+    if (s != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    cks_geom g1 = *g;
+    g1.sh = g1.sw = 1;
+    if ((s = launch_split(g1, dt, w, base + Z.filt, st)) != CKS_OK) return s;  // W^rot180, OHWI with O=IC, I=OCp
+    if ((s = launch_zero_insert(Z, dt, g->N, dy, base + Z.stage, st)) != CKS_OK) return s;
+    return cks_conv2d_fwd(&Z.inner, dt, base + Z.stage, base + Z.filt, dx, base + Z.inner_ws, Z.inner_ws_bytes,
+                          stream);
+}
+
+cks_status cks_zins_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, void* ws,
+                          size_t ws_bytes, void* stream) {
+    if (!g || !x || !dy || !dw || !ws) return CKS_ERR_NULL;
+    if (!aligned16(x) || !aligned16(dy) || !aligned16(dw)) return CKS_ERR_ALIGNMENT;
+    ZinsLayout Z;
+    cks_status s = zins_prepare(g, dt, CKS_OP_WGRAD, ws, ws_bytes, &Z);
+    if (s != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    if ((s = launch_zero_insert(Z, dt, g->N, dy, base + Z.stage, st)) != CKS_OK) return s;
+    return cks_dilated_wgrad(&Z.inner, dt, x, base + Z.stage, dw, 0, base + Z.inner_ws, Z.inner_ws_bytes, stream);
 }
 
 }  // extern "C"

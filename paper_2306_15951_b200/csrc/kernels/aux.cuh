@@ -3,6 +3,8 @@
 //   KB-REDUCE  fixed-order G_Z aggregation of Sk-dilated partials
 //   KB-PAD     zero-padded channel staging for rows not a 16-byte multiple
 //              ("last dimensions ... implicitly padded to multiples of 4")
+//   KB-ZINS    staging of the zero-inserted / zero-padded operand of the
+//              textbook formulation (measurement baseline, not the C-K-S path)
 #pragma once
 #include <cstdint>
 
@@ -94,6 +96,35 @@ __global__ void pad_channels_kernel(const T* __restrict__ src, T* __restrict__ d
         const long long r = i / Cp;
         const int c = int(i - r * Cp);
         dst[i] = c < C ? src[r * C + c] : T(0);
+    }
+}
+
+// KB-ZINS staging (the formulation C-K-S avoids: zero insertion P:114, Fig. 1
+// and zero padding, Eqs (1)-(3) as written).  One block per destination row
+// (n, i); in units of V (a 16-byte vector when both channel counts allow it):
+//   dst[n][i][j][c] = src[n][(i-top)/sh][(j-left)/sw][c]  if i-top, j-left are
+//                     non-negative multiples of sh, sw inside the source and
+//                     c < Cs,  else 0.
+template <typename V>
+__global__ void __launch_bounds__(256) zero_insert_kernel(const V* __restrict__ src, V* __restrict__ dst, int Hs,
+                                                          int Ws, int Cs, int Hd, int Wd, int Cd, int sh, int sw,
+                                                          int top, int left) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    const long long row = blockIdx.x;  // n * Hd + i
+    const int n = int(row / Hd), i = int(row - static_cast<long long>(n) * Hd);
+    const int di = i - top;
+    const int si = di >= 0 && di % sh == 0 ? di / sh : -1;
+    const bool live_row = si >= 0 && si < Hs;
+    V* out = dst + row * Wd * Cd;
+    const V* in = src + (static_cast<long long>(n) * Hs + (live_row ? si : 0)) * Ws * Cs;
+    const V zero = V();  // V is a raw bit type: uint4, uint32_t (fp32) or uint16_t (bf16)
+    for (int q = threadIdx.x; q < Wd * Cd; q += blockDim.x) {
+        const int j = q / Cd, c = q - j * Cd;
+        const int dj = j - left;
+        V v = zero;
+        if (live_row && dj >= 0 && dj % sw == 0 && dj / sw < Ws && c < Cs) v = in[(dj / sw) * Cs + c];
+        out[q] = v;
     }
 }
 

@@ -144,3 +144,57 @@ def dilated_wgrad(x, dy, filter_hw, stride=1, padding=0, gz=0, out=None, stream=
     ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_WGRAD, gz), x.device, stream)
     L.cks_dilated_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), gz, *_ws_args(ws), _stream_ptr(stream))
     return out
+
+
+# ----------------------------------------------------------------- KB-ZINS
+# The zero-inserting / zero-padding formulation (include/cks.h KB-ZINS), on the
+# same tensor-core kernels: a measurement baseline for the zeros C-K-S skips.
+def zins_conv2d_fwd(x, w, stride=1, padding=0, out=None, stream=None):
+    """Eq (1) on an explicitly zero-padded X (Fig. 1)."""
+    _check_dev(x, w, out)
+    dt = _dtype_code(x)
+    g = geom_of(tuple(x.shape), tuple(w.shape), stride, padding)
+    OH, OW = L.cks_output_shape(g)
+    if out is None:
+        out = torch.empty((g.N, OH, OW, g.OC), dtype=torch.float32, device=x.device)
+    ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_FWD), x.device, stream)
+    L.cks_zins_conv2d_fwd(g, dt, x.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out
+
+
+def zins_deconv2d(dy, w, x_hw, stride=1, padding=0, out=None, stream=None):
+    """Eq (2) as P:114 states it: zero-inserted, padded dY conv W^rot180."""
+    _check_dev(dy, w, out)
+    dt = _dtype_code(dy)
+    N, _, _, OC = dy.shape
+    _, FH, FW, C = w.shape
+    H, W = x_hw
+    sh, sw = _pair(stride)
+    ph, pw = _pair(padding)
+    g = make_geom(N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+    if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = torch.empty((N, H, W, C), dtype=torch.float32, device=dy.device)
+    ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
+    L.cks_zins_deconv2d(g, dt, dy.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out
+
+
+def zins_wgrad(x, dy, filter_hw, stride=1, padding=0, out=None, stream=None):
+    """Eq (3): the zero-inserted dY as the filter over padded X."""
+    _check_dev(x, dy, out)
+    dt = _dtype_code(x)
+    N, H, W, C = x.shape
+    OC = dy.shape[3]
+    FH, FW = filter_hw
+    sh, sw = _pair(stride)
+    ph, pw = _pair(padding)
+    g = make_geom(N, C, H, W, OC, FH, FW, sh, sw, ph, pw)
+    if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = torch.empty((OC, FH, FW, C), dtype=torch.float32, device=x.device)
+    ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_WGRAD), x.device, stream)
+    L.cks_zins_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out

@@ -334,3 +334,38 @@ def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
         ref = O.wgrad_ref_taps(a["X"], a["dY"], lay.FH, lay.FW, *s, taps)
         check(np.stack([got["wgrad"][:, fh, fw, :] for fh, fw in taps]), ref, "bf16", f"{lay.name} wgrad sampled",
               red_len(lay, "wgrad"))
+
+
+# ------------------------------------------ KB-ZINS (zero-inserted baseline)
+def _zins_layers():
+    lays = [get_config(0)[1][0],
+            Layer("zds", 5, 64, 8, 8, 128, 1, 1, 2, 2, 0, 0),       # 1x1 s2: empty KS phase
+            Layer("zdc", 7, 40, 8, 8, 24, 4, 4, 2, 2, 1, 1),        # DCGAN 4x4 s2 p1
+            Layer("zt", 3, 16, 6, 7, 24, 3, 3, 2, 2, 0, 0),         # output padding r = 1
+            Layer("zn", 9, 3, 16, 16, 64, 7, 7, 2, 2, 3, 3),        # narrow channels (row kernels)
+            Layer("z3", 4, 24, 11, 13, 5, 5, 3, 3, 2, 2, 1)]        # s3, OC not a 16-byte multiple
+    return lays + _rand_layers(6, 31)
+
+
+@pytest.mark.parametrize("lay", _zins_layers(), ids=lambda l: f"{l.name}-{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_zins_formulation_matches_oracle(torch_cuda, lay, dtype):
+    """cks_zins_*: the textbook zero-padding / zero-inserting formulation
+    (Eqs (1)-(3) as written) on the same kernels equals the oracle --
+    the extra terms are exact zeros."""
+    torch = torch_cuda
+    from paper_2306_15951_b200 import ops as K
+    a = make_layer_inputs(lay, 12, 0, dtype)
+    X, W, G = dev(torch, a["X"], dtype), dev(torch, a["W"], dtype), dev(torch, a["dY"], dtype)
+    s, p = (lay.sh, lay.sw), (lay.ph, lay.pw)
+    y = K.zins_conv2d_fwd(X, W, s, p)
+    dx = K.zins_deconv2d(G, W, (lay.H, lay.W), s, p)
+    dw = K.zins_wgrad(X, G, (lay.FH, lay.FW), s, p)
+    torch.cuda.synchronize()
+    g = (lay.sh, lay.sw, lay.ph, lay.pw)
+    check(y.cpu().numpy(), O.conv_ref(a["X"], a["W"], *g), dtype, f"{lay} zins fwd", red_len(lay, "fwd"))
+    check(dx.cpu().numpy(), O.deconv_ref(a["dY"], a["W"], lay.H, lay.W, *g), dtype, f"{lay} zins deconv",
+          lay.FH * lay.FW * lay.OC)
+    OH, OW = lay.out_hw()
+    check(dw.cpu().numpy(), O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, *g), dtype, f"{lay} zins wgrad",
+          lay.N * ((OH - 1) * lay.sh + 1) * ((OW - 1) * lay.sw + 1))

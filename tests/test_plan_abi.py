@@ -151,3 +151,28 @@ def test_narrow_row_path_plan():
     # row pitch not a multiple of 16 bytes -> padded per-tap path
     g = L.make_geom(70, 3, 33, 33, 64, 3, 3, 1, 1, 1, 1)
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 3
+
+
+def test_zins_workspace_holds_the_zero_inserted_operand():
+    """KB-ZINS workspace = staged operand with every structural zero of the
+    textbook formulation (+ rotated filter + inner workspace): the sizes follow
+    from P:114 / Table III's O_H^p = (O_H - 1)*sh + 1."""
+    N, C, I, OC, F, s, p = 128, 64, 32, 128, 3, 2, 1
+    g = L.make_geom(N, C, I, I, OC, F, F, s, s, p, p)
+    O_ = (I + 2 * p - F) // s + 1                      # 16
+    r = (I + 2 * p - F) % s                            # output padding (reading c10): 1
+    q = F - 1 - p
+    zd = (O_ - 1) * s + 1 + 2 * q + r                  # deconv staging extent: 34 = I + F - 1
+    assert zd == I + F - 1
+    assert L.cks_zins_workspace_size(g, L.CKS_BF16, L.CKS_OP_DECONV) >= N * zd * zd * OC * 2 + C * F * F * OC * 2
+    zw = (O_ - 1) * s + 1 + r                          # wgrad: zero-inserted dY = unit-stride output extent
+    assert zw == I + 2 * p - F + 1
+    assert L.cks_zins_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD) >= N * zw * zw * OC * 2
+    assert L.cks_zins_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) >= N * (I + 2 * p) ** 2 * C * 2
+    lib = L.lib()
+    assert lib.cks_zins_deconv2d(ctypes.byref(g), 1, 16, 16, 16, None, 0, None) == 1     # ws required
+    assert lib.cks_zins_wgrad(ctypes.byref(g), 1, 16, 16, 16, 16, 0, None) == 5          # ws too small
+    bad = L.make_geom(1, 4, 8, 8, 8, 3, 3, 1, 1, 3, 1)
+    with pytest.raises(L.CksError) as e:
+        L.cks_zins_workspace_size(bad, L.CKS_BF16, L.CKS_OP_FWD)
+    assert e.value.status == 2
