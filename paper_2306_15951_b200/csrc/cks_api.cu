@@ -74,6 +74,15 @@ int debug_flags() {
     return f;
 }
 
+// TMA-store epilogue for every igemm tile (0: only the last tile per CTA; experiments)
+bool epi_tma_all() {
+    static const bool on = [] {
+        const char* e = getenv("CKS_EPI_TMA");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 // fp32 output map (TMA store), 128B swizzle
 bool make_tmap4_f32(CUtensorMap* m, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
                     const uint32_t box[4]) {
@@ -175,12 +184,14 @@ cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUte
                           int smem, cudaStream_t st) {
     auto kern = igemm_kernel<BN, TF, KB>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
-    long long grid = std::min<long long>(p.num_tiles, device_sms() / p.cm * p.cm);  // whole clusters
+    // cluster split-K: one output tile per cluster of zsplit CTAs, one tile per CTA
+    const int cl = p.zc ? p.zsplit : p.cm;
+    long long grid = p.zc ? p.num_tiles : std::min<long long>(p.num_tiles, device_sms() / p.cm * p.cm);  // whole clusters
     if (grid < 1) grid = 1;
-    if (p.cm > 1 &&
+    if (cl > 1 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return last_cuda();
-    return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(256), smem, st, p.cm, a, b, y, p);
+    return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(256), smem, st, cl, a, b, y, p);
 }
 
 template <bool TF, int KB>
@@ -213,6 +224,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     IgemmCfg cfg = cfg_in;
     if (debug_flags() & 16) {  // experiment: no split-K
         cfg.Z = 1;
+        cfg.zc = 0;
         cfg.tiles = cfg.out_tiles;
     }
     IgemmParams p;
@@ -245,6 +257,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.out_W = out_W;
     p.out_C = out_C;
     p.zsplit = cfg.Z;
+    p.zc = cfg.zc;
     p.fd_z = make_fastdiv(uint32_t(cfg.Z));
     p.fd_nbs = make_fastdiv(uint32_t(cfg.nbs));
     p.fd_nblk = make_fastdiv(uint32_t(cfg.nblk));
@@ -266,8 +279,8 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.cm = cfg.cm;
     p.unified = cfg.unified;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
-                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes : 0);
-    if (cfg.Z > 1) {
+                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes + 1024 : 0);
+    if (cfg.Z > 1 && !cfg.zc) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
         p.sem = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + L.sem);
@@ -284,7 +297,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
         uint64_t d[4] = {uint64_t(out_C), uint64_t(out_W), uint64_t(out_H), uint64_t(N)};
         uint64_t sb[3] = {uint64_t(out_C) * 4, uint64_t(out_W) * out_C * 4, uint64_t(out_H) * out_W * out_C * 4};
         uint32_t box[4] = {32, 1, 1, 32};
-        if (make_tmap4_f32(&ty, out, d, sb, box)) p.tma_store = 1;
+        if (make_tmap4_f32(&ty, out, d, sb, box)) p.tma_store = (cfg.epi && epi_tma_all()) ? 2 : 1;
     }
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }

@@ -124,7 +124,7 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -132,6 +132,7 @@ struct Knobs {
         if (const char* e = getenv("CKS_UNIFIED")) unified = atoi(e) != 0;
         if (const char* e = getenv("CKS_MCAST")) mcast = atoi(e) == 1;
         if (const char* e = getenv("CKS_WGRAD_KIMG")) kimg128 = atoi(e) == 128;
+        if (const char* e = getenv("CKS_IGEMM_ZC")) zc = atoi(e) != 0;  // 0: legacy global split-K
     }
 };
 static const Knobs& knobs() {
@@ -154,7 +155,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     IgemmCfg c;
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
     c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
-    const int64_t budget = kSmemBudget - (c.epi ? kEpiStageBytes : 0);
+    const int64_t budget = kSmemBudget - (c.epi ? kEpiStageBytes + 1024 : 0);  // + 1 KB alignment of the staging
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
     c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);
@@ -227,9 +228,26 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // split-K to fill the SMs (one wave); at least 2 row steps per segment
     const int64_t rs_full = std::max<int64_t>(max_taps_h * c.kc_blocks, 1);
     c.Z = 1;
-    if (c.out_tiles < 32 && rs_full >= 16) c.Z = 2;  // only very under-filled grids (sweep: Z = 2 at < 100 tiles was slower)
-    (void)num_sms;
-    if (ov && ov_z > 0) c.Z = int(std::min<int64_t>(ov_z, rs_full));
+    c.zc = 0;
+    // cluster split-K (zc): Z in {2, 4, 8} CTAs per output tile while the grid
+    // stays one wave (out_tiles * Z <= SMs) with >= 2 row steps per segment; the
+    // tile's fp32 accumulators are staged in the idle rings for the DSMEM reduce
+    const int64_t ring = int64_t(c.a_stages) * c.apos * 128 * c.KB + int64_t(c.stages) * c.stage_bytes;
+    const bool zc_ok = knobs().zc && int64_t(128) * c.pbw * c.BN * 4 <= ring;
+    if (zc_ok) {
+        int z = 8;
+        while (z > 1 && (c.out_tiles * z > num_sms || rs_full < 2 * z)) z /= 2;
+        if (z > 1) {
+            c.Z = z;
+            c.zc = 1;
+        }
+    } else if (c.out_tiles < 32 && rs_full >= 16) {
+        c.Z = 2;  // legacy global split-K: only very under-filled grids (sweep: Z = 2 at < 100 tiles was slower)
+    }
+    if (ov && ov_z > 0) {
+        c.Z = int(std::min<int64_t>(ov_z, rs_full));
+        c.zc = zc_ok && c.Z > 1 && c.Z <= 8 && c.out_tiles * c.Z <= num_sms;
+    }
     c.tiles = c.out_tiles * c.Z;
     // A-tile multicast across the BN blocks of one pixel (thread-block cluster):
     // every CTA loads 128/cm of the images of each activation column
@@ -417,7 +435,7 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
     if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
     if ((op == CKS_OP_FWD && !row) || op == CKS_OP_DECONV) {
         IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
-        if (c.Z > 1) {
+        if (c.Z > 1 && !c.zc) {
             take(size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4, L.partial, L.partial_bytes);
             take(size_t(c.out_tiles) * 4, L.sem, L.sem_bytes);
         }

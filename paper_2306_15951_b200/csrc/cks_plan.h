@@ -73,6 +73,7 @@ struct IgemmCfg {
     int nblk = 1;       // ceil(N / 128)
     int wblocks = 1;
     int Z = 1;          // split-K segments
+    int zc = 0;         // cluster split-K (Z CTAs of one cluster per output tile, DSMEM reduce)
     int kc_blocks = 1;
     int KB = 128;       // bytes per K row: 32 / 64 / 128 (swizzle width)
     int ntap = 1;       // taps per filter row (B box)

@@ -28,10 +28,15 @@
 //                 (Stage1), a0 = oh_s = u + a_y, out = u*sh + ih_s (T2): the
 //                 epilogue is Stage3's phase-strided composition.
 //
-// Under-filled grids split the row steps into Z segments (split-K); each
-// segment writes fp32 partials and the LAST arriving CTA of an output tile
-// sums the Z partials in fixed order z = 0..Z-1 (deterministic, no extra
-// launch, no inter-CTA waiting).
+// Under-filled grids split the row steps into Z segments (split-K).  Cluster
+// split-K (zc, the default): the Z CTAs of one thread-block cluster compute
+// the Z segments of ONE output tile (one tile per CTA), stage their fp32
+// accumulators in their own (then idle) shared-memory rings, and after a
+// cluster barrier CTA r sums column slice r of the tile over z = 0..Z-1 in
+// fixed order through distributed shared memory and stores it
+// (deterministic; no global partials, no counters, no extra launch).
+// Legacy global split-K: each segment writes fp32 partials and the LAST
+// arriving CTA of an output tile sums the Z partials in fixed order.
 //
 // Warp roles (256 threads, 1 CTA/SM, persistent over tiles):
 //   warp 0 lane 0  TMA producer (B-row ring + A-position ring, mbarriers)
@@ -86,11 +91,13 @@ struct IgemmParams {
     int unit_step;             // consecutive pixels' tap-0 columns differ by 1 (N-merged MMAs)
     int a0_step;               // a0 of pixel j = a0 of pixel 0 + j * a0_step (T1: stride, T2: 1)
     int zsplit;
+    int zc;  // cluster split-K: cluster = the zsplit segments of one output tile, DSMEM reduction
     FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
     int cm;               // cluster size along the O_C blocks: the A tile of a pixel is multicast (1 = off)
     int unified;          // one A slot per row step: A slot + B row share one full/empty barrier pair
-    int tma_store;        // last tile per CTA: stage in the idle rings, TMA-store the output
+    int tma_store;        // 1: last tile per CTA staged in the idle rings and TMA-stored; 2: also every
+                          // other tile, through the per-warp 4 KB epilogue buffers
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
@@ -241,7 +248,8 @@ __global__ void __launch_bounds__(256, 1)
     KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
     // 2 program slots x (2 header + 2 x 64 entries)
     int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));
-    float* epi = reinterpret_cast<float*>(prog + 2 * kProgSlot);  // epilogue staging (p.epi_stage): 4 x 4 KB
+    // epilogue staging (p.epi_stage): 4 x 4 KB, 1 KB aligned (128B-swizzled TMA-store source)
+    float* epi = reinterpret_cast<float*>(smem + ((ptx::smem_u32(prog + 2 * kProgSlot) - ptx::smem_u32(smem) + 1023u) & ~1023u));
     {
         const uint4* src = reinterpret_cast<const uint4*>(&p.ah);
         uint4* dst = reinterpret_cast<uint4*>(tab);
@@ -542,6 +550,47 @@ __global__ void __launch_bounds__(256, 1)
             const bool any = c.rs1 > c.rs0;
             // the CTA's last tile: the smem rings are idle (all MMAs done), so stage
             // 32x32 fp32 blocks there (128B swizzle) and write full lines by TMA store
+            // other tiles (p.tma_store == 2): the same 32x32 blocks through this warp's
+            // 4 KB epilogue buffer, one TMA store in flight per warp (the buffer is
+            // reused once the previous store has read it): async full-line stores
+            if (p.tma_store == 2 && !split && t + gridDim.x < p.num_tiles && !(p.dbg & 1)) {
+                float* blk = epi + sub * 1024;
+#pragma unroll 1
+                for (int j = 0; j < c.len; ++j) {
+                    const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
+                                           c0, r);
+                        ptx::tmem_ld_wait();
+                        if (c0 >= cvalid) continue;
+                        if (ptx::elect_one()) ptx::bulk_wait_read0();  // previous store has read the buffer
+                        __syncwarp();
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 v = live ? make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                                __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                            *reinterpret_cast<float4*>(blk + lane * 32 + ((q ^ (lane & 7)) << 2)) = v;
+                        }
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (ptx::elect_one()) {
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], tab[0].out[c.rh], nrow0);
+                            ptx::bulk_commit();
+                        }
+                        __syncwarp();
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+                if (++acc == uint32_t(p.acc_stages)) {
+                    acc = 0;
+                    acc_ph ^= 1;
+                }
+                continue;
+            }
             if (p.tma_store && !split && t + gridDim.x >= p.num_tiles && !(p.dbg & 1)) {
                 uint8_t* stg = smem + sub * uint32_t(c.len * (BN / 32)) * 4096u;
                 int k = 0;
@@ -586,7 +635,9 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < c.len; ++j) {
                 const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
                 float* dst = nullptr;
-                if (split)  // column group q = (j*BN + c)/4 of row `row`
+                if (split && p.zc)  // own smem (idle rings): column group q = (j*BN + c)/4, [q][128 rows] float4
+                    dst = reinterpret_cast<float*>(smem) + (j * (BN / 4)) * 512 + row * 4;
+                else if (split)  // column group q = (j*BN + c)/4 of row `row`
                     dst = p.part + ((c.out_tile * p.zsplit + c.z) * (pw_cols / 4) + j * (BN / 4)) * 512LL + row * 4;
                 else if (n < p.N)
                     dst = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
@@ -653,7 +704,7 @@ __global__ void __launch_bounds__(256, 1)
                 acc = 0;
                 acc_ph ^= 1;
             }
-            if (split) {
+            if (split && !p.zc) {
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (et == 0) {
@@ -712,7 +763,65 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
     __syncthreads();
-    if (p.cm > 1) ptx::cluster_sync();  // no CTA leaves while peers may still signal it
+    if (p.zc) {
+        // cluster split-K reduce: every rank's segment is staged in its smem
+        ptx::cluster_sync();
+        if (warp >= 4 && blockIdx.x < p.num_tiles && !(p.dbg & 1)) {
+            const Tile c = decode_tile(blockIdx.x, p, tab[0], tab[1]);
+            const int row = int(threadIdx.x) - 128;  // accumulator row = image
+            const int n = c.nblk * 128 + row;
+            const int G = c.len * (BN / 4);  // float4 column groups of the tile
+            const int g0 = (c.z * G) / p.zsplit, g1 = ((c.z + 1) * G) / p.zsplit;
+            const int cbase = c.nb * BN;
+            const int cvalid = min(BN, p.out_C - cbase);
+            const uint32_t sbase = ptx::smem_u32(smem) + uint32_t(row) * 16u;
+            if (n < p.N) {
+                // two column groups x Z ranks of DSMEM loads in flight, then the fixed-order sums
+#pragma unroll 1
+                for (int gq = g0; gq < g1; gq += 2) {
+                    const bool two = gq + 1 < g1;
+                    const uint32_t off = sbase + uint32_t(gq) * 2048u;
+                    float4 a[8], b[8];
+#pragma unroll
+                    for (int z = 0; z < 8; ++z) {
+                        if (z < p.zsplit) {
+                            a[z] = ptx::ld_dsmem_f4(ptx::mapa(off, uint32_t(z)));
+                            if (two) b[z] = ptx::ld_dsmem_f4(ptx::mapa(off + 2048u, uint32_t(z)));
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && !two) break;
+                        float4 v = h ? b[0] : a[0];
+#pragma unroll
+                        for (int z = 1; z < 8; ++z) {  // fixed order z = 0..Z-1
+                            if (z < p.zsplit) {
+                                const float4 w = h ? b[z] : a[z];
+                                v.x += w.x;
+                                v.y += w.y;
+                                v.z += w.z;
+                                v.w += w.w;
+                            }
+                        }
+                        const int gg = gq + h;
+                        const int j = gg / (BN / 4), cc = (gg % (BN / 4)) * 4;
+                        if (cc >= cvalid) continue;
+                        float* o = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                                            tab[1].out[c.j0 + j]) * p.out_C + cbase + cc;
+                        if ((p.out_C % 4) == 0 && cc + 4 <= cvalid) {
+                            *reinterpret_cast<float4*>(o) = v;
+                        } else {
+                            const float e[4] = {v.x, v.y, v.z, v.w};
+                            for (int u = 0; u < 4 && cc + u < cvalid; ++u) o[u] = e[u];
+                        }
+                    }
+                }
+            }
+        }
+        ptx::cluster_sync();  // peers finished reading this CTA's staging
+    } else if (p.cm > 1) {
+        ptx::cluster_sync();  // no CTA leaves while peers may still signal it
+    }
     if (threadIdx.x == 0) trace_gt(p, 5);
     if (warp == 2) {
         ptx::tc_fence_after();
