@@ -217,6 +217,16 @@ cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const C
     return launch_igemm_kb<false, 128>(BN, a, b, y, p, smem, st);
 }
 
+// experiments: print the igemm tile plan (CKS_PLAN_DEBUG set; host only, before any CUDA call)
+void plan_debug(const IgemmCfg& cfg) {
+    static const bool plan_dbg = getenv("CKS_PLAN_DEBUG") != nullptr;
+    if (plan_dbg)
+        fprintf(stderr, "[cks plan] igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d "
+                        "out_tiles=%lld Z=%d zc=%d kc=%d\n",
+                cfg.BN, cfg.pbw, cfg.KB, cfg.ntap, cfg.pa, cfg.apos, cfg.stages, cfg.a_stages, cfg.unified,
+                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks);
+}
+
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
 cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRow>& rh, const std::vector<KRow>& rw,
                      const CUtensorMap& ta, const CUtensorMap& tb, float* out, int out_H, int out_W, int out_C,
@@ -638,6 +648,7 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
         wsrc = wp;
     }
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
+    plan_debug(cfg);
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
@@ -694,6 +705,7 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
     }
     const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
     IgemmCfg cfg = igemm_cfg_deconv(*g, dt, kPlanSMs);
+    plan_debug(cfg);
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
@@ -846,6 +858,7 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]) {
     out[4] = 2 * (g->C * g->N * g->H * g->W * g->FH * g->FW * g->OC);
     out[5] = 2 * (g->OC * g->FH * g->FW * g->C * OHp * OWp) * g->N;
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
+    plan_debug(cfg);
     const int64_t Cp = pad_ch(g->C, dt), BK = cfg.KB / elem_bytes(dt);
     out[6] = int64_t(cfg.nblk) * 128 * int64_t(cfg.nbs) * cfg.BN * VH * VW * ((Cp + BK - 1) / BK * BK);
     out[7] = cfg.tiles;

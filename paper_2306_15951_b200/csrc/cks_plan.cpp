@@ -230,14 +230,17 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     c.Z = 1;
     c.zc = 0;
     // cluster split-K (zc): Z in {2, 4, 8} CTAs per output tile while the grid
-    // stays one wave (out_tiles * Z <= SMs) with >= 2 row steps per segment; the
+    // stays one wave (out_tiles * Z <= SMs) with >= 2 row steps per segment and
+    // >= 8 row steps saved per tile; the
     // tile's fp32 accumulators are staged in the idle rings for the DSMEM reduce
     const int64_t ring = int64_t(c.a_stages) * c.apos * 128 * c.KB + int64_t(c.stages) * c.stage_bytes;
     const bool zc_ok = knobs().zc && int64_t(128) * c.pbw * c.BN * 4 <= ring;
     if (zc_ok) {
         int z = 8;
         while (z > 1 && (c.out_tiles * z > num_sms || rs_full < 2 * z)) z /= 2;
-        if (z > 1) {
+        // the DSMEM reduce costs a few row steps: split only when >= 8 row steps
+        // per tile are saved (tools/sweep_zc.sh on the C2 layers)
+        if (z > 1 && rs_full * (z - 1) >= 8 * z) {
             c.Z = z;
             c.zc = 1;
         }
