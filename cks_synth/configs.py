@@ -84,6 +84,20 @@ def _c4(N=512):
             Layer("G32to64", N, 3, 64, 64, 128, 4, 4, 2, 2, 1, 1, ops)]
 
 
+def _c6(N=128):
+    # The paper's second operator test set (Exp. 1, Figs 10/12/14):
+    # 5x5 filters, padding 2, 8 cases with shrinking maps and growing channels.
+    # The per-case shapes are not printed (figures missing), so this follows
+    # the C2 progression, strides 1 and 2.
+    shapes = [(32, 64, 64), (16, 64, 128), (16, 128, 128), (8, 128, 256),
+              (8, 256, 256), (4, 256, 512), (4, 512, 512), (32, 3, 64)]
+    out = []
+    for (I, ic, oc) in shapes:
+        for s in (1, 2):
+            out.append(Layer(f"f5_{I}_{ic}to{oc}_s{s}", N, ic, I, I, oc, 5, 5, s, s, 2, 2))
+    return out
+
+
 CONFIGS = {
     0: ("C1 tiny: N=2 C=4 8x8 OC=8 3x3 s2 p1", _c1),
     1: ("C2 Cifar10 VGG-16 layer sweep N=128, 3x3 p1, s1/s2", _c2),
@@ -91,6 +105,7 @@ CONFIGS = {
     3: ("C4 DCGAN generator 4x4 s2 p1 N=512 (KS-deconv + Sk-dilated)", _c4),
     # C5 (configs[4]) is the C3 layer list as a full train step, batch-sharded.
     4: ("C5 ResNet-18 conv-layer train step, batch-sharded, NCCL wgrad allreduce", _c3),
+    5: ("C6 5x5 p2 layer sweep (the paper's second test set) N=128, s1/s2", _c6),
 }
 
 

@@ -198,3 +198,59 @@ def zins_wgrad(x, dy, filter_hw, stride=1, padding=0, out=None, stream=None):
     ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_WGRAD), x.device, stream)
     L.cks_zins_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
     return out
+
+
+# ------------------------------------------------------- autograd wrappers
+# Conv-layer training through the three C-K-S operators: the
+# forward of a convolution is ConvV2 (Eq 1) and its backward is KS-deconv
+# (Eq 2, dX) + Sk-dilated (Eq 3, dW); a deconvolutional layer (the DCGAN
+# generator) is the mirror image: forward KS-deconv, backward ConvV2 for
+# the input gradient and Sk-dilated for the weight gradient.  The incoming
+# gradient is rounded to the input dtype (bf16 / fp32) before the kernels.
+class CKSConv2dFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, stride, padding):
+        ctx.save_for_backward(x, w)
+        ctx.stride, ctx.padding = _pair(stride), _pair(padding)
+        return conv2d_fwd(x.contiguous(), w.contiguous(), ctx.stride, ctx.padding)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        g = gy.to(x.dtype).contiguous()
+        dx = dw = None
+        if ctx.needs_input_grad[0]:
+            dx = deconv2d(g, w, (x.shape[1], x.shape[2]), ctx.stride, ctx.padding).to(x.dtype)
+        if ctx.needs_input_grad[1]:
+            dw = dilated_wgrad(x, g, (w.shape[1], w.shape[2]), ctx.stride, ctx.padding).to(w.dtype)
+        return dx, dw, None, None
+
+
+class CKSConvTranspose2dFunction(torch.autograd.Function):
+    """y = deconv2D(z, W^rot180) with W in the conv layout OHWI [O_C][F_H][F_W][I_C]
+    (z has O_C channels, y has I_C channels and spatial extent ``out_hw``)."""
+
+    @staticmethod
+    def forward(ctx, z, w, out_hw, stride, padding):
+        ctx.save_for_backward(z, w)
+        ctx.stride, ctx.padding = _pair(stride), _pair(padding)
+        return deconv2d(z.contiguous(), w.contiguous(), tuple(out_hw), ctx.stride, ctx.padding)
+
+    @staticmethod
+    def backward(ctx, gy):
+        z, w = ctx.saved_tensors
+        g = gy.to(z.dtype).contiguous()
+        dz = dw = None
+        if ctx.needs_input_grad[0]:
+            dz = conv2d_fwd(g, w, ctx.stride, ctx.padding).to(z.dtype)
+        if ctx.needs_input_grad[1]:
+            dw = dilated_wgrad(g, z, (w.shape[1], w.shape[2]), ctx.stride, ctx.padding).to(w.dtype)
+        return dz, dw, None, None, None
+
+
+def cks_conv2d(x, w, stride=1, padding=0):
+    return CKSConv2dFunction.apply(x, w, stride, padding)
+
+
+def cks_conv_transpose2d(z, w, out_hw, stride=1, padding=0):
+    return CKSConvTranspose2dFunction.apply(z, w, out_hw, stride, padding)

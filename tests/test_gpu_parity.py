@@ -16,7 +16,10 @@ from cks_synth import Layer, bf16_bits, get_config, make_layer_inputs
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"bf16": 2e-2, "tf32": 5e-3}
+TOL = {"bf16": 2e-2, "tf32": 5e-3,
+       # gradients returned in the input dtype by the autograd wrappers: one extra
+       # rounding of the fp32 result to bf16 (u = 2^-9) / none for fp32
+       "bf16_grad": 2e-2, "tf32_grad": 5e-3}
 U32 = 2.0 ** -24  # fp32 unit roundoff
 
 
@@ -60,6 +63,8 @@ def nrm_err(got, ref):
 def check(got, ref, dtype, what, k=1):
     e = nrm_err(got, ref)
     assert e <= TOL[dtype], f"{what}: normwise error {e:.3e} > {TOL[dtype]}"
+    if dtype == "bf16_grad":
+        assert e <= 2.0 ** -8 + tight_bf16(k), f"{what}: normwise error {e:.3e} > bf16 output rounding bound"
     if dtype == "bf16":
         assert e <= tight_bf16(k), f"{what}: normwise error {e:.3e} > tight bound {tight_bf16(k):.2e}"
     return e
@@ -282,7 +287,7 @@ def test_wgrad_gz_segments_deterministic(torch_cuda, gz):
 # ------------------------------------------- config layers, reduced batch
 def _config_layers():
     out = []
-    for cfg in (1, 2, 3):
+    for cfg in (1, 2, 3, 5):
         for i, lay in enumerate(get_config(cfg)[1]):
             if lay.name.startswith(("l1_", "l2_", "l3_", "l4_")) and not lay.name.endswith("_0"):
                 continue  # repeated shapes
@@ -308,7 +313,7 @@ def test_config_layers_reduced_batch_tf32(torch_cuda, cfg, i, lay):
 
 
 # ------------------------------------------ full size, sampled outputs
-@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3)][::2] +
+@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3, 5)][::2] +
                          [c for c in _config_layers() if c[0] == 2][::3],
                          ids=lambda v: v.name if isinstance(v, Layer) else str(v))
 def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
@@ -369,3 +374,50 @@ def test_zins_formulation_matches_oracle(torch_cuda, lay, dtype):
     OH, OW = lay.out_hw()
     check(dw.cpu().numpy(), O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, *g), dtype, f"{lay} zins wgrad",
           lay.N * ((OH - 1) * lay.sh + 1) * ((OW - 1) * lay.sw + 1))
+
+
+# ------------------------------------------------ autograd (conv-layer training)
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_autograd_conv_layer(torch_cuda, dtype):
+    """CKSConv2dFunction: loss = <conv(X, W), T>; autograd's dX, dW come from
+    KS-deconv and Sk-dilated with dY = T -- checked against the
+    oracle definitions."""
+    torch = torch_cuda
+    from paper_2306_15951_b200 import ops as K
+    lay = Layer("ag", 131, 24, 11, 10, 40, 3, 3, 2, 2, 1, 1)
+    a = make_layer_inputs(lay, 13, 0, dtype)
+    X = dev(torch, a["X"], dtype).requires_grad_(True)
+    W = dev(torch, a["W"], dtype).requires_grad_(True)
+    T = dev(torch, a["dY"], dtype)
+    y = K.cks_conv2d(X, W, 2, 1)
+    (y * T.float()).sum().backward()
+    torch.cuda.synchronize()
+    g = (2, 2, 1, 1)
+    check(y.detach().cpu().numpy(), O.conv_ref(a["X"], a["W"], *g), dtype, "autograd fwd", red_len(lay, "fwd"))
+    check(X.grad.float().cpu().numpy(), O.deconv_ref(a["dY"], a["W"], lay.H, lay.W, *g), dtype + "_grad",
+          "autograd dX", red_len(lay, "deconv"))
+    check(W.grad.float().cpu().numpy(), O.wgrad_ref(a["X"], a["dY"], 3, 3, *g), dtype + "_grad", "autograd dW",
+          red_len(lay, "wgrad"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_autograd_generator_layer(torch_cuda, dtype):
+    """CKSConvTranspose2dFunction, a DCGAN generator layer (4x4 s2 p1):
+    forward = KS-deconv of z; backward dz = ConvV2 of dY, dW = Sk-dilated(dY, z)."""
+    torch = torch_cuda
+    from paper_2306_15951_b200 import ops as K
+    lay = Layer("gen", 70, 16, 16, 16, 64, 4, 4, 2, 2, 1, 1)   # conv view: X = the big side (16x16x16)
+    a = make_layer_inputs(lay, 14, 0, dtype)
+    Z = dev(torch, a["dY"], dtype).requires_grad_(True)        # generator input (8x8x64)
+    W = dev(torch, a["W"], dtype).requires_grad_(True)
+    T = dev(torch, a["X"], dtype)                              # upstream gradient of the 16x16x16 output
+    y = K.cks_conv_transpose2d(Z, W, (16, 16), 2, 1)
+    (y * T.float()).sum().backward()
+    torch.cuda.synchronize()
+    g = (2, 2, 1, 1)
+    check(y.detach().cpu().numpy(), O.deconv_ref(a["dY"], a["W"], 16, 16, *g), dtype, "generator fwd",
+          red_len(lay, "deconv"))
+    check(Z.grad.float().cpu().numpy(), O.conv_ref(a["X"], a["W"], *g), dtype + "_grad", "generator dz",
+          red_len(lay, "fwd"))
+    check(W.grad.float().cpu().numpy(), O.wgrad_ref(a["X"], a["dY"], 4, 4, *g), dtype + "_grad", "generator dW",
+          red_len(lay, "wgrad"))
