@@ -191,7 +191,7 @@ cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUte
     if (cl > 1 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return last_cuda();
-    return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(256), smem, st, cl, a, b, y, p);
+    return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(384), smem, st, cl, a, b, y, p);
 }
 
 template <bool TF, int KB>
@@ -222,9 +222,9 @@ void plan_debug(const IgemmCfg& cfg) {
     static const bool plan_dbg = getenv("CKS_PLAN_DEBUG") != nullptr;
     if (plan_dbg)
         fprintf(stderr, "[cks plan] igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d "
-                        "out_tiles=%lld Z=%d zc=%d kc=%d\n",
+                        "out_tiles=%lld Z=%d zc=%d kc=%d epi_warps=%d\n",
                 cfg.BN, cfg.pbw, cfg.KB, cfg.ntap, cfg.pa, cfg.apos, cfg.stages, cfg.a_stages, cfg.unified,
-                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks);
+                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks, cfg.epi_warps);
 }
 
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
@@ -268,6 +268,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.out_C = out_C;
     p.zsplit = cfg.Z;
     p.zc = cfg.zc;
+    p.epi_warps = cfg.epi ? cfg.epi_warps : 4;
     p.fd_z = make_fastdiv(uint32_t(cfg.Z));
     p.fd_nbs = make_fastdiv(uint32_t(cfg.nbs));
     p.fd_nblk = make_fastdiv(uint32_t(cfg.nblk));
@@ -289,7 +290,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.cm = cfg.cm;
     p.unified = cfg.unified;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
-                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? kEpiStageBytes + 1024 : 0);
+                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? epi_stage_bytes(cfg.epi_warps) + 1024 : 0);
     if (cfg.Z > 1 && !cfg.zc) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);

@@ -124,7 +124,7 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -133,6 +133,8 @@ struct Knobs {
         if (const char* e = getenv("CKS_MCAST")) mcast = atoi(e) == 1;
         if (const char* e = getenv("CKS_WGRAD_KIMG")) kimg128 = atoi(e) == 128;
         if (const char* e = getenv("CKS_IGEMM_ZC")) zc = atoi(e) != 0;  // 0: legacy global split-K
+        // 1: 8 epilogue warps where free, 2: always (measured: no gain, tools/ab.sh) -- experiments
+        if (const char* e = getenv("CKS_EPI8")) epi8 = atoi(e);
     }
 };
 static const Knobs& knobs() {
@@ -150,12 +152,14 @@ static bool cfg_override(int& bn, int& pbw, int& z) {
 
 bool epi_staging() { return knobs().epi != 0; }
 
-IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
-                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
+static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout,
+                            int64_t kchan, int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms,
+                            int force_pbw, int epi_warps) {
     IgemmCfg c;
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
     c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
-    const int64_t budget = kSmemBudget - (c.epi ? kEpiStageBytes + 1024 : 0);  // + 1 KB alignment of the staging
+    c.epi_warps = epi_warps;
+    const int64_t budget = kSmemBudget - (c.epi ? epi_stage_bytes(epi_warps) + 1024 : 0);  // + 1 KB alignment
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
     c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);
@@ -260,6 +264,21 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
         else if (c.nbs % 2 == 0) c.cm = 2;
     }
     return c;
+}
+
+// 8 epilogue warps (two per TMEM sub-partition, twice the output stores in
+// flight) when their 4 KB staging buffers cost no pipeline depth or tile width.
+IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
+                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
+    const IgemmCfg c4 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
+                                    force_pbw, 4);
+    if (knobs().epi8 == 0) return c4;
+    const IgemmCfg c8 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
+                                    force_pbw, 8);
+    const bool same = c8.pbw == c4.pbw && c8.apos == c4.apos && c8.stages == c4.stages &&
+                      c8.a_stages == c4.a_stages && c8.unified == c4.unified && c8.BN == c4.BN && c8.Z == c4.Z &&
+                      c8.zc == c4.zc;
+    return (same || knobs().epi8 == 2) ? c8 : c4;
 }
 
 static int64_t max_window(const std::vector<KRow>& rows) {

@@ -99,6 +99,7 @@ struct IgemmParams {
     int tma_store;        // 1: last tile per CTA staged in the idle rings and TMA-stored; 2: also every
                           // other tile, through the per-warp 4 KB epilogue buffers
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
+    int epi_warps;        // epilogue warps: 4 (one per TMEM sub-partition) or 8 (two, alternate 32-column chunks)
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
 };
@@ -221,7 +222,7 @@ __device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
 }
 
 template <int BN, bool kTF32, int KB>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ IgemmParams p) {
     using S = IgemmShape<BN, kTF32, KB>;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 128);
+            ptx::mbar_init(&tempty[i], 32 * p.epi_warps);
             ptx::mbar_init(&pfull[i], 32);
             ptx::mbar_init(&pempty[i], 32);
         }
@@ -297,6 +298,8 @@ __global__ void __launch_bounds__(256, 1)
         // rows (all taps of one filter row, one box).
         const bool is_b = warp == 3;
         uint32_t aq = 0, bq = 0;  // A / B sequence numbers
+        uint32_t as = 0, aph = 0, bs = 0, bph = 0;  // ring slots / phases, stepped (no runtime division)
+        const uint32_t na = uint32_t(p.a_stages), nb = uint32_t(p.b_stages);
         int ti = 0;
         const int trole = warp == 0 ? 0 : 4;
         if (lane == 0) trace_ev(p, trole, ti, 0);
@@ -309,7 +312,6 @@ __global__ void __launch_bounds__(256, 1)
                 const int rq = int(fdivu(uint32_t(r), p.fd_kc));
                 const int ch = c.chs + rq, kc = r - rq * p.kc_blocks;
                 if (is_b) {
-                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
                     uint64_t* bf = p.unified ? &afull[bs] : &bfull[bs];
                     ptx::mbar_wait(p.unified ? &aempty[bs] : &bempty[bs], bph ^ 1);
                     if (ptx::elect_one()) {
@@ -324,10 +326,13 @@ __global__ void __launch_bounds__(256, 1)
                     __syncwarp();
                     if (lane == 0) trace_ev(p, trole, ti, 1);
                     ++bq;
+                    if (++bs == nb) {
+                        bs = 0;
+                        bph ^= 1u;
+                    }
                     continue;
                 }
                 for (int iw0 = c.pos_lo; iw0 < c.pos_hi; iw0 += p.apos) {
-                    const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
                     ++aq;
                     ptx::mbar_wait(&aempty[as], aph ^ 1);
                     if (ptx::elect_one()) {
@@ -349,6 +354,10 @@ __global__ void __launch_bounds__(256, 1)
                     }
                     __syncwarp();
                     if (lane == 0) trace_ev(p, trole, ti, 2);
+                    if (++as == na) {
+                        as = 0;
+                        aph ^= 1u;
+                    }
                 }
             }
         }
@@ -357,7 +366,9 @@ __global__ void __launch_bounds__(256, 1)
             // ---------------- MMA issuer (single thread)
             // K-major SW128 descriptor without the start address: LBO 16 B, SBO 1 KB
             const uint64_t dconst = ptx::smem_desc_kmajor(0, KB);
-            uint32_t aq = 0, bq = 0, acc = 0, acc_ph = 0;
+            uint32_t acc = 0, acc_ph = 0;
+            uint32_t as = 0, aph = 0, bs = 0, bph = 0;  // ring slots / phases, stepped (no runtime division)
+            const uint32_t na = uint32_t(p.a_stages), nb = uint32_t(p.b_stages);
             int ti = 0;
             if (lane == 0) trace_ev(p, 1, ti, 0);
             uint32_t ps = 0, pph = 0;
@@ -375,7 +386,6 @@ __global__ void __launch_bounds__(256, 1)
                 const uint32_t idesc0 = ptx::instr_desc(128, 0, kTF32, false, false);
                 bool first = true;
                 for (int ri = rs0; ri < rs1; ++ri) {
-                    const uint32_t bs = bq % uint32_t(p.b_stages), bph = (bq / uint32_t(p.b_stages)) & 1u;
                     if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
                     if (lane == 0) trace_ev(p, 1, ti, 1);
                     const uint64_t bdesc0 = dconst | uint64_t(ptx::smem_u32(bbuf + bs * p.b_stage_bytes) >> 4);
@@ -384,8 +394,6 @@ __global__ void __launch_bounds__(256, 1)
                     first = false;
                     int e = 0;
                     for (int k = 0; pos_lo + k * p.apos < pos_hi; ++k) {
-                        const uint32_t as = aq % uint32_t(p.a_stages), aph = (aq / uint32_t(p.a_stages)) & 1u;
-                        ++aq;
                         ptx::mbar_wait(&afull[as], aph);
                         if (lane == 0) trace_ev(p, 1, ti, 2);
                         ptx::tc_fence_after();
@@ -418,10 +426,17 @@ __global__ void __launch_bounds__(256, 1)
                         }
                         __syncwarp();
                         if (lane == 0) trace_ev(p, 1, ti, 4);
+                        if (++as == na) {
+                            as = 0;
+                            aph ^= 1u;
+                        }
                     }
                     if (!p.unified && ptx::elect_one()) ptx::mma_commit(&bempty[bs]);  // B row free
                     __syncwarp();
-                    ++bq;
+                    if (++bs == nb) {
+                        bs = 0;
+                        bph ^= 1u;
+                    }
                 }
                 ptx::mbar_arrive(&pempty[ps]);  // program slot consumed (all 32 lanes)
                 if (++ps == 2) {
@@ -525,12 +540,16 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && int(warp) < 4 + p.epi_warps) {
         // ---------------- epilogue: TMEM -> registers -> fp32 stores
-        // (thread = accumulator row = one image; 16-byte vector stores)
+        // (thread = accumulator row = one image; 16-byte vector stores).  With 8
+        // epilogue warps, warps w and w + 4 share TMEM sub-partition w & 3 and
+        // take alternate 32-column chunks (twice the stores in flight).
         const uint32_t sub = warp & 3;  // TMEM sub-partition: lanes [32*sub, 32*sub+32)
+        const uint32_t ew = warp - 4;   // epilogue warp 0..epi_warps-1
+        const uint32_t half = ew >> 2, nhalf = uint32_t(p.epi_warps) >> 2;
         const int row = int(sub * 32 + lane);
-        const int et = threadIdx.x - 128;  // 0..127
+        const int et = threadIdx.x - 128;  // 0..32*epi_warps-1
         uint32_t acc = 0, acc_ph = 0;
         const int pw_cols = p.pbw * BN;
         const bool split = p.zsplit > 1;
@@ -554,12 +573,12 @@ __global__ void __launch_bounds__(256, 1)
             // 4 KB epilogue buffer, one TMA store in flight per warp (the buffer is
             // reused once the previous store has read it): async full-line stores
             if (p.tma_store == 2 && !split && t + gridDim.x < p.num_tiles && !(p.dbg & 1)) {
-                float* blk = epi + sub * 1024;
+                float* blk = epi + ew * 1024;
 #pragma unroll 1
                 for (int j = 0; j < c.len; ++j) {
                     const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
 #pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                    for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
                         uint32_t r[32];
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
                                            c0, r);
@@ -593,12 +612,12 @@ __global__ void __launch_bounds__(256, 1)
             }
             if (p.tma_store && !split && t + gridDim.x >= p.num_tiles && !(p.dbg & 1)) {
                 uint8_t* stg = smem + sub * uint32_t(c.len * (BN / 32)) * 4096u;
-                int k = 0;
 #pragma unroll 1
                 for (int j = 0; j < c.len; ++j) {
                     const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
 #pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 32, ++k) {
+                    for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
+                        const int k = j * (BN / 32) + c0 / 32;
                         uint32_t r[32];
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
                                            c0, r);
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(256, 1)
                                    tab[1].out[c.j0 + j]) * p.out_C + cbase;
                 const int lim = split ? BN : cvalid;
 #pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
                     uint32_t r[32];
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN + c0,
                                    r);
@@ -657,7 +676,7 @@ __global__ void __launch_bounds__(256, 1)
                     if (stage) {
                         // transpose through a 128B-swizzled 32 x 32 block: 8 lanes write one
                         // image's 32 channels (128 B, a full line) per store instruction
-                        float* blk = epi + sub * 1024;
+                        float* blk = epi + ew * 1024;
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
                             *reinterpret_cast<float4*>(blk + lane * 32 + ((q ^ (lane & 7)) << 2)) =
@@ -706,7 +725,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             if (split && !p.zc) {
                 __threadfence();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");
                 if (et == 0) {
                     const int old = atomicAdd(&p.sem[c.out_tile], 1);
                     const int last = old == p.zsplit - 1;
@@ -714,9 +733,9 @@ __global__ void __launch_bounds__(256, 1)
                     *red_flag = last;
                     __threadfence();
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");
                 if (et == 0) trace_ev(p, 2, ti, 3);
-                if (*red_flag && n < p.N) {
+                if (*red_flag && n < p.N && half == 0) {
                     // last segment: sum the Z partials in order z = 0..Z-1; thread = row,
                     // 8 column groups x Z vector loads in flight, coalesced 512 B per warp load
                     const float4* base = reinterpret_cast<const float4*>(p.part) +
@@ -757,7 +776,7 @@ __global__ void __launch_bounds__(256, 1)
                         }
                     }
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");  // red_flag reuse guard
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");  // red_flag reuse guard
                 if (et == 0) trace_ev(p, 2, ti, 4);
             }
         }
@@ -766,7 +785,7 @@ __global__ void __launch_bounds__(256, 1)
     if (p.zc) {
         // cluster split-K reduce: every rank's segment is staged in its smem
         ptx::cluster_sync();
-        if (warp >= 4 && blockIdx.x < p.num_tiles && !(p.dbg & 1)) {
+        if (warp >= 4 && warp < 8 && blockIdx.x < p.num_tiles && !(p.dbg & 1)) {
             const Tile c = decode_tile(blockIdx.x, p, tab[0], tab[1]);
             const int row = int(threadIdx.x) - 128;  // accumulator row = image
             const int n = c.nblk * 128 + row;
