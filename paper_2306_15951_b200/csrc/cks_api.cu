@@ -313,10 +313,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }
 
-template <int BN, bool TF, int KIMG>
+template <int BN, bool TF, int KIMG, int MT = 1>
 cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
-    using S = WgradShape<BN, TF, KIMG>;
-    auto kern = wgrad_kernel<BN, TF, KIMG>;
+    using S = WgradShape<BN, TF, KIMG, MT>;
+    auto kern = wgrad_kernel<BN, TF, KIMG, MT>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
@@ -458,8 +458,18 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.nblk64 = cfg.nblk64;
     p.num_tiles = cfg.base_tiles * cfg.gz;
     p.part_stride = part_stride;
+    p.ouw_s = 1 << 20;
+    p.ouw_e = -(1 << 20);
+    for (auto& b : tw)
+        if (b.oh_e > b.oh_s) {
+            p.ouw_s = std::min<int>(p.ouw_s, int(b.oh_s));
+            p.ouw_e = std::max<int>(p.ouw_e, int(b.oh_e));
+        }
+    if (p.ouw_e < p.ouw_s) p.ouw_e = p.ouw_s = 0;
     const bool tf = dt == CKS_TF32;
     const bool k128 = cfg.kimg == 128;
+    if (cfg.mt == 3 && !tf && cfg.BN == 64)  // row tiles: the F_W = 3 taps of a filter row share the dY block
+        return k128 ? launch_wgrad_t<64, false, 128, 3>(ta, tb, p, st) : launch_wgrad_t<64, false, 64, 3>(ta, tb, p, st);
 #define CKS_WG(BN_)                                                                                   \
     (tf ? (k128 ? launch_wgrad_t<BN_, true, 128>(ta, tb, p, st) : launch_wgrad_t<BN_, true, 64>(ta, tb, p, st)) \
         : (k128 ? launch_wgrad_t<BN_, false, 128>(ta, tb, p, st) : launch_wgrad_t<BN_, false, 64>(ta, tb, p, st)))

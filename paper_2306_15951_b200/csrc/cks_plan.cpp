@@ -124,7 +124,7 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -135,6 +135,7 @@ struct Knobs {
         if (const char* e = getenv("CKS_IGEMM_ZC")) zc = atoi(e) != 0;  // 0: legacy global split-K
         // 1: 8 epilogue warps where free, 2: always (measured: no gain, tools/ab.sh) -- experiments
         if (const char* e = getenv("CKS_EPI8")) epi8 = atoi(e);
+        if (const char* e = getenv("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
     }
 };
 static const Knobs& knobs() {
@@ -404,16 +405,39 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     // small enough for a 4-deep ring (BN = 64); measured slower for BN >= 128
     c.kimg = (g.N >= 128 && c.BN == 64 && knobs().kimg128) ? 128 : 64;
     c.nblk64 = int((g.N + c.kimg - 1) / c.kimg);
+    // row tiles (all F_W = 3 taps of a filter row per tile, the dY block shared):
+    // bf16, IC <= 64 (three double-buffered 64-column accumulators fit TMEM)
+    c.mt = (dt == CKS_BF16 && c.BN == 64 && g.FW == 3 && knobs().wmt) ? 3 : 1;
     Axis ah = axis_h(g), aw = axis_w(g);
     auto th = table_t3(ah), tw = table_t3(aw);
+    int64_t uws = INT64_MAX, uwe = INT64_MIN;
+    for (auto& b : tw)
+        if (b.oh_e > b.oh_s) { uws = std::min(uws, b.oh_s); uwe = std::max(uwe, b.oh_e); }
     int64_t lmin = INT64_MAX, ntaps = 0;
-    for (auto& a : th)
+    for (auto& a : th) {
+        if (c.mt > 1) {
+            int64_t L = (a.oh_e - a.oh_s) * std::max<int64_t>(uwe - uws, 0) * c.nblk64;
+            if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
+            continue;
+        }
         for (auto& b : tw) {
             int64_t L = (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
             if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
         }
+    }
     if (ntaps == 0) lmin = 1;
-    c.base_tiles = int64_t(g.FH) * g.FW * c.mblocks * c.nbs;
+    if (c.mt > 1 && lmin < 2048) {  // small maps: row tiles cost parallelism (C2 sweep slower); one tap per tile
+        c.mt = 1;
+        lmin = INT64_MAX;
+        ntaps = 0;
+        for (auto& a : th)
+            for (auto& b : tw) {
+                int64_t L = (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
+                if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
+            }
+        if (ntaps == 0) lmin = 1;
+    }
+    c.base_tiles = int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
     if (gz_req > 0) {
         c.gz = gz_req;
     } else {

@@ -123,6 +123,7 @@ struct WgradCfg {
     int64_t base_tiles;
     bool row = false;  // narrow-channel row kernel
     int kimg = 64;     // images per k-block (64 or 128)
+    int mt = 1;        // taps per tile along w: 1, or F_W (row tiles sharing the dY block)
 };
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 

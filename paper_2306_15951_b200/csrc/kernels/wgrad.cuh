@@ -16,6 +16,15 @@
 // covers k-blocks [z*L/G_Z, (z+1)*L/G_Z) of the tap's L k-blocks; with G_Z > 1
 // each segment writes fp32 partials that KB-REDUCE sums in a fixed order
 // ("the results obtained from each segment are aggregated").
+//
+// Row tiles (MT = F_W taps per tile, narrow-IC layers): a tile is one filter
+// ROW fh and all its F_W taps, each with its own TMEM accumulator; a k-block
+// loads the dY block ONCE and the F_W leaping X columns iw = ow*sw + fw - pw,
+// so the dY operand is shared by F_W MMAs (1/F_W of its L2->SM traffic).  The
+// k range is the union of the taps' trimmed ow ranges; a tap whose ow is
+// outside its own range [ow_s(fw), ow_e(fw)) (T3) neither loads nor multiplies
+// (trimming stays exact).  Only the valid rows of the dY block (O_C channels)
+// are loaded; accumulator rows >= O_C are never stored.
 #pragma once
 #include "ptx.cuh"
 
@@ -23,6 +32,7 @@ namespace cks {
 
 struct WgradParams {
     int16_t oh_s[32], oh_e[32], ow_s[32], ow_e[32];  // T3 per tap row / column
+    int ouw_s, ouw_e;       // row tiles: union of the taps' ow ranges
     float* out;             // dW (gz == 1) or partials [gz][OC][FH*FW][C]
     int FH, FW, sh, sw, ph, pw;
     int N, OC, C;
@@ -35,7 +45,7 @@ struct WgradParams {
 // an MN-major swizzle atom column.  BF16: SWIZZLE_128B (16 B chunks, 8-row
 // K groups, SBO 1 KB).  TF32: SWIZZLE_128B_BASE32B (32 B chunks, 4-row K
 // groups, SBO 512 B) -- the MN-major layout tcgen05 kind::tf32 requires.
-template <int BN, bool kTF32 = false, int KIMG = 64>
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1>
 struct WgradShape {
     static constexpr int EB = kTF32 ? 4 : 2;
     static constexpr int CH = 128 / EB;                 // channels per box
@@ -44,10 +54,11 @@ struct WgradShape {
     static constexpr int B_BYTES = (BN / CH) * ATOM;    // BN IC x KIMG images
     static constexpr int UK = 32 / EB;                  // K (images) per MMA
     static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGE_BYTES = A_BYTES + MT * B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr uint32_t TMEM_COLS = 2 * MT * BN <= 128 ? 128 : 2 * MT * BN <= 256 ? 256 : 512;
+    static_assert(2 * MT * BN <= 512, "two accumulator buffers of MT taps must fit TMEM");
 };
 
 struct WTile {
@@ -57,6 +68,7 @@ struct WTile {
     int ohs, ows;
 };
 
+template <int MT>
 __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     WTile c;
     uint32_t t = uint32_t(t64);  // 32-bit decode (64-bit div/mod is slow)
@@ -67,11 +79,11 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     c.z = int(t % uint32_t(p.gz));
     t /= uint32_t(p.gz);
     const int tap = int(t);
-    c.fh = tap / p.FW;
-    c.fw = tap % p.FW;
+    c.fh = MT > 1 ? tap : tap / p.FW;
+    c.fw = MT > 1 ? 0 : tap % p.FW;
     c.ohs = p.oh_s[c.fh];
-    c.ows = p.ow_s[c.fw];
-    const int hn = p.oh_e[c.fh] - c.ohs, wn = p.ow_e[c.fw] - c.ows;
+    c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
+    const int hn = p.oh_e[c.fh] - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     c.wn = wn;
     const uint32_t L = uint32_t(hn) * uint32_t(wn) * uint32_t(p.nblk64);
     c.kb0 = int(uint64_t(L) * uint32_t(c.z) / uint32_t(p.gz));
@@ -79,11 +91,25 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     return c;
 }
 
-template <int BN, bool kTF32 = false, int KIMG = 64>
+// row tiles: does tap fw see any k-block of the segment (else its partial is 0)?
+__device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& p, int fw) {
+    if (c.kb1 <= c.kb0 || c.wn <= 0) return false;
+    const int s = p.ow_s[fw] - c.ows, e = p.ow_e[fw] - c.ows;  // tap range, relative to the union start
+    if (e <= s) return false;
+    const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
+    if (p1 - p0 + 1 >= c.wn) return true;  // the segment covers every ow
+    for (int q = p0; q <= p1; ++q) {
+        const int w = q % c.wn;
+        if (w >= s && w < e) return true;
+    }
+    return false;
+}
+
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
-    using S = WgradShape<BN, kTF32, KIMG>;
+    using S = WgradShape<BN, kTF32, KIMG, MT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
@@ -123,7 +149,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool is_b = warp == 3;
         uint32_t stage = 0, phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode(t, p);
+            const WTile c = wdecode<MT>(t, p);
             for (int kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = kb % p.nblk64;
                 const int pos = kb / p.nblk64;
@@ -132,19 +158,27 @@ __global__ void __launch_bounds__(256, 1)
                 uint8_t* sa = smem + stage * S::STAGE_BYTES;
                 if (ptx::elect_one()) {
                     if (!is_b) {
-                        ptx::mbar_arrive_expect_tx(&full[stage], S::A_BYTES);
-#pragma unroll
-                        for (int j = 0; j < 128 / S::CH; ++j)
+                        // only the atoms holding valid O_C rows (the rest of the MMA's M rows are never stored)
+                        const int a_atoms = min(128 / S::CH, (p.OC - c.mb * 128 + S::CH - 1) / S::CH);
+                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(a_atoms * S::ATOM));
+                        for (int j = 0; j < a_atoms; ++j)
                             ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow, oh,
                                              n64 * KIMG);
                     } else {
                         const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
-                        const int iw = ow * p.sw + c.fw - p.pw;
-                        ptx::mbar_arrive_expect_tx(&full[stage], S::B_BYTES);
+                        uint32_t nv = 0;
 #pragma unroll
-                        for (int j = 0; j < BN / S::CH; ++j)
-                            ptx::tma_load_4d(sa + S::A_BYTES + j * S::ATOM, &tmX, &full[stage], c.nb * BN + j * S::CH,
-                                             iw, ih, n64 * KIMG);
+                        for (int f = 0; f < MT; ++f) nv += (MT == 1 || (ow >= p.ow_s[f] && ow < p.ow_e[f])) ? 1u : 0u;
+                        ptx::mbar_arrive_expect_tx(&full[stage], nv * S::B_BYTES);
+#pragma unroll
+                        for (int f = 0; f < MT; ++f) {
+                            if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
+                            const int iw = ow * p.sw + (MT > 1 ? f : c.fw) - p.pw;
+#pragma unroll
+                            for (int j = 0; j < BN / S::CH; ++j)
+                                ptx::tma_load_4d(sa + S::A_BYTES + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
+                                                 c.nb * BN + j * S::CH, iw, ih, n64 * KIMG);
+                        }
                     }
                 }
                 __syncwarp();
@@ -161,21 +195,29 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t dconst = kTF32 ? ptx::smem_desc_mn_b32(0, S::ATOM, 512) : ptx::smem_desc_sw128(0, S::ATOM, 1024);
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode(t, p);
+            const WTile c = wdecode<MT>(t, p);
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
-            const uint32_t d = tmem_base + acc * BN;
+            const uint32_t d = tmem_base + acc * (MT * BN);
+            uint32_t started = 0;  // row tiles: taps that already accumulated in this tile
             for (int kb = c.kb0; kb < c.kb1; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
                 const uint64_t ad = dconst | uint64_t(a_addr >> 4);
-                const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES) >> 4);
+                const int ow = c.ows + (kb / p.nblk64) % max(c.wn, 1);
                 if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
-                        ptx::mma_ss<kTF32>(d, ad + uint64_t(kk * (S::KSTEP >> 4)), bd + uint64_t(kk * (S::KSTEP >> 4)),
-                                           idesc, ((kb - c.kb0) | kk) != 0);
+                    for (int f = 0; f < MT; ++f) {
+                        if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
+                        const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES + f * S::B_BYTES) >> 4);
+                        const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
+#pragma unroll
+                        for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
+                            ptx::mma_ss<kTF32>(d + uint32_t(f * BN), ad + uint64_t(kk * (S::KSTEP >> 4)),
+                                               bd + uint64_t(kk * (S::KSTEP >> 4)), idesc, (acc0 | uint32_t(kk)) != 0);
+                        started |= 1u << f;
+                    }
                     ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
@@ -198,24 +240,27 @@ __global__ void __launch_bounds__(256, 1)
         const bool vec4 = (p.C % 4) == 0;
         uint32_t acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode(t, p);
+            const WTile c = wdecode<MT>(t, p);
             const bool zero = c.kb1 <= c.kb0;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             const int oc = c.mb * 128 + row;
             const int cbase = c.nb * BN;
             const int cvalid = min(BN, p.C - cbase);
+#pragma unroll 1
+            for (int f = 0; f < MT; ++f) {
+            const bool fzero = zero || (MT > 1 && !tap_has_work(c, p, f));
             float* dst = nullptr;
             if (oc < p.OC)
-                dst = p.out + c.z * p.part_stride + (static_cast<long long>(oc) * taps + c.fh * p.FW + c.fw) * p.C +
-                      cbase;
+                dst = p.out + c.z * p.part_stride +
+                      (static_cast<long long>(oc) * taps + c.fh * p.FW + (MT > 1 ? f : c.fw)) * p.C + cbase;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r[32];
-                ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * BN + c0, r);
+                ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * (MT * BN) + f * BN + c0, r);
                 ptx::tmem_ld_wait();
                 if (dst != nullptr && c0 < cvalid) {
-                    if (zero) {
+                    if (fzero) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) r[j] = 0u;
                     }
@@ -231,6 +276,7 @@ __global__ void __launch_bounds__(256, 1)
                             if (c0 + j < cvalid) dst[c0 + j] = __uint_as_float(r[j]);
                     }
                 }
+            }
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);

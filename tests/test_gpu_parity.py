@@ -421,3 +421,22 @@ def test_autograd_generator_layer(torch_cuda, dtype):
           red_len(lay, "fwd"))
     check(W.grad.float().cpu().numpy(), O.wgrad_ref(a["X"], a["dY"], 4, 4, *g), dtype + "_grad", "generator dW",
           red_len(lay, "wgrad"))
+
+
+# ------------------------------------- Sk-dilated row tiles (F_W taps per tile)
+@pytest.mark.parametrize("lay,gz", [(Layer("rt0", 130, 64, 40, 40, 48, 3, 3, 1, 1, 1, 1), 0),
+                                    (Layer("rt1", 130, 40, 40, 37, 64, 3, 3, 1, 1, 1, 1), 3),
+                                    (Layer("rt2", 200, 64, 81, 80, 24, 3, 3, 2, 2, 1, 1), 0),
+                                    (Layer("rt3", 130, 64, 40, 40, 64, 3, 3, 1, 1, 0, 0), 7),
+                                    (Layer("rt4", 130, 64, 40, 40, 64, 5, 3, 1, 1, 2, 1), 1)],
+                         ids=lambda v: v.name if isinstance(v, Layer) else f"gz{v}")
+def test_wgrad_row_tiles(torch_cuda, lay, gz):
+    """Large-map 3-wide filters with I_C <= 64 take the row-tile Sk-dilated
+    kernel (one filter row's F_W taps per tile share the dY block, per-tap
+    trimmed ow ranges, O_C < 128 loads only the valid dY rows): against the
+    oracle, for several G_Z segmentations, deterministic on repeat."""
+    a, got = run_all(torch_cuda, lay, "bf16", config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)
+    ref = O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+    check(got["wgrad"], ref, "bf16", f"{lay} row-tile wgrad gz={gz}", red_len(lay, "wgrad"))
+    again = run_all(torch_cuda, lay, "bf16", config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)[1]["wgrad"]
+    np.testing.assert_array_equal(got["wgrad"], again)
