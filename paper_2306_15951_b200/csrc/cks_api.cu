@@ -179,14 +179,16 @@ bool rows_ok(const std::vector<KRow>& rows) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <int BN, bool TF, int KB>
+template <int BN, bool TF, int KB, bool PAIR = false>
 cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const IgemmParams& p,
                           int smem, cudaStream_t st) {
-    auto kern = igemm_kernel<BN, TF, KB>;
+    auto kern = igemm_kernel<BN, TF, KB, PAIR>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     // cluster split-K: one output tile per cluster of zsplit CTAs, one tile per CTA
-    const int cl = p.zc ? p.zsplit : p.cm;
-    long long grid = p.zc ? p.num_tiles : std::min<long long>(p.num_tiles, device_sms() / p.cm * p.cm);  // whole clusters
+    const int cl = p.zc ? p.zsplit : (p.pair ? 2 : p.cm);
+    long long grid = p.zc ? p.num_tiles
+                          : (p.pair ? 2 * std::min<long long>(p.num_tiles, device_sms() / 2)
+                                    : std::min<long long>(p.num_tiles, device_sms() / p.cm * p.cm));  // whole clusters
     if (grid < 1) grid = 1;
     if (cl > 1 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
@@ -207,6 +209,10 @@ cks_status launch_igemm_kb(int BN, const CUtensorMap& a, const CUtensorMap& b, c
 
 cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y,
                         const IgemmParams& p, int smem, cudaStream_t st) {
+    if (p.pair) {  // CTA pairs: bf16, 128 B K blocks, 128 output channels per CTA (plan invariant)
+        if (tf32 || KB != 128 || BN != 128) return CKS_ERR_UNSUPPORTED;
+        return launch_igemm_t<128, false, 128, true>(a, b, y, p, smem, st);
+    }
     if (tf32) {
         if (KB == 32) return launch_igemm_kb<true, 32>(BN, a, b, y, p, smem, st);
         if (KB == 64) return launch_igemm_kb<true, 64>(BN, a, b, y, p, smem, st);
@@ -222,9 +228,9 @@ void plan_debug(const IgemmCfg& cfg) {
     static const bool plan_dbg = getenv("CKS_PLAN_DEBUG") != nullptr;
     if (plan_dbg)
         fprintf(stderr, "[cks plan] igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d "
-                        "out_tiles=%lld Z=%d zc=%d kc=%d epi_warps=%d\n",
+                        "out_tiles=%lld Z=%d zc=%d kc=%d epi_warps=%d pair=%d\n",
                 cfg.BN, cfg.pbw, cfg.KB, cfg.ntap, cfg.pa, cfg.apos, cfg.stages, cfg.a_stages, cfg.unified,
-                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks, cfg.epi_warps);
+                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks, cfg.epi_warps, cfg.pair);
 }
 
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
@@ -268,6 +274,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.out_C = out_C;
     p.zsplit = cfg.Z;
     p.zc = cfg.zc;
+    p.pair = cfg.pair;
     p.epi_warps = cfg.epi ? cfg.epi_warps : 4;
     p.fd_z = make_fastdiv(uint32_t(cfg.Z));
     p.fd_nbs = make_fastdiv(uint32_t(cfg.nbs));
@@ -302,7 +309,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     // the (then idle) A/B rings: 4 warps x PBW x BN/32 blocks of 4 KB
     CUtensorMap ty;
     memset(&ty, 0, sizeof(ty));
-    const int64_t stage_need = int64_t(4) * cfg.pbw * (cfg.BN / 32) * 4096;
+    const int64_t stage_need = int64_t(4) * cfg.pbw * (cfg.BN * (cfg.pair ? 2 : 1) / 32) * 4096;
     const int64_t ring = int64_t(p.a_stages) * p.apos * 128 * cfg.KB + int64_t(p.b_stages) * p.b_stage_bytes;
     if (cfg.Z == 1 && out_C % 4 == 0 && stage_need <= ring && !(debug_flags() & 32)) {
         uint64_t d[4] = {uint64_t(out_C), uint64_t(out_W), uint64_t(out_H), uint64_t(N)};

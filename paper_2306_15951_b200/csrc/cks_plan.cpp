@@ -124,7 +124,7 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -136,6 +136,7 @@ struct Knobs {
         // 1: 8 epilogue warps where free, 2: always (measured: no gain, tools/ab.sh) -- experiments
         if (const char* e = getenv("CKS_EPI8")) epi8 = atoi(e);
         if (const char* e = getenv("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
+        if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
     }
 };
 static const Knobs& knobs() {
@@ -155,8 +156,9 @@ bool epi_staging() { return knobs().epi != 0; }
 
 static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout,
                             int64_t kchan, int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms,
-                            int force_pbw, int epi_warps) {
+                            int force_pbw, int epi_warps, bool pair = false) {
     IgemmCfg c;
+    c.pair = pair ? 1 : 0;
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
     c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
     c.epi_warps = epi_warps;
@@ -168,6 +170,11 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     const bool ov = cfg_override(ov_bn, ov_pbw, ov_z);
     if (ov && ov_bn > 0) c.BN = ov_bn;
     if (ov && ov_pbw > 0) force_pbw = ov_pbw;
+    if (pair) {  // CTA pair: 2 x 128 images, 2 x 128 output channels, one pixel per tile
+        c.BN = 128;
+        force_pbw = 1;
+        c.nblk = int((c.nblk + 1) / 2);
+    }
     c.nbs = int((nout + c.BN - 1) / c.BN);
     // K block: the narrowest swizzle row (32 / 64 / 128 B) holding all channels,
     // else 128 B blocks
@@ -189,11 +196,11 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // (Z = 2) only for long K loops (>= 16 row steps) on grids of < 32 tiles.
     int pbw = int(std::min<int64_t>({256 / c.BN, 8, maxrow}));
     while (pbw > 1 && tiles_for(c.BN, pbw) < 120) --pbw;
-    if (tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0)) {
+    if (!pair && tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0)) {
         c.BN = 64;
         pbw = 1;
     }
-    c.nbs = int((nout + c.BN - 1) / c.BN);
+    c.nbs = int((nout + c.BN * (pair ? 2 : 1) - 1) / (c.BN * (pair ? 2 : 1)));
     if (force_pbw > 0) pbw = std::min<int>(force_pbw, int(std::min<int64_t>(256 / c.BN, 8)));
     // smem: ring of B rows (ntap x BN x 128 B) and ring of A slots holding all
     // pa activation columns of a row step (one TMA box, one barrier)
@@ -239,7 +246,7 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // >= 8 row steps saved per tile; the
     // tile's fp32 accumulators are staged in the idle rings for the DSMEM reduce
     const int64_t ring = int64_t(c.a_stages) * c.apos * 128 * c.KB + int64_t(c.stages) * c.stage_bytes;
-    const bool zc_ok = knobs().zc && int64_t(128) * c.pbw * c.BN * 4 <= ring;
+    const bool zc_ok = !pair && knobs().zc && int64_t(128) * c.pbw * c.BN * 4 <= ring;
     if (zc_ok) {
         int z = 8;
         while (z > 1 && (c.out_tiles * z > num_sms || rs_full < 2 * z)) z /= 2;
@@ -249,10 +256,10 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
             c.Z = z;
             c.zc = 1;
         }
-    } else if (c.out_tiles < 32 && rs_full >= 16) {
+    } else if (!pair && c.out_tiles < 32 && rs_full >= 16) {
         c.Z = 2;  // legacy global split-K: only very under-filled grids (sweep: Z = 2 at < 100 tiles was slower)
     }
-    if (ov && ov_z > 0) {
+    if (ov && ov_z > 0 && !pair) {
         c.Z = int(std::min<int64_t>(ov_z, rs_full));
         c.zc = zc_ok && c.Z > 1 && c.Z <= 8 && c.out_tiles * c.Z <= num_sms;
     }
@@ -260,7 +267,7 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // A-tile multicast across the BN blocks of one pixel (thread-block cluster):
     // every CTA loads 128/cm of the images of each activation column
     c.cm = 1;
-    if (c.Z == 1 && knobs().mcast) {  // measured slower on B200: off by default
+    if (c.Z == 1 && !pair && knobs().mcast) {  // measured slower on B200: off by default
         if (c.nbs % 4 == 0) c.cm = 4;
         else if (c.nbs % 2 == 0) c.cm = 2;
     }
@@ -271,8 +278,23 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
 // flight) when their 4 KB staging buffers cost no pipeline depth or tile width.
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
+    // CTA pairs (cta_group::2, M = 256 images x N = 256 channels per MMA): the same
+    // smem stage (this CTA's A slot + half the B row) feeds twice the MMA work of a
+    // 128 x 128 tile, so the latency-bound 2-stage ring carries twice the math.
+    // BF16, >= 256 output channels and >= 2 image blocks, 128 B K blocks, and a
+    // pair grid of >= 1 wave; the stage must leave a 2-deep unified ring.
+    // Measured (tools/ab.sh, CKS_PAIR): a win where the single-CTA plan is one
+    // pixel wide with >= 2 channel blocks (the pair loads each activation column
+    // once instead of once per 128-channel block: C3 l3 -9 %) and the pair grid
+    // is >= 2.5 waves; a loss against 2-pixel tiles (C4) and on short grids (C3 l4).
     const IgemmCfg c4 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
                                     force_pbw, 4);
+    if (knobs().pair && eb == 2 && nout >= 256 && N > 128 && kchan * eb >= 128 && force_pbw == 0 && c4.pbw == 1 &&
+        c4.nbs >= 2 && c4.Z == 1) {
+        const IgemmCfg cp = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
+                                        0, 4, true);
+        if (cp.unified && cp.stages >= 2 && cp.KB == 128 && cp.out_tiles * 2 * 2 >= int64_t(num_sms) * 5) return cp;
+    }
     if (knobs().epi8 == 0) return c4;
     const IgemmCfg c8 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
                                     force_pbw, 8);

@@ -75,6 +75,7 @@ struct IgemmCfg {
     int Z = 1;          // split-K segments
     int zc = 0;         // cluster split-K (Z CTAs of one cluster per output tile, DSMEM reduce)
     int epi_warps = 4;  // epilogue warps (4 or 8)
+    int pair = 0;       // CTA pair (cta_group::2): nblk counts image-block pairs, BN = this CTA's half
     int kc_blocks = 1;
     int KB = 128;       // bytes per K row: 32 / 64 / 128 (swizzle width)
     int ntap = 1;       // taps per filter row (B box)

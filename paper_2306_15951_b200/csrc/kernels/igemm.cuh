@@ -92,6 +92,8 @@ struct IgemmParams {
     int a0_step;               // a0 of pixel j = a0 of pixel 0 + j * a0_step (T1: stride, T2: 1)
     int zsplit;
     int zc;  // cluster split-K: cluster = the zsplit segments of one output tile, DSMEM reduction
+    int pair;  // CTA pair (cta_group::2): the even/odd CTA of a cluster hold image blocks 2q / 2q+1 of one
+               // tile (M = 256) and B columns [0, BN) / [BN, 2 BN) of its 2 BN outputs; nblk counts pairs
     FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
     int cm;               // cluster size along the O_C blocks: the A tile of a pixel is multicast (1 = off)
@@ -162,6 +164,7 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
     t = q;
     q = fdivu(t, p.fd_nblk);
     c.nblk = int(t - q * uint32_t(p.nblk));
+    if (p.pair) c.nblk = 2 * c.nblk + int(blockIdx.x & 1u);  // this CTA's image block of the pair
     t = q;
     q = fdivu(t, p.fd_wb);
     const int wb = int(t - q * uint32_t(p.wblocks));
@@ -199,7 +202,8 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
     const int rs = empty ? 0 : (che - chs) * p.kc_blocks;
     c.rs0 = p.zsplit == 1 ? 0 : int(fdivu(uint32_t(rs) * uint32_t(c.z), p.fd_z));
     c.rs1 = p.zsplit == 1 ? rs : int(fdivu(uint32_t(rs) * uint32_t(c.z + 1), p.fd_z));
-    c.rot = c.rs1 > c.rs0 ? int((blockIdx.x / unsigned(p.cm)) % unsigned(c.rs1 - c.rs0)) : 0;  // cluster-uniform
+    c.rot = c.rs1 > c.rs0 ? int(((blockIdx.x >> (p.pair ? 1 : 0)) / unsigned(p.cm)) % unsigned(c.rs1 - c.rs0))
+                          : 0;  // cluster-uniform
     return c;
 }
 
@@ -221,10 +225,13 @@ __device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
     return m;
 }
 
-template <int BN, bool kTF32, int KB>
+template <int BN, bool kTF32, int KB, bool PAIR = false>
 __global__ void __launch_bounds__(384, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ IgemmParams p) {
+    // CTA-pair kernels are separate instantiations: a kernel containing
+    // cta_group::2 tcgen05 instructions must be launched with pair clusters
+    constexpr bool kPair = PAIR;
     using S = IgemmShape<BN, kTF32, KB>;
     extern __shared__ uint8_t smem_raw[];
     // 1 KB alignment by offset arithmetic (keeps the shared address space visible to the compiler)
@@ -273,19 +280,28 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
-            ptx::mbar_init(&tempty[i], 32 * p.epi_warps);
+            ptx::mbar_init(&tempty[i], 32 * p.epi_warps * (kPair ? 2 : 1));  // pair: both CTAs' epilogues
             ptx::mbar_init(&pfull[i], 32);
             ptx::mbar_init(&pempty[i], 32);
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
+    if (warp == 2) {
+        if (kPair)
+            ptx::tmem_alloc_pair(tmem_slot, tmem_cols);
+        else
+            ptx::tmem_alloc(tmem_slot, tmem_cols);
+    }
     ptx::tc_fence_before();
     __syncthreads();
-    if (p.cm > 1) ptx::cluster_sync();  // peers' barriers exist before the first multicast
+    if (p.cm > 1 || kPair) ptx::cluster_sync();  // peers' barriers exist before the first multicast / pair op
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t crank = p.cm > 1 ? blockIdx.x % uint32_t(p.cm) : 0u;
+    const bool leader = !kPair || (blockIdx.x & 1u) == 0;  // pair: the even CTA issues the MMAs
+    const long long t0 = kPair ? (blockIdx.x >> 1) : blockIdx.x;
+    const long long tstep = kPair ? (gridDim.x >> 1) : gridDim.x;
+    const int BNo = kPair ? 2 * BN : BN;  // output channels per tile (MMA N of one pixel)
     const uint16_t cmask = uint16_t((1u << p.cm) - 1u);
     if (threadIdx.x == 0) trace_gt(p, 1);
     ptx::pdl_wait();  // inputs of this op may come from the previous kernel
@@ -304,7 +320,7 @@ __global__ void __launch_bounds__(384, 1)
         const int trole = warp == 0 ? 0 : 4;
         if (lane == 0) trace_ev(p, trole, ti, 0);
         const uint32_t btx = uint32_t(p.ntap * S::TILE_B);
-        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (long long t = t0; t < p.num_tiles; t += tstep) {
             const Tile c = decode_tile(t, p, tab[0], tab[1]);
             const int a0h = tab[0].a0[c.rh];
             for (int ri = c.rs0; ri < c.rs1; ++ri) {
@@ -315,7 +331,15 @@ __global__ void __launch_bounds__(384, 1)
                     uint64_t* bf = p.unified ? &afull[bs] : &bfull[bs];
                     ptx::mbar_wait(p.unified ? &aempty[bs] : &bempty[bs], bph ^ 1);
                     if (ptx::elect_one()) {
-                        if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
+                        if (kPair) {
+                            // this CTA's half of the 2 BN columns; bytes complete on the leader's barrier,
+                            // which the leader arms for both CTAs
+                            const uint32_t bfc = ptx::mapa(ptx::smem_u32(bf), 0);
+                            if (leader) ptx::mbar_arrive_expect_tx_cluster(bfc, 2 * btx);
+                            ptx::tma_load_4d_pair(bbuf + bs * p.b_stage_bytes, &tmB, bfc, kc * S::BK,
+                                                  c.nb * 2 * BN + int(blockIdx.x & 1u) * BN, ch * p.slot_stride,
+                                                  c.ph);
+                        } else if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
                             ptx::mbar_arrive(bf);  // experiment: B traffic removed (wrong results)
                         } else {
                             ptx::mbar_arrive_expect_tx(bf, btx);
@@ -336,7 +360,13 @@ __global__ void __launch_bounds__(384, 1)
                     ++aq;
                     ptx::mbar_wait(&aempty[as], aph ^ 1);
                     if (ptx::elect_one()) {
-                        if ((p.dbg & 8) && aq > uint32_t(p.a_stages)) {
+                        if (kPair) {
+                            // this CTA's 128 images (rows 128*rank.. of the pair's M = 256)
+                            const uint32_t afc = ptx::mapa(ptx::smem_u32(&afull[as]), 0);
+                            if (leader) ptx::mbar_arrive_expect_tx_cluster(afc, 2 * a_slot);
+                            ptx::tma_load_4d_pair(abuf + as * a_slot, &tmA, afc, kc * S::BK, c.nblk * 128, iw0,
+                                                  a0h + ch);
+                        } else if ((p.dbg & 8) && aq > uint32_t(p.a_stages)) {
                             ptx::mbar_arrive(&afull[as]);  // experiment: A traffic removed (wrong results)
                         } else if (p.cm > 1) {
                             // this CTA's 128/cm images of every column, multicast to the cluster
@@ -372,7 +402,7 @@ __global__ void __launch_bounds__(384, 1)
             int ti = 0;
             if (lane == 0) trace_ev(p, 1, ti, 0);
             uint32_t ps = 0, pph = 0;
-            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (long long t = t0; t < p.num_tiles && leader; t += tstep) {
                 ptx::mbar_wait(&pfull[ps], pph);  // program of this tile (warp 2)
                 const int4* pg = prog + ps * kProgSlot;
                 const int4 h0 = pg[0], h1 = pg[1];
@@ -381,9 +411,9 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::mbar_wait(&tempty[acc], acc_ph ^ 1);
                 if (lane == 0) trace_ev(p, 1, ti, 3);
                 ptx::tc_fence_after();
-                const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BN);
+                const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BNo);
                 __syncwarp();
-                const uint32_t idesc0 = ptx::instr_desc(128, 0, kTF32, false, false);
+                const uint32_t idesc0 = ptx::instr_desc(kPair ? 256 : 128, 0, kTF32, false, false);
                 bool first = true;
                 for (int ri = rs0; ri < rs1; ++ri) {
                     if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
@@ -406,20 +436,29 @@ __global__ void __launch_bounds__(384, 1)
                             const uint64_t adesc = aslot + uint64_t(uint32_t(en.y) * (S::A_BYTES >> 4));
                             const uint64_t bdesc = bdesc0 + uint64_t(uint32_t(en.w & 0xFF) * (S::TILE_B >> 4));
                             const uint32_t cnt = uint32_t(en.w >> 8) & 0xFFu;
-                            const uint32_t idesc = idesc0 | (((cnt * BN) >> 3) << 17);
+                            const uint32_t idesc = idesc0 | (((cnt * uint32_t(BNo)) >> 3) << 17);
                             const uint32_t d = dbase + uint32_t(en.z);
                             const uint32_t acc0 = uint32_t(en.w >> 16) & 1u;
                             if (!(p.dbg & 2) && ptx::elect_one()) {
+                                if (!kTF32 && kPair) {
 #pragma unroll
-                                for (int kk = 0; kk < S::BK / S::UK; ++kk)
-                                    ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
-                                                       kk ? 1u : acc0);
+                                    for (int kk = 0; kk < S::BK / S::UK; ++kk)
+                                        ptx::mma_ss_pair(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
+                                                         kk ? 1u : acc0);
+                                } else {
+#pragma unroll
+                                    for (int kk = 0; kk < S::BK / S::UK; ++kk)
+                                        ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2),
+                                                           idesc, kk ? 1u : acc0);
+                                }
                             }
                             __syncwarp();
                             en = nx;
                         }
                         if (ptx::elect_one()) {  // A slot free (in every CTA that multicasts into it)
-                            if (p.cm > 1)
+                            if (kPair)
+                                ptx::mma_commit_pair(&aempty[as]);
+                            else if (p.cm > 1)
                                 ptx::mma_commit_mc(&aempty[as], cmask);
                             else
                                 ptx::mma_commit(&aempty[as]);
@@ -444,7 +483,12 @@ __global__ void __launch_bounds__(384, 1)
                     pph ^= 1;
                 }
                 if (lane == 0) trace_gt(p, 4);
-                if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);  // accumulators ready (immediately if no MMA)
+                if (ptx::elect_one()) {  // accumulators ready (immediately if no MMA)
+                    if (kPair)
+                        ptx::mma_commit_pair(&tfull[acc]);
+                    else
+                        ptx::mma_commit(&tfull[acc]);
+                }
                 __syncwarp();
                 if (++acc == uint32_t(p.acc_stages)) {
                     acc = 0;
@@ -457,7 +501,7 @@ __global__ void __launch_bounds__(384, 1)
         // ---------------- MMA-program builder (runs ahead of the MMA warp by one tile)
         {
             uint32_t ps = 0, pph = 0;
-            for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (long long t = t0; t < p.num_tiles && leader; t += tstep) {
                 const Tile c = decode_tile(t, p, tab[0], tab[1]);
                 ptx::mbar_wait(&pempty[ps], pph ^ 1);
                 int4* pg = prog + ps * kProgSlot;
@@ -551,34 +595,42 @@ __global__ void __launch_bounds__(384, 1)
         const int row = int(sub * 32 + lane);
         const int et = threadIdx.x - 128;  // 0..32*epi_warps-1
         uint32_t acc = 0, acc_ph = 0;
-        const int pw_cols = p.pbw * BN;
+        const int pw_cols = p.pbw * BNo;
+        // accumulator buffer released to the MMA issuer (pair: on the leader's barrier)
+        const uint32_t tempty_c = ptx::mapa(ptx::smem_u32(tempty), 0);
+        auto release = [&](uint32_t a) {
+            if (kPair)
+                ptx::mbar_arrive_cluster(tempty_c + 8u * a);
+            else
+                ptx::mbar_arrive(&tempty[a]);
+        };
         const bool split = p.zsplit > 1;
         const bool vec4 = (p.out_C % 4) == 0;
         const bool stage = !split && p.epi_stage && vec4;  // coalesced-store epilogue
         int ti = 0;
         if (et == 0) trace_ev(p, 2, ti, 0);
-        for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        for (long long t = t0; t < p.num_tiles; t += tstep) {
             const Tile c = decode_tile(t, p, tab[0], tab[1]);
             ptx::mbar_wait(&tfull[acc], acc_ph);
             if (et == 0) trace_ev(p, 2, ti, 1);
             ptx::tc_fence_after();
             const int nrow0 = c.nblk * 128 + int(sub) * 32;  // image of lane 0
             const int n = nrow0 + int(lane);
-            const int cbase = c.nb * BN;
-            const int cvalid = min(BN, p.out_C - cbase);
+            const int cbase = c.nb * BNo;
+            const int cvalid = min(BNo, p.out_C - cbase);
             const bool any = c.rs1 > c.rs0;
             // the CTA's last tile: the smem rings are idle (all MMAs done), so stage
             // 32x32 fp32 blocks there (128B swizzle) and write full lines by TMA store
             // other tiles (p.tma_store == 2): the same 32x32 blocks through this warp's
             // 4 KB epilogue buffer, one TMA store in flight per warp (the buffer is
             // reused once the previous store has read it): async full-line stores
-            if (p.tma_store == 2 && !split && t + gridDim.x < p.num_tiles && !(p.dbg & 1)) {
+            if (p.tma_store == 2 && !split && t + tstep < p.num_tiles && !(p.dbg & 1)) {
                 float* blk = epi + ew * 1024;
 #pragma unroll 1
                 for (int j = 0; j < c.len; ++j) {
                     const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
 #pragma unroll 1
-                    for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
+                    for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
                         uint32_t r[32];
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
                                            c0, r);
@@ -603,21 +655,21 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[acc]);
+                release(acc);
                 if (++acc == uint32_t(p.acc_stages)) {
                     acc = 0;
                     acc_ph ^= 1;
                 }
                 continue;
             }
-            if (p.tma_store && !split && t + gridDim.x >= p.num_tiles && !(p.dbg & 1)) {
-                uint8_t* stg = smem + sub * uint32_t(c.len * (BN / 32)) * 4096u;
+            if (p.tma_store && !split && t + tstep >= p.num_tiles && !(p.dbg & 1)) {
+                uint8_t* stg = smem + sub * uint32_t(c.len * (BNo / 32)) * 4096u;
 #pragma unroll 1
                 for (int j = 0; j < c.len; ++j) {
                     const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
 #pragma unroll 1
-                    for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
-                        const int k = j * (BN / 32) + c0 / 32;
+                    for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
+                        const int k = j * (BNo / 32) + c0 / 32;
                         uint32_t r[32];
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
                                            c0, r);
@@ -643,7 +695,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (ptx::elect_one()) ptx::bulk_wait_read0();  // smem must outlive the TMA reads
                 __syncwarp();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&tempty[acc]);
+                release(acc);
                 if (++acc == uint32_t(p.acc_stages)) {
                     acc = 0;
                     acc_ph ^= 1;
@@ -663,7 +715,7 @@ __global__ void __launch_bounds__(384, 1)
                                    tab[1].out[c.j0 + j]) * p.out_C + cbase;
                 const int lim = split ? BN : cvalid;
 #pragma unroll 1
-                for (int c0 = 32 * int(half); c0 < BN; c0 += 32 * int(nhalf)) {
+                for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
                     uint32_t r[32];
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN + c0,
                                    r);
@@ -718,7 +770,7 @@ __global__ void __launch_bounds__(384, 1)
             // TMEM drained: release the accumulator buffer before the split-K reduce
             if (et == 0) trace_ev(p, 2, ti, 2);
             ptx::tc_fence_before();
-            ptx::mbar_arrive(&tempty[acc]);
+            release(acc);
             if (++acc == uint32_t(p.acc_stages)) {
                 acc = 0;
                 acc_ph ^= 1;
@@ -838,13 +890,16 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
         ptx::cluster_sync();  // peers finished reading this CTA's staging
-    } else if (p.cm > 1) {
+    } else if (p.cm > 1 || kPair) {
         ptx::cluster_sync();  // no CTA leaves while peers may still signal it
     }
     if (threadIdx.x == 0) trace_gt(p, 5);
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, tmem_cols);
+        if (kPair)
+            ptx::tmem_dealloc_pair(tmem_base, tmem_cols);
+        else
+            ptx::tmem_dealloc(tmem_base, tmem_cols);
     }
 }
 

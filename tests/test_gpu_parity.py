@@ -440,3 +440,17 @@ def test_wgrad_row_tiles(torch_cuda, lay, gz):
     check(got["wgrad"], ref, "bf16", f"{lay} row-tile wgrad gz={gz}", red_len(lay, "wgrad"))
     again = run_all(torch_cuda, lay, "bf16", config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)[1]["wgrad"]
     np.testing.assert_array_equal(got["wgrad"], again)
+
+
+# ---------------------------------------------- CTA-pair (cta_group::2) tiles
+@pytest.mark.parametrize("lay", [Layer("pr0", 300, 128, 14, 14, 256, 3, 3, 1, 1, 1, 1),
+                                 Layer("pr1", 256, 256, 7, 9, 384, 3, 3, 1, 1, 1, 1),
+                                 Layer("pr2", 260, 128, 15, 14, 512, 3, 3, 2, 2, 1, 1),
+                                 Layer("pr3", 384, 512, 8, 8, 256, 4, 4, 2, 2, 1, 1)],
+                         ids=lambda l: l.name)
+def test_pair_tiles(torch_cuda, lay):
+    """>= 256 output channels and > 128 images: 2-CTA tiles (M = 256 images of one
+    pixel across a CTA pair, N = 256 channels, each CTA holding half of B); odd
+    image-block counts leave the last pair's second CTA out of range.  Forward
+    and KS-deconv (whose output channels are I_C) against the oracle."""
+    check_full(torch_cuda, lay, "bf16", config=16, idx=int(lay.name[2:]), ops=("fwd", "deconv"))
