@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--layers", action="store_true", help="per-layer breakdown on stderr")
     ap.add_argument("--no-zins", action="store_true", help="skip the zero-inserted-formulation comparison")
+    ap.add_argument("--dtype", choices=("bf16", "tf32"), default="bf16",
+                    help="bf16 inputs, or fp32 inputs multiplied as TF32 (fp32 accumulate and outputs either way)")
     return ap.parse_args()
 
 
@@ -211,14 +213,17 @@ def load_traffic(kernel):
 class LayerBufs:
     """Device buffers + the C-ABI calls of one layer (argument marshalling only)."""
 
-    def __init__(self, torch, lay, config, idx, rank, device):
+    def __init__(self, torch, lay, config, idx, rank, device, dtype="bf16"):
         import numpy as np
         from cks_synth import bf16_bits, make_layer_inputs
         from paper_2306_15951_b200 import _lib as L
         self.lay, self.L = lay, L
-        a = make_layer_inputs(lay, config + 100 * rank, idx, "bf16")
+        self.dt = L.CKS_BF16 if dtype == "bf16" else L.CKS_TF32
+        a = make_layer_inputs(lay, config + 100 * rank, idx, dtype)
 
         def dev(x):
+            if dtype == "tf32":
+                return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device)
             return torch.from_numpy(bf16_bits(x).view(np.int16)).view(torch.bfloat16).to(device)
         self.host = {k: v for k, v in a.items()}
         self.X, self.W, self.G = dev(a["X"]), dev(a["W"]), dev(a["dY"])
@@ -232,44 +237,45 @@ class LayerBufs:
         cnt = L.cks_op_counts(g)
         self.flops = 2 * cnt["zero_free_macs"]
         # algorithmic bytes (read inputs once, write the fp32 output once)
-        xb, wb, gb = lay.N * lay.H * lay.W * lay.C * 2, lay.OC * lay.FH * lay.FW * lay.C * 2, lay.N * OH * OW * lay.OC * 2
-        self.algo_bytes = {"fwd": xb + wb + gb * 2, "deconv": gb + wb + xb * 2,
-                           "wgrad": xb + gb + wb * 2, "split": 2 * wb}
-        self.cp = torch.empty(L.cks_ks_split_size(g, L.CKS_BF16) // 2, dtype=torch.bfloat16, device=device)
+        eb = 2 if dtype == "bf16" else 4
+        xb, wb, gb = lay.N * lay.H * lay.W * lay.C * eb, lay.OC * lay.FH * lay.FW * lay.C * eb, lay.N * OH * OW * lay.OC * eb
+        self.algo_bytes = {"fwd": xb + wb + (gb // eb) * 4,
+                           "deconv": gb + wb + (xb // eb) * 4, "wgrad": xb + gb + (wb // eb) * 4, "split": 2 * wb}
+        self.cp = torch.empty(L.cks_ks_split_size(g, self.dt) // eb, dtype=self.X.dtype, device=device)
         self.ws = {}
         for op, code in (("fwd", L.CKS_OP_FWD), ("deconv", L.CKS_OP_DECONV), ("wgrad", L.CKS_OP_WGRAD)):
-            n = L.cks_workspace_size(g, L.CKS_BF16, code)
+            n = L.cks_workspace_size(g, self.dt, code)
             self.ws[op] = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
         self.launches = {
-            "fwd": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD),
+            "fwd": L.cks_launch_count(g, self.dt, L.CKS_OP_FWD),
             "split": 1,
-            "deconv": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True),
-            "wgrad": L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD),
+            "deconv": L.cks_launch_count(g, self.dt, L.CKS_OP_DECONV, c_packed_given=True),
+            "wgrad": L.cks_launch_count(g, self.dt, L.CKS_OP_WGRAD),
         }
 
     def run_split(self, stream_ptr):
-        self.L.cks_ks_split(self.g, self.L.CKS_BF16, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+        self.L.cks_ks_split(self.g, self.dt, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
 
     def run(self, op, stream_ptr):
         L, g = self.L, self.g
         if op == "split":  # Stage1 alone
-            L.cks_ks_split(g, L.CKS_BF16, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+            L.cks_ks_split(g, self.dt, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
             return
         if op == "deconv_only":  # Stage2&3 from the already split sub-filters
             ws = self.ws["deconv"]
-            L.cks_deconv2d(g, L.CKS_BF16, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),
+            L.cks_deconv2d(g, self.dt, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),
                            ws.data_ptr(), ws.numel(), stream_ptr)
             return
         ws = self.ws[op]
         if op == "fwd":
-            L.cks_conv2d_fwd(g, L.CKS_BF16, self.X.data_ptr(), self.W.data_ptr(), self.Y.data_ptr(), ws.data_ptr(),
+            L.cks_conv2d_fwd(g, self.dt, self.X.data_ptr(), self.W.data_ptr(), self.Y.data_ptr(), ws.data_ptr(),
                              ws.numel(), stream_ptr)
         elif op == "deconv":  # Stage1 (W changes every training step) + fused Stage2&3
-            L.cks_ks_split(g, L.CKS_BF16, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
-            L.cks_deconv2d(g, L.CKS_BF16, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),
+            L.cks_ks_split(g, self.dt, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+            L.cks_deconv2d(g, self.dt, self.G.data_ptr(), None, self.cp.data_ptr(), self.dX.data_ptr(),
                            ws.data_ptr(), ws.numel(), stream_ptr)
         else:
-            L.cks_dilated_wgrad(g, L.CKS_BF16, self.X.data_ptr(), self.G.data_ptr(), self.dW.data_ptr(), 0,
+            L.cks_dilated_wgrad(g, self.dt, self.X.data_ptr(), self.G.data_ptr(), self.dW.data_ptr(), 0,
                                 ws.data_ptr(), ws.numel(), stream_ptr)
 
 
@@ -294,7 +300,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=device)
     build.build()
     desc, layers = get_config(args.config, args.batch)
-    bufs = [LayerBufs(torch, lay, args.config, i, rank, device) for i, lay in enumerate(layers)]
+    bufs = [LayerBufs(torch, lay, args.config, i, rank, device, args.dtype) for i, lay in enumerate(layers)]
     # flat dW buffer: one NCCL all_reduce per step for all layers
     sizes = [b.lay.OC * b.lay.FH * b.lay.FW * b.lay.C for b in bufs]
     flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
@@ -511,12 +517,15 @@ def run_gpu(args):
     else:
         kname, kms, kfl, nl = "wgrad_kernel", fam["wgrad"][0], fam["wgrad"][1], sum(1 for _, op in ops_seq if op == "wgrad")
     peaks = load_peaks()
+    if args.dtype == "tf32":  # dense TF32 = half the BF16 rate (guide's nominal 1.1 vs 2.25 PFLOP/s)
+        peaks = dict(peaks, bf16=peaks["bf16"] / 2, src=peaks["src"] + " bf16 x 1/2 (nominal TF32:BF16)")
     achieved = kfl / (kms / 1e3) / 1e12
     kops = ("fwd", "deconv_only") if kname == "igemm_kernel" else ("wgrad",)
     algo_b = [bufs[i].algo_bytes[OPF[op]] for i, op in ops_seq if op in kops]
     roofline = {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 2), "peak": peaks["bf16"],
                 "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4), "traffic": load_traffic(kname),
-                "launches_per_step": nl, "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)",
+                "launches_per_step": nl, "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)" if args.dtype == "bf16" else
+                    f"{peaks['src']} (MEASURED_PEAKS.json bf16 burst x 0.5)",
                 "algorithmic_bytes_per_launch": round(sum(algo_b) / max(len(algo_b), 1)),
                 "traffic_src": "profiles/ncu_traffic.json: mean ncu dram__bytes_read+write per launch (cold-cache replay)",
                 "timing": "op-level CUDA event nodes inside the step graph (kernel + its staging kernels)"}
@@ -524,7 +533,7 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded U[-1,1) X/dY, kaiming-uniform W)",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded U[-1,1) X/dY, kaiming-uniform W)",
         "config": {"workload": desc, "layers": len(layers), "per_gpu_batch": layers[0].N,
                    "global_batch": layers[0].N * n_gpus, "ops_per_step": len(ops_seq),
                    "zero_free_gflop_per_gpu_step": round(flops_step / 1e9, 3),
@@ -577,20 +586,20 @@ def run_zins(torch, bufs, steps, device, flush, cks_ms, per_layer):
             if op in b.lay.ops:
                 seq.append((i, op))
     code = {"fwd": L.CKS_OP_FWD, "deconv": L.CKS_OP_DECONV, "wgrad": L.CKS_OP_WGRAD}
-    need = max(L.cks_zins_workspace_size(bufs[i].g, L.CKS_BF16, code[op]) for i, op in seq)
+    need = max(L.cks_zins_workspace_size(bufs[i].g, bufs[i].dt, code[op]) for i, op in seq)
     ws = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
     dw = torch.empty(max(b.dW.numel() for b in bufs), dtype=torch.float32, device=device)
 
     def run(i, op, sp):
         b = bufs[i]
         if op == "fwd":
-            L.cks_zins_conv2d_fwd(b.g, L.CKS_BF16, b.X.data_ptr(), b.W.data_ptr(), b.Y.data_ptr(), ws.data_ptr(),
+            L.cks_zins_conv2d_fwd(b.g, b.dt, b.X.data_ptr(), b.W.data_ptr(), b.Y.data_ptr(), ws.data_ptr(),
                                   ws.numel(), sp)
         elif op == "deconv":
-            L.cks_zins_deconv2d(b.g, L.CKS_BF16, b.G.data_ptr(), b.W.data_ptr(), b.dX.data_ptr(), ws.data_ptr(),
+            L.cks_zins_deconv2d(b.g, b.dt, b.G.data_ptr(), b.W.data_ptr(), b.dX.data_ptr(), ws.data_ptr(),
                                 ws.numel(), sp)
         else:
-            L.cks_zins_wgrad(b.g, L.CKS_BF16, b.X.data_ptr(), b.G.data_ptr(), dw.data_ptr(), ws.data_ptr(),
+            L.cks_zins_wgrad(b.g, b.dt, b.X.data_ptr(), b.G.data_ptr(), dw.data_ptr(), ws.data_ptr(),
                              ws.numel(), sp)
 
     stream = torch.cuda.Stream(device)
