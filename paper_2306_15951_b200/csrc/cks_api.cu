@@ -74,6 +74,12 @@ int debug_flags() {
     return f;
 }
 
+// experiments: allocate all 512 TMEM columns per igemm CTA (the former behaviour)
+bool tmem_full() {
+    static const bool on = getenv("CKS_TMEM_FULL") != nullptr;
+    return on;
+}
+
 // TMA-store epilogue for every igemm tile (0: only the last tile per CTA; experiments)
 bool epi_tma_all() {
     static const bool on = [] {
@@ -276,6 +282,12 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.zc = cfg.zc;
     p.pair = cfg.pair;
     p.epi_warps = cfg.epi ? cfg.epi_warps : 4;
+    {
+        const int need = cfg.acc_stages * cfg.pbw * cfg.BN * (cfg.pair ? 2 : 1);
+        int cols = 32;
+        while (cols < need) cols *= 2;
+        p.tmem_cols = tmem_full() ? 512 : cols;
+    }
     p.fd_z = make_fastdiv(uint32_t(cfg.Z));
     p.fd_nbs = make_fastdiv(uint32_t(cfg.nbs));
     p.fd_nblk = make_fastdiv(uint32_t(cfg.nblk));

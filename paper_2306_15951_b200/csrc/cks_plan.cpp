@@ -124,7 +124,7 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -137,6 +137,7 @@ struct Knobs {
         if (const char* e = getenv("CKS_EPI8")) epi8 = atoi(e);
         if (const char* e = getenv("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
         if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
+        if (const char* e = getenv("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
     }
 };
 static const Knobs& knobs() {
@@ -162,7 +163,8 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
     c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
     c.epi_warps = epi_warps;
-    const int64_t budget = kSmemBudget - (c.epi ? epi_stage_bytes(epi_warps) + 1024 : 0);  // + 1 KB alignment
+    int64_t budget = kSmemBudget - (c.epi ? epi_stage_bytes(epi_warps) + 1024 : 0);  // + 1 KB alignment
+    if (knobs().smem_cap > 0) budget = std::min<int64_t>(budget, int64_t(knobs().smem_cap) * 1024);  // experiments
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
     c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);

@@ -101,6 +101,8 @@ struct IgemmParams {
     int tma_store;        // 1: last tile per CTA staged in the idle rings and TMA-stored; 2: also every
                           // other tile, through the per-warp 4 KB epilogue buffers
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
+    int tmem_cols;        // TMEM columns allocated (only what the accumulators need: a small
+                          // layer's CTA can share its SM with the next kernel's CTA)
     int epi_warps;        // epilogue warps: 4 (one per TMEM sub-partition) or 8 (two, alternate 32-column chunks)
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* pempty = pfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
     int* red_flag = reinterpret_cast<int*>(tmem_slot + 1);
-    const uint32_t tmem_cols = 512;
+    const uint32_t tmem_cols = uint32_t(p.tmem_cols);  // power of two >= acc_stages x pbw x BNo
     // per-axis plan tables copied to smem once (one parallel pass of independent
     // constant loads instead of dependent cold loads in every role's decode)
     KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
