@@ -12,6 +12,7 @@ if [ "$PART" = bench ]; then
   timeout 300 python bench.py --config 3 --steps 50 --no-cpu-baseline --layers > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
   timeout 300 python bench.py --config 5 --steps 30 --no-cpu-baseline --no-e2e --layers > gpurun_out/bench_c6.json 2> gpurun_out/bench_c6.err
   timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+  timeout 300 python bench.py --dtype tf32 --steps 30 --no-cpu-baseline > gpurun_out/bench_c2_tf32.json 2> gpurun_out/bench_c2_tf32.err
 elif [ "$PART" = lists ]; then
   # ncu lists the eager warm-up pass (one full step, same kernels and arguments);
   # its replay of the bench's CUDA graph then stops at the first igemm node with
@@ -32,4 +33,5 @@ else
   bash tools/ncu_full.sh ${TAG}_wgrad_l1 2 l1_0 wgrad wgrad_kernel
   bash tools/ncu_full.sh ${TAG}_fwdrow_stem 2 stem fwd fwd_row
   bash tools/ncu_full.sh ${TAG}_wgradrow_stem 2 stem wgrad wgrad_row
+  bash tools/ncu_full.sh ${TAG}_pair_l3 2 l3_1 fwd igemm
 fi
