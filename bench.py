@@ -646,7 +646,8 @@ def run_zins(torch, bufs, steps, device, flush, cks_ms, per_layer):
 
 def run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, steps, device):
     """The same step through the public torch API (paper_2306_15951_b200.ops):
-    pinned host inputs -> device, the three operators, results -> host."""
+    pinned host inputs -> device, the three operators, results -> host, every
+    byte of every layer every step (copies overlapped with compute)."""
     from paper_2306_15951_b200 import ops as K
     host_in, host_out = [], []
     for b in bufs:
@@ -660,38 +661,73 @@ def run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, steps, device):
             opname = {"Y": "fwd", "dX": "deconv", "dW": "wgrad"}[k]
             if opname in b.lay.ops:
                 d2h += d[k].numel() * 4
-    s = torch.cuda.Stream(device)
+    # three streams: H2D copies, the C-K-S ops, D2H copies -- PCIe traffic in
+    # both directions overlaps the compute of other layers (copy engines run
+    # concurrently with the SMs); per-layer events carry the dependencies, and
+    # the device buffers of a layer are reused across steps behind its events
+    s_in, s_comp, s_out = (torch.cuda.Stream(device) for _ in range(3))
+    dev_in = [{k: torch.empty_like(getattr(b, k)) for k in ("X", "W", "G")} for b in bufs]
+    dev_out = []
+    for b in bufs:
+        lay = b.lay
+        OH, OW = lay.out_hw()
+        f32 = dict(dtype=torch.float32, device=device)
+        dev_out.append({"Y": torch.empty((lay.N, OH, OW, lay.OC), **f32),
+                        "dX": torch.empty((lay.N, lay.H, lay.W, lay.C), **f32),
+                        "dW": torch.empty((lay.OC, lay.FH, lay.FW, lay.C), **f32)})
+    nl = len(bufs)
+    ev_in = [torch.cuda.Event() for _ in range(nl)]
+    ev_comp = [torch.cuda.Event() for _ in range(nl)]
+    ev_out = [torch.cuda.Event() for _ in range(nl)]
+    started = [False] * nl
 
     def one():
-        outs = []
-        for b, hi, ho in zip(bufs, host_in, host_out):
+        for i, (b, hi, ho) in enumerate(zip(bufs, host_in, host_out)):
             lay = b.lay
-            X = hi["X"].to(device, non_blocking=True)
-            W = hi["W"].to(device, non_blocking=True)
-            G = hi["G"].to(device, non_blocking=True)
-            st, pd = (lay.sh, lay.sw), (lay.ph, lay.pw)
-            if "fwd" in lay.ops:
-                ho["Y"].copy_(K.conv2d_fwd(X, W, st, pd), non_blocking=True)
-            if "deconv" in lay.ops:
-                ho["dX"].copy_(K.deconv2d(G, W, (lay.H, lay.W), st, pd), non_blocking=True)
-            if "wgrad" in lay.ops:
-                dW = K.dilated_wgrad(X, G, (lay.FH, lay.FW), st, pd)
-                if n_gpus > 1:
-                    dist.all_reduce(dW)
-                ho["dW"].copy_(dW, non_blocking=True)
-        return outs
+            di, do = dev_in[i], dev_out[i]
+            with torch.cuda.stream(s_in):
+                if started[i]:
+                    s_in.wait_event(ev_comp[i])  # the previous step's ops of this layer read these buffers
+                for k in ("X", "W", "G"):
+                    di[k].copy_(hi[k], non_blocking=True)
+                ev_in[i].record(s_in)
+            with torch.cuda.stream(s_comp):
+                s_comp.wait_event(ev_in[i])
+                if started[i]:
+                    s_comp.wait_event(ev_out[i])  # the previous step's results were copied out
+                st, pd = (lay.sh, lay.sw), (lay.ph, lay.pw)
+                X, W, G = di["X"], di["W"], di["G"]
+                if "fwd" in lay.ops:
+                    K.conv2d_fwd(X, W, st, pd, out=do["Y"], stream=s_comp)
+                if "deconv" in lay.ops:
+                    K.deconv2d(G, W, (lay.H, lay.W), st, pd, out=do["dX"], stream=s_comp)
+                if "wgrad" in lay.ops:
+                    K.dilated_wgrad(X, G, (lay.FH, lay.FW), st, pd, out=do["dW"], stream=s_comp)
+                    if n_gpus > 1:
+                        dist.all_reduce(do["dW"])
+                ev_comp[i].record(s_comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[i])
+                for k, opname in (("Y", "fwd"), ("dX", "deconv"), ("dW", "wgrad")):
+                    if opname in lay.ops:
+                        ho[k].copy_(do[k], non_blocking=True)
+                ev_out[i].record(s_out)
+            started[i] = True
 
-    with torch.cuda.stream(s):
+    one()
+    torch.cuda.synchronize()
+    if n_gpus > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    s_comp.wait_event(e0)
+    s_out.wait_event(e0)
+    for _ in range(steps):
         one()
-        torch.cuda.synchronize()
-        if n_gpus > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(steps):
-            one()
-        e1.record(s)
-        torch.cuda.synchronize()
+    s_out.wait_stream(s_in)
+    s_out.wait_stream(s_comp)
+    e1.record(s_out)
+    torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     if n_gpus > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=device)
