@@ -124,7 +124,8 @@ std::vector<KRow> krows_deconv(const Axis& a) {
 struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
-    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0;
+    int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
+        gz_max = 64;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -138,6 +139,7 @@ struct Knobs {
         if (const char* e = getenv("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
         if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = getenv("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
+        if (const char* e = getenv("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
     }
 };
 static const Knobs& knobs() {
@@ -467,7 +469,7 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     } else {
         int64_t want = std::max<int64_t>(1, num_sms / std::max<int64_t>(c.base_tiles, 1));  // one wave
         int64_t cap = std::max<int64_t>(lmin / 4, 1);
-        c.gz = int(std::max<int64_t>(1, std::min<int64_t>({want, cap, 64})));
+        c.gz = int(std::max<int64_t>(1, std::min<int64_t>({want, cap, int64_t(knobs().gz_max)})));
     }
     return c;
 }
