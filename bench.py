@@ -379,6 +379,10 @@ def run_gpu(args):
     # (KS-deconv on the main stream) with each layer's Sk-dilated wgrad on a
     # second side stream, released when the layer above finished its deconv.
     s1, s2, s3 = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
+    # Sk-dilated streams: the per-layer wgrads are independent of each other, so
+    # consecutive layers' wgrads may run on alternate streams (CKS_BENCH_WSTREAMS)
+    nws = max(1, int(os.environ.get("CKS_BENCH_WSTREAMS", "2")))  # measured: 2 best (C2 0.624 -> 0.597 ms)
+    wst = [s2] + [torch.cuda.Stream(device) for _ in range(nws - 1)]
     # data-parallel: the flat dW is all-reduced in buckets of layers, each
     # launched (on s3, NCCL) as soon as the bucket's wgrads are done, so the
     # communication overlaps the rest of the backward chain.  The step graph is
@@ -422,7 +426,8 @@ def run_gpu(args):
             fork = torch.cuda.Event()
             fork.record(main)
             s1.wait_event(fork)
-            s2.wait_event(fork)
+            for w in wst:
+                w.wait_event(fork)
             with torch.cuda.stream(s1):
                 for i, b in enumerate(bufs):
                     if "deconv" in b.lay.ops:
@@ -433,27 +438,30 @@ def run_gpu(args):
                 if "fwd" in b.lay.ops:
                     b.run("fwd", main.cuda_stream)
             main.wait_event(split_done)
-            for i in order:
+            for k, i in enumerate(order):
                 b = bufs[i]
                 ev = torch.cuda.Event()
                 ev.record(main)
+                ws_k = wst[k % nws]
                 if "wgrad" in b.lay.ops:
-                    s2.wait_event(ev)
-                    with torch.cuda.stream(s2):
-                        b.run("wgrad", s2.cuda_stream)
+                    ws_k.wait_event(ev)
+                    with torch.cuda.stream(ws_k):
+                        b.run("wgrad", ws_k.cuda_stream)
                 if use_dist and ar_graph and i in last_of_bucket:
                     # this bucket's dW is complete: NCCL all_reduce captured as graph nodes on s3
-                    done = torch.cuda.Event()
-                    done.record(s2)
-                    s3.wait_event(done)
+                    for w in wst:
+                        done = torch.cuda.Event()
+                        done.record(w)
+                        s3.wait_event(done)
                     lo, hi = buckets[last_of_bucket[i]]
                     with torch.cuda.stream(s3):
                         dist.all_reduce(flat[lo:hi])
                 if "deconv" in b.lay.ops:
                     b.run("deconv_only", main.cuda_stream)
-            join = torch.cuda.Event()
-            join.record(s2)
-            main.wait_event(join)
+            for w in wst:
+                join = torch.cuda.Event()
+                join.record(w)
+                main.wait_event(join)
             if use_dist and ar_graph:
                 join3 = torch.cuda.Event()
                 join3.record(s3)
@@ -539,7 +547,8 @@ def run_gpu(args):
                    "zero_free_gflop_per_gpu_step": round(flops_step / 1e9, 3),
                    "l2": "flushed (256 MB write) before every timed step, outside the timed events",
                    "parallelism": f"dp{n_gpus}",
-                   "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad (CUDA graph)"
+                   "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad on %d "
+                               "alternating streams (CUDA graph)" % nws
                                + (("; dW all_reduce in %d buckets overlapping the backward (NCCL in the graph)"
                                    % len(buckets) if ar_in_graph else "; dW all_reduce after the step graph")
                                   if use_dist else ""),
