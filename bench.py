@@ -34,6 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "zero-free TFLOP/s and ms per op (fwd/deconv/wgrad) at 1/2/4/8 B200"
+_JSON_OUT = None  # original stdout when fd 1 is redirected (multi-rank runs)
 
 
 def parse():
@@ -297,6 +298,13 @@ def run_gpu(args):
     # exercises it with a single rank under torchrun (testing on one GPU)
     use_dist = n_gpus > 1 or (os.environ.get("CKS_BENCH_DIST") == "1" and "RANK" in os.environ)
     if use_dist:
+        # keep stdout to the one JSON line: library output written to fd 1 (NCCL's
+        # version banner under NCCL_DEBUG=VERSION) is sent to stderr; the line goes
+        # to the original stdout
+        global _JSON_OUT
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        sys.stdout.flush()
+        os.dup2(2, 1)
         dist.init_process_group("nccl", device_id=device)
     build.build()
     desc, layers = get_config(args.config, args.batch)
@@ -576,7 +584,7 @@ def run_gpu(args):
             print(f"  {bufs[i].lay.name:22s} {op:11s} {ms * 1e3:9.2f} us  {fl / ms / 1e9:9.1f} TFLOP/s",
                   file=sys.stderr)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
     if use_dist:
         dist.destroy_process_group()
     return 0
