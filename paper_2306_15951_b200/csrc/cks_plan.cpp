@@ -125,7 +125,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64;
+        gz_max = 64, wzc = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -140,6 +140,8 @@ struct Knobs {
         if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = getenv("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = getenv("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
+        // 1: G_Z reduce inside a cluster, 2: cluster launch but partials + KB-REDUCE (debug)
+        if (const char* e = getenv("CKS_WGRAD_ZC")) wzc = atoi(e);
     }
 };
 static const Knobs& knobs() {
@@ -471,6 +473,22 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
         int64_t cap = std::max<int64_t>(lmin / 4, 1);
         c.gz = int(std::max<int64_t>(1, std::min<int64_t>({want, cap, int64_t(knobs().gz_max)})));
     }
+    // cluster reduce (zc): gz <= 8 segments of a tile as one thread-block cluster,
+    // one tile per CTA (one wave), the tile's fp32 sums staged in the idle ring
+    // (same stage arithmetic as WgradShape) -- no partials in HBM, no KB-REDUCE launch
+    {
+        const int eb = dt == CKS_TF32 ? 4 : 2, ch = 128 / eb;
+        const int64_t atom = int64_t(c.kimg) * 128;
+        const int64_t stage = (128 / ch) * atom + int64_t(c.mt) * (c.BN / ch) * atom;
+        const int64_t stages = std::min<int64_t>(8, 200 * 1024 / stage);
+        const bool fits = int64_t(128) * c.mt * c.BN * 4 <= stages * stage;
+        // every cluster must be resident at once (one tile per CTA): B200 GPCs hold
+        // 9 pairs but only 4 clusters of 4 / 2 of 8 (measured: 144 CTAs in clusters
+        // of 4 or 8 run in two waves and lose; 72 in clusters of 4 and 144 in pairs win)
+        const int64_t tiles = c.base_tiles * c.gz;
+        const bool one_wave = c.gz == 2 ? tiles <= num_sms : tiles <= 128;
+        c.zc = (knobs().wzc && c.gz >= 2 && c.gz <= 8 && one_wave && fits) ? 1 : 0;
+    }
     return c;
 }
 
@@ -514,7 +532,7 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
     }
     if (op == CKS_OP_WGRAD) {
         WgradCfg c = wgrad_cfg(g, dt, gz, num_sms);
-        if (c.gz > 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+        if (c.gz > 1 && c.zc != 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
     }
     L.total = off;
     return L;

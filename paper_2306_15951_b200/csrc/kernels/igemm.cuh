@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int ri = rs0; ri < rs1; ++ri) {
                     if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
                     if (lane == 0) trace_ev(p, 1, ti, 1);
-                    const uint64_t bdesc0 = dconst | uint64_t(ptx::smem_u32(bbuf + bs * p.b_stage_bytes) >> 4);
+                    const uint64_t bdesc0 = dconst | ptx::desc_addr(ptx::smem_u32(bbuf + bs * p.b_stage_bytes));
                     const int4* pl = pg + 2 + (first ? 0 : 64);
                     const int np = first ? np0 : np1;
                     first = false;
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::mbar_wait(&afull[as], aph);
                         if (lane == 0) trace_ev(p, 1, ti, 2);
                         ptx::tc_fence_after();
-                        const uint64_t aslot = dconst | uint64_t(ptx::smem_u32(abuf + as * a_slot) >> 4);
+                        const uint64_t aslot = dconst | ptx::desc_addr(ptx::smem_u32(abuf + as * a_slot));
                         // entries of this A slot; the next entry is loaded while the
                         // current one issues (hides the shared-memory load latency)
                         int4 en = e < np ? pl[e] : make_int4(-1, 0, 0, 0);

@@ -267,6 +267,12 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // Shared-memory matrix descriptor (sm_100 UMMA): start>>4 [0,14), LBO>>4
 // [16,30), SBO>>4 [32,46), version=1 [46,48), base offset 0, layout [61,64)
 // (2 = SWIZZLE_128B).
+// Start-address field of a shared-memory matrix descriptor: the CTA-local
+// offset >> 4 (14 bits).  Inside a thread-block cluster cvta.to.shared returns
+// the shared::cluster address, whose CTA-rank bits (24+) must not leak into the
+// neighbouring leading-byte-offset field.
+__device__ __forceinline__ uint64_t desc_addr(uint32_t saddr) { return uint64_t((saddr >> 4) & 0x3FFFu); }
+
 __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     uint64_t d = 0;
     d |= uint64_t((saddr >> 4) & 0x3FFFu);

@@ -39,6 +39,9 @@ struct WgradParams {
     int mblocks, nbs, gz, nblk64;  // nblk64: image blocks of KIMG (64 or 128) images
     long long num_tiles;
     long long part_stride;  // OC*FH*FW*C
+    int zc;                 // cluster reduce: the gz segments of one tile are the gz CTAs of one cluster;
+                            // partials staged in smem, summed in fixed order through DSMEM into dW
+    int dbg_cluster;        // debug: cluster size of a launch without the in-cluster reduce (0 = off)
 };
 
 // One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
@@ -72,12 +75,18 @@ template <int MT>
 __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     WTile c;
     uint32_t t = uint32_t(t64);  // 32-bit decode (64-bit div/mod is slow)
+    if (p.zc) {  // segments fastest: the gz CTAs of a cluster share (tap, mb, nb)
+        c.z = int(t % uint32_t(p.gz));
+        t /= uint32_t(p.gz);
+    }
     c.nb = int(t % uint32_t(p.nbs));
     t /= uint32_t(p.nbs);
     c.mb = int(t % uint32_t(p.mblocks));
     t /= uint32_t(p.mblocks);
-    c.z = int(t % uint32_t(p.gz));
-    t /= uint32_t(p.gz);
+    if (!p.zc) {
+        c.z = int(t % uint32_t(p.gz));
+        t /= uint32_t(p.gz);
+    }
     const int tap = int(t);
     c.fh = MT > 1 ? tap : tap / p.FW;
     c.fw = MT > 1 ? 0 : tap % p.FW;
@@ -204,13 +213,13 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
-                const uint64_t ad = dconst | uint64_t(a_addr >> 4);
+                const uint64_t ad = dconst | ptx::desc_addr(a_addr);
                 const int ow = c.ows + (kb / p.nblk64) % max(c.wn, 1);
                 if (ptx::elect_one()) {
 #pragma unroll
                     for (int f = 0; f < MT; ++f) {
                         if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
-                        const uint64_t bd = dconst | uint64_t((a_addr + S::A_BYTES + f * S::B_BYTES) >> 4);
+                        const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_BYTES + f * S::B_BYTES);
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
 #pragma unroll
                         for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
@@ -251,7 +260,9 @@ __global__ void __launch_bounds__(256, 1)
             for (int f = 0; f < MT; ++f) {
             const bool fzero = zero || (MT > 1 && !tap_has_work(c, p, f));
             float* dst = nullptr;
-            if (oc < p.OC)
+            if (p.zc)  // own smem (the ring is idle: one tile per CTA): column group q = (f*BN + c)/4, [q][128 rows]
+                dst = reinterpret_cast<float*>(smem) + (f * (BN / 4)) * 512 + row * 4;
+            else if (oc < p.OC)
                 dst = p.out + c.z * p.part_stride +
                       (static_cast<long long>(oc) * taps + c.fh * p.FW + (MT > 1 ? f : c.fw)) * p.C + cbase;
 #pragma unroll 1
@@ -259,7 +270,17 @@ __global__ void __launch_bounds__(256, 1)
                 uint32_t r[32];
                 ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * (MT * BN) + f * BN + c0, r);
                 ptx::tmem_ld_wait();
-                if (dst != nullptr && c0 < cvalid) {
+                if (p.zc) {
+                    if (fzero) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) r[j] = 0u;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<float4*>(dst + (c0 + j) / 4 * 512) =
+                            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                        __uint_as_float(r[j + 3]));
+                } else if (dst != nullptr && c0 < cvalid) {
                     if (fzero) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) r[j] = 0u;
@@ -287,6 +308,61 @@ __global__ void __launch_bounds__(256, 1)
         }
     }
     __syncthreads();
+    if (p.zc) {
+        // G_Z map-reduce inside the cluster: CTA z sums column slice z of the
+        // tile over the gz segments in fixed order z' = 0..gz-1 and writes dW
+        ptx::cluster_sync();
+        if (warp >= 4 && blockIdx.x < p.num_tiles) {
+            const WTile c = wdecode<MT>(blockIdx.x, p);
+            const int row = int(threadIdx.x) - 128;
+            const int oc = c.mb * 128 + row;
+            const int G = MT * BN / 4;
+            const int g0 = (c.z * G) / p.gz, g1 = ((c.z + 1) * G) / p.gz;
+            const uint32_t sbase = ptx::smem_u32(smem) + uint32_t(row) * 16u;
+            const int taps = p.FH * p.FW;
+            if (oc < p.OC) {
+#pragma unroll 1
+                for (int gq = g0; gq < g1; gq += 2) {
+                    const bool two = gq + 1 < g1;
+                    const uint32_t off = sbase + uint32_t(gq) * 2048u;
+                    float4 a[8], b[8];
+#pragma unroll
+                    for (int z = 0; z < 8; ++z) {
+                        if (z < p.gz) {
+                            a[z] = ptx::ld_dsmem_f4(ptx::mapa(off, uint32_t(z)));
+                            if (two) b[z] = ptx::ld_dsmem_f4(ptx::mapa(off + 2048u, uint32_t(z)));
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 1 && !two) break;
+                        float4 v = h ? b[0] : a[0];
+#pragma unroll
+                        for (int z = 1; z < 8; ++z) {
+                            if (z < p.gz) {
+                                const float4 w = h ? b[z] : a[z];
+                                v.x += w.x;
+                                v.y += w.y;
+                                v.z += w.z;
+                                v.w += w.w;
+                            }
+                        }
+                        const int gg = gq + h;
+                        const int f = gg / (BN / 4), ic = c.nb * BN + (gg % (BN / 4)) * 4;
+                        if (ic >= p.C) continue;
+                        float* o = p.out + (static_cast<long long>(oc) * taps + c.fh * p.FW + (MT > 1 ? f : c.fw)) * p.C + ic;
+                        if ((p.C % 4) == 0) {
+                            *reinterpret_cast<float4*>(o) = v;
+                        } else {
+                            const float e[4] = {v.x, v.y, v.z, v.w};
+                            for (int u = 0; u < 4 && ic + u < p.C; ++u) o[u] = e[u];
+                        }
+                    }
+                }
+            }
+        }
+        ptx::cluster_sync();  // peers finished reading this CTA's staging
+    }
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, S::TMEM_COLS);

@@ -123,8 +123,14 @@ def test_workspace_and_launch_counts():
     gz = L.cks_choose_gz(g, L.CKS_BF16)
     assert 1 <= gz <= 64
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + (gz > 1)
+    # G_Z = 4 segments: either fp32 partials in the workspace + a KB-REDUCE launch,
+    # or (one-wave grids, gz <= 8) the cluster reduce with neither
     ws = L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=4)
-    assert ws >= 4 * 64 * 9 * 64 * 4
+    n4 = L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=4)
+    assert (ws >= 4 * 64 * 9 * 64 * 4 and n4 == 2) or (ws == 0 and n4 == 1)
+    g_big = L.make_geom(256, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)   # 3 row tiles x gz 40: partials + reduce
+    assert L.cks_workspace_size(g_big, L.CKS_BF16, L.CKS_OP_WGRAD, gz=40) >= 40 * 64 * 9 * 64 * 4
+    assert L.cks_launch_count(g_big, L.CKS_BF16, L.CKS_OP_WGRAD, gz=40) == 2
     assert L.cks_ks_split_size(g, L.CKS_BF16) == 4 * 64 * 2 * 2 * 64 * 2
 
 
