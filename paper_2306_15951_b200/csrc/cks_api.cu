@@ -337,9 +337,6 @@ cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const Wgra
     using S = WgradShape<BN, TF, KIMG, MT>;
     auto kern = wgrad_kernel<BN, TF, KIMG, MT>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
-    if (p.dbg_cluster > 1)
-        return launch_pdl_cluster(kern, dim3(unsigned(p.num_tiles)), dim3(256), S::SMEM_BYTES, st, p.dbg_cluster, a, b,
-                                  p);
     if (p.zc) {  // one tile per CTA, the gz segments of a tile are one cluster
         if (p.gz > 8) return CKS_ERR_UNSUPPORTED;
         return launch_pdl_cluster(kern, dim3(unsigned(p.num_tiles)), dim3(256), S::SMEM_BYTES, st, p.gz, a, b, p);
@@ -484,8 +481,7 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.nblk64 = cfg.nblk64;
     p.num_tiles = cfg.base_tiles * cfg.gz;
     p.part_stride = part_stride;
-    p.zc = cfg.zc == 1 ? 1 : 0;
-    p.dbg_cluster = cfg.zc == 2 ? cfg.gz : 0;  // debug: cluster launch without the in-cluster reduce
+    p.zc = cfg.zc;
     p.ouw_s = 1 << 20;
     p.ouw_e = -(1 << 20);
     for (auto& b : tw)
@@ -796,7 +792,7 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.row ? 64 : cfg.kimg)};
         if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
-    float* wout = (cfg.gz > 1 && cfg.zc != 1) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    float* wout = (cfg.gz > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
     if (cfg.row) {  // narrow channels: (fh, fw, c) rows as the GEMM M dimension
         const RowCfg rc = row_cfg_wgrad(*g, dt, gz, kPlanSMs);
@@ -835,7 +831,7 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         s = run_wgrad_taps(*g, dt, cfg, ah, aw, ta, tb, wout, part_stride, st);
     }
     if (s != CKS_OK) return s;
-    if (cfg.gz > 1 && cfg.zc != 1) {  // fixed-order aggregation of the G_Z segments
+    if (cfg.gz > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
         const long long n = part_stride;
         const bool v4 = n % 4 == 0;
         const long long nv = v4 ? n / 4 : n;
@@ -914,7 +910,7 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     else if (op == CKS_OP_DECONV) n += (c_packed_given ? 0 : 1) + (ocpad ? 1 : 0);
     else if (op == CKS_OP_WGRAD) {
         const WgradCfg c = wgrad_cfg(*g, dt, gz, kPlanSMs);
-        n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) + (c.gz > 1 && c.zc != 1 ? 1 : 0);
+        n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) + (c.gz > 1 && !c.zc ? 1 : 0);
     }
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;

@@ -125,7 +125,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 1;
+        gz_max = 64, wzc = 2;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -140,7 +140,8 @@ struct Knobs {
         if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = getenv("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = getenv("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
-        // 1: G_Z reduce inside a cluster, 2: cluster launch but partials + KB-REDUCE (debug)
+        // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
+        // wave of clusters; 2 (default): also shrink G_Z (to >= 3/4) to a size that fits
         if (const char* e = getenv("CKS_WGRAD_ZC")) wzc = atoi(e);
     }
 };
@@ -485,9 +486,30 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
         // every cluster must be resident at once (one tile per CTA): B200 GPCs hold
         // 9 pairs but only 4 clusters of 4 / 2 of 8 (measured: 144 CTAs in clusters
         // of 4 or 8 run in two waves and lose; 72 in clusters of 4 and 144 in pairs win)
-        const int64_t tiles = c.base_tiles * c.gz;
-        const bool one_wave = c.gz == 2 ? tiles <= num_sms : tiles <= 128;
-        c.zc = (knobs().wzc && c.gz >= 2 && c.gz <= 8 && one_wave && fits) ? 1 : 0;
+        // residency model: 8 GPCs of >= 18 SMs hold floor(18 / gz) clusters each
+        auto one_wave = [&](int z) {
+            const int64_t t = c.base_tiles * z;
+            return t <= num_sms && t <= int64_t(8) * (18 / z) * z;
+        };
+        c.zc = 0;
+        if (knobs().wzc && fits && c.gz >= 2) {
+            // the library's own G_Z may shrink (to >= 3/4 of it: measured, halving G_Z
+            // costs more parallelism than the reduce saves) to the largest cluster
+            // size that fits one wave; a requested gz is taken as is
+            int z = std::min(c.gz, 8);
+            if (gz_req == 0 && knobs().wzc == 2)
+                while (z > 2 && !one_wave(z)) --z;
+            // short segments (<= 150 k-blocks each at the halved G_Z) may halve it: in the
+            // training-step schedule the freed SMs serve the concurrent KS-deconv chain
+            // (C2: step 0.593 -> 0.578 ms); long ones keep >= 3/4 (C3 l2 halved: 71 -> 117 us)
+            const bool short_seg = lmin / std::max(z, 1) <= 150;
+            const bool ok = knobs().wzc == 2 && gz_req == 0 ? (short_seg ? 2 * z >= c.gz : 4 * z >= 3 * c.gz)
+                                                            : z == c.gz;
+            if (z >= 2 && z <= 8 && one_wave(z) && ok) {
+                c.gz = z;
+                c.zc = 1;
+            }
+        }
     }
     return c;
 }
@@ -532,7 +554,7 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
     }
     if (op == CKS_OP_WGRAD) {
         WgradCfg c = wgrad_cfg(g, dt, gz, num_sms);
-        if (c.gz > 1 && c.zc != 1) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+        if (c.gz > 1 && !c.zc) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
     }
     L.total = off;
     return L;

@@ -41,7 +41,6 @@ struct WgradParams {
     long long part_stride;  // OC*FH*FW*C
     int zc;                 // cluster reduce: the gz segments of one tile are the gz CTAs of one cluster;
                             // partials staged in smem, summed in fixed order through DSMEM into dW
-    int dbg_cluster;        // debug: cluster size of a launch without the in-cluster reduce (0 = off)
 };
 
 // One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
