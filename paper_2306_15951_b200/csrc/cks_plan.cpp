@@ -256,7 +256,9 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     const bool zc_ok = !pair && knobs().zc && int64_t(128) * c.pbw * c.BN * 4 <= ring;
     if (zc_ok) {
         int z = 8;
-        while (z > 1 && (c.out_tiles * z > num_sms || rs_full < 2 * z)) z /= 2;
+        // one wave of resident clusters (8 GPCs x floor(18 / z) clusters, as for KB-WGRAD)
+        while (z > 1 && (c.out_tiles * z > num_sms || c.out_tiles * z > int64_t(8) * (18 / z) * z || rs_full < 2 * z))
+            z /= 2;
         // the DSMEM reduce costs a few row steps: split only when >= 8 row steps
         // per tile are saved (tools/sweep_zc.sh on the C2 layers)
         if (z > 1 && rs_full * (z - 1) >= 8 * z) {
