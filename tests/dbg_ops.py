@@ -1,9 +1,9 @@
-"""Run fwd / deconv / wgrad of one layer separately with a sync after each (debug).
-usage: python tools/dbg_ops.py N C H W OC FH FW sh sw ph pw [ops]"""
+"""Run fwd / deconv / wgrad of one layer separately with a sync after each (debug; test infrastructure: compares with the oracle).
+usage: python tests/dbg_ops.py N C H W OC FH FW sh sw ph pw [ops]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # repo root
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
