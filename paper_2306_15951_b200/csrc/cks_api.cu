@@ -282,6 +282,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.zc = cfg.zc;
     p.pair = cfg.pair;
     p.epi_warps = cfg.epi ? cfg.epi_warps : 4;
+    p.epi_bufs = cfg.epi ? cfg.epi_bufs : 1;
     {
         const int need = cfg.acc_stages * cfg.pbw * cfg.BN * (cfg.pair ? 2 : 1);
         int cols = 32;
@@ -309,7 +310,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.cm = cfg.cm;
     p.unified = cfg.unified;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
-                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? epi_stage_bytes(cfg.epi_warps) + 1024 : 0);
+                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? epi_stage_bytes(cfg.epi_warps, cfg.epi_bufs) + 1024 : 0);
     if (cfg.Z > 1 && !cfg.zc) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);

@@ -125,7 +125,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2;
+        gz_max = 64, wzc = 2, epi_bufs = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -143,6 +143,7 @@ struct Knobs {
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
         // wave of clusters; 2 (default): also shrink G_Z (to >= 3/4) to a size that fits
         if (const char* e = getenv("CKS_WGRAD_ZC")) wzc = atoi(e);
+        if (const char* e = getenv("CKS_EPI_BUFS")) epi_bufs = atoi(e) == 2 ? 2 : 1;  // TMA-store staging depth
     }
 };
 static const Knobs& knobs() {
@@ -162,13 +163,14 @@ bool epi_staging() { return knobs().epi != 0; }
 
 static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout,
                             int64_t kchan, int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms,
-                            int force_pbw, int epi_warps, bool pair = false) {
+                            int force_pbw, int epi_warps, bool pair = false, int epi_bufs = 1) {
     IgemmCfg c;
     c.pair = pair ? 1 : 0;
+    c.epi_bufs = epi_bufs;
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
     c.epi = (epi_staging() && nout % 4 == 0) ? 1 : 0;
     c.epi_warps = epi_warps;
-    int64_t budget = kSmemBudget - (c.epi ? epi_stage_bytes(epi_warps) + 1024 : 0);  // + 1 KB alignment
+    int64_t budget = kSmemBudget - (c.epi ? epi_stage_bytes(epi_warps, epi_bufs) + 1024 : 0);  // + 1 KB alignment
     if (knobs().smem_cap > 0) budget = std::min<int64_t>(budget, int64_t(knobs().smem_cap) * 1024);  // experiments
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
@@ -296,8 +298,15 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
     // pixel wide with >= 2 channel blocks (the pair loads each activation column
     // once instead of once per 128-channel block: C3 l3 -9 %) and the pair grid
     // is >= 2.5 waves; a loss against 2-pixel tiles (C4) and on short grids (C3 l4).
-    const IgemmCfg c4 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
-                                    force_pbw, 4);
+    IgemmCfg c4 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
+                              force_pbw, 4);
+    if (knobs().epi_bufs == 2 && c4.epi) {  // double-buffered TMA-store staging where it costs no ring depth
+        const IgemmCfg c2 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
+                                        force_pbw, 4, false, 2);
+        if (c2.pbw == c4.pbw && c2.apos == c4.apos && c2.stages == c4.stages && c2.a_stages == c4.a_stages &&
+            c2.unified == c4.unified && c2.BN == c4.BN && c2.Z == c4.Z && c2.zc == c4.zc)
+            c4 = c2;
+    }
     if (knobs().pair && eb == 2 && nout >= 256 && N > 128 && kchan * eb >= 128 && force_pbw == 0 && c4.pbw == 1 &&
         c4.nbs >= 2 && c4.Z == 1) {
         const IgemmCfg cp = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,

@@ -75,6 +75,7 @@ struct IgemmCfg {
     int Z = 1;          // split-K segments
     int zc = 0;         // cluster split-K (Z CTAs of one cluster per output tile, DSMEM reduce)
     int epi_warps = 4;  // epilogue warps (4 or 8)
+    int epi_bufs = 1;   // TMA-store staging buffers per epilogue warp (1 or 2)
     int pair = 0;       // CTA pair (cta_group::2): nblk counts image-block pairs, BN = this CTA's half
     int kc_blocks = 1;
     int KB = 128;       // bytes per K row: 32 / 64 / 128 (swizzle width)
@@ -95,7 +96,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 4160;  // minus alignment, barriers, tables, MMA programs
 constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
-constexpr int epi_stage_bytes(int epi_warps) { return epi_warps * 4096; }
+constexpr int epi_stage_bytes(int epi_warps, int bufs = 1) { return epi_warps * bufs * 4096; }
 bool epi_staging();                       // coalesced-store epilogue (default on; CKS_EPI_STAGE=0 disables)
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);

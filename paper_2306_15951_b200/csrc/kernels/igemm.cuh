@@ -103,6 +103,7 @@ struct IgemmParams {
     int epi_stage;        // 16 KB epilogue staging: transpose 32x32 blocks, store full 128 B lines
     int tmem_cols;        // TMEM columns allocated (only what the accumulators need: a small
                           // layer's CTA can share its SM with the next kernel's CTA)
+    int epi_bufs;         // 4 KB TMA-store staging buffers per epilogue warp (1 or 2)
     int epi_warps;        // epilogue warps: 4 (one per TMEM sub-partition) or 8 (two, alternate 32-column chunks)
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t half = ew >> 2, nhalf = uint32_t(p.epi_warps) >> 2;
         const int row = int(sub * 32 + lane);
         const int et = threadIdx.x - 128;  // 0..32*epi_warps-1
+        uint32_t ebuf = 0;                 // TMA-store epilogue buffer sequence
         uint32_t acc = 0, acc_ph = 0;
         const int pw_cols = p.pbw * BNo;
         // accumulator buffer released to the MMA issuer (pair: on the leader's barrier)
@@ -627,7 +629,9 @@ __global__ void __launch_bounds__(384, 1)
             // 4 KB epilogue buffer, one TMA store in flight per warp (the buffer is
             // reused once the previous store has read it): async full-line stores
             if (p.tma_store == 2 && !split && t + tstep < p.num_tiles && !(p.dbg & 1)) {
-                float* blk = epi + ew * 1024;
+                // epi_bufs 4 KB buffers per warp: with 2, one store may still be reading
+                // the other buffer while this one is filled
+                const uint32_t nbuf = uint32_t(p.epi_bufs);
 #pragma unroll 1
                 for (int j = 0; j < c.len; ++j) {
                     const bool live = any && (tab[1].te[c.j0 + j] > tab[1].ts[c.j0 + j]);
@@ -638,7 +642,14 @@ __global__ void __launch_bounds__(384, 1)
                                            c0, r);
                         ptx::tmem_ld_wait();
                         if (c0 >= cvalid) continue;
-                        if (ptx::elect_one()) ptx::bulk_wait_read0();  // previous store has read the buffer
+                        float* blk = epi + (ew * nbuf + (ebuf & (nbuf - 1u))) * 1024;
+                        ++ebuf;
+                        if (ptx::elect_one()) {  // the store that last used this buffer has read it
+                            if (nbuf == 2)
+                                ptx::bulk_wait_read1();
+                            else
+                                ptx::bulk_wait_read0();
+                        }
                         __syncwarp();
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
@@ -730,7 +741,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (stage) {
                         // transpose through a 128B-swizzled 32 x 32 block: 8 lanes write one
                         // image's 32 channels (128 B, a full line) per store instruction
-                        float* blk = epi + ew * 1024;
+                        float* blk = epi + ew * uint32_t(p.epi_bufs) * 1024;
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
                             *reinterpret_cast<float4*>(blk + lane * 32 + ((q ^ (lane & 7)) << 2)) =
