@@ -333,10 +333,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
 }
 
-template <int BN, bool TF, int KIMG, int MT = 1>
+template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false>
 cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
-    using S = WgradShape<BN, TF, KIMG, MT>;
-    auto kern = wgrad_kernel<BN, TF, KIMG, MT>;
+    using S = WgradShape<BN, TF, KIMG, MT, A1>;
+    auto kern = wgrad_kernel<BN, TF, KIMG, MT, A1>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     if (p.zc) {  // one tile per CTA, the gz segments of a tile are one cluster
         if (p.gz > 8) return CKS_ERR_UNSUPPORTED;
@@ -493,6 +493,13 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     if (p.ouw_e < p.ouw_s) p.ouw_e = p.ouw_s = 0;
     const bool tf = dt == CKS_TF32;
     const bool k128 = cfg.kimg == 128;
+    if (cfg.a1 && !tf && cfg.BN == 64) {  // O_C <= 64: one dY atom per stage
+        if (cfg.mt == 3)
+            return k128 ? launch_wgrad_t<64, false, 128, 3, true>(ta, tb, p, st)
+                        : launch_wgrad_t<64, false, 64, 3, true>(ta, tb, p, st);
+        return k128 ? launch_wgrad_t<64, false, 128, 1, true>(ta, tb, p, st)
+                    : launch_wgrad_t<64, false, 64, 1, true>(ta, tb, p, st);
+    }
     if (cfg.mt == 3 && !tf && cfg.BN == 64)  // row tiles: the F_W = 3 taps of a filter row share the dY block
         return k128 ? launch_wgrad_t<64, false, 128, 3>(ta, tb, p, st) : launch_wgrad_t<64, false, 64, 3>(ta, tb, p, st);
 #define CKS_WG(BN_)                                                                                   \

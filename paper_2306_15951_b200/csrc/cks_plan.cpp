@@ -125,7 +125,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1;
     Knobs() {
         if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
@@ -144,6 +144,7 @@ struct Knobs {
         // wave of clusters; 2 (default): also shrink G_Z (to >= 3/4) to a size that fits
         if (const char* e = getenv("CKS_WGRAD_ZC")) wzc = atoi(e);
         if (const char* e = getenv("CKS_EPI_BUFS")) epi_bufs = atoi(e) == 2 ? 2 : 1;  // TMA-store staging depth
+        if (const char* e = getenv("CKS_WGRAD_A1")) wa1 = atoi(e) != 0;  // O_C <= 64: one dY atom per stage
     }
 };
 static const Knobs& knobs() {
@@ -488,10 +489,11 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     // cluster reduce (zc): gz <= 8 segments of a tile as one thread-block cluster,
     // one tile per CTA (one wave), the tile's fp32 sums staged in the idle ring
     // (same stage arithmetic as WgradShape) -- no partials in HBM, no KB-REDUCE launch
+    c.a1 = (dt == CKS_BF16 && c.BN == 64 && g.OC <= 64 && knobs().wa1) ? 1 : 0;
     {
         const int eb = dt == CKS_TF32 ? 4 : 2, ch = 128 / eb;
         const int64_t atom = int64_t(c.kimg) * 128;
-        const int64_t stage = (128 / ch) * atom + int64_t(c.mt) * (c.BN / ch) * atom;
+        const int64_t stage = (c.a1 ? 1 : 128 / ch) * atom + int64_t(c.mt) * (c.BN / ch) * atom;
         const int64_t stages = std::min<int64_t>(8, 200 * 1024 / stage);
         const bool fits = int64_t(128) * c.mt * c.BN * 4 <= stages * stage;
         // every cluster must be resident at once (one tile per CTA): B200 GPCs hold

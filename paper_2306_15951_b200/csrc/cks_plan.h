@@ -127,6 +127,7 @@ struct WgradCfg {
     int kimg = 64;     // images per k-block (64 or 128)
     int mt = 1;        // taps per tile along w: 1, or F_W (row tiles sharing the dY block)
     int zc = 0;        // cluster reduce: the gz segments of a tile form one cluster (DSMEM sum, no partials)
+    int a1 = 0;        // O_C <= 64 (bf16, BN = 64): one dY atom per ring stage
 };
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 

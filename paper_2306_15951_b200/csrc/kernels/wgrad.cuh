@@ -47,7 +47,10 @@ struct WgradParams {
 // an MN-major swizzle atom column.  BF16: SWIZZLE_128B (16 B chunks, 8-row
 // K groups, SBO 1 KB).  TF32: SWIZZLE_128B_BASE32B (32 B chunks, 4-row K
 // groups, SBO 512 B) -- the MN-major layout tcgen05 kind::tf32 requires.
-template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1>
+// A1: O_C <= 64 -- the stage holds ONE dY atom; the MMA's other 64 A rows read
+// the stage's first X block (garbage rows of D, never stored), so the ring
+// carries one more stage instead of a zero-filled atom.
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false>
 struct WgradShape {
     static constexpr int EB = kTF32 ? 4 : 2;
     static constexpr int CH = 128 / EB;                 // channels per box
@@ -56,7 +59,8 @@ struct WgradShape {
     static constexpr int B_BYTES = (BN / CH) * ATOM;    // BN IC x KIMG images
     static constexpr int UK = 32 / EB;                  // K (images) per MMA
     static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
-    static constexpr int STAGE_BYTES = A_BYTES + MT * B_BYTES;
+    static constexpr int A_STAGE = A1 ? ATOM : A_BYTES;  // dY bytes reserved per stage
+    static constexpr int STAGE_BYTES = A_STAGE + MT * B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * MT * BN <= 128 ? 128 : 2 * MT * BN <= 256 ? 256 : 512;
@@ -113,11 +117,11 @@ __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& 
     return false;
 }
 
-template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1>
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
-    using S = WgradShape<BN, kTF32, KIMG, MT>;
+    using S = WgradShape<BN, kTF32, KIMG, MT, A1>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(256, 1)
                             const int iw = ow * p.sw + (MT > 1 ? f : c.fw) - p.pw;
 #pragma unroll
                             for (int j = 0; j < BN / S::CH; ++j)
-                                ptx::tma_load_4d(sa + S::A_BYTES + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
+                                ptx::tma_load_4d(sa + S::A_STAGE + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
                                                  c.nb * BN + j * S::CH, iw, ih, n64 * KIMG);
                         }
                     }
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                     for (int f = 0; f < MT; ++f) {
                         if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
-                        const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_BYTES + f * S::B_BYTES);
+                        const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_STAGE + f * S::B_BYTES);
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
 #pragma unroll
                         for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
