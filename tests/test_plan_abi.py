@@ -5,6 +5,7 @@ counts, validation and error codes.  No compute call is made (no GPU here)."""
 import ctypes
 import os
 import re
+import sys
 
 import pytest
 
@@ -184,3 +185,32 @@ def test_zins_workspace_holds_the_zero_inserted_operand():
     with pytest.raises(L.CksError) as e:
         L.cks_zins_workspace_size(bad, L.CKS_BF16, L.CKS_OP_FWD)
     assert e.value.status == 2
+
+
+def _plans(cfg, op):
+    """Tile plans the library picks (tools/plan_dump.py: CKS_PLAN_DEBUG, host only)."""
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "plan_dump.py"), str(cfg), op],
+                         stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, timeout=300, cwd=ROOT)
+    plans, name = {}, None
+    for ln in out.stdout.splitlines():
+        if ln.startswith("[cks plan]"):
+            plans[name] = dict(kv.split("=") for kv in ln.split()[3:] if "=" in kv)
+        elif ln and not ln.startswith("[") and " " not in ln.strip():
+            name = ln.strip()
+    return plans
+
+
+def test_plan_choices_on_the_workloads():
+    """Regression guard for the measured plan heuristics: CTA
+    pairs on C3 l3 (one-pixel plans with >= 2 channel blocks, >= 2.5 waves),
+    cluster split-K on the 4x4 C2 layers, single-CTA tiles elsewhere."""
+    fwd3 = _plans(2, "fwd")
+    assert fwd3["l3_0"]["pair"] == "1" and fwd3["l3a"]["pair"] == "1"
+    assert fwd3["l4_0"]["pair"] == "0" and fwd3["l2_0"]["pair"] == "0"
+    fwd2 = _plans(1, "fwd")
+    assert fwd2["vgg4_512to512_s2"]["zc"] == "1" and int(fwd2["vgg4_512to512_s2"]["Z"]) >= 2
+    assert fwd2["vgg32_64to64_s1"]["zc"] == "0" and fwd2["vgg32_64to64_s1"]["pair"] == "0"
+    for name, pl in list(fwd2.items()) + list(fwd3.items()):
+        if pl["zc"] == "1":   # one wave of resident clusters
+            assert int(pl["out_tiles"]) * int(pl["Z"]) <= 148, name

@@ -6,6 +6,7 @@ import ctypes
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["CKS_PLAN_DEBUG"] = "1"
+os.environ["CUDA_VISIBLE_DEVICES"] = ""  # plan only: never launch on the fake pointers below, even on a GPU box
 from cks_synth import get_config  # noqa: E402
 from paper_2306_15951_b200 import _lib as L  # noqa: E402
 
