@@ -86,17 +86,20 @@ cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz
 /* The G_Z the library would use for this geometry with gz = 0 (P:212:
  * "G_Z can be positive related to (N_a + N_b)/N_g ... the upper-bound can be
  * decided by the number of streaming multi-processors").  For narrow-channel
- * bf16 layers (FW*C <= 64, C <= 16, W*C*2 a multiple of 16: the filter-row
- * kernel) the segments are per column class and the returned G_Z, like a
- * requested gz, is a multiple of the class count P = 8 / gcd(sw*C, 8)
- * (a requested gz is rounded up).  Host only. */
+ * layers (the filter-row kernel: FW*C plus its alignment shift fits a 64-
+ * element bf16 / 32-element fp32 row, C <= 16 bf16 / 8 fp32, 16-byte X row
+ * pitch) the segments are per output-column class (interior columns grouped
+ * by box alignment, each border column its own class): the returned G_Z is
+ * the total segment count, at least the number of classes; a requested gz is
+ * spread over the classes the same way.  Host only. */
 cks_status cks_choose_gz(const cks_geom* g, cks_dtype dt, int* gz);
 
 /* Eq (1) via ConvV2 (Alg. 1): Y[n,oh,ow,oc] = sum over the TRIMMED
  * window fh in [fh_s, fh_e), fw in [fw_s, fw_e), ic of
  * X[n, oh*sh-ph+fh, ow*sw-pw+fw, ic] * W[oc,fh,fw,ic]; padded zeros are never
- * loaded or multiplied (narrow-channel bf16 layers, FW*C <= 64: trimmed in h,
- * the w-direction padding of a filter-row run is TMA zero fill).
+ * loaded or multiplied (the narrow-channel filter-row kernel trims at its
+ * 32-byte K-chunk granularity with chunk grids aligned to the image edge:
+ * cks_padding_macs reports the products, 0 on every config).
  * x: N*H*W*C (dtype), w: OC*FH*FW*C (dtype), y: N*OH*OW*OC fp32 (overwritten). */
 cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const void* w, float* y,
                           void* ws, size_t ws_bytes, void* stream);
@@ -161,6 +164,26 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]);
  * the bench's gpu_launches claim).  c_packed_given: deconv skips Stage1. */
 cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, int c_packed_given,
                             int* launches);
+
+/* Text description of the plan the library uses for (g, dt, op, gz): the
+ * kernel kind ("igemm", "row_fwd", "wgrad", "row_wgrad") followed by its tile
+ * configuration as space-separated key=value pairs (host only; for tests and
+ * tools).  *len receives strlen + 1; if it exceeds cap, nothing is written
+ * and CKS_ERR_CAPACITY is returned. */
+cks_status cks_plan_describe(const cks_geom* g, cks_dtype dt, cks_op op, int gz, char* buf, size_t cap,
+                             size_t* len);
+
+/* Multiply-accumulates the op's kernels spend on SPATIAL-PADDING zeros for the
+ * whole batch (host only; accounting next to cks_op_counts, Table III).  0
+ * for the trimmed-window kernels (every ConvV2 / KS-deconv / Sk-dilated tile
+ * iterates its valid window only, Alg. 1-3B).  The narrow-channel row kernels
+ * trim at the granularity of their tensor-core operands: ConvV2 loads only
+ * valid filter rows and issues only the 32-byte K chunks that hold valid
+ * elements, with the chunk grid of a border column aligned to the image edge,
+ * so its count is 0 unless a window overhangs both ends of the row;
+ * Sk-dilated multiplies the zero-filled rows / border elements inside an
+ * issued 128-row M-block (M-blocks entirely outside X are skipped). */
+cks_status cks_padding_macs(const cks_geom* g, cks_dtype dt, cks_op op, int64_t* macs);
 
 /* ------------------------------------------------------------ KB-ZINS
  * The formulation C-K-S removes, for measurement ("measured

@@ -21,7 +21,8 @@ STATUS = {0: "CKS_OK", 1: "CKS_ERR_NULL", 2: "CKS_ERR_GEOMETRY", 3: "CKS_ERR_UNS
 EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2d_fwd", "cks_ks_split_size",
            "cks_ks_split", "cks_deconv2d", "cks_dilated_wgrad", "cks_axis_table", "cks_op_counts",
            "cks_launch_count", "cks_status_string", "cks_version", "cks_zins_workspace_size",
-           "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad")
+           "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad", "cks_plan_describe",
+           "cks_padding_macs")
 
 
 class CksError(RuntimeError):
@@ -69,6 +70,8 @@ def lib():
             "cks_zins_conv2d_fwd": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
             "cks_zins_deconv2d": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
             "cks_zins_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_plan_describe": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.c_char_p, sz, C.POINTER(sz)]),
+            "cks_padding_macs": (C.c_int, [G, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
             "cks_status_string": (C.c_char_p, [C.c_int]),
             "cks_version": (C.c_int, []),
         }
@@ -158,6 +161,30 @@ def cks_op_counts(g: cks_geom, dtype: int = CKS_BF16) -> dict:
 def cks_launch_count(g: cks_geom, dtype: int, op: int, gz: int = 0, c_packed_given: bool = False) -> int:
     v = C.c_int()
     _check(lib().cks_launch_count(C.byref(g), dtype, op, gz, int(c_packed_given), C.byref(v)), "cks_launch_count")
+    return v.value
+
+
+def cks_plan_describe(g: cks_geom, dtype: int, op: int, gz: int = 0) -> str:
+    n = C.c_size_t()
+    st = lib().cks_plan_describe(C.byref(g), dtype, op, gz, None, 0, C.byref(n))
+    if st not in (0, 7):
+        _check(st, "cks_plan_describe")
+    buf = C.create_string_buffer(n.value)
+    _check(lib().cks_plan_describe(C.byref(g), dtype, op, gz, buf, n.value, C.byref(n)), "cks_plan_describe")
+    return buf.value.decode()
+
+
+def plan_dict(g: cks_geom, dtype: int, op: int, gz: int = 0) -> dict:
+    """cks_plan_describe parsed: {'kind': ..., key: value (str)}."""
+    parts = cks_plan_describe(g, dtype, op, gz).split()
+    d = {"kind": parts[0]}
+    d.update(kv.split("=", 1) for kv in parts[1:])
+    return d
+
+
+def cks_padding_macs(g: cks_geom, dtype: int, op: int) -> int:
+    v = C.c_int64()
+    _check(lib().cks_padding_macs(C.byref(g), dtype, op, C.byref(v)), "cks_padding_macs")
     return v.value
 
 

@@ -1,6 +1,7 @@
 """Build libcks.so in-tree with nvcc for sm_100a (no GPU needed)."""
 from __future__ import annotations
 
+import fcntl
 import os
 import shutil
 import subprocess
@@ -30,15 +31,31 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libcks.so in-tree.  Safe under concurrent callers (every torchrun
+    rank calls this): an exclusive file lock serialises them, the first one
+    compiles into a per-process temporary and renames it into place, the
+    others then see an up-to-date library and return."""
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", "-o", LIB + ".tmp"] + SOURCES
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_build():  # another process built it meanwhile
+                return LIB
+            tmp = f"{LIB}.{os.getpid()}.tmp"
+            cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+                   "-Xcompiler", "-fPIC", "-shared", "-o", tmp] + SOURCES
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+                print(" ".join(cmd), file=sys.stderr)
+            try:
+                subprocess.run(cmd, check=True)
+                os.replace(tmp, LIB)
+            finally:
+                if os.path.exists(tmp):
+                    os.remove(tmp)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
     return LIB
 
 

@@ -229,16 +229,6 @@ cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const C
     return launch_igemm_kb<false, 128>(BN, a, b, y, p, smem, st);
 }
 
-// experiments: print the igemm tile plan (CKS_PLAN_DEBUG set; host only, before any CUDA call)
-void plan_debug(const IgemmCfg& cfg) {
-    static const bool plan_dbg = getenv("CKS_PLAN_DEBUG") != nullptr;
-    if (plan_dbg)
-        fprintf(stderr, "[cks plan] igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d "
-                        "out_tiles=%lld Z=%d zc=%d kc=%d epi_warps=%d pair=%d\n",
-                cfg.BN, cfg.pbw, cfg.KB, cfg.ntap, cfg.pa, cfg.apos, cfg.stages, cfg.a_stages, cfg.unified,
-                (long long)cfg.out_tiles, cfg.Z, cfg.zc, cfg.kc_blocks, cfg.epi_warps, cfg.pair);
-}
-
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
 cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRow>& rh, const std::vector<KRow>& rw,
                      const CUtensorMap& ta, const CUtensorMap& tb, float* out, int out_H, int out_W, int out_C,
@@ -372,81 +362,136 @@ cks_status launch_split(const cks_geom& g, cks_dtype dt, const void* w, void* ou
 }
 
 // ------------------------------------------------------------------ narrow-channel row path
-// X viewed as (W*C elements, N, H, 1): a box (JB, imgs, FH, 1) is the
-// contiguous (fw, c) run of all FH filter rows for `imgs` images, element-
-// addressed at (ow*sw - pw)*C (negative / past-the-end = padding, zero fill).
-bool make_row_xmap(CUtensorMap* m, const void* x, const cks_geom& g, uint32_t JB, uint32_t imgs) {
+// X viewed as (W*C elements, N, H, 1): a box (JB, imgs, rows, 1) is the
+// contiguous (fw, c) run of `rows` consecutive X rows for `imgs` images,
+// element-addressed at (ow*sw - pw)*C + off (past-the-end / negative rows =
+// zero fill).  K-major (ConvV2): swizzle of the row width; MN-major tf32
+// (Sk-dilated): SWIZZLE_128B_ATOM_32B.
+bool make_row_xmap(CUtensorMap* m, const void* x, const cks_geom& g, cks_dtype dt, uint32_t JB, uint32_t imgs,
+                   uint32_t rows, bool mn_tf32) {
+    const uint64_t eb = uint64_t(elem_bytes(dt));
     uint64_t d[4] = {uint64_t(g.W * g.C), uint64_t(g.N), uint64_t(g.H), 1};
-    uint64_t sb[3] = {uint64_t(g.H * g.W * g.C * 2), uint64_t(g.W * g.C * 2), uint64_t(g.N * g.H * g.W * g.C * 2)};
-    uint32_t box[4] = {JB, imgs, uint32_t(g.FH), 1};
-    return make_tmap4(m, CKS_BF16, x, d, sb, box, int(JB * 2));
+    uint64_t sb[3] = {uint64_t(g.H * g.W * g.C) * eb, uint64_t(g.W * g.C) * eb, uint64_t(g.N * g.H * g.W * g.C) * eb};
+    uint32_t box[4] = {JB, imgs, rows, 1};
+    return make_tmap4(m, dt, x, d, sb, box, int(JB * eb), mn_tf32);
 }
 
-template <int JB, int BN>
+void fill_row_classes(RowClass* dst, const std::vector<RowClassH>& src) {
+    for (size_t k = 0; k < src.size(); ++k) {
+        dst[k].col0 = int16_t(src[k].col0);
+        dst[k].cstep = int16_t(src[k].cstep);
+        dst[k].ncols = int16_t(src[k].ncols);
+        dst[k].off = int16_t(src[k].off);
+        dst[k].kc0 = int8_t(src[k].kc0);
+        dst[k].kc1 = int8_t(src[k].kc1);
+        dst[k].base = int16_t(src[k].base);
+        dst[k].cnt = int16_t(src[k].cnt);
+    }
+}
+
+template <int ROWB, int BN, bool TF>
 cks_status launch_fwd_row_t(const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem, int grid,
                             cudaStream_t st) {
-    auto kern = fwd_row_kernel<JB, BN>;
+    auto kern = fwd_row_kernel<ROWB, BN, TF>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, ty, p);
 }
 
-template <int JB>
-cks_status launch_fwd_row_jb(int BN, const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem,
+template <int ROWB, bool TF>
+cks_status launch_fwd_row_rb(int BN, const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem,
                              int grid, cudaStream_t st) {
     switch (BN) {
-        case 32: return launch_fwd_row_t<JB, 32>(tx, ty, p, smem, grid, st);
-        case 64: return launch_fwd_row_t<JB, 64>(tx, ty, p, smem, grid, st);
-        case 128: return launch_fwd_row_t<JB, 128>(tx, ty, p, smem, grid, st);
-        case 256: return launch_fwd_row_t<JB, 256>(tx, ty, p, smem, grid, st);
+        case 32: return launch_fwd_row_t<ROWB, 32, TF>(tx, ty, p, smem, grid, st);
+        case 64: return launch_fwd_row_t<ROWB, 64, TF>(tx, ty, p, smem, grid, st);
+        case 128: return launch_fwd_row_t<ROWB, 128, TF>(tx, ty, p, smem, grid, st);
+        case 256:
+            if constexpr (!TF) return launch_fwd_row_t<ROWB, 256, TF>(tx, ty, p, smem, grid, st);
+            break;
     }
     return CKS_ERR_UNSUPPORTED;
 }
 
-cks_status run_fwd_row(const cks_geom& g, const RowCfg& rc, const void* x, const void* w, float* y, cudaStream_t st) {
+cks_status run_fwd_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, const void* x, const void* w, float* y,
+                       cudaStream_t st) {
     CUtensorMap tx, ty;
     memset(&ty, 0, sizeof(ty));
-    if (!make_row_xmap(&tx, x, g, uint32_t(rc.JB), 128)) return CKS_ERR_CUDA;
+    if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 128, 1, false)) return CKS_ERR_CUDA;
     RowFwdParams p;
     memset(&p, 0, sizeof(p));
-    p.w = static_cast<const uint16_t*>(w);
+    p.w = w;
     p.y = y;
     p.N = int(g.N), p.H = int(g.H), p.W = int(g.W), p.C = int(g.C), p.OC = int(g.OC);
     p.FH = int(g.FH), p.FW = int(g.FW), p.sh = g.sh, p.sw = g.sw, p.ph = g.ph, p.pw = g.pw;
     p.OH = int(axis_h(g).O), p.OW = int(axis_w(g).O);
     p.nblk = rc.nblk;
-    p.P = rc.P;
-    for (int k = 0; k < 8; ++k) p.delta[k] = rc.delta[k];
+    p.R = rc.R;
+    p.ncls = int(rc.cls.size());
+    fill_row_classes(p.cls, rc.cls);
     p.stages = rc.stages;
-    if (g.OC % 32 == 0 && !(debug_flags() & 32)) {  // TMA-store epilogue: 32 channels x 32 images boxes
+    if (g.OC % 32 == 0) {  // TMA-store epilogue: 32 channels x 32 images boxes
         uint64_t d[4] = {uint64_t(g.OC), uint64_t(p.OW), uint64_t(p.OH), uint64_t(g.N)};
         uint64_t sb[3] = {uint64_t(g.OC) * 4, uint64_t(p.OW) * g.OC * 4, uint64_t(p.OH) * p.OW * g.OC * 4};
         uint32_t box[4] = {32, 1, 1, 32};
         if (make_tmap4_f32(&ty, y, d, sb, box)) p.tma_store = 1;
     }
-    switch (rc.JB) {
-        case 16: return launch_fwd_row_jb<16>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
-        case 32: return launch_fwd_row_jb<32>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
-        case 64: return launch_fwd_row_jb<64>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+    const bool tf = dt == CKS_TF32;
+    switch (rc.ROWB) {
+        case 32: return tf ? launch_fwd_row_rb<32, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
+                           : launch_fwd_row_rb<32, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+        case 64: return tf ? launch_fwd_row_rb<64, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
+                           : launch_fwd_row_rb<64, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+        case 128: return tf ? launch_fwd_row_rb<128, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
+                            : launch_fwd_row_rb<128, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
 
-template <int JB, int BN>
+template <int ROWB, int BN, bool TF>
 cks_status launch_wgrad_row_t(const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p, int smem,
                               cudaStream_t st) {
-    auto kern = wgrad_row_kernel<JB, BN>;
+    auto kern = wgrad_row_kernel<ROWB, BN, TF>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::max<long long>(1, std::min<long long>(p.num_tiles, device_sms()));
     return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, tdy, p);
 }
 
-template <int JB>
-cks_status launch_wgrad_row_jb(int BN, const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p,
+template <int ROWB, bool TF>
+cks_status launch_wgrad_row_rb(int BN, const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p,
                                int smem, cudaStream_t st) {
     switch (BN) {
-        case 64: return launch_wgrad_row_t<JB, 64>(tx, tdy, p, smem, st);
-        case 128: return launch_wgrad_row_t<JB, 128>(tx, tdy, p, smem, st);
-        case 256: return launch_wgrad_row_t<JB, 256>(tx, tdy, p, smem, st);
+        case 64: return launch_wgrad_row_t<ROWB, 64, TF>(tx, tdy, p, smem, st);
+        case 128: return launch_wgrad_row_t<ROWB, 128, TF>(tx, tdy, p, smem, st);
+        case 256: return launch_wgrad_row_t<ROWB, 256, TF>(tx, tdy, p, smem, st);
+    }
+    return CKS_ERR_UNSUPPORTED;
+}
+
+cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, const void* x, const CUtensorMap& tdy,
+                         float* wout, long long part_stride, cudaStream_t st) {
+    const bool tf = dt == CKS_TF32;
+    CUtensorMap tx;
+    if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 64, uint32_t(g.FH), tf)) return CKS_ERR_CUDA;
+    RowWgradParams q;
+    memset(&q, 0, sizeof(q));
+    q.out = wout;
+    q.part_stride = part_stride;
+    q.N = int(g.N), q.H = int(g.H), q.W = int(g.W), q.C = int(g.C), q.OC = int(g.OC);
+    q.FH = int(g.FH), q.FW = int(g.FW), q.sh = g.sh, q.sw = g.sw, q.ph = g.ph, q.pw = g.pw;
+    q.OH = int(axis_h(g).O), q.OW = int(axis_w(g).O);
+    q.mb = rc.mb;
+    q.nbs = rc.nbs;
+    q.ncls = int(rc.cls.size());
+    fill_row_classes(q.cls, rc.cls);
+    q.gz = rc.gz;
+    q.nblk64 = rc.nblk;
+    q.num_tiles = int(rc.tiles);
+    q.stages = rc.stages;
+    q.a_bytes = rc.mb * 128 * 64 * int(elem_bytes(dt));
+    if (tf) return rc.ROWB == 128 ? launch_wgrad_row_rb<128, true>(rc.BN, tx, tdy, q, rc.smem, st) : CKS_ERR_UNSUPPORTED;
+    switch (rc.ROWB) {
+        case 32: return launch_wgrad_row_rb<32, false>(rc.BN, tx, tdy, q, rc.smem, st);
+        case 64: return launch_wgrad_row_rb<64, false>(rc.BN, tx, tdy, q, rc.smem, st);
+        case 128: return launch_wgrad_row_rb<128, false>(rc.BN, tx, tdy, q, rc.smem, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
@@ -678,7 +723,7 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
     if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const RowCfg rc = row_cfg_fwd(*g, dt);
-    if (rc.ok) return run_fwd_row(*g, rc, x, w, y, st);  // narrow channels: filter-row K-blocks
+    if (rc.ok) return run_fwd_row(*g, dt, rc, x, w, y, st);  // narrow channels: filter-row K-blocks
     const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt);
     const void* xs = x;
     const void* wsrc = w;
@@ -691,7 +736,6 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
         wsrc = wp;
     }
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
-    plan_debug(cfg);
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
@@ -748,7 +792,6 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
     }
     const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
     IgemmCfg cfg = igemm_cfg_deconv(*g, dt, kPlanSMs);
-    plan_debug(cfg);
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
     {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
@@ -803,31 +846,7 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     float* wout = (cfg.gz > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
     if (cfg.row) {  // narrow channels: (fh, fw, c) rows as the GEMM M dimension
-        const RowCfg rc = row_cfg_wgrad(*g, dt, gz, kPlanSMs);
-        CUtensorMap tx;
-        if (!make_row_xmap(&tx, x, *g, uint32_t(rc.JB), 64)) return CKS_ERR_CUDA;
-        RowWgradParams q;
-        memset(&q, 0, sizeof(q));
-        q.out = wout;
-        q.part_stride = part_stride;
-        q.N = int(g->N), q.H = int(g->H), q.W = int(g->W), q.C = int(g->C), q.OC = int(g->OC);
-        q.FH = int(g->FH), q.FW = int(g->FW), q.sh = g->sh, q.sw = g->sw, q.ph = g->ph, q.pw = g->pw;
-        q.OH = int(ah.O), q.OW = int(aw.O);
-        q.mb = rc.mb;
-        q.nbs = rc.nbs;
-        q.P = rc.P;
-        for (int k = 0; k < 8; ++k) q.delta[k] = rc.delta[k];
-        q.gzc = rc.gzc;
-        q.nblk64 = rc.nblk;
-        q.num_tiles = int(rc.tiles);
-        q.stages = rc.stages;
-        q.a_bytes = rc.mb * 16384;
-        switch (rc.JB) {
-            case 16: s = launch_wgrad_row_jb<16>(rc.BN, tx, ta, q, rc.smem, st); break;
-            case 32: s = launch_wgrad_row_jb<32>(rc.BN, tx, ta, q, rc.smem, st); break;
-            case 64: s = launch_wgrad_row_jb<64>(rc.BN, tx, ta, q, rc.smem, st); break;
-            default: return CKS_ERR_UNSUPPORTED;
-        }
+        s = run_wgrad_row(*g, dt, row_cfg_wgrad(*g, dt, gz, kPlanSMs), x, ta, wout, part_stride, st);
     } else {
         CUtensorMap tb;  // X viewed as (C, W, H, N): leaping rows ih = oh*sh + fh - ph
         {
@@ -901,7 +920,6 @@ cks_status cks_op_counts(const cks_geom* g, cks_dtype dt, int64_t out[8]) {
     out[4] = 2 * (g->C * g->N * g->H * g->W * g->FH * g->FW * g->OC);
     out[5] = 2 * (g->OC * g->FH * g->FW * g->C * OHp * OWp) * g->N;
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
-    plan_debug(cfg);
     const int64_t Cp = pad_ch(g->C, dt), BK = cfg.KB / elem_bytes(dt);
     out[6] = int64_t(cfg.nblk) * 128 * int64_t(cfg.nbs) * cfg.BN * VH * VW * ((Cp + BK - 1) / BK * BK);
     out[7] = cfg.tiles;
@@ -922,6 +940,32 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     }
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;
+    return CKS_OK;
+}
+
+cks_status cks_plan_describe(const cks_geom* g, cks_dtype dt, cks_op op, int gz, char* buf, size_t cap,
+                              size_t* len) {
+    if (!g || !len) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
+    const std::string d = describe_plan(*g, dt, op, gz, kPlanSMs);
+    *len = d.size() + 1;
+    if (d.size() + 1 > cap) return CKS_ERR_CAPACITY;
+    if (!buf) return CKS_ERR_NULL;
+    memcpy(buf, d.c_str(), d.size() + 1);
+    return CKS_OK;
+}
+
+cks_status cks_padding_macs(const cks_geom* g, cks_dtype dt, cks_op op, int64_t* macs) {
+    if (!g || !macs) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
+    int64_t per = 0;  // the igemm / per-tap paths iterate trimmed windows only: 0
+    if (op == CKS_OP_FWD) per = std::max<int64_t>(row_fwd_padding_macs(*g, dt), 0);
+    if (op == CKS_OP_WGRAD && wgrad_cfg(*g, dt, 0, kPlanSMs).row) per = std::max<int64_t>(row_wgrad_padding_macs(*g, dt), 0);
+    *macs = per * g->N;
     return CKS_OK;
 }
 

@@ -212,6 +212,11 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     }
     c.nbs = int((nout + c.BN * (pair ? 2 : 1) - 1) / (c.BN * (pair ? 2 : 1)));
     if (force_pbw > 0) pbw = std::min<int>(force_pbw, int(std::min<int64_t>(256 / c.BN, 8)));
+    // MMA-program capacity (kernels/igemm.cuh kProgSlot: 64 entries per list):
+    // the entries of one tile are bounded by prog_entries_bound(); narrow the
+    // pixel block until the worst case fits (a wide filter with stride > 1
+    // emits one entry per (pixel, tap)).
+    while (pbw > 1 && prog_entries_bound(pbw, ntap, a0_step, c.BN) > kProgEntries) --pbw;
     // smem: ring of B rows (ntap x BN x 128 B) and ring of A slots holding all
     // pa activation columns of a row step (one TMA box, one barrier)
     for (; pbw >= 1; --pbw) {
@@ -344,60 +349,191 @@ IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
                      num_sms);
 }
 
-// G_Z choice (P:210-212): the paper makes G_Z grow with (N_a + N_b)/N_g and
-// bounds it above by the SM count.  Here: enough segments that the
-// taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
-// with at least 4 K-blocks (256 images*positions) per segment.
-// Column classes: the (fw, c) run of output column ow starts at element
-// (ow*sw - pw)*C; TMA needs 16-byte (8-element) aligned box origins, so the
-// box starts delta = start mod 8 elements early; delta has period
-// P = 8 / gcd(sw*C, 8) in ow.
-static void row_classes(const cks_geom& g, RowCfg& c) {
-    int64_t q = (int64_t(g.sw) * g.C) % 8, a = 8;
-    while (q) { int64_t t = a % q; a = q; q = t; }  // gcd(sw*C, 8)
-    c.P = int(8 / a);
-    for (int k = 0; k < c.P; ++k) c.delta[k] = int(fmod_pos((int64_t(k) * g.sw - g.pw) * g.C, 8));
+// ---------------------------------------------------------------- narrow-channel row path
+// Column classes (kernels/narrow.cuh): the (fw, c) run of output column ow
+// starts at element start = (ow*sw - pw)*C of the flattened X row; TMA box
+// origins must be 16-byte aligned.  Interior columns (whole window inside X)
+// are grouped by delta = start mod (16 / eb) -- period P = (16/eb) / gcd(sw*C,
+// 16/eb) in ow -- and load from start - delta; every border column is a class
+// of its own: a left-border one loads from element 0 (its first valid
+// element), a right-border one ends its chunks at (origin chosen so the 32-byte K-chunk grid ends exactly at the
+// last element of X).  kc0 / kc1: the 32-byte K chunks of the box row that
+// hold valid run elements.
+static bool row_classes(const cks_geom& g, cks_dtype dt, std::vector<RowClassH>& cls, int& emax) {
+    const int64_t eb = elem_bytes(dt), align = 16 / eb, ke = 32 / eb;
+    const int64_t jn = g.FW * g.C, rowlen = g.W * g.C;
+    const int64_t OW = out_extent(g.W, g.FW, g.sw, g.pw);
+    int64_t q = (int64_t(g.sw) * g.C) % align, a = align;
+    while (q) { int64_t t = a % q; a = q; q = t; }  // gcd(sw*C, align)
+    const int64_t P = align / a;
+    cls.clear();
+    emax = 0;
+    std::vector<int64_t> interior;
+    for (int64_t ow = 0; ow < OW; ++ow) {
+        const int64_t start = (ow * g.sw - g.pw) * g.C;
+        const int64_t jlo = std::max<int64_t>(0, -start), jhi = std::min<int64_t>(jn, rowlen - start);
+        if (jlo == 0 && jhi == jn) { interior.push_back(ow); continue; }
+        RowClassH c;
+        c.col0 = int(ow), c.cstep = 1, c.ncols = 1;
+        // left border: origin 0 (the first valid element starts chunk 0); right border:
+        // the chunk grid ends exactly at the row end, origin = rowlen - ke*ceil((rowlen - start)/ke)
+        // (16-byte aligned: rowlen*eb and ke*eb = 32 are), so no issued K chunk reaches past X
+        c.off = int(start < 0 ? -start : rowlen - ke * cdiv(rowlen - start, ke) - start);
+        c.kc0 = int((jlo - c.off) / ke);
+        c.kc1 = int(cdiv(jhi - c.off, ke));
+        emax = std::max(emax, int(jhi - c.off));
+        cls.push_back(c);
+    }
+    if (!interior.empty()) {  // interior columns are contiguous; residues mod P
+        const int64_t lo = interior.front(), hi = interior.back() + 1;
+        for (int64_t r = 0; r < P && lo + r < hi; ++r) {
+            RowClassH c;
+            c.col0 = int(lo + r), c.cstep = int(P), c.ncols = int(cdiv(hi - lo - r, P));
+            const int64_t delta = fmod_pos((c.col0 * g.sw - g.pw) * g.C, align);
+            c.off = int(-delta);
+            c.kc0 = int(delta / ke);
+            c.kc1 = int(cdiv(delta + jn, ke));
+            emax = std::max(emax, int(delta + jn));
+            cls.push_back(c);
+        }
+    }
+    std::sort(cls.begin(), cls.end(), [](const RowClassH& x, const RowClassH& y) { return x.col0 < y.col0; });
+    return int(cls.size()) <= kRowClasses;
 }
 
 static bool row_setup(const cks_geom& g, cks_dtype dt, RowCfg& c) {
-    if (dt != CKS_BF16 || g.C > 16) return false;
-    if ((g.W * g.C * 2) % 16 != 0) return false;  // TMA row pitch
-    row_classes(g, c);
-    int dmax = 0;
-    for (int k = 0; k < c.P; ++k) dmax = std::max(dmax, c.delta[k]);
-    const int64_t jn = g.FW * g.C + dmax;
-    c.JB = jn <= 16 ? 16 : (jn <= 32 ? 32 : (jn <= 64 ? 64 : 0));
-    return c.JB != 0;
+    const int64_t eb = elem_bytes(dt);
+    if (g.C > (dt == CKS_BF16 ? 16 : 8)) return false;
+    if ((g.W * g.C * eb) % 16 != 0) return false;  // TMA row pitch
+    if (g.W * g.C > (int64_t(1) << 31) / eb) return false;
+    int emax = 0;
+    if (!row_classes(g, dt, c.cls, emax)) return false;
+    c.ROWB = emax * eb <= 32 ? 32 : (emax * eb <= 64 ? 64 : (emax * eb <= 128 ? 128 : 0));
+    c.JB = int(c.ROWB / eb);
+    return c.ROWB != 0;
 }
 
-// Narrow fwd: tile = output pixel x 128 images x all OC; W rows resident.
+// Spread `total` workers over the classes (>= 1 each, at most `cap(c)` each),
+// minimising the largest work / workers.
+static void row_spread(std::vector<RowClassH>& cls, int64_t total, const std::vector<int64_t>& cap) {
+    for (size_t k = 0; k < cls.size(); ++k) cls[k].cnt = 1;
+    int64_t used = int64_t(cls.size());
+    while (used < total) {
+        int best = -1;
+        double bw = 0;
+        for (size_t k = 0; k < cls.size(); ++k) {
+            if (cls[k].cnt >= cap[k]) continue;
+            const double w = double(cls[k].work) / cls[k].cnt;
+            if (w > bw) { bw = w; best = int(k); }
+        }
+        if (best < 0) break;
+        ++cls[best].cnt;
+        ++used;
+    }
+    int base = 0;
+    for (auto& k : cls) { k.base = base; base += k.cnt; }
+}
+
+// Narrow ConvV2: tile = R output rows x one column x 128 images x all OC,
+// the class's filter rows resident in shared memory.
 RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
     RowCfg c;
-    if (!row_setup(g, dt, c) || g.OC > 256) return c;
+    if (!row_setup(g, dt, c) || g.OC > (dt == CKS_TF32 ? 128 : 256)) return c;  // instantiated BN range
     c.BN = 32;
     while (c.BN < g.OC) c.BN *= 2;
-    const int wbytes = int((g.FH * c.BN * c.JB * 2 + 1023) / 1024 * 1024);
-    const int sbytes = int((g.FH * 128 * c.JB * 2 + 1023) / 1024 * 1024);
+    const int wbytes = int((g.FH * c.BN * c.ROWB + 1023) / 1024 * 1024);
+    const int stage = 128 * c.ROWB;
     const int staging = 4 * 2 * 4096;
-    const int budget = 227 * 1024 - 1024 - 256;
-    c.stages = std::min(8, (budget - wbytes - staging) / sbytes);
-    if (c.stages < 2) return c;
-    c.smem = 1024 + wbytes + c.stages * sbytes + staging + 256;
+    const int budget = 227 * 1024 - 1024 - 512;
+    c.stages = std::min(16, (budget - wbytes - staging) / stage);
+    if (c.stages < 3) return c;
+    c.smem = 1024 + wbytes + c.stages * stage + staging + 512;
     c.nblk = int((g.N + 127) / 128);
-    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph), OW = out_extent(g.W, g.FW, g.sw, g.pw);
-    c.tiles = OH * OW * c.nblk;
-    const int64_t per_class = OH * ((OW + c.P - 1) / c.P) * c.nblk;
-    c.grid = int(c.P * std::max<int64_t>(1, std::min<int64_t>(148 / c.P, per_class)));
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    // output rows per tile: X rows are loaded once per tile (h reuse), as many as
+    // TMEM holds while the grid keeps >= 2 tiles per SM
+    const int rmax = std::min(8, 256 / c.BN);
+    auto tiles_for = [&](int r) {
+        int64_t t = 0;
+        for (auto& k : c.cls) t += cdiv(OH, r) * k.ncols * c.nblk;
+        return t;
+    };
+    c.R = 1;
+    for (int r = rmax; r >= 1; --r)
+        if (r == 1 || (r <= OH && tiles_for(r) >= 2 * 148)) { c.R = r; break; }
+    c.tiles = tiles_for(c.R);
+    std::vector<int64_t> cap;
+    for (auto& k : c.cls) {
+        k.work = cdiv(OH, c.R) * k.ncols * c.nblk;
+        cap.push_back(k.work);
+    }
+    row_spread(c.cls, std::max<int64_t>(int64_t(c.cls.size()), 148), cap);
+    c.grid = 0;
+    for (auto& k : c.cls) c.grid += k.cnt;
     c.ok = true;
     return c;
 }
 
-// Narrow wgrad: M = (fh, j) rows, 128/JB filter rows per M-block; N = OC
-// block; K = (oh, ow, 64 images) of one column class, split into segments;
-// all P * gzc segments are G_Z map-reduce partials.
+int64_t row_fwd_padding_macs(const cks_geom& g, cks_dtype dt) {
+    const RowCfg c = row_cfg_fwd(g, dt);
+    if (!c.ok) return -1;
+    const int64_t ke = 32 / elem_bytes(dt), jn = g.FW * g.C, rowlen = g.W * g.C;
+    int64_t n = 0;
+    for (auto& k : c.cls)
+        for (int i = 0; i < k.ncols; ++i) {
+            const int64_t start = (int64_t(k.col0 + k.cstep * i) * g.sw - g.pw) * g.C;
+            // box elements [kc0*ke, kc1*ke) <-> run j = off + e; padding: j in the window range but X outside
+            for (int64_t e = k.kc0 * ke; e < k.kc1 * ke; ++e) {
+                const int64_t j = k.off + e, x = start + j;
+                if (j >= 0 && j < jn && (x < 0 || x >= rowlen)) ++n;
+            }
+        }
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    int64_t vh = 0;
+    for (int64_t oh = 0; oh < OH; ++oh) {
+        const int64_t ih0 = oh * g.sh - g.ph;
+        vh += std::min(g.H - ih0, g.FH) - std::max<int64_t>(-ih0, 0);
+    }
+    return n * vh * g.OC;  // per image; every valid filter row of every output row
+}
+
+int64_t row_wgrad_padding_macs(const cks_geom& g, cks_dtype dt) {
+    const RowCfg c = row_cfg_wgrad(g, dt, 0, 148);
+    if (!c.ok) return -1;
+    const int64_t jn = g.FW * g.C, rowlen = g.W * g.C, R = 128 / c.JB;
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    int64_t n = 0;
+    for (auto& k : c.cls)
+        for (int i = 0; i < k.ncols; ++i) {
+            const int64_t start = (int64_t(k.col0 + k.cstep * i) * g.sw - g.pw) * g.C;
+            for (int64_t oh = 0; oh < OH; ++oh) {
+                const int64_t ih0 = oh * g.sh - g.ph;
+                const int64_t fs = std::max<int64_t>(-ih0, 0), fe = std::min(g.H - ih0, g.FH);
+                for (int64_t m = 0; m < c.mb; ++m) {
+                    if (!(m * R < fe && (m + 1) * R > fs)) continue;  // M-block not issued
+                    for (int64_t fh = m * R; fh < std::min<int64_t>((m + 1) * R, g.FH); ++fh)
+                        for (int64_t e = 0; e < c.JB; ++e) {
+                            const int64_t j = k.off + e, x = start + j;
+                            if (j < 0 || j >= jn) continue;  // not a stored dW row
+                            if (fh < fs || fh >= fe || x < 0 || x >= rowlen) ++n;
+                        }
+                }
+            }
+        }
+    return n * g.OC;  // per image
+}
+
+// Narrow Sk-dilated: M = (fh, e) rows, 128/JB filter rows per M-block; N = OC
+// block; K = (oh, column, 64 images) of one column class, split into
+// segments; every segment of every class is one G_Z map-reduce partial.
 RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     RowCfg c;
     if (!row_setup(g, dt, c)) return c;
+    if (dt == CKS_TF32) {  // MN-major tf32 needs the 128-byte (BASE32B) swizzle
+        c.ROWB = 128;
+        c.JB = 32;
+    }
+    const int64_t eb = elem_bytes(dt);
     const int R = 128 / c.JB;
     c.mb = int((g.FH + R - 1) / R);
     if (c.mb > 4) return c;
@@ -407,16 +543,17 @@ RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     if (c.BN > cap) return c;
     c.nbs = int((pad_ch(g.OC, dt) + c.BN - 1) / c.BN);
     c.nblk = int((g.N + 63) / 64);
-    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph), OW = out_extent(g.W, g.FW, g.sw, g.pw);
-    const int64_t Lk = OH * ((OW + c.P - 1) / c.P) * c.nblk;  // k-blocks of the largest class
-    if (gz_req > 0) {
-        c.gzc = int((gz_req + c.P - 1) / c.P);
-    } else {
-        int64_t want = std::max<int64_t>(1, num_sms / (int64_t(c.nbs) * c.P));
-        c.gzc = int(std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(Lk / 8, 1))));
+    const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    std::vector<int64_t> segcap;
+    for (auto& k : c.cls) {
+        k.work = OH * k.ncols * c.nblk;
+        segcap.push_back(gz_req > 0 ? k.work : std::max<int64_t>(1, k.work / 8));  // >= 8 k-blocks per segment
     }
-    c.gz = c.P * c.gzc;
-    const int stage = c.mb * 16384 + c.BN * 128;
+    const int64_t want = gz_req > 0 ? gz_req : std::max<int64_t>(1, num_sms / c.nbs);
+    row_spread(c.cls, std::max<int64_t>(want, int64_t(c.cls.size())), segcap);
+    c.gz = 0;
+    for (auto& k : c.cls) c.gz += k.cnt;
+    const int stage = int(c.mb * 128 * 64 * eb + c.BN * 64 * eb);
     c.stages = std::min(8, (227 * 1024 - 2048) / stage);
     if (c.stages < 2) return c;
     c.smem = 1024 + c.stages * stage + 256;
@@ -426,6 +563,52 @@ RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     return c;
 }
 
+static std::string row_classes_str(const std::vector<RowClassH>& cls) {
+    std::string o;
+    char b[96];
+    for (size_t k = 0; k < cls.size(); ++k) {
+        snprintf(b, sizeof b, "%s%d:%d:%d:%d:%d:%d:%d:%d", k ? "," : "", cls[k].col0, cls[k].cstep, cls[k].ncols,
+                 cls[k].off, cls[k].kc0, cls[k].kc1, cls[k].base, cls[k].cnt);
+        o += b;
+    }
+    return o;
+}
+
+std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, int num_sms) {
+    char b[512];
+    if (op == CKS_OP_FWD || op == CKS_OP_DECONV) {
+        if (op == CKS_OP_FWD) {
+            const RowCfg r = row_cfg_fwd(g, dt);
+            if (r.ok) {
+                snprintf(b, sizeof b, "row_fwd ROWB=%d JB=%d BN=%d R=%d stages=%d grid=%d tiles=%lld classes=%d cls=",
+                         r.ROWB, r.JB, r.BN, r.R, r.stages, r.grid, (long long)r.tiles, int(r.cls.size()));
+                return std::string(b) + row_classes_str(r.cls);
+            }
+        }
+        const IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
+        snprintf(b, sizeof b,
+                 "igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d out_tiles=%lld "
+                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d",
+                 c.BN, c.pbw, c.KB, c.ntap, c.pa, c.apos, c.stages, c.a_stages, c.unified, (long long)c.out_tiles, c.Z,
+                 c.zc, c.kc_blocks, c.epi_warps, c.pair);
+        return b;
+    }
+    const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);
+    if (w.row) {
+        const RowCfg r = row_cfg_wgrad(g, dt, gz, num_sms);
+        snprintf(b, sizeof b, "row_wgrad ROWB=%d JB=%d BN=%d mb=%d nbs=%d gz=%d stages=%d tiles=%lld classes=%d cls=",
+                 r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, (long long)r.tiles, int(r.cls.size()));
+        return std::string(b) + row_classes_str(r.cls);
+    }
+    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d base_tiles=%lld", w.BN, w.nbs,
+             w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, (long long)w.base_tiles);
+    return b;
+}
+
+// G_Z choice (P:210-212): the paper makes G_Z grow with (N_a + N_b)/N_g and
+// bounds it above by the SM count.  Here: enough segments that the
+// taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
+// with at least 4 K-blocks (256 images*positions) per segment.
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     WgradCfg c;
     RowCfg rc = row_cfg_wgrad(g, dt, gz_req, num_sms);

@@ -7,6 +7,7 @@
 // enumeration (tests/test_plan_abi.py).
 #pragma once
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "../../include/cks.h"
@@ -53,6 +54,13 @@ int64_t axis_valid_pairs(const Axis& a);         // V
 struct KRow { int64_t a0, ts, te, out, phase; };
 std::vector<KRow> krows_fwd(const Axis& a);
 std::vector<KRow> krows_deconv(const Axis& a);
+
+// MMA-program capacity of the implicit GEMM (kernels/igemm.cuh): entries per
+// list.  Every entry is one MMA group covering >= 1 (pixel, tap) pair of the
+// tile and no pair appears twice in a list, so pbw * ntap bounds a tile's
+// entries; the plan narrows the pixel block until that fits.
+constexpr int kProgEntries = 64;
+inline int64_t prog_entries_bound(int64_t pbw, int64_t ntap, int64_t /*a0_step*/, int /*BN*/) { return pbw * ntap; }
 
 // channel padding to 16-byte rows
 inline int64_t pad_ch(int64_t c, cks_dtype dt) {
@@ -102,23 +110,39 @@ IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
 
 // Narrow-channel row path (kernels/narrow.cuh): one filter row's contiguous
-// (fw, c) run is one K-block of JB elements.  Eligible for bf16 with
-// FW*C <= 64, C <= 16 and 16-byte X row pitch (W*C*2 % 16 == 0).
+// (fw, c) run is one K-block of JB elements (ROWB = JB * element bytes).
+// Eligible for FW*C small enough that a run (+ its alignment shift) fits a
+// 64-element bf16 / 32-element fp32 row, C <= 16 (bf16) / 8 (fp32), and a
+// 16-byte X row pitch (W*C*eb % 16 == 0).
+constexpr int kRowClasses = 24;  // column classes per launch (kernels/narrow.cuh RowClass table)
+struct RowClassH {
+    int col0 = 0, cstep = 1, ncols = 0;  // output columns col0 + cstep * i
+    int off = 0;                         // box origin = (ow*sw - pw)*C + off
+    int kc0 = 0, kc1 = 0;                // 32-byte K chunks holding valid elements (ConvV2)
+    int base = 0, cnt = 1;               // ConvV2: CTA range; Sk-dilated: partial range
+    int64_t work = 0;                    // tiles (ConvV2) / k-blocks (Sk-dilated) of the class
+};
 struct RowCfg {
     bool ok = false;
-    int JB = 0;          // K-block / M-atom width in elements: 16, 32, 64
+    int ROWB = 0;        // bytes per box row: 32 / 64 / 128
+    int JB = 0;          // elements per box row
     int BN = 0;          // OC tile
+    int R = 1;           // ConvV2: output rows per tile
     int stages = 0;      // pipeline depth
     int smem = 0;        // dynamic shared memory bytes
-    int mb = 1, nbs = 1, gz = 1, nblk = 1;  // wgrad: M-blocks, OC blocks, G_Z (total), 64-image blocks
-    int P = 1;           // column classes of equal run alignment delta
-    int delta[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int gzc = 1;         // wgrad: segments per class (gz = P * gzc)
-    int grid = 1;        // CTAs (a multiple of P for the fwd kernel)
+    int mb = 1, nbs = 1, gz = 1, nblk = 1;  // wgrad: M-blocks, OC blocks, G_Z (total partials), 64-image blocks
+    std::vector<RowClassH> cls;
+    int grid = 1;        // CTAs
     int64_t tiles = 0;
 };
 RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt);
 RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
+// Products of the row kernels with spatial-padding zeros (host model, per
+// image): ConvV2 (the partial last K chunk of right-border columns) and
+// Sk-dilated (zero-fill rows inside an issued M-block, box elements beyond
+// the image in w).  Reported in DESIGN.md; tests pin the ConvV2 count.
+int64_t row_fwd_padding_macs(const cks_geom& g, cks_dtype dt);
+int64_t row_wgrad_padding_macs(const cks_geom& g, cks_dtype dt);
 
 struct WgradCfg {
     int BN, nbs, mblocks, nblk64, gz;
@@ -138,5 +162,9 @@ struct WsLayout {
 };
 WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms);
 size_t ks_split_bytes(const cks_geom& g, cks_dtype dt);
+
+// Text form of the plan the library uses for (g, dt, op, gz) -- kernel kind
+// and tile configuration as key=value pairs (tests, tools/plan_dump.py).
+std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, int num_sms);
 
 }  // namespace cks

@@ -46,11 +46,12 @@
 #pragma once
 #include "ptx.cuh"
 #include "../../../include/cks.h"
+#include "../cks_plan.h"
 
 namespace cks {
 
 constexpr int kMaxPBW = 8;
-constexpr int kProgSlot = 2 + 2 * 64;  // int4: header {np0, np1, rs0, rs1}, {pos_lo, pos_hi, -, -}, 2 lists
+constexpr int kProgSlot = 2 + 2 * kProgEntries;  // int4: header {np0, np1, rs0, rs1}, {pos_lo, pos_hi, -, -}, 2 lists
 
 // Division by a launch constant d via a host-computed multiplier:
 // n / d = (n * m) >> sh with l = ceil(log2 d), sh = 31 + l, m = ceil(2^sh / d);
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
                     if (lane == 0) trace_ev(p, 1, ti, 1);
                     const uint64_t bdesc0 = dconst | ptx::desc_addr(ptx::smem_u32(bbuf + bs * p.b_stage_bytes));
-                    const int4* pl = pg + 2 + (first ? 0 : 64);
+                    const int4* pl = pg + 2 + (first ? 0 : kProgEntries);
                     const int np = first ? np0 : np1;
                     first = false;
                     int e = 0;
@@ -568,12 +569,13 @@ __global__ void __launch_bounds__(384, 1)
                             }
                         }
                         groups(excl, np0 + s0 - n0, true);
-                        groups(0xFFu, 64 + np1 + s1 - n1, true);
+                        groups(0xFFu, kProgEntries + np1 + s1 - n1, true);
                         np0 += __shfl_sync(0xffffffffu, s0, 31);
                         np1 += __shfl_sync(0xffffffffu, s1, 31);
                         carry |= __shfl_sync(0xffffffffu, incl, 31);
                     }
                 }
+                if (np0 > kProgEntries || np1 > kProgEntries) __trap();  // plan invariant (prog_entries_bound)
                 if (lane == 0) {
                     pg[0] = make_int4(np0, np1, c.rs0, c.rs1);
                     pg[1] = make_int4(c.pos_lo, c.pos_hi, 0, 0);

@@ -1,99 +1,134 @@
 // narrow.cuh -- KB-CONV-ROW / KB-WGRAD-ROW: ConvV2 forward and Sk-dilated
-// weight gradient for narrow-channel layers (FW*C <= 64 bf16, the C = 3 input
-// layers of all three workloads) on tcgen05 tensor cores.
+// weight gradient for narrow-channel layers (FW*C <= 64 bf16 / <= 32 fp32:
+// the C = 3 input layers of all three workloads) on tcgen05 tensor cores,
+// BF16 (kind::f16) or TF32 (kind::tf32, fp32 storage).
 //
 // In NHWC the (fw, c) run of one filter row is CONTIGUOUS in X: for output
 // column ow and filter row fh it is X[n][ih][(ow*sw - pw)*C + j], j = fw*C + c,
 // j < FW*C.  So instead of one GEMM step per tap with a 3-of-64 used channel
-// block (the generic path), a whole filter row is one K-block of JB = 16/32/64
-// elements loaded by ONE TMA box element-addressed in the flattened (W*C) row;
-// the w-direction padding is the box's out-of-bounds zero fill.  The row
-// (h) direction keeps the paper's trimming: ConvV2 issues MMAs only for the
-// valid filter rows [fh_s, fh_e) of each output row (T1, Alg. 1);
-// Sk-dilated reads X with the leaping row ih = oh*sh + fh - ph (Fig. 7) and
-// the out-of-range rows arrive as TMA zero fill (no DRAM traffic).
+// block (the generic path), a whole filter row is one K-block of JB elements
+// (ROWB = JB * element bytes = 32 / 64 / 128 B) loaded by ONE TMA box
+// element-addressed in the flattened (W*C) row.
 //
-// TMA box origins must be 16-byte aligned in the innermost dimension, while
-// the run starts at element (ow*sw - pw)*C.  With delta = that start mod 8
-// elements, output columns fall into P = 8 / gcd(sw*C, 8) classes of equal
-// delta; every CTA serves ONE class, loads the box from the aligned start
-// (start - delta) and uses the filter row shifted right by delta (fwd), or
-// drops the first delta rows of its result (wgrad).  JB covers delta + FW*C.
+// Column classes.  TMA box origins must be 16-byte aligned in the innermost
+// dimension, while the run of column ow starts at element start = (ow*sw -
+// pw)*C.  Every output column belongs to one class c with a box origin
+// start + off_c (off_c = -delta, delta = start mod (16 / eb), for interior
+// columns; a border column, whose window overhangs the padding, is a class
+// of its own: origin 0 on the left, rowlen - 32 B * m on the right).  Box element e holds run element j = off + e.  Each CTA
+// serves one class; the host lists the classes (RowClass) with the K-chunk
+// range [kc0, kc1) of the box row that holds valid elements.
 //
-// KB-CONV-ROW  tile = one output pixel x 128 images x OC (<= 256):
-//   D[n][oc] = sum_{fh valid} sum_j A_fh[n][j] * Wrow_fh[oc][j]
-//   A: one box (JB, 128 images, FH rows) per tile, K-major (JB*2-byte rows);
-//   B: all FH filter rows resident in shared memory for the whole kernel.
+// Trimming (Alg. 1 / Alg. 3B):
+//   * ConvV2, h: only the valid filter rows of an output row are loaded and
+//     multiplied (T1): one TMA box per valid X row, no zero fill.
+//   * ConvV2, w: MMAs run over the K chunks [kc0, kc1) of the class only;
+//     a left-border column's chunk grid starts at its first valid element,
+//     a right-border column's ends at the last element of the X row, so no
+//     issued chunk holds a padding position (cks_padding_macs: 0 unless a
+//     window overhangs BOTH ends of a row narrower than the filter).
+//   * Sk-dilated, h/w: the leaping rows ih = oh*sh + fh - ph outside X arrive
+//     as TMA zero fill inside an M-block (M = 128 (fh, j) rows); an M-block
+//     whose filter rows are all outside X for this oh is not issued.
+//
+// KB-CONV-ROW  tile = R consecutive output rows x one output column x 128
+//   images x OC (<= 256): D_r[n][oc] = sum_{fh valid} sum_e A_ih[n][e] *
+//   B_fh[oc][e], ih = (oh0 + r)*sh - ph + fh.  An X row is loaded ONCE per
+//   tile and multiplied into every accumulator r that uses it (h reuse: a
+//   7x7 s2 filter reads 13 rows for 4 outputs instead of 28).  B = the class's
+//   filter rows, resident in shared memory (K-major, swizzled).
 // KB-WGRAD-ROW tile = OC block x segment z of the G_Z map-reduce:
-//   D[(fh, j)][oc] = sum_k X[n][oh*sh+fh-ph][(ow*sw-pw)*C + j] * dY[n][oh][ow][oc]
-//   over k = (oh, ow, n) blocks of 64 images; both operands MN-major, M =
-//   (fh, j) packed 128/JB filter rows per M-block.
+//   D[(fh, e)][oc] = sum_k X[n][oh*sh+fh-ph][origin + e] * dY[n][oh][ow][oc]
+//   over k = (oh, ow, n) blocks of 64 images of ONE class; both operands
+//   MN-major, M = (fh, e) packed 128/JB filter rows per M-block.  Every
+//   segment writes a full partial dW (zeros where the class contributes
+//   nothing); KB-REDUCE sums them in a fixed order.
 #pragma once
 #include "ptx.cuh"
+#include "../cks_plan.h"
 
 namespace cks {
 
+struct RowClass {
+    int16_t col0, cstep, ncols;  // output columns ow = col0 + cstep * i, i < ncols
+    int16_t off;                 // box origin = (ow*sw - pw)*C + off; run element j = off + e
+    int8_t kc0, kc1;             // ConvV2: 32-byte K chunks of the box row with valid elements
+    int16_t base, cnt;           // ConvV2: CTA range; Sk-dilated: partial (segment) range
+};
+
 struct RowFwdParams {
-    const uint16_t* w;  // W [OC][FH][FW*C] bf16 (dense, any alignment)
-    float* y;           // Y [N][OH][OW][OC] fp32
+    const void* w;  // W [OC][FH][FW*C] (bf16 or fp32, dense, any alignment)
+    float* y;       // Y [N][OH][OW][OC] fp32
     int N, H, W, C, OC, FH, FW, sh, sw, ph, pw, OH, OW;
-    int nblk;           // ceil(N / 128)
-    int P;              // column classes (gridDim.x is a multiple of P)
-    int delta[8];       // per class: run start mod 8 (elements)
-    int stages;         // A ring depth
-    int tma_store;      // 1: epilogue via TMA store (OC % 32 == 0)
+    int nblk;       // ceil(N / 128)
+    int R;          // output rows per tile
+    int ncls;
+    RowClass cls[kRowClasses];
+    int stages;     // A ring depth (one X row per stage)
+    int tma_store;  // 1: epilogue via TMA store (OC % 32 == 0)
 };
 
-// Tiles of column class k = blockIdx.x % P, in the order (oh, ow, nb) with nb fastest.
-struct RowClassIter {
-    int k, owk, first, step, count;
-    __device__ RowClassIter(int P, int OH, int OW, int nblk) {
-        k = int(blockIdx.x) % P;
-        owk = OW > k ? (OW - k + P - 1) / P : 0;
-        first = int(blockIdx.x) / P;
-        step = int(gridDim.x) / P;
-        count = OH * owk * nblk;
-    }
-    __device__ void decode(int t, int P, int nblk, int& nb, int& oh, int& ow) const {
-        nb = t % nblk;
-        const int r = t / nblk;
-        ow = k + P * (r % owk);
-        oh = r / owk;
-    }
-};
-
-template <int JB, int BN>
+template <int ROWB, int BN, bool TF>
 struct RowFwdShape {
-    static constexpr int ROWB = JB * 2;                      // K bytes per row (swizzle width)
-    static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-    static constexpr int STAGING = 4 * 2 * 4096;             // 4 epilogue warps x 2 x (32 rows x 128 B)
+    static constexpr int EB = TF ? 4 : 2;
+    static constexpr int JB = ROWB / EB;           // elements per box row
+    static constexpr int STAGE = 128 * ROWB;       // one X row of 128 images
+    static constexpr int STAGING = 4 * 2 * 4096;   // 4 epilogue warps x 2 x (32 rows x 128 B)
+    static constexpr int RMAX = 256 / BN < 8 ? 256 / BN : 8;  // 2 x R x BN TMEM columns <= 512
 };
 
-__host__ __device__ constexpr int row_fwd_w_bytes(int JB, int BN, int FH) {
-    return ((FH * BN * JB * 2) + 1023) / 1024 * 1024;
+__host__ __device__ constexpr int row_fwd_w_bytes(int ROWB, int BN, int FH) {
+    return ((FH * BN * ROWB) + 1023) / 1024 * 1024;
 }
-__host__ __device__ constexpr int row_fwd_stage_bytes(int JB, int FH) { return ((FH * 128 * JB * 2) + 1023) / 1024 * 1024; }
 
-template <int JB, int BN>
+__device__ __forceinline__ int row_class_of(const RowClass* cls, int ncls, int b) {
+    int k = 0;
+    while (k + 1 < ncls && b >= cls[k + 1].base) ++k;
+    return k;
+}
+
+// Tile t of class k: (row block ob, column i, image block nb), nb fastest.
+struct RowFwdTile {
+    int nb, ow, oh0, rn;  // rn: rows in this block
+    __device__ RowFwdTile(int t, const RowClass& c, const RowFwdParams& p) {
+        nb = t % p.nblk;
+        const int r = t / p.nblk;
+        ow = c.col0 + c.cstep * (r % c.ncols);
+        oh0 = (r / c.ncols) * p.R;
+        rn = min(p.R, p.OH - oh0);
+    }
+};
+
+// accumulators r of a tile that X row ih feeds: fh = ih - ((oh0 + r)*sh - ph) in [0, FH)
+__device__ __forceinline__ void row_users(int ih, int oh0, int rn, const RowFwdParams& p, int& r0, int& r1) {
+    const int d = ih - oh0 * p.sh + p.ph;  // = fh + r*sh
+    r1 = min(rn, d / p.sh + 1);            // r <= d / sh
+    const int lo = d - p.FH + 1;           // r*sh >= d - FH + 1
+    r0 = lo <= 0 ? 0 : (lo + p.sh - 1) / p.sh;
+}
+
+template <int ROWB, int BN, bool TF>
 __global__ void __launch_bounds__(256, 1)
     fwd_row_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
                    const __grid_constant__ RowFwdParams p) {
-    using S = RowFwdShape<JB, BN>;
+    using S = RowFwdShape<ROWB, BN, TF>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int wbytes = row_fwd_w_bytes(JB, BN, p.FH);
-    const int sbytes = row_fwd_stage_bytes(JB, p.FH);
+    const int wbytes = row_fwd_w_bytes(ROWB, BN, p.FH);
     uint8_t* wsm = smem;
     uint8_t* abuf = smem + wbytes;
-    uint8_t* stg = abuf + p.stages * sbytes;
+    uint8_t* stg = abuf + p.stages * S::STAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(stg + S::STAGING);
-    uint64_t* empty = full + 8;
-    uint64_t* tfull = empty + 8;
+    uint64_t* empty = full + 16;
+    uint64_t* tfull = empty + 16;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    constexpr uint32_t TMEM_COLS = 2 * S::RMAX * BN <= 64 ? 64 : (2 * S::RMAX * BN <= 128 ? 128 : (2 * S::RMAX * BN <= 256 ? 256 : 512));
 
     ptx::pdl_launch_dependents();
     const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+    const int k = row_class_of(p.cls, p.ncls, int(blockIdx.x));
+    const RowClass cl = p.cls[k];
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmX);
         if (p.tma_store) ptx::prefetch_tmap(&tmY);
@@ -109,27 +144,31 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, S::TMEM_COLS);
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
     ptx::pdl_wait();  // W and X may come from the previous kernel
-    {   // all threads: gather the filter rows into the K-major swizzled B layout
-        // (row r = fh*BN + oc, K = j), zero for oc >= OC and j >= FW*C
+    {   // all threads: this class's filter rows in the K-major swizzled B layout,
+        // row r = fh*BN + oc, K = box element e <-> run element off + e (zero outside [0, FW*C))
+        constexpr int PER16 = 16 / S::EB;
         const int jn = p.FW * p.C;
-        const int dl = p.delta[int(blockIdx.x) % p.P];
-        const int chunks = p.FH * BN * (JB / 8);
+        const int chunks = p.FH * BN * (ROWB / 16);
         for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
-            const int r = q / (JB / 8), c8 = q % (JB / 8);
+            const int r = q / (ROWB / 16), c16 = q % (ROWB / 16);
             const int fh = r / BN, oc = r % BN;
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (oc < p.OC) {
-                const uint16_t* src = p.w + (static_cast<long long>(oc) * p.FH + fh) * jn;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int j = c8 * 8 + e - dl;
-                    const uint32_t x = (j >= 0 && j < jn) ? uint32_t(src[j]) : 0u;
-                    v[e >> 1] |= x << (16 * (e & 1));
+                for (int e = 0; e < PER16; ++e) {
+                    const int j = cl.off + c16 * PER16 + e;
+                    if (j >= 0 && j < jn) {
+                        const long long at = (static_cast<long long>(oc) * p.FH + fh) * jn + j;
+                        if constexpr (TF)
+                            v[e] = static_cast<const uint32_t*>(p.w)[at];
+                        else
+                            v[e >> 1] |= uint32_t(static_cast<const uint16_t*>(p.w)[at]) << (16 * (e & 1));
+                    }
                 }
             }
-            const uint32_t off = ptx::swz(uint32_t(r * S::ROWB + c8 * 16), S::ROWB);
+            const uint32_t off = ptx::swz(uint32_t(r * ROWB + c16 * 16), ROWB);
             *reinterpret_cast<uint4*>(wsm + off) = make_uint4(v[0], v[1], v[2], v[3]);
         }
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
@@ -138,97 +177,117 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const int ci = int(blockIdx.x) - cl.base;
+    const int ntiles = ((p.OH + p.R - 1) / p.R) * cl.ncols * p.nblk;
 
-    if (warp == 0 || warp == 3) {
-        // ---------------- TMA producers: warps 0 / 3 take alternate tiles
-        const uint32_t mine = warp == 3 ? 1u : 0u;
-        const RowClassIter it(p.P, p.OH, p.OW, p.nblk);
-        const int dl = p.delta[it.k];
-        uint32_t i = 0;
-        for (int t = it.first; t < it.count; t += it.step, ++i) {
-            if ((i & 1u) != mine) continue;
-            int nb, oh, ow;
-            it.decode(t, p.P, p.nblk, nb, oh, ow);
-            const uint32_t s = i % uint32_t(p.stages), ph = (i / uint32_t(p.stages)) & 1u;
-            ptx::mbar_wait(&empty[s], ph ^ 1u);
-            if (ptx::elect_one()) {
-                ptx::mbar_arrive_expect_tx(&full[s], uint32_t(p.FH * 128 * JB * 2));
-                ptx::tma_load_4d(abuf + s * sbytes, &tmX, &full[s], (ow * p.sw - p.pw) * p.C - dl, nb * 128,
-                                 oh * p.sh - p.ph, 0);
+    if (warp == 0) {
+        // ---------------- TMA producer: one box per VALID X row of the tile (T1 trimming)
+        uint32_t s = 0, ph = 0;
+        for (int t = ci; t < ntiles; t += cl.cnt) {
+            const RowFwdTile tl(t, cl, p);
+            const int ih0 = tl.oh0 * p.sh - p.ph;
+            const int rl = max(ih0, 0), rh = min(p.H, ih0 + p.sh * (tl.rn - 1) + p.FH);
+            const int origin = (tl.ow * p.sw - p.pw) * p.C + cl.off;
+            for (int ih = rl; ih < rh; ++ih) {
+                int r0, r1;
+                row_users(ih, tl.oh0, tl.rn, p, r0, r1);
+                if (r0 >= r1) continue;  // stride gap: no output uses this row
+                ptx::mbar_wait(&empty[s], ph ^ 1u);
+                if (ptx::elect_one()) {
+                    ptx::mbar_arrive_expect_tx(&full[s], uint32_t(S::STAGE));
+                    ptx::tma_load_4d(abuf + s * S::STAGE, &tmX, &full[s], origin, tl.nb * 128, ih, 0);
+                }
+                __syncwarp();
+                if (++s == uint32_t(p.stages)) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer: trimmed filter rows [fh_s, fh_e) (T1)
-        constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, false, false);
+        // ---------------- MMA issuer: each loaded row into every accumulator that uses it,
+        // K chunks [kc0, kc1) only
+        constexpr uint32_t idesc = ptx::instr_desc(128, BN, TF, false, false);
         const uint32_t a0 = ptx::smem_u32(abuf), w0 = ptx::smem_u32(wsm);
-        const RowClassIter it(p.P, p.OH, p.OW, p.nblk);
-        uint32_t i = 0;
-        for (int t = it.first; t < it.count; t += it.step, ++i) {
-            int nb, oh, ow;
-            it.decode(t, p.P, p.nblk, nb, oh, ow);
-            const int ih0 = oh * p.sh - p.ph;
-            const int fs = max(-ih0, 0), fe = min(p.H - ih0, p.FH);
-            const uint32_t s = i % uint32_t(p.stages), ph = (i / uint32_t(p.stages)) & 1u;
+        uint32_t s = 0, ph = 0, i = 0;
+        for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
+            const RowFwdTile tl(t, cl, p);
+            const int ih0 = tl.oh0 * p.sh - p.ph;
+            const int rl = max(ih0, 0), rh = min(p.H, ih0 + p.sh * (tl.rn - 1) + p.FH);
             const uint32_t acc = i & 1u, aph = (i >> 1) & 1u;
             ptx::mbar_wait(&tempty[acc], aph ^ 1u);
-            ptx::mbar_wait(&full[s], ph);
             ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-                const uint32_t d = tmem_base + acc * BN;
-                for (int fh = fs; fh < fe; ++fh) {
-                    const uint32_t sa = a0 + s * uint32_t(sbytes) + uint32_t(fh * 128 * S::ROWB);
-                    const uint32_t sb = w0 + uint32_t(fh * BN * S::ROWB);
-#pragma unroll
-                    for (int k = 0; k < JB / 16; ++k)
-                        ptx::mma_ss<false>(d, ptx::smem_desc_kmajor(sa + 32u * k, S::ROWB),
-                                           ptx::smem_desc_kmajor(sb + 32u * k, S::ROWB), idesc,
-                                           (fh > fs || k > 0) ? 1u : 0u);
+            const uint32_t dbase = tmem_base + acc * uint32_t(S::RMAX * BN);
+            uint32_t started = 0;
+            for (int ih = rl; ih < rh; ++ih) {
+                int r0, r1;
+                row_users(ih, tl.oh0, tl.rn, p, r0, r1);
+                if (r0 >= r1) continue;
+                ptx::mbar_wait(&full[s], ph);
+                ptx::tc_fence_after();
+                if (ptx::elect_one()) {
+                    const uint32_t sa = a0 + s * uint32_t(S::STAGE);
+                    for (int r = r0; r < r1; ++r) {
+                        const int fh = ih - ih0 - r * p.sh;
+                        const uint32_t sb = w0 + uint32_t(fh * BN * ROWB);
+                        for (int kc = cl.kc0; kc < cl.kc1; ++kc)
+                            ptx::mma_ss<TF>(dbase + uint32_t(r * BN), ptx::smem_desc_kmajor(sa + 32u * kc, ROWB),
+                                            ptx::smem_desc_kmajor(sb + 32u * kc, ROWB), idesc,
+                                            (((started >> r) & 1u) || kc > cl.kc0) ? 1u : 0u);
+                        started |= 1u << r;  // (elected lane's copy; all lanes update below)
+                    }
+                    ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&empty[s]);
-                ptx::mma_commit(&tfull[acc]);
+                __syncwarp();
+                started |= ((1u << r1) - 1u) & ~((1u << r0) - 1u);
+                if (++s == uint32_t(p.stages)) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
+            if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
             __syncwarp();
         }
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> (swizzled staging -> TMA store | direct stores)
         const uint32_t sub = warp & 3u;
         uint8_t* my = stg + sub * 2 * 4096;
-        const RowClassIter it(p.P, p.OH, p.OW, p.nblk);
         uint32_t i = 0, q = 0;
-        for (int t = it.first; t < it.count; t += it.step, ++i) {
-            int nb, oh, ow;
-            it.decode(t, p.P, p.nblk, nb, oh, ow);
+        for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
+            const RowFwdTile tl(t, cl, p);
             const uint32_t acc = i & 1u, aph = (i >> 1) & 1u;
             ptx::mbar_wait(&tfull[acc], aph);
             ptx::tc_fence_after();
-            const int n = nb * 128 + int(sub * 32 + lane);
+            const int n = tl.nb * 128 + int(sub * 32 + lane);
+            for (int r = 0; r < tl.rn; ++r) {
+                const int oh = tl.oh0 + r;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
-                uint32_t r[32];
-                ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * BN + c0, r);
-                ptx::tmem_ld_wait();
-                if (p.tma_store) {
-                    if (c0 >= p.OC) continue;
-                    uint8_t* buf = my + (q++ & 1u) * 4096;
-                    if (ptx::elect_one()) ptx::bulk_wait_read1();  // buffer of chunk q-2 drained
-                    __syncwarp();
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    if (c0 >= p.OC) break;
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(S::RMAX * BN) + uint32_t(r * BN + c0), v);
+                    ptx::tmem_ld_wait();
+                    if (p.tma_store) {
+                        uint8_t* buf = my + (q++ & 1u) * 4096;
+                        if (ptx::elect_one()) ptx::bulk_wait_read1();  // buffer of chunk q-2 drained
+                        __syncwarp();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        *reinterpret_cast<uint4*>(buf + ptx::swz(lane * 128u + c * 16u, 128)) =
-                            make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (ptx::elect_one()) {
-                        ptx::tma_store_4d(&tmY, buf, c0, ow, oh, nb * 128 + int(sub * 32));
-                        ptx::bulk_commit();
+                        for (int c = 0; c < 8; ++c)
+                            *reinterpret_cast<uint4*>(buf + ptx::swz(lane * 128u + c * 16u, 128)) =
+                                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (ptx::elect_one()) {
+                            ptx::tma_store_4d(&tmY, buf, c0, tl.ow, oh, tl.nb * 128 + int(sub * 32));
+                            ptx::bulk_commit();
+                        }
+                        __syncwarp();
+                    } else if (n < p.N) {
+                        float* dst = p.y + ((static_cast<long long>(n) * p.OH + oh) * p.OW + tl.ow) * p.OC;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < p.OC) dst[c0 + j] = __uint_as_float(v[j]);
                     }
-                    __syncwarp();
-                } else if (n < p.N) {
-                    float* dst = p.y + ((static_cast<long long>(n) * p.OH + oh) * p.OW + ow) * p.OC;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < p.OC) dst[c0 + j] = __uint_as_float(r[j]);
                 }
             }
             ptx::tc_fence_before();
@@ -240,50 +299,63 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, S::TMEM_COLS);
+        ptx::tmem_dealloc(tmem_base, TMEM_COLS);
     }
 }
 
 // ------------------------------------------------------------------ wgrad
 struct RowWgradParams {
-    float* out;  // dW [OC][FH][FW*C] (gz == 1) or partials [gz][OC][FH][FW*C]
+    float* out;  // dW [OC][FH][FW*C] (one partial) or partials [gz][OC][FH][FW*C]
     long long part_stride;
     int N, H, W, C, OC, FH, FW, sh, sw, ph, pw, OH, OW;
-    int mb;       // M-blocks of 128 (fh, j) rows
+    int mb;       // M-blocks of 128 (fh, e) rows
     int nbs;      // OC blocks of BN
-    int P;        // column classes
-    int delta[8]; // per class: run start mod 8 (elements)
-    int gzc;      // map-reduce segments per class; partial index = z * P + k
+    int ncls;
+    RowClass cls[kRowClasses];  // base / cnt: partial (segment) range of the class
+    int gz;       // total segments (partials)
     int nblk64;   // ceil(N / 64)
-    int num_tiles;  // nbs * P * gzc
+    int num_tiles;  // nbs * gz
     int stages;
-    int a_bytes;  // mb * 128 * 64 * 2
+    int a_bytes;  // mb * 128 * 64 * eb
 };
 
-// Tile t -> OC block nb, class k, segment z, and its k-block range [kb0, kb1)
-// over the class's (oh, ow, 64-image) positions.
+// Tile t -> OC block nb, segment (partial) part of class k, its k-block range
+// [kb0, kb1) over the class's (oh, column, 64-image) positions.
 struct RowWTile {
-    int nb, k, z, part, owk;
+    int nb, k, part;
     uint32_t kb0, kb1;
     __device__ RowWTile(int t, const RowWgradParams& p) {
         nb = t % p.nbs;
         part = t / p.nbs;
-        k = part % p.P;
-        z = part / p.P;
-        owk = p.OW > k ? (p.OW - k + p.P - 1) / p.P : 0;
-        const uint32_t L = uint32_t(p.OH) * uint32_t(owk) * uint32_t(p.nblk64);
-        kb0 = uint32_t(uint64_t(L) * uint32_t(z) / uint32_t(p.gzc));
-        kb1 = uint32_t(uint64_t(L) * uint32_t(z + 1) / uint32_t(p.gzc));
+        k = row_class_of(p.cls, p.ncls, part);
+        const int z = part - p.cls[k].base, gzc = p.cls[k].cnt;
+        const uint32_t L = uint32_t(p.OH) * uint32_t(p.cls[k].ncols) * uint32_t(p.nblk64);
+        kb0 = uint32_t(uint64_t(L) * uint32_t(z) / uint32_t(gzc));
+        kb1 = uint32_t(uint64_t(L) * uint32_t(z + 1) / uint32_t(gzc));
     }
 };
 
-template <int JB, int BN>
+// M-blocks (R filter rows each) holding at least one filter row that is inside X for output row oh
+__device__ __forceinline__ uint32_t row_wgrad_mmask(int oh, int R, const RowWgradParams& p) {
+    const int ih0 = oh * p.sh - p.ph;
+    const int fs = max(-ih0, 0), fe = min(p.H - ih0, p.FH);
+    uint32_t m = 0;
+    for (int b = 0; b < p.mb; ++b)
+        if (b * R < fe && (b + 1) * R > fs) m |= 1u << b;
+    return m;
+}
+
+template <int ROWB, int BN, bool TF>
 __global__ void __launch_bounds__(256, 1)
     wgrad_row_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
                      const __grid_constant__ RowWgradParams p) {
-    constexpr int ROWB = JB * 2;       // MN bytes per K row of A (one filter row)
-    constexpr int R = 128 / JB;        // filter rows per M-block
-    constexpr int B_BYTES = BN * 128;  // BN OC x 64 images bf16
+    constexpr int EB = TF ? 4 : 2;
+    constexpr int JB = ROWB / EB;       // MN elements per filter row of A
+    constexpr int R = 128 / JB;         // filter rows per M-block
+    constexpr int CH = 128 / EB;        // dY channels per 128-byte box
+    constexpr int B_BYTES = BN * 64 * EB;  // BN OC x 64 images
+    constexpr int UK = 32 / EB;         // images per MMA K step
+    static_assert(!TF || ROWB == 128, "TF32 MN-major operands use the 128-byte (BASE32B) swizzle");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int stage_bytes = p.a_bytes + B_BYTES;
@@ -322,23 +394,23 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t stage = 0, phase = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const RowWTile c(t, p);
-            const int nb = c.nb, dl = p.delta[c.k];
+            const RowClass cl = p.cls[c.k];
             for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = int(kb % uint32_t(p.nblk64));
                 const int pos = int(kb / uint32_t(p.nblk64));
-                const int oh = pos / c.owk, ow = c.k + p.P * (pos % c.owk);
+                const int oh = pos / cl.ncols, ow = cl.col0 + cl.cstep * (pos % cl.ncols);
                 ptx::mbar_wait(&empty[stage], phase ^ 1u);
                 uint8_t* st = smem + stage * stage_bytes;
                 if (ptx::elect_one()) {
                     if (!is_b) {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(p.FH * 64 * ROWB));
-                        ptx::tma_load_4d(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C - dl, n64 * 64,
+                        ptx::tma_load_4d(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
                                          oh * p.sh - p.ph, 0);
                     } else {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(B_BYTES));
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_4d(st + p.a_bytes + j * 8192, &tmDY, &full[stage], nb * BN + j * 64, ow, oh,
+                        for (int j = 0; j < BN / CH; ++j)
+                            ptx::tma_load_4d(st + p.a_bytes + j * 8192, &tmDY, &full[stage], c.nb * BN + j * CH, ow, oh,
                                              n64 * 64);
                     }
                 }
@@ -351,32 +423,43 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
-        constexpr uint32_t idesc = ptx::instr_desc(128, BN, false, true, true);
+        constexpr uint32_t idesc = ptx::instr_desc(128, BN, TF, true, true);
         uint32_t stage = 0, phase = 0, tph = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const RowWTile c(t, p);
-            const uint32_t kb0 = c.kb0, kb1 = c.kb1;
+            const RowClass cl = p.cls[c.k];
             ptx::mbar_wait(tempty, tph ^ 1u);
             ptx::tc_fence_after();
-            for (uint32_t kb = kb0; kb < kb1; ++kb) {
+            uint32_t started = 0;
+            for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
+                const int oh = int(kb / uint32_t(p.nblk64)) / cl.ncols;
+                const uint32_t mm = row_wgrad_mmask(oh, R, p);
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
                 const uint32_t sb = sa + uint32_t(p.a_bytes);
                 if (ptx::elect_one()) {
                     for (int m = 0; m < p.mb; ++m) {
+                        if (!((mm >> m) & 1u)) continue;  // all filter rows of the block outside X
+                        const uint32_t acc0 = (started >> m) & 1u;
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)  // 64 images = 4 x K16
-                            ptx::mma_ss<false>(
-                                tmem_base + uint32_t(m * BN),
-                                ptx::smem_desc_mn(sa + uint32_t(m * R * 64 * ROWB + kk * 16 * ROWB), 64 * ROWB,
-                                                  8 * ROWB, ROWB),
-                                ptx::smem_desc_sw128(sb + uint32_t(kk * 2048), 8192, 1024), idesc,
-                                (kb > kb0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < 64 / UK; ++kk) {
+                            uint64_t ad, bd;
+                            if constexpr (TF) {
+                                ad = ptx::smem_desc_mn_b32(sa + uint32_t(m * R * 64 * ROWB + kk * UK * ROWB), 64 * ROWB, 512);
+                                bd = ptx::smem_desc_mn_b32(sb + uint32_t(kk * UK * 128), 8192, 512);
+                            } else {
+                                ad = ptx::smem_desc_mn(sa + uint32_t(m * R * 64 * ROWB + kk * UK * ROWB), 64 * ROWB,
+                                                       8 * ROWB, ROWB);
+                                bd = ptx::smem_desc_sw128(sb + uint32_t(kk * UK * 128), 8192, 1024);
+                            }
+                            ptx::mma_ss<TF>(tmem_base + uint32_t(m * BN), ad, bd, idesc, (acc0 | uint32_t(kk)) != 0);
+                        }
                     }
                     ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
+                started |= mm;
                 if (++stage == uint32_t(p.stages)) {
                     stage = 0;
                     phase ^= 1u;
@@ -387,21 +470,30 @@ __global__ void __launch_bounds__(256, 1)
             tph ^= 1u;
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: row (fh, j) of M-block m -> dW[oc][fh][j]
+        // ---------------- epilogue: row (fh, e) of M-block m -> dW[oc][fh][off + e];
+        // run elements outside the class's box window are written as 0 (full partial)
         const uint32_t sub = warp & 3u;
         const int jn = p.FW * p.C;
         uint32_t tph = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const RowWTile c(t, p);
+            const RowClass cl = p.cls[c.k];
             const int nb = c.nb;
-            const uint32_t kb0 = c.kb0, kb1 = c.kb1;
+            uint32_t started = 0;  // M-blocks that received an MMA (the same walk as the issuer)
+            for (uint32_t kb = c.kb0; kb < c.kb1;) {
+                const int pos = int(kb / uint32_t(p.nblk64));
+                started |= row_wgrad_mmask(pos / cl.ncols, R, p);
+                kb = uint32_t(pos + 1) * uint32_t(p.nblk64);  // next position
+            }
             ptx::mbar_wait(tfull, tph);
             ptx::tc_fence_after();
+            float* part = p.out + c.part * p.part_stride;
             for (int m = 0; m < p.mb; ++m) {
                 const int g = m * 128 + int(sub * 32 + lane);
-                const int fh = g / JB, j = g % JB - p.delta[c.k];  // row j' of the shifted window
+                const int fh = g / JB, j = g % JB + cl.off;
                 const bool ok = fh < p.FH && j >= 0 && j < jn;
-                float* dst = p.out + c.part * p.part_stride + static_cast<long long>(fh) * jn + j;
+                const bool live = (started >> m) & 1u;
+                float* dst = part + static_cast<long long>(fh) * jn + j;
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
                     uint32_t r[32];
@@ -411,10 +503,21 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                         for (int q = 0; q < 32; ++q) {
                             const int oc = nb * BN + c0 + q;
-                            if (oc < p.OC)
-                                dst[static_cast<long long>(oc) * p.FH * jn] = kb1 > kb0 ? __uint_as_float(r[q]) : 0.f;
+                            if (oc < p.OC) dst[static_cast<long long>(oc) * p.FH * jn] = live ? __uint_as_float(r[q]) : 0.f;
                         }
                     }
+                }
+            }
+            // run elements j outside [off, off + JB): no D row, the class contributes 0
+            {
+                const int jlo = max(cl.off, 0), jhi = min(cl.off + JB, jn);
+                const int nz = jlo + (jn - jhi);
+                const int ocn = min(BN, p.OC - nb * BN);
+                for (int q = int(threadIdx.x) - 128; q < p.FH * nz * ocn; q += 128) {
+                    const int oc = nb * BN + q / (p.FH * nz), rr = q % (p.FH * nz);
+                    const int fh = rr / nz, jj = rr % nz;
+                    const int j = jj < jlo ? jj : jhi + (jj - jlo);
+                    part[(static_cast<long long>(oc) * p.FH + fh) * jn + j] = 0.f;
                 }
             }
             ptx::tc_fence_before();

@@ -7,6 +7,8 @@ There is no CPU fallback: non-CUDA tensors raise.
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 
 from . import _lib as L
@@ -38,14 +40,28 @@ def _stream_ptr(stream) -> int:
     return s.cuda_stream
 
 
+def _on(stream):
+    """Allocate on the stream the kernels run on: the caching allocator then
+    only hands a freed block to later work of that same stream (stream order),
+    so a grown workspace or an output cannot be reused while queued kernels
+    still read or write it."""
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+def _empty(shape, dtype, device, stream):
+    with _on(stream):
+        return torch.empty(shape, dtype=dtype, device=device)
+
+
 def workspace(nbytes: int, device, stream=None) -> torch.Tensor | None:
-    """Reusable per-(device, stream) scratch buffer (grown on demand)."""
+    """Reusable per-(device, stream) scratch buffer (grown on demand; allocated
+    on ``stream``, see _on)."""
     if nbytes == 0:
         return None
     key = (torch.device(device).index, _stream_ptr(stream))
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        buf = _empty(max(nbytes, 1 << 20), torch.uint8, device, stream)
         _WS[key] = buf
     return buf
 
@@ -75,7 +91,7 @@ def conv2d_fwd(x, w, stride=1, padding=0, out=None, stream=None):
     g = geom_of(tuple(x.shape), tuple(w.shape), stride, padding)
     OH, OW = L.cks_output_shape(g)
     if out is None:
-        out = torch.empty((g.N, OH, OW, g.OC), dtype=torch.float32, device=x.device)
+        out = _empty((g.N, OH, OW, g.OC), torch.float32, x.device, stream)
     ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_FWD), x.device, stream)
     L.cks_conv2d_fwd(g, dt, x.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
     return out
@@ -91,7 +107,7 @@ def ks_split(w, stride, x_hw=None, out=None, stream=None):
     g = make_geom(1, C, max(H, FH), max(W, FW), OC, FH, FW, sh, sw, 0, 0)
     nbytes = L.cks_ks_split_size(g, dt)
     if out is None:
-        out = torch.empty(nbytes // w.element_size(), dtype=w.dtype, device=w.device)
+        out = _empty(nbytes // w.element_size(), w.dtype, w.device, stream)
     L.cks_ks_split(g, dt, w.data_ptr(), out.data_ptr(), _stream_ptr(stream))
     return out
 
@@ -114,7 +130,7 @@ def deconv2d(dy, w, x_hw, stride=1, padding=0, c_packed=None, in_channels=None, 
     if L.cks_output_shape(g) != (OH_, OW_):
         raise ValueError("dY spatial shape does not match the geometry")
     if out is None:
-        out = torch.empty((N, H, W, C), dtype=torch.float32, device=dy.device)
+        out = _empty((N, H, W, C), torch.float32, dy.device, stream)
     if c_packed is None:
         _check_dev(w)
         ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
@@ -140,7 +156,7 @@ def dilated_wgrad(x, dy, filter_hw, stride=1, padding=0, gz=0, out=None, stream=
     if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
         raise ValueError("dY spatial shape does not match the geometry")
     if out is None:
-        out = torch.empty((OC, FH, FW, C), dtype=torch.float32, device=x.device)
+        out = _empty((OC, FH, FW, C), torch.float32, x.device, stream)
     ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_WGRAD, gz), x.device, stream)
     L.cks_dilated_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), gz, *_ws_args(ws), _stream_ptr(stream))
     return out
@@ -156,7 +172,7 @@ def zins_conv2d_fwd(x, w, stride=1, padding=0, out=None, stream=None):
     g = geom_of(tuple(x.shape), tuple(w.shape), stride, padding)
     OH, OW = L.cks_output_shape(g)
     if out is None:
-        out = torch.empty((g.N, OH, OW, g.OC), dtype=torch.float32, device=x.device)
+        out = _empty((g.N, OH, OW, g.OC), torch.float32, x.device, stream)
     ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_FWD), x.device, stream)
     L.cks_zins_conv2d_fwd(g, dt, x.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
     return out
@@ -175,7 +191,7 @@ def zins_deconv2d(dy, w, x_hw, stride=1, padding=0, out=None, stream=None):
     if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
         raise ValueError("dY spatial shape does not match the geometry")
     if out is None:
-        out = torch.empty((N, H, W, C), dtype=torch.float32, device=dy.device)
+        out = _empty((N, H, W, C), torch.float32, dy.device, stream)
     ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
     L.cks_zins_deconv2d(g, dt, dy.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
     return out
@@ -194,7 +210,7 @@ def zins_wgrad(x, dy, filter_hw, stride=1, padding=0, out=None, stream=None):
     if L.cks_output_shape(g) != tuple(dy.shape[1:3]):
         raise ValueError("dY spatial shape does not match the geometry")
     if out is None:
-        out = torch.empty((OC, FH, FW, C), dtype=torch.float32, device=x.device)
+        out = _empty((OC, FH, FW, C), torch.float32, x.device, stream)
     ws = workspace(L.cks_zins_workspace_size(g, dt, L.CKS_OP_WGRAD), x.device, stream)
     L.cks_zins_wgrad(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
     return out
@@ -210,9 +226,10 @@ def zins_wgrad(x, dy, filter_hw, stride=1, padding=0, out=None, stream=None):
 class CKSConv2dFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, stride, padding):
+        x, w = x.contiguous(), w.contiguous()  # backward's kernels take dense tensors too
         ctx.save_for_backward(x, w)
         ctx.stride, ctx.padding = _pair(stride), _pair(padding)
-        return conv2d_fwd(x.contiguous(), w.contiguous(), ctx.stride, ctx.padding)
+        return conv2d_fwd(x, w, ctx.stride, ctx.padding)
 
     @staticmethod
     def backward(ctx, gy):
@@ -232,9 +249,10 @@ class CKSConvTranspose2dFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, z, w, out_hw, stride, padding):
+        z, w = z.contiguous(), w.contiguous()  # backward's kernels take dense tensors too
         ctx.save_for_backward(z, w)
         ctx.stride, ctx.padding = _pair(stride), _pair(padding)
-        return deconv2d(z.contiguous(), w.contiguous(), tuple(out_hw), ctx.stride, ctx.padding)
+        return deconv2d(z, w, tuple(out_hw), ctx.stride, ctx.padding)
 
     @staticmethod
     def backward(ctx, gy):

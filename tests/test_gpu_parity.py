@@ -157,22 +157,26 @@ def test_random_geometries_tf32(torch_cuda, lay):
     check_full(torch_cuda, lay, "tf32", config=8, idx=int(lay.name[4:]))
 
 
-def _narrow_layers(n, seed):
-    """Narrow-channel layers (FW*C <= 64): the filter-row kernels
-    (kernels/narrow.cuh); a few have a row pitch W*C*2 that is not a multiple
+def _narrow_layers(n, seed, dtype="bf16"):
+    """Narrow-channel layers (FW*C <= 64 bf16 / 32 fp32): the filter-row kernels
+    (kernels/narrow.cuh); a few have a row pitch W*C*eb that is not a multiple
     of 16 bytes and take the padded per-tap path instead."""
     rng = np.random.default_rng(seed)
     out = []
+    lim, align = (64, 8) if dtype == "bf16" else (32, 4)
     while len(out) < n:
-        C = int(rng.choice([1, 2, 3, 4, 8, 16]))
-        FW = int(rng.choice([f for f in (1, 2, 3, 4, 5, 7) if f * C <= 64]))
+        C = int(rng.choice([1, 2, 3, 4, 8, 16] if dtype == "bf16" else [1, 2, 3, 4, 8]))
+        fws = [f for f in (1, 2, 3, 4, 5, 7) if f * C <= lim]
+        if not fws:
+            continue
+        FW = int(rng.choice(fws))
         FH = int(rng.choice([1, 2, 3, 4, 5, 7]))
         sh, sw = int(rng.integers(1, 4)), int(rng.integers(1, 4))
         ph, pw = int(rng.integers(0, FH)), int(rng.integers(0, FW))
         H = int(rng.integers(max(1, FH - 2 * ph), 24))
         W = int(rng.integers(max(1, FW - 2 * pw), 24))
         if rng.random() < 0.8:  # mostly 16-byte row pitch (row path)
-            q = 8 // np.gcd(8, C)
+            q = align // np.gcd(align, C)
             W = max(q, (W + q - 1) // q * q)
         OC = int(rng.choice([5, 8, 32, 64, 96, 128, 200]))
         N = int(rng.choice([1, 63, 130, 257]))
@@ -192,16 +196,49 @@ def test_narrow_channel_geometries(torch_cuda, lay):
     check_full(torch_cuda, lay, "bf16", config=7, idx=int(lay.name[6:]))
 
 
+@pytest.mark.parametrize("lay", _narrow_layers(20, 17, "tf32"), ids=lambda l: f"tf32-{l.N}x{l.H}x{l.W}x{l.C}-{l.OC}-f{l.FH}{l.FW}s{l.sh}{l.sw}p{l.ph}{l.pw}")
+def test_narrow_channel_geometries_tf32(torch_cuda, lay):
+    """The filter-row kernels in TF32 (fp32 rows, kind::tf32; MN-major
+    SWIZZLE_128B_BASE32B operands for Sk-dilated)."""
+    check_full(torch_cuda, lay, "tf32", config=7, idx=100 + int(lay.name[6:]))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("lay", [Layer("nb0", 5, 3, 6, 8, 8, 7, 7, 1, 1, 3, 3),     # windows overhang both sides
+                                 Layer("nb1", 130, 3, 17, 24, 64, 5, 5, 1, 1, 2, 2),  # 2 border columns per side
+                                 Layer("nb2", 67, 1, 12, 16, 8, 3, 3, 3, 3, 1, 1),    # stride 3, one channel
+                                 Layer("nb3", 129, 4, 9, 12, 32, 7, 3, 2, 1, 6, 2),   # ph = FH - 1
+                                 Layer("nb4", 64, 2, 20, 8, 40, 3, 7, 1, 2, 1, 6)],   # pw = FW - 1, s = (1, 2)
+                         ids=lambda l: l.name)
+def test_narrow_border_classes(torch_cuda, lay, dtype):
+    """Border columns are classes of their own (left: box origin 0; right: the
+    32-byte K-chunk grid ends at the row end); output rows trimmed to their
+    valid filter rows; R-row tiles."""
+    check_full(torch_cuda, lay, dtype, config=7, idx=200 + int(lay.name[2:]))
+
+
 @pytest.mark.parametrize("gz", [1, 3, 200])
-def test_narrow_wgrad_segments(torch_cuda, gz):
-    """Row-path Sk-dilated with explicit G_Z: same result for every
-    segment count, bit-identical on repeat."""
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_narrow_wgrad_segments_dtypes(torch_cuda, gz, dtype):
+    """Row-path Sk-dilated with explicit G_Z spread over the column
+    classes: bit-identical on repeat, equal to the oracle."""
     lay = Layer("nz", 70, 3, 20, 16, 64, 7, 7, 2, 2, 3, 3)
-    a, got = run_all(torch_cuda, lay, "bf16", config=7, idx=99, ops=("wgrad",), gz=gz)
-    _, got2 = run_all(torch_cuda, lay, "bf16", config=7, idx=99, ops=("wgrad",), gz=gz)
+    a, got = run_all(torch_cuda, lay, dtype, config=7, idx=98, ops=("wgrad",), gz=gz)
+    _, got2 = run_all(torch_cuda, lay, dtype, config=7, idx=98, ops=("wgrad",), gz=gz)
     assert np.array_equal(got["wgrad"], got2["wgrad"])
     ref = O.wgrad_ref(a["X"], a["dY"], 7, 7, 2, 2, 3, 3)
-    check(got["wgrad"], ref, "bf16", f"narrow wgrad gz={gz}", red_len(lay, "wgrad"))
+    check(got["wgrad"], ref, dtype, f"narrow wgrad gz={gz}", red_len(lay, "wgrad"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("lay", [Layer("wf0", 20, 8, 128, 128, 32, 10, 10, 2, 2, 4, 4),
+                                 Layer("wf1", 9, 3, 96, 224, 64, 11, 11, 2, 2, 5, 5)],
+                         ids=lambda l: l.name)
+def test_wide_filter_stride2_program_capacity(torch_cuda, lay, dtype):
+    """Wide filters with stride > 1 on wide maps: one MMA-program entry per
+    (pixel, tap), so the plan must narrow the pixel block to fit the 64-entry
+    program lists (kernels/igemm.cuh kProgSlot)."""
+    check_full(torch_cuda, lay, dtype, config=17, idx=int(lay.name[2:]), ops=("fwd",))
 
 
 @pytest.mark.parametrize("lay", [Layer("sk0", 100, 512, 4, 4, 256, 3, 3, 2, 2, 1, 1),
@@ -313,13 +350,22 @@ def test_config_layers_reduced_batch_tf32(torch_cuda, cfg, i, lay):
 
 
 # ------------------------------------------ full size, sampled outputs
-@pytest.mark.parametrize("cfg,i,lay", [c for c in _config_layers() if c[0] in (1, 3, 5)][::2] +
-                         [c for c in _config_layers() if c[0] == 2][::3],
+def _full_tf32():
+    """TF32 at full size: the headline workload's distinct shapes (C3 stem, l1,
+    l2a, l2ds, l3, l4 -- the plans at N = 256: G_Z, clusters, row kernels) and
+    the C4 generator layers."""
+    keep = {"stem", "l1_0", "l2a", "l2ds", "l3_0", "l4a", "l4_0"}
+    return [c for c in _config_layers() if (c[0] == 2 and c[2].name in keep) or c[0] == 3]
+
+
+@pytest.mark.parametrize("cfg,i,lay,dtype", [c + ("bf16",) for c in _config_layers() if c[0] in (1, 3, 5)][::2] +
+                         [c + ("bf16",) for c in _config_layers() if c[0] == 2][::3] +
+                         [c + ("tf32",) for c in _full_tf32()],
                          ids=lambda v: v.name if isinstance(v, Layer) else str(v))
-def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
+def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay, dtype):
     """Full BASELINE batch, the bench's launch configuration; the oracle
     computes sampled outputs one by one (rows for fwd/deconv, taps for wgrad)."""
-    a, got = run_all(torch_cuda, lay, "bf16", config=cfg, idx=i, ops=lay.ops)
+    a, got = run_all(torch_cuda, lay, dtype, config=cfg, idx=i, ops=lay.ops)
     rng = np.random.default_rng(cfg * 100 + i)
     s = (lay.sh, lay.sw, lay.ph, lay.pw)
     OH, OW = lay.out_hw()
@@ -327,17 +373,17 @@ def test_config_layers_full_size_sampled(torch_cuda, cfg, i, lay):
         smp = [(int(rng.integers(lay.N)), int(rng.integers(OH)), int(rng.integers(OW))) for _ in range(24)]
         smp += [(lay.N - 1, 0, 0), (0, OH - 1, OW - 1)]
         ref = O.conv_ref_rows(a["X"], a["W"], *s, smp)
-        check(np.stack([got["fwd"][t] for t in smp]), ref, "bf16", f"{lay.name} fwd sampled", red_len(lay, "fwd"))
+        check(np.stack([got["fwd"][t] for t in smp]), ref, dtype, f"{lay.name} fwd sampled", red_len(lay, "fwd"))
     if "deconv" in got:
         smp = [(int(rng.integers(lay.N)), int(rng.integers(lay.H)), int(rng.integers(lay.W))) for _ in range(24)]
         smp += [(lay.N - 1, lay.H - 1, lay.W - 1), (0, 0, 0)]
         ref = O.deconv_ref_rows(a["dY"], a["W"], lay.H, lay.W, *s, smp)
-        check(np.stack([got["deconv"][t] for t in smp]), ref, "bf16", f"{lay.name} deconv sampled",
+        check(np.stack([got["deconv"][t] for t in smp]), ref, dtype, f"{lay.name} deconv sampled",
               red_len(lay, "deconv"))
     if "wgrad" in got:
         taps = [(0, 0), (lay.FH - 1, lay.FW - 1), (lay.FH // 2, lay.FW // 2)]
         ref = O.wgrad_ref_taps(a["X"], a["dY"], lay.FH, lay.FW, *s, taps)
-        check(np.stack([got["wgrad"][:, fh, fw, :] for fh, fw in taps]), ref, "bf16", f"{lay.name} wgrad sampled",
+        check(np.stack([got["wgrad"][:, fh, fw, :] for fh, fw in taps]), ref, dtype, f"{lay.name} wgrad sampled",
               red_len(lay, "wgrad"))
 
 

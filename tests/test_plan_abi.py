@@ -115,7 +115,7 @@ def test_workspace_and_launch_counts():
     g = L.make_geom(128, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)   # narrow row path: X read unpadded
     assert L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_FWD) == 0
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 1
-    assert L.cks_launch_count(g, L.CKS_TF32, L.CKS_OP_FWD) == 3   # TF32 keeps the per-tap path
+    assert L.cks_launch_count(g, L.CKS_TF32, L.CKS_OP_FWD) == 1   # TF32 filter-row kernel too
     gz = L.cks_choose_gz(g, L.CKS_BF16)
     # G_Z partials + KB-REDUCE, or the cluster reduce (neither): the launch count follows the workspace
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + (L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD) > 0)
@@ -137,29 +137,82 @@ def test_workspace_and_launch_counts():
     assert L.cks_ks_split_size(g, L.CKS_BF16) == 4 * 64 * 2 * 2 * 64 * 2
 
 
+def _classes(desc: dict):
+    return [tuple(int(v) for v in c.split(":")) for c in desc["cls"].split(",")]
+
+
 def test_narrow_row_path_plan():
-    """Narrow-channel bf16 layers (FW*C <= 64, C <= 16, W*C*2 % 16 == 0) take the
-    filter-row kernels: no channel padding pass, and the Sk-dilated G_Z is a
-    multiple of the column-class count P = 8 / gcd(sw*C, 8) (include/cks.h)."""
-    from math import gcd
+    """Narrow-channel layers take the filter-row kernels (kernels/narrow.cuh) in
+    BF16 and TF32: no channel padding pass; the output columns are partitioned
+    into classes (interior columns by box alignment, every border column its
+    own class); the Sk-dilated G_Z is the total of the per-class segments
+    (include/cks.h cks_choose_gz)."""
     for (C, W, FW, sw, OC) in [(3, 224, 7, 2, 64), (3, 32, 3, 1, 64), (3, 64, 4, 2, 128), (1, 16, 5, 1, 8),
                                (2, 24, 7, 3, 32), (4, 8, 3, 2, 8), (8, 16, 3, 1, 16), (16, 8, 3, 2, 40)]:
         g = L.make_geom(70, C, W, W, OC, FW, FW, sw, sw, FW // 2, FW // 2)
-        P = 8 // gcd(sw * C, 8)
-        gz = L.cks_choose_gz(g, L.CKS_BF16)
-        assert gz % P == 0 and gz >= P, (C, W, FW, sw, gz, P)
-        assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 1          # no X/W padding pass
-        ocpad = OC % 8 != 0
-        assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + ocpad + (gz > 1)
-        # a requested gz is rounded up to a multiple of P
-        ws = L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD, gz=P + 1)
-        assert ws >= 2 * P * OC * FW * FW * C * 4
-        # TF32 keeps the per-tap path (channel padding to 4)
-        cpad = C % 4 != 0
-        assert L.cks_launch_count(g, L.CKS_TF32, L.CKS_OP_FWD) == 1 + 2 * cpad
+        OW = (W + 2 * (FW // 2) - FW) // sw + 1
+        for dt in (L.CKS_BF16, L.CKS_TF32):
+            eb = 2 if dt == L.CKS_BF16 else 4
+            fwd, wg = L.plan_dict(g, dt, L.CKS_OP_FWD), L.plan_dict(g, dt, L.CKS_OP_WGRAD)
+            if dt == L.CKS_TF32 and C > 8:
+                assert fwd["kind"] == "igemm" and wg["kind"] == "wgrad", (C, W, FW, sw)
+                continue
+            assert fwd["kind"] == "row_fwd" and wg["kind"] == "row_wgrad", (C, W, FW, sw, dt)
+            assert L.cks_launch_count(g, dt, L.CKS_OP_FWD) == 1          # no X/W padding pass
+            for d in (fwd, wg):
+                cls = _classes(d)
+                cols = sorted(c0 + st * i for (c0, st, n, *_r) in cls for i in range(n))
+                assert cols == list(range(OW)), (C, W, FW, sw, dt)    # classes partition the columns
+                for (c0, st, n, off, kc0, kc1, base, cnt) in cls:
+                    for i in range(n):
+                        start = ((c0 + st * i) * sw - FW // 2) * C
+                        assert ((start + off) * eb) % 16 == 0       # 16-byte aligned box origin
+                        assert 0 <= kc0 < kc1 <= int(d["JB"]) * eb // 32
+            gz = L.cks_choose_gz(g, dt)
+            assert gz == int(wg["gz"]) and gz >= int(wg["classes"]), (C, W, FW, sw, gz)
+            assert gz == sum(c[7] for c in _classes(wg))
+            ocpad = OC % (8 if dt == L.CKS_BF16 else 4) != 0
+            assert L.cks_launch_count(g, dt, L.CKS_OP_WGRAD) == 1 + ocpad + (gz > 1)
+            ws = L.cks_workspace_size(g, dt, L.CKS_OP_WGRAD, gz=gz + 1)
+            assert ws >= (gz + 1) * OC * FW * FW * C * 4
+            # exact C-K-S at the K-chunk granularity: no ConvV2 product with a padding zero
+            assert L.cks_padding_macs(g, dt, L.CKS_OP_FWD) == 0, (C, W, FW, sw, dt)
     # row pitch not a multiple of 16 bytes -> padded per-tap path
     g = L.make_geom(70, 3, 33, 33, 64, 3, 3, 1, 1, 1, 1)
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_FWD) == 3
+    assert L.plan_dict(g, L.CKS_BF16, L.CKS_OP_FWD)["kind"] == "igemm"
+
+
+def test_padding_macs_accounting():
+    """cks_padding_macs: 0 for the trimmed-window kernels; the row-path Sk-dilated
+    count equals a brute-force recount of the zero-filled operand rows inside its
+    issued M-blocks (a stored dW row times a padding position of X)."""
+    g = L.make_geom(256, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)
+    for op in (L.CKS_OP_FWD, L.CKS_OP_DECONV, L.CKS_OP_WGRAD):
+        assert L.cks_padding_macs(g, L.CKS_BF16, op) == 0
+    N, C, H, W, OC, F, s, p = 2, 3, 9, 8, 8, 3, 2, 1
+    g = L.make_geom(N, C, H, W, OC, F, F, s, s, p, p)
+    for dt in (L.CKS_BF16, L.CKS_TF32):
+        d = L.plan_dict(g, dt, L.CKS_OP_WGRAD)
+        assert d["kind"] == "row_wgrad"
+        JB, R = int(d["JB"]), 128 // int(d["JB"])
+        OH = (H + 2 * p - F) // s + 1
+        n = 0
+        for (c0, st, nc, off, *_r) in _classes(d):
+            for i in range(nc):
+                start = ((c0 + st * i) * s - p) * C
+                for oh in range(OH):
+                    ih0 = oh * s - p
+                    fs, fe = max(-ih0, 0), min(H - ih0, F)
+                    for m in range((F + R - 1) // R):
+                        if not (m * R < fe and (m + 1) * R > fs):
+                            continue
+                        for fh in range(m * R, min((m + 1) * R, F)):
+                            for e in range(JB):
+                                j = off + e
+                                if 0 <= j < F * C and (fh < fs or fh >= fe or not 0 <= start + j < W * C):
+                                    n += 1
+        assert L.cks_padding_macs(g, dt, L.CKS_OP_WGRAD) == n * OC * N
 
 
 def test_zins_workspace_holds_the_zero_inserted_operand():
@@ -187,18 +240,16 @@ def test_zins_workspace_holds_the_zero_inserted_operand():
     assert e.value.status == 2
 
 
-def _plans(cfg, op):
-    """Tile plans the library picks (tools/plan_dump.py: CKS_PLAN_DEBUG, host only)."""
-    import subprocess
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "plan_dump.py"), str(cfg), op],
-                         stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, timeout=300, cwd=ROOT)
-    plans, name = {}, None
-    for ln in out.stdout.splitlines():
-        if ln.startswith("[cks plan]"):
-            plans[name] = dict(kv.split("=") for kv in ln.split()[3:] if "=" in kv)
-        elif ln and not ln.startswith("[") and " " not in ln.strip():
-            name = ln.strip()
-    return plans
+def _plans(cfg, op, dt=None):
+    """Tile plans the library picks for every layer of a config (cks_plan_describe, host only)."""
+    from cks_synth import get_config
+    dt = L.CKS_BF16 if dt is None else dt
+    code = {"fwd": L.CKS_OP_FWD, "deconv": L.CKS_OP_DECONV, "wgrad": L.CKS_OP_WGRAD}[op]
+    out = {}
+    for lay in get_config(cfg)[1]:
+        g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+        out[lay.name] = L.plan_dict(g, dt, code)
+    return out
 
 
 def test_plan_choices_on_the_workloads():
@@ -212,5 +263,19 @@ def test_plan_choices_on_the_workloads():
     assert fwd2["vgg4_512to512_s2"]["zc"] == "1" and int(fwd2["vgg4_512to512_s2"]["Z"]) >= 2
     assert fwd2["vgg32_64to64_s1"]["zc"] == "0" and fwd2["vgg32_64to64_s1"]["pair"] == "0"
     for name, pl in list(fwd2.items()) + list(fwd3.items()):
-        if pl["zc"] == "1":   # one wave of resident clusters
+        if pl.get("zc") == "1":   # one wave of resident clusters
             assert int(pl["out_tiles"]) * int(pl["Z"]) <= 148, name
+
+
+def test_mma_program_capacity_bound():
+    """an igemm tile's MMA-program entries (<= pbw x taps per filter
+    row) must fit the 64-entry lists; wide stride-2 filters narrow the pixel block."""
+    for geo in [(128, 8, 128, 128, 32, 10, 10, 2, 2, 4, 4), (20, 8, 128, 128, 32, 10, 10, 2, 2, 4, 4),
+                (128, 3, 224, 224, 64, 11, 11, 2, 2, 5, 5), (128, 3, 227, 227, 64, 11, 11, 4, 4, 0, 0),
+                (64, 16, 64, 64, 32, 32, 32, 1, 1, 16, 16), (256, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)]:
+        g = L.make_geom(*geo)
+        for dt in (L.CKS_BF16, L.CKS_TF32):
+            for op in (L.CKS_OP_FWD, L.CKS_OP_DECONV):
+                d = L.plan_dict(g, dt, op)
+                if d["kind"] == "igemm":
+                    assert int(d["pbw"]) * int(d["ntap"]) <= 64, (geo, dt, op, d)

@@ -1,24 +1,16 @@
-"""Print the igemm tile plan of every layer (no GPU needed: plan only) --
-python tools/plan_dump.py CONFIG OP   (OP = fwd | deconv)"""
+"""Print the tile plan of every layer (host only: cks_plan_describe) --
+python tools/plan_dump.py CONFIG OP [DTYPE]   (OP = fwd | deconv | wgrad, DTYPE = bf16 | tf32)"""
 import os
 import sys
-import ctypes
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["CKS_PLAN_DEBUG"] = "1"
-os.environ["CUDA_VISIBLE_DEVICES"] = ""  # plan only: never launch on the fake pointers below, even on a GPU box
 from cks_synth import get_config  # noqa: E402
 from paper_2306_15951_b200 import _lib as L  # noqa: E402
 
 cfg, op = int(sys.argv[1]), sys.argv[2]
+dt = L.CKS_TF32 if len(sys.argv) > 3 and sys.argv[3] == "tf32" else L.CKS_BF16
+code = {"fwd": L.CKS_OP_FWD, "deconv": L.CKS_OP_DECONV, "wgrad": L.CKS_OP_WGRAD}[op]
 for lay in get_config(cfg)[1]:
     g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
-    print(lay.name, flush=True)
-    # fake 16-byte aligned device pointers: the launch fails after the plan is printed
-    try:
-        if op == "fwd":
-            L.lib().cks_conv2d_fwd(ctypes.byref(g), 1, 256, 256, 256, 256, 1 << 40, None)
-        else:
-            L.lib().cks_deconv2d(ctypes.byref(g), 1, 256, None, 256, 256, 256, 1 << 40, None)
-    except Exception:
-        pass
+    print(lay.name)
+    print("[cks plan]", L.cks_plan_describe(g, dt, code))
