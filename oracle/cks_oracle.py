@@ -600,9 +600,4 @@ def op_counts(g: Geom):
     )
 
 
-def pad_zero_fraction(g: Geom):
-    """Fig. 2: proportion of padded zeros in the padded input."""
-    return 1.0 - (g.H * g.W) / ((g.H + 2 * g.ph) * (g.W + 2 * g.pw))
-
-
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("annotations", "math", "np", "dataclass")]

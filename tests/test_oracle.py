@@ -121,6 +121,16 @@ def test_axis_tables_golden(ax):
         for k in ("y", "CH", "oph", "ih_s", "U", "a"):
             assert ph_got[k] == ph_exp[k], (k, ph_got, ph_exp)
         assert [list(r) for r in ph_got["rows"]] == ph_exp["rows"]
+    assert [list(r) for r in O.table_T4(I, F, s, p)] == ax["T4"]
+
+
+@pytest.mark.parametrize("ax", _load("axis_tables.json")["t4_axes"], ids=lambda a: a["name"])
+def test_t4_trim_classes_golden(ax):
+    """T4 (trim classes) on config-sized axes, hand-derived: a version
+    that never merges equal neighbours, or merges unequal ones, fails."""
+    I, F, s, p = ax["I"], ax["F"], ax["s"], ax["p"]
+    assert O.out_extent(I, F, s, p) == ax["O"]
+    assert [list(r) for r in O.table_T4(I, F, s, p)] == ax["T4"]
 
 
 def _axis_grid():
@@ -154,6 +164,9 @@ def test_table_invariants_grid():
                     assert 0 <= f < F and 0 <= oh_s + ch < O_ and (oh_s + ch) * s + f - p == i
         runs = O.table_T4(I, F, s, p)
         assert runs[0][0] == 0 and runs[-1][1] == O_
+        for a, b in zip(runs, runs[1:]):                             # contiguous and maximal
+            assert a[1] == b[0] and (a[2], a[3]) != (b[2], b[3])
+        assert sum((r[1] - r[0]) * (r[3] - r[2]) for r in runs) == V  # classes cover the valid pairs
         n += 1
     assert n > 1000
 
