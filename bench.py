@@ -5,18 +5,24 @@ wgrad) of the C-K-S hot path on B200 (BASELINE.json metric).
 A "step" is one pass of the whole hot path over one batch of the workload:
 for every layer of the workload, ConvV2 forward, KS-deconv-V2 (Stage1 split
 + fused Stage2&3) and Sk-dilated-V2 weight gradient (+ G_Z reduce), as in a
-conv-layer training step.  Default workload: configs[1], the
-Cifar10 VGG-16 layer sweep, N = 128 per GPU (weak scaling; the global batch
-is 128 x n_gpus).  Under torchrun (N > 1 GPUs) every rank runs its batch
-shard and the per-layer dW are summed with one NCCL all_reduce per step.
+conv-layer training step.  Default workload: configs[4], C5 --
+the ResNet-18 conv-layer train step (the 20 conv layers of ResNet-18 @224),
+N = 256 per GPU, the largest single-GPU configuration (2,521 zero-free GFLOP
+per step); weak scaling, global batch 256 x n_gpus.  Headline precision:
+fp32 inputs multiplied as TF32 (the paper computes in fp32), with the
+same step in BF16 reported beside it.  With N > 1 GPUs every rank runs its
+batch shard and the per-layer dW are summed with bucketed NCCL all_reduces
+overlapping the backward (``--gpus N`` without torchrun launches the N ranks).
 
 Timing: inputs resident in HBM; the step is one CUDA graph (the C-ABI calls
 captured once) replayed K times after W warm-ups; L2 is flushed (256 MB
-write) before every timed step, outside the timed events; per-op durations
-come from event nodes inside the graph (device clock); the step time is the
-max over ranks.  ``e2e`` repeats the step through the public Python API
-without graphs, with the step's inputs copied host->device from pinned
-memory and the results copied back inside the timed region.
+write) before every timed step, outside the timed events; the step time is
+the max over ranks.  The roofline's kernel durations come from a copy of the
+same schedule graph with events on each op's launching stream; per-op /
+per-layer numbers follow the paper's per-op protocol (each op alone).
+``e2e`` repeats the step through the public Python API without graphs, with
+the step's inputs copied host->device from pinned memory and the results
+copied back inside the timed region.
 ``--impl reference`` times the fp64 CPU oracle (oracle/) on a bounded
 sample of the same workload on the host cores (rank 0 only).
 """
@@ -39,20 +45,40 @@ _JSON_OUT = None  # original stdout when fd 1 is redirected (multi-rank runs)
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="GPUs of this node; without torchrun, N > 1 launches N ranks itself (torch.distributed.run)")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("cks", "reference"), default="cks")
-    ap.add_argument("--config", type=int, default=1, help="BASELINE configs index (default 1: C2 VGG sweep)")
+    ap.add_argument("--config", type=int, default=4,
+                    help="BASELINE configs index (default 4: C5, the ResNet-18 conv-layer train step, N=256 per GPU "
+                         "-- the largest single-GPU workload; 1: C2 VGG sweep, 2: C3 layers, 3: C4 DCGAN, 5: C6 5x5)")
     ap.add_argument("--batch", type=int, default=None, help="override per-GPU batch")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--layers", action="store_true", help="per-layer breakdown on stderr")
     ap.add_argument("--no-zins", action="store_true", help="skip the zero-inserted-formulation comparison")
-    ap.add_argument("--dtype", choices=("bf16", "tf32"), default="bf16",
-                    help="bf16 inputs, or fp32 inputs multiplied as TF32 (fp32 accumulate and outputs either way)")
+    ap.add_argument("--dtype", choices=("bf16", "tf32"), default="tf32",
+                    help="headline: fp32 inputs multiplied as TF32 (the paper computes in fp32, P:262), or bf16 "
+                         "inputs; fp32 accumulate and outputs either way")
+    ap.add_argument("--companion", choices=("bf16", "tf32", "none"), default="bf16",
+                    help="also time the step in this input precision and report it beside the headline")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """--gpus N without torchrun: run this script as N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -200,13 +226,14 @@ def load_peaks():
         return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
 
 
-def load_traffic(kernel):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def load_traffic(kernel, config, dtype):
+    """dram bytes per launch of a kernel family on this workload (config, dtype)
+    from the committed ncu capture (tools/summarize_profiles.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        return d.get(f"config{config}/{dtype}", {}).get(kernel, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -280,15 +307,343 @@ class LayerBufs:
                                 ws.data_ptr(), ws.numel(), stream_ptr)
 
 
+KIND_KERNEL = {"igemm": "igemm_kernel", "row_fwd": "fwd_row_kernel", "row_wgrad": "wgrad_row_kernel",
+               "wgrad": "wgrad_kernel"}
+
+
+def op_kernel(b, op):
+    """Kernel family an op of the step launches (its plan's main kernel; the
+    op's time includes its staging kernels: G_Z reduce, channel padding)."""
+    if op == "split":
+        return "ks_split_kernel"
+    code = {"fwd": 0, "deconv_only": 1, "deconv": 1, "wgrad": 2}[op]
+    kind = b.L.plan_dict(b.g, b.dt, code)["kind"]
+    return KIND_KERNEL.get(kind, kind)
+
+
+def union_ms(iv):
+    """Length of the union of intervals [(s, e)] (ms)."""
+    tot, cur_s, cur_e = 0.0, None, None
+    for s, e in sorted(iv):
+        if cur_e is None or s > cur_e:
+            if cur_e is not None:
+                tot += cur_e - cur_s
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    if cur_e is not None:
+        tot += cur_e - cur_s
+    return tot
+
+
+def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, headline=True):
+    """Build one workload in `dtype` and time it.  Returns the bench fields."""
+    from cks_synth import get_config
+    desc, layers = get_config(args.config, args.batch)
+    bufs = [LayerBufs(torch, lay, args.config, i, rank, device, dtype) for i, lay in enumerate(layers)]
+    # flat dW buffer: the bucketed NCCL all_reduce works on slices of it
+    sizes = [b.lay.OC * b.lay.FH * b.lay.FW * b.lay.C for b in bufs]
+    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
+    off = 0
+    for b, s in zip(bufs, sizes):
+        b.dW = flat[off:off + s].view(b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C)
+        off += s
+    ops_seq = []
+    for i, b in enumerate(bufs):
+        for op in ("fwd", "deconv", "wgrad"):
+            if op in b.lay.ops:
+                if op == "deconv":
+                    ops_seq.append((i, "split"))
+                ops_seq.append((i, "deconv_only" if op == "deconv" else op))
+    OPF = {"fwd": "fwd", "deconv_only": "deconv", "wgrad": "wgrad", "split": "split"}
+    flops_step = sum(bufs[i].flops for i, op in ops_seq if op != "split")
+    launches_step = sum(bufs[i].launches[OPF[op]] for i, op in ops_seq)
+    kern = {(i, op): op_kernel(bufs[i], op) for i, op in ops_seq}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MB > 126 MB L2
+    peaks = load_peaks()
+    tc_peak = peaks["bf16"] if dtype == "bf16" else peaks["bf16"] / 2  # dense TF32 = 1/2 BF16 (guide's nominal ratio)
+
+    stream = torch.cuda.Stream(device)
+    with torch.cuda.stream(stream):
+        for i, op in ops_seq:  # eager warm-up (sets smem attributes, checks errors)
+            bufs[i].run(op, stream.cuda_stream)
+    torch.cuda.synchronize()
+
+    # ---- (1) per-op protocol (P:272: each op timed on its own): the ops
+    # serialized in one graph with event nodes between them, L2 flushed
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(ops_seq) + 1)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        sp = torch.cuda.current_stream().cuda_stream
+        for k, (i, op) in enumerate(ops_seq):
+            evs[k].record()
+            bufs[i].run(op, sp)
+        evs[-1].record()
+    nser = max(3, min(args.steps, 20))
+    per_op_ms = [0.0] * len(ops_seq)
+    with torch.cuda.stream(stream):
+        for it in range(nser + 2):
+            flush.fill_(float(it))
+            graph.replay()
+            stream.synchronize()
+            if it >= 2:
+                for k in range(len(ops_seq)):
+                    per_op_ms[k] += evs[k].elapsed_time(evs[k + 1]) / nser
+    del graph
+
+    # ---- (2) the step as a training-step schedule (one CUDA graph): forward
+    # chain on the main stream with the weight-only KS Stage1 splits on a side
+    # stream; then the backward chain in reverse layer order (KS-deconv on the
+    # main stream) with each layer's Sk-dilated wgrad on one of two alternating
+    # side streams, released when the layer above finished its deconv.
+    s1, s3 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    nws = max(1, int(os.environ.get("CKS_BENCH_WSTREAMS", "2")))  # measured: 2 best (C2 0.624 -> 0.597 ms)
+    wst = [torch.cuda.Stream(device) for _ in range(nws)]
+    # data-parallel: the flat dW is all-reduced in buckets of layers, each
+    # launched (on s3, NCCL) as soon as the bucket's wgrads are done, so the
+    # communication overlaps the rest of the backward chain
+    order = list(reversed(range(len(bufs))))  # backward order
+    cuts = []
+    nbuck = int(os.environ.get("CKS_BENCH_BUCKETS", "3"))
+    if use_dist and nbuck > 1:
+        tot, acc = sum(sizes), 0
+        for k, i in enumerate(order):
+            acc += sizes[i]
+            if acc >= tot / nbuck * (len(cuts) + 1) - 1 and k < len(order) - 1:
+                cuts.append(k)
+    cuts.append(len(order) - 1)
+    offs = [0]
+    for sz in sizes:
+        offs.append(offs[-1] + sz)
+    buckets, k0 = [], 0
+    for k1 in cuts:
+        layers_k = order[k0:k1 + 1]
+        buckets.append((offs[min(layers_k)], offs[max(layers_k) + 1]))
+        k0 = k1 + 1
+    last_of_bucket = {order[k1]: bi for bi, k1 in enumerate(cuts)}
+    ar_in_graph = os.environ.get("CKS_BENCH_AR_GRAPH", "1") == "1"
+    if use_dist:
+        s3.wait_stream(stream)
+        with torch.cuda.stream(s3):  # communicator warm-up on the capture-side stream
+            dist.all_reduce(flat)
+        stream.wait_stream(s3)
+        torch.cuda.synchronize()
+
+    def capture(ar_graph, timed):
+        """timed: an event on the launching stream before and after every op
+        (the in-schedule kernel durations for the roofline)."""
+        tev = {}
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            main = torch.cuda.current_stream()
+            if timed:
+                t0 = torch.cuda.Event(enable_timing=True, external=True)
+                t0.record(main)
+                tev["t0"] = t0
+
+            def run(i, op, s):
+                if timed:
+                    a, z = (torch.cuda.Event(enable_timing=True, external=True) for _ in range(2))
+                    a.record(s)
+                    bufs[i].run(op, s.cuda_stream)
+                    z.record(s)
+                    tev[(i, op)] = (a, z)
+                else:
+                    bufs[i].run(op, s.cuda_stream)
+
+            fork = torch.cuda.Event()
+            fork.record(main)
+            s1.wait_event(fork)
+            for w in wst:
+                w.wait_event(fork)
+            with torch.cuda.stream(s1):
+                for i, b in enumerate(bufs):
+                    if "deconv" in b.lay.ops:
+                        run(i, "split", s1)
+                split_done = torch.cuda.Event()
+                split_done.record(s1)
+            for i, b in enumerate(bufs):
+                if "fwd" in b.lay.ops:
+                    run(i, "fwd", main)
+            main.wait_event(split_done)
+            for k, i in enumerate(order):
+                b = bufs[i]
+                ev = torch.cuda.Event()
+                ev.record(main)
+                ws_k = wst[k % nws]
+                if "wgrad" in b.lay.ops:
+                    ws_k.wait_event(ev)
+                    with torch.cuda.stream(ws_k):
+                        run(i, "wgrad", ws_k)
+                if use_dist and ar_graph and i in last_of_bucket:
+                    for w in wst:  # this bucket's dW is complete: NCCL all_reduce on s3
+                        done = torch.cuda.Event()
+                        done.record(w)
+                        s3.wait_event(done)
+                    lo, hi = buckets[last_of_bucket[i]]
+                    with torch.cuda.stream(s3):
+                        dist.all_reduce(flat[lo:hi])
+                if "deconv" in b.lay.ops:
+                    run(i, "deconv_only", main)
+            for w in wst + ([s3] if use_dist and ar_graph else []):
+                join = torch.cuda.Event()
+                join.record(w)
+                main.wait_event(join)
+            if timed:
+                t1 = torch.cuda.Event(enable_timing=True, external=True)
+                t1.record(main)
+                tev["t1"] = t1
+        return g, tev
+
+    try:
+        graph2, _ = capture(ar_in_graph, False)
+    except Exception as exc:  # NCCL capture unavailable: reduce after the graph instead
+        if not (use_dist and ar_in_graph):
+            raise
+        print(f"[bench] NCCL graph capture failed ({exc}); all_reduce after the step graph", file=sys.stderr)
+        torch.cuda.synchronize()
+        ar_in_graph = False
+        graph2, _ = capture(False, False)
+
+    def replay(g):
+        g.replay()
+        if use_dist and not ar_in_graph:  # fallback: one all_reduce after the step
+            dist.all_reduce(flat)
+
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    noev = []
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            flush.fill_(2.0)
+            replay(graph2)
+        torch.cuda.synchronize()
+        if use_dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                t_start.record(stream)
+                replay(graph2)
+                t_end.record(stream)
+                stream.synchronize()
+                noev.append(t_start.elapsed_time(t_end))
+    if use_dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(noev)
+    if use_dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = flops_step * n_gpus / (ms_per_step / 1e3) / 1e12
+    del graph2
+
+    # ---- (3) the same schedule with an event before and after every op on
+    # its launching stream: in-step kernel durations (roofline), per kernel
+    # family the union of its launches' intervals, so it fits in the step
+    graph3, tev = capture(ar_in_graph, True)
+    nt = max(3, min(args.steps, 20))
+    fam_iv = {}
+    fam_busy = {}
+    step3 = 0.0
+    with torch.cuda.stream(stream):
+        for it in range(nt + 2):
+            flush.fill_(float(it))
+            replay(graph3)
+            stream.synchronize()
+            if it < 2:
+                continue
+            t0 = tev["t0"]
+            step3 += t0.elapsed_time(tev["t1"]) / nt
+            iv = {}
+            for key, ev in tev.items():
+                if key in ("t0", "t1"):
+                    continue
+                a, z = ev
+                iv.setdefault(kern[key], []).append((t0.elapsed_time(a), t0.elapsed_time(z)))
+                fam_iv.setdefault(kern[key], {}).setdefault(key, 0.0)
+                fam_iv[kern[key]][key] += (t0.elapsed_time(z) - t0.elapsed_time(a)) / nt
+            for kname, v in iv.items():
+                fam_busy[kname] = fam_busy.get(kname, 0.0) + union_ms(v) / nt
+    del graph3
+    torch.cuda.synchronize()
+
+    # ---- roofline of the dominant kernel family (largest in-step busy time)
+    kname = max(fam_busy, key=fam_busy.get)
+    keys = [k for k in fam_iv[kname]]
+    kfl = sum(bufs[i].flops for i, op in keys if op != "split")
+    kby = sum(bufs[i].algo_bytes[OPF[op]] for i, op in keys)
+    busy = fam_busy[kname]
+    t_tc = kfl / (tc_peak * 1e12)
+    t_hbm = kby / (peaks["hbm"] * 1e9)
+    bound = "tensor" if t_tc >= t_hbm else "hbm"
+    ach_tc = kfl / (busy / 1e3) / 1e12
+    ach_hbm = kby / (busy / 1e3) / 1e9
+    tc_frac, hbm_frac = ach_tc / tc_peak, ach_hbm / peaks["hbm"]
+    roofline = {"bound": bound, "kernel": kname,
+                "achieved": round(ach_tc if bound == "tensor" else ach_hbm, 2),
+                "peak": round(tc_peak if bound == "tensor" else peaks["hbm"], 1),
+                "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+                "frac": round(tc_frac if bound == "tensor" else hbm_frac, 4),
+                "traffic": load_traffic(kname, args.config, dtype),
+                "tc_frac": round(tc_frac, 4), "hbm_frac": round(hbm_frac, 4),
+                "launches_per_step": len(keys),
+                "algorithmic_flops_per_launch": round(kfl / len(keys)),
+                "algorithmic_bytes_per_launch": round(kby / len(keys)),
+                "busy_ms_per_step": round(busy, 5), "evented_step_ms": round(step3, 5),
+                "share_of_step": round(busy / step3, 4),
+                "peak_src": (f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)" if dtype == "bf16" else
+                             f"{peaks['src']} bf16 burst x 1/2 (nominal TF32:BF16)") + f"; HBM {peaks['hbm']} GB/s",
+                "timing": "CUDA events on each op's launching stream inside the step schedule graph (a copy of the "
+                          "headline graph with event nodes); busy = union of the family's launch intervals per step",
+                "traffic_src": "profiles/ncu_traffic.json: ncu dram__bytes_read+write per launch (cold-cache replay)"}
+    fams = {k: {"busy_ms": round(v, 5), "share": round(v / step3, 4)} for k, v in sorted(fam_busy.items(),
+                                                                                         key=lambda kv: -kv[1])}
+
+    # ---- per-op families and the per-layer table (per-op protocol)
+    fam = {"fwd": [0.0, 0], "split": [0.0, 0], "deconv": [0.0, 0], "wgrad": [0.0, 0]}
+    rows = []
+    for k, (i, op) in enumerate(ops_seq):
+        f = OPF[op]
+        b = bufs[i]
+        ms = per_op_ms[k]
+        fam[f][0] += ms
+        fl = b.flops if f != "split" else 0
+        fam[f][1] += fl
+        by = b.algo_bytes[f]
+        tc = fl / (ms / 1e3) / 1e12 / tc_peak
+        hb = by / (ms / 1e3) / 1e9 / peaks["hbm"]
+        lb = "tensor" if fl / (tc_peak * 1e12) >= by / (peaks["hbm"] * 1e9) else "hbm"
+        rows.append({"layer": b.lay.name, "op": f, "kernel": kern[(i, op)], "us": round(ms * 1e3, 2),
+                     "tflops": round(fl / (ms / 1e3) / 1e12, 1) if fl else None, "bound": lb,
+                     "tc_frac": round(tc, 3), "hbm_frac": round(hb, 3),
+                     "frac": round(tc if lb == "tensor" else hb, 3)})
+    per_op = {op: {"ms": round(v[0], 5), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 2) if v[1] else None}
+              for op, v in fam.items() if v[0]}
+    out = {"desc": desc, "layers": layers, "bufs": bufs, "ops_seq": ops_seq, "flops_step": flops_step, "flush": flush,
+           "value": value, "ms_per_step": ms_per_step, "per_op": per_op, "roofline": roofline, "families": fams,
+           "per_layer": rows, "gpu_launches": launches_step * args.steps, "clocks": clk.summary(), "nws": nws,
+           "buckets": len(buckets), "ar_in_graph": ar_in_graph, "serialized_ms": sum(per_op_ms),
+           "fam_ms": {"fwd": fam["fwd"][0], "deconv": fam["deconv"][0] + fam["split"][0], "wgrad": fam["wgrad"][0]}}
+    if args.layers and rank == 0:
+        for r in rows:
+            print(f"  {r['layer']:22s} {r['op']:7s} {r['kernel']:17s} {r['us']:9.2f} us  "
+                  f"{(r['tflops'] or 0):8.1f} TFLOP/s  {r['bound']:6s} tc {r['tc_frac']:.3f} hbm {r['hbm_frac']:.3f}",
+                  file=sys.stderr)
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
-    from cks_synth import get_config
     from paper_2306_15951_b200 import build
 
     ws_, rank, local = dist_env()
-    if args.gpus != ws_ and ws_ > 1:
-        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE {ws_}", file=sys.stderr)
+    if args.gpus != ws_:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE {ws_}: running {ws_} rank(s)", file=sys.stderr)
     n_gpus = ws_
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
@@ -306,283 +661,63 @@ def run_gpu(args):
         sys.stdout.flush()
         os.dup2(2, 1)
         dist.init_process_group("nccl", device_id=device)
-    build.build()
-    desc, layers = get_config(args.config, args.batch)
-    bufs = [LayerBufs(torch, lay, args.config, i, rank, device, args.dtype) for i, lay in enumerate(layers)]
-    # flat dW buffer: one NCCL all_reduce per step for all layers
-    sizes = [b.lay.OC * b.lay.FH * b.lay.FW * b.lay.C for b in bufs]
-    flat = torch.zeros(sum(sizes), dtype=torch.float32, device=device)
-    off = 0
-    for b, s in zip(bufs, sizes):
-        b.dW = flat[off:off + s].view(b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C)
-        off += s
-    ops_seq = []
-    for i, b in enumerate(bufs):
-        for op in ("fwd", "deconv", "wgrad"):
-            if op in b.lay.ops:
-                if op == "deconv":
-                    ops_seq.append((i, "split"))
-                ops_seq.append((i, "deconv_only" if op == "deconv" else op))
-    OPF = {"fwd": "fwd", "deconv_only": "deconv", "wgrad": "wgrad", "split": "split"}
-    flops_step = sum(bufs[i].flops for i, op in ops_seq if op != "split")
-    launches_step = sum(bufs[i].launches[OPF[op]] for i, op in ops_seq)
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MB > 126 MB L2
-
-    # ---- capture the step as one CUDA graph with event nodes between ops
-    # stream priority of the forward / KS-deconv chain (experiments: a high
-    # priority for this critical path measured slower, 0.73 vs 0.70 ms on C2)
-    prio = int(os.environ.get("CKS_BENCH_PRIO", "0"))
-    stream = torch.cuda.Stream(device, priority=prio)
-    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(ops_seq) + 1)]
-    with torch.cuda.stream(stream):
-        for i, op in ops_seq:  # eager warm-up (sets smem attributes, checks errors)
-            bufs[i].run_split(stream.cuda_stream) if op == "split" else bufs[i].run(op, stream.cuda_stream)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        sp = torch.cuda.current_stream().cuda_stream
-        for k, (i, op) in enumerate(ops_seq):
-            evs[k].record()
-            bufs[i].run_split(sp) if op == "split" else bufs[i].run(op, sp)
-        evs[-1].record()
-
-    def step(sync_read=True):
-        graph.replay()
-        if use_dist:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(flat)
-        if sync_read:
-            stream.synchronize()
-            return [evs[k].elapsed_time(evs[k + 1]) for k in range(len(ops_seq))]
-
-    with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):
-            flush.fill_(1.0)
-            step()
-    # ---- timed region
+    if local == 0:
+        build.build()
     if use_dist:
         dist.barrier()
-    torch.cuda.synchronize()
-    per_op_ms = [0.0] * len(ops_seq)
-    step_ms = []
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        for _ in range(args.steps):
-            flush.fill_(float(_))
-            t_start.record(stream)
-            ms = step()
-            if use_dist:
-                t_end.record(stream)
-                stream.synchronize()
-                step_ms.append(t_start.elapsed_time(t_end))
-            else:
-                step_ms.append(sum(ms))
-            for k, v in enumerate(ms):
-                per_op_ms[k] += v
-    torch.cuda.synchronize()
-    # ---- headline: the step as a training-step schedule (one graph, no event
-    # nodes): forward chain on the main stream with the weight-only KS Stage1
-    # splits on a side stream; then the backward chain in reverse layer order
-    # (KS-deconv on the main stream) with each layer's Sk-dilated wgrad on a
-    # second side stream, released when the layer above finished its deconv.
-    s1, s2, s3 = torch.cuda.Stream(device), torch.cuda.Stream(device), torch.cuda.Stream(device)
-    # Sk-dilated streams: the per-layer wgrads are independent of each other, so
-    # consecutive layers' wgrads may run on alternate streams (CKS_BENCH_WSTREAMS)
-    nws = max(1, int(os.environ.get("CKS_BENCH_WSTREAMS", "2")))  # measured: 2 best (C2 0.624 -> 0.597 ms)
-    wst = [s2] + [torch.cuda.Stream(device) for _ in range(nws - 1)]
-    # data-parallel: the flat dW is all-reduced in buckets of layers, each
-    # launched (on s3, NCCL) as soon as the bucket's wgrads are done, so the
-    # communication overlaps the rest of the backward chain.  The step graph is
-    # cut at the bucket boundaries; single-GPU runs use one graph.
-    order = list(reversed(range(len(bufs))))  # backward order
-    cuts = []  # index into `order` after which a bucket closes
-    nbuck = int(os.environ.get("CKS_BENCH_BUCKETS", "3"))
-    if use_dist and nbuck > 1:
-        tot, acc = sum(sizes), 0
-        for k, i in enumerate(order):
-            acc += sizes[i]
-            if acc >= tot / nbuck * (len(cuts) + 1) - 1 and k < len(order) - 1:
-                cuts.append(k)
-    cuts.append(len(order) - 1)
-    offs = [0]
-    for sz in sizes:
-        offs.append(offs[-1] + sz)
-    # one graph for the whole step; after the last wgrad of every bucket the
-    # bucket's NCCL all_reduce (captured on s3) overlaps the remaining backward
-    # (host-side external events for this measured ~25 us slower on C2)
-    bucket_of = {}
-    buckets, k0 = [], 0
-    for k1 in cuts:
-        layers_k = order[k0:k1 + 1]
-        buckets.append((offs[min(layers_k)], offs[max(layers_k) + 1]))
-        for i in layers_k:
-            bucket_of[i] = len(buckets) - 1
-        k0 = k1 + 1
-    last_of_bucket = {order[k1]: bi for bi, k1 in enumerate(cuts)}
-    ar_in_graph = os.environ.get("CKS_BENCH_AR_GRAPH", "1") == "1"
-    if use_dist and ar_in_graph:
-        s3.wait_stream(stream)
-        with torch.cuda.stream(s3):  # communicator warm-up on the capture-side stream
-            dist.all_reduce(flat)
-        stream.wait_stream(s3)
-        torch.cuda.synchronize()
-    def capture(ar_graph):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            main = torch.cuda.current_stream()
-            fork = torch.cuda.Event()
-            fork.record(main)
-            s1.wait_event(fork)
-            for w in wst:
-                w.wait_event(fork)
-            with torch.cuda.stream(s1):
-                for i, b in enumerate(bufs):
-                    if "deconv" in b.lay.ops:
-                        b.run_split(s1.cuda_stream)
-                split_done = torch.cuda.Event()
-                split_done.record(s1)
-            for i, b in enumerate(bufs):
-                if "fwd" in b.lay.ops:
-                    b.run("fwd", main.cuda_stream)
-            main.wait_event(split_done)
-            for k, i in enumerate(order):
-                b = bufs[i]
-                ev = torch.cuda.Event()
-                ev.record(main)
-                ws_k = wst[k % nws]
-                if "wgrad" in b.lay.ops:
-                    ws_k.wait_event(ev)
-                    with torch.cuda.stream(ws_k):
-                        b.run("wgrad", ws_k.cuda_stream)
-                if use_dist and ar_graph and i in last_of_bucket:
-                    # this bucket's dW is complete: NCCL all_reduce captured as graph nodes on s3
-                    for w in wst:
-                        done = torch.cuda.Event()
-                        done.record(w)
-                        s3.wait_event(done)
-                    lo, hi = buckets[last_of_bucket[i]]
-                    with torch.cuda.stream(s3):
-                        dist.all_reduce(flat[lo:hi])
-                if "deconv" in b.lay.ops:
-                    b.run("deconv_only", main.cuda_stream)
-            for w in wst:
-                join = torch.cuda.Event()
-                join.record(w)
-                main.wait_event(join)
-            if use_dist and ar_graph:
-                join3 = torch.cuda.Event()
-                join3.record(s3)
-                main.wait_event(join3)
-        return g
-
-    try:
-        graph2 = capture(ar_in_graph)
-    except Exception as exc:  # NCCL capture unavailable: reduce after the graph instead
-        if not (use_dist and ar_in_graph):
-            raise
-        print(f"[bench] NCCL graph capture failed ({exc}); all_reduce after the step graph", file=sys.stderr)
-        torch.cuda.synchronize()
-        ar_in_graph = False
-        graph2 = capture(False)
-    skip_ar = os.environ.get("CKS_BENCH_NOAR") == "1"  # experiments: no collective at all
-
-    def replay_step():
-        graph2.replay()
-        if use_dist and not skip_ar and not ar_in_graph:  # fallback: one all_reduce after the step
-            dist.all_reduce(flat)
-
-    noev = []
-    with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):
-            flush.fill_(2.0)
-            replay_step()
-        torch.cuda.synchronize()
-        if use_dist:
-            dist.barrier()
-        with ClockSampler(local) as clk:
-            for k in range(args.steps):
-                flush.fill_(float(k))
-                t_start.record(stream)
-                replay_step()
-                t_end.record(stream)
-                stream.synchronize()
-                noev.append(t_start.elapsed_time(t_end))
-    if use_dist:
-        dist.barrier()
-    serial_ms = sum(step_ms) / args.steps
-    total_ms = sum(noev)
-    if use_dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = flops_step * n_gpus / (ms_per_step / 1e3) / 1e12
-
-    # ---- per-op breakdown and roofline of the dominant kernel
-    fam = {"fwd": [0.0, 0], "split": [0.0, 0], "deconv": [0.0, 0], "wgrad": [0.0, 0]}
-    for k, (i, op) in enumerate(ops_seq):
-        f = OPF[op]
-        fam[f][0] += per_op_ms[k] / args.steps
-        fam[f][1] += bufs[i].flops if f != "split" else 0
-    per_op = {op: {"ms": round(v[0], 5), "tflops": round(v[1] / (v[0] / 1e3) / 1e12, 2) if v[1] else None}
-              for op, v in fam.items() if v[0]}
-    igemm_ms, igemm_fl = fam["fwd"][0] + fam["deconv"][0], fam["fwd"][1] + fam["deconv"][1]
-    if igemm_ms >= fam["wgrad"][0]:
-        kname, kms, kfl, nl = "igemm_kernel", igemm_ms, igemm_fl, sum(1 for _, op in ops_seq if op in ("fwd", "deconv_only"))
-    else:
-        kname, kms, kfl, nl = "wgrad_kernel", fam["wgrad"][0], fam["wgrad"][1], sum(1 for _, op in ops_seq if op == "wgrad")
-    peaks = load_peaks()
-    if args.dtype == "tf32":  # dense TF32 = half the BF16 rate (guide's nominal 1.1 vs 2.25 PFLOP/s)
-        peaks = dict(peaks, bf16=peaks["bf16"] / 2, src=peaks["src"] + " bf16 x 1/2 (nominal TF32:BF16)")
-    achieved = kfl / (kms / 1e3) / 1e12
-    kops = ("fwd", "deconv_only") if kname == "igemm_kernel" else ("wgrad",)
-    algo_b = [bufs[i].algo_bytes[OPF[op]] for i, op in ops_seq if op in kops]
-    roofline = {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 2), "peak": peaks["bf16"],
-                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16"], 4), "traffic": load_traffic(kname),
-                "launches_per_step": nl, "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json)" if args.dtype == "bf16" else
-                    f"{peaks['src']} (MEASURED_PEAKS.json bf16 burst x 0.5)",
-                "algorithmic_bytes_per_launch": round(sum(algo_b) / max(len(algo_b), 1)),
-                "traffic_src": "profiles/ncu_traffic.json: mean ncu dram__bytes_read+write per launch (cold-cache replay)",
-                "timing": "op-level CUDA event nodes inside the step graph (kernel + its staging kernels)"}
-
+    build.build()  # loads the library (up to date now)
+    m = measure(args, torch, dist, device, rank, local, n_gpus, use_dist, args.dtype)
+    desc, layers, bufs = m["desc"], m["layers"], m["bufs"]
     line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded U[-1,1) X/dY, kaiming-uniform W)",
+        "metric": METRIC, "value": round(m["value"], 3), "unit": "TFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(m["ms_per_step"], 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (seeded U[-1,1) X/dY, kaiming-uniform W)" +
+                ("; fp32 inputs multiplied as TF32, fp32 accumulate and outputs" if args.dtype == "tf32" else
+                 "; bf16 inputs, fp32 accumulate and outputs"),
         "config": {"workload": desc, "layers": len(layers), "per_gpu_batch": layers[0].N,
-                   "global_batch": layers[0].N * n_gpus, "ops_per_step": len(ops_seq),
-                   "zero_free_gflop_per_gpu_step": round(flops_step / 1e9, 3),
+                   "global_batch": layers[0].N * n_gpus, "ops_per_step": len(m["ops_seq"]),
+                   "zero_free_gflop_per_gpu_step": round(m["flops_step"] / 1e9, 3),
                    "l2": "flushed (256 MB write) before every timed step, outside the timed events",
                    "parallelism": f"dp{n_gpus}",
                    "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad on %d "
-                               "alternating streams (CUDA graph)" % nws
+                               "alternating streams (CUDA graph)" % m["nws"]
                                + (("; dW all_reduce in %d buckets overlapping the backward (NCCL in the graph)"
-                                   % len(buckets) if ar_in_graph else "; dW all_reduce after the step graph")
+                                   % m["buckets"] if m["ar_in_graph"] else "; dW all_reduce after the step graph")
                                   if use_dist else ""),
-                   "serialized_step_ms_with_op_events": round(serial_ms, 5)},
-        "per_op": per_op, "roofline": roofline, "gpu_launches": launches_step * args.steps,
-        "clocks": clk.summary(),
+                   "serialized_step_ms_per_op_protocol": round(m["serialized_ms"], 5)},
+        "per_op": m["per_op"], "roofline": m["roofline"], "kernel_families_in_step": m["families"],
+        "gpu_launches": m["gpu_launches"], "clocks": m["clocks"],
     }
     # ---- the zero-inserted / zero-padded formulation on the same kernels
     if not args.no_zins and n_gpus == 1:
-        fam_cks = {"fwd": fam["fwd"][0], "deconv": fam["deconv"][0] + fam["split"][0], "wgrad": fam["wgrad"][0]}
-        line["zins"] = run_zins(torch, bufs, max(3, min(args.steps, 20)), device, flush, fam_cks, args.layers)
+        line["zins"] = run_zins(torch, bufs, max(3, min(args.steps, 20)), device, m["flush"], m["fam_ms"], args.layers)
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
-        line["e2e"] = run_e2e(torch, dist, bufs, ops_seq, flops_step, n_gpus, max(2, min(args.steps, 10)), device)
+        line["e2e"] = run_e2e(torch, dist, bufs, m["ops_seq"], m["flops_step"], n_gpus, max(2, min(args.steps, 10)),
+                              device)
+    line["per_layer"] = m["per_layer"]
+    del m, bufs
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # ---- the other input precision beside the headline (same workload)
+    if args.companion and args.companion != args.dtype:
+        c = measure(args, torch, dist, device, rank, local, n_gpus, use_dist, args.companion)
+        line[args.companion] = {"value": round(c["value"], 3), "ms_per_step": round(c["ms_per_step"], 5),
+                                "per_op": c["per_op"], "roofline": c["roofline"],
+                                "kernel_families_in_step": c["families"], "gpu_launches": c["gpu_launches"],
+                                "clocks": c["clocks"],
+                                "per_layer": [{k: r[k] for k in ("layer", "op", "us", "tflops", "frac")}
+                                              for r in c["per_layer"]]}
+        del c
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     # ---- CPU oracle baseline (rank 0, N=1 only)
     if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         el, f, passes = oracle_sample(layers, args.config, 1, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": f / el / 1e12, "unit": "TFLOP/s", "cores": blas_threads(), "kind": "oracle",
                                 "sample": f"{passes} passes over all {len(layers)} layers x ops at N=1 image "
                                           f"({el:.1f} s; oracle cost is linear in N)"}
-    if args.layers and rank == 0:
-        for k, (i, op) in enumerate(ops_seq):
-            ms = per_op_ms[k] / args.steps
-            fl = bufs[i].flops if op != "split" else 0
-            print(f"  {bufs[i].lay.name:22s} {op:11s} {ms * 1e3:9.2f} us  {fl / ms / 1e9:9.1f} TFLOP/s",
-                  file=sys.stderr)
     if rank == 0:
         print(json.dumps(line), file=_JSON_OUT or sys.stdout, flush=True)
     if use_dist:
@@ -758,6 +893,10 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.companion == "none":
+        args.companion = None
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     return run_gpu(args)
 
 

@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("CKS_LIB_VARIANT") or os.path.join(_PKG, "libcks.so")  # variant: experiments only
+# CKS_EXPERIMENTS=1 loads the experiments build (libcks_exp.so: environment
+# knobs for tools/ sweeps); the product path loads libcks.so, which has none
+LIB_PATH = os.path.join(_PKG, "libcks_exp.so" if os.environ.get("CKS_EXPERIMENTS") == "1" else "libcks.so")
 
 CKS_TF32, CKS_BF16 = 0, 1
 CKS_OP_FWD, CKS_OP_DECONV, CKS_OP_WGRAD = 0, 1, 2

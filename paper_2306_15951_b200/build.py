@@ -9,7 +9,10 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libcks.so")
+# CKS_EXPERIMENTS=1: the experiments build (environment knobs for tools/
+# sweeps, debug timeline) goes to its own file; the production libcks.so has none
+EXPERIMENTS = os.environ.get("CKS_EXPERIMENTS") == "1"
+LIB = os.path.join(PKG, "libcks_exp.so" if EXPERIMENTS else "libcks.so")
 SOURCES = [os.path.join(CSRC, "cks_api.cu"), os.path.join(CSRC, "cks_plan.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("cks_plan.h", "kernels/ptx.cuh", "kernels/igemm.cuh",
                                                   "kernels/wgrad.cuh", "kernels/aux.cuh", "kernels/narrow.cuh")] + \
@@ -44,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 return LIB
             tmp = f"{LIB}.{os.getpid()}.tmp"
             cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-                   "-Xcompiler", "-fPIC", "-shared", "-o", tmp] + SOURCES
+                   "-Xcompiler", "-fPIC", "-shared", "-o", tmp] + (["-DCKS_EXPERIMENTS"] if EXPERIMENTS else []) + SOURCES
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), file=sys.stderr)

@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 #include <utility>
 
 #include "../../include/cks.h"
@@ -41,6 +43,43 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+// Tensor-map cache: encoding is a pure function of its arguments (base
+// pointer, shape, strides, box, swizzle ...), so a training loop that calls
+// an op again on the same buffers reuses the encoded CUtensorMap (thread-safe,
+// bounded).
+CUresult encode_cached(EncodeTiledFn enc, CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* base,
+                       const cuuint64_t* gd, const cuuint64_t* gs, const cuuint32_t* bd, const cuuint32_t* es,
+                       CUtensorMapInterleave il, CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                       CUtensorMapFloatOOBfill oob) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, CUtensorMap> cache;
+    uint64_t k[32];
+    int n = 0;
+    k[n++] = uint64_t(dt);
+    k[n++] = rank;
+    k[n++] = reinterpret_cast<uint64_t>(base);
+    for (cuuint32_t i = 0; i < rank; ++i) k[n++] = gd[i];
+    for (cuuint32_t i = 0; i + 1 < rank; ++i) k[n++] = gs[i];
+    for (cuuint32_t i = 0; i < rank; ++i) k[n++] = (uint64_t(bd[i]) << 32) | es[i];
+    k[n++] = (uint64_t(il) << 48) | (uint64_t(sw) << 32) | (uint64_t(l2) << 16) | uint64_t(oob);
+    const std::string key(reinterpret_cast<const char*>(k), sizeof(uint64_t) * n);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *m = it->second;
+            return CUDA_SUCCESS;
+        }
+    }
+    const CUresult r = enc(m, dt, rank, base, gd, gs, bd, es, il, sw, l2, oob);
+    if (r == CUDA_SUCCESS) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (cache.size() >= 4096) cache.clear();
+        cache.emplace(key, *m);
+    }
+    return r;
+}
+
 int device_sms() {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return kPlanSMs;
@@ -57,7 +96,7 @@ bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t d
     cuuint64_t gs[3] = {strides_b[0], strides_b[1], strides_b[2]};
     cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    CUresult r = enc(m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+    CUresult r = encode_cached(enc, m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                      const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B  // MN-major tf32 (SWIZZLE_128B_BASE32B)
                             : (row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -68,7 +107,7 @@ bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t d
 
 int debug_flags() {
     static int f = [] {
-        const char* e = getenv("CKS_DEBUG_FLAGS");  // experiments only; unset in production
+        const char* e = cks_knob("CKS_DEBUG_FLAGS");  // experiments only; unset in production
         return e ? atoi(e) : 0;
     }();
     return f;
@@ -76,14 +115,14 @@ int debug_flags() {
 
 // experiments: allocate all 512 TMEM columns per igemm CTA (the former behaviour)
 bool tmem_full() {
-    static const bool on = getenv("CKS_TMEM_FULL") != nullptr;
+    static const bool on = cks_knob("CKS_TMEM_FULL") != nullptr;
     return on;
 }
 
 // TMA-store epilogue for every igemm tile (0: only the last tile per CTA; experiments)
 bool epi_tma_all() {
     static const bool on = [] {
-        const char* e = getenv("CKS_EPI_TMA");
+        const char* e = cks_knob("CKS_EPI_TMA");
         return e ? atoi(e) != 0 : true;
     }();
     return on;
@@ -98,7 +137,7 @@ bool make_tmap4_f32(CUtensorMap* m, const void* base, const uint64_t dims[4], co
     cuuint64_t gs[3] = {strides_b[0], strides_b[1], strides_b[2]};
     cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), gd, gs, bd, es,
+    return encode_cached(enc, m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), gd, gs, bd, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -166,15 +205,36 @@ FastDiv make_fastdiv(uint32_t d) {
     return f;
 }
 
-void fill_axis(KAxis& k, const std::vector<KRow>& rows) {
+// Compact axis table for the kernel parameters (KAxisC): per-row windows and
+// per-phase affine (a0, out) maps.  Returns false (-> CKS_ERR_UNSUPPORTED) if
+// the rows are not affine per phase or exceed the phase limit; the expansion in
+// the kernel reproduces the KRow table exactly.
+bool fill_axis(KAxisC& k, const std::vector<KRow>& rows) {
     memset(&k, 0, sizeof(k));
+    int nph = 0;
     for (size_t i = 0; i < rows.size(); ++i) {
-        k.a0[i] = int16_t(rows[i].a0);
-        k.out[i] = int16_t(rows[i].out);
-        k.ts[i] = uint8_t(rows[i].ts);
-        k.te[i] = uint8_t(rows[i].te);
-        k.phase[i] = uint8_t(rows[i].phase);
+        const KRow& r = rows[i];
+        if (i == 0 || r.phase != rows[i - 1].phase) {  // a new run (phase) starts here
+            if (nph == kMaxPhases || r.phase > 255) return false;
+            k.row0[nph] = int16_t(i);
+            k.phid[nph] = int16_t(r.phase);
+            k.a00[nph] = int16_t(r.a0);
+            k.out0[nph] = int16_t(r.out);
+            if (i + 1 < rows.size() && rows[i + 1].phase == r.phase) {
+                k.a0st[nph] = int16_t(rows[i + 1].a0 - r.a0);
+                k.outst[nph] = int16_t(rows[i + 1].out - r.out);
+            }
+            ++nph;
+        }
+        const int x = nph - 1, u = int(i) - k.row0[x];
+        if (r.a0 != k.a00[x] + int64_t(u) * k.a0st[x] || r.out != k.out0[x] + int64_t(u) * k.outst[x]) return false;
+        k.ts[i] = uint8_t(r.ts);
+        k.te[i] = uint8_t(r.te);
     }
+    k.row0[nph] = int16_t(rows.size());
+    k.nph = int16_t(nph);
+    k.nrows = int16_t(rows.size());
+    return true;
 }
 
 bool rows_ok(const std::vector<KRow>& rows) {
@@ -241,8 +301,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     }
     IgemmParams p;
     memset(&p, 0, sizeof(p));
-    fill_axis(p.ah, rh);
-    fill_axis(p.aw, rw);
+    if (!fill_axis(p.ah, rh) || !fill_axis(p.aw, rw)) return CKS_ERR_UNSUPPORTED;
     p.out = out;
     p.rows_h = int(rh.size());
     p.nph_w = int(cfg.wph_cnt.size());
@@ -286,7 +345,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.fd_kc = make_fastdiv(uint32_t(cfg.kc_blocks));
     p.num_tiles = cfg.tiles;
     p.dbg = debug_flags();
-    if (const char* tp = getenv("CKS_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(strtoull(tp, nullptr, 0));
+#ifdef CKS_EXPERIMENTS
+    // debug timeline (tools/trace_op.py); absent from the production library
+    if (const char* tp = cks_knob("CKS_TRACE_PTR")) p.trace = reinterpret_cast<unsigned long long*>(strtoull(tp, nullptr, 0));
+#endif
     // shared memory: A-position ring (16 KB slots) + B-row ring (all taps of a filter row)
     p.a_stages = cfg.a_stages;
     p.b_stages = cfg.stages;

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 namespace cks {
 
@@ -116,7 +118,8 @@ std::vector<KRow> krows_deconv(const Axis& a) {
     return r;
 }
 
-// Experiment knobs (tools/ sweeps only; all unset in production), read once
+// Experiment knobs (tools/ sweeps only; compiled in only with -DCKS_EXPERIMENTS,
+// i.e. the separate libcks_exp.so that CKS_EXPERIMENTS=1 builds and loads), read once
 // per process: CKS_IGEMM_CFG="BN,PBW,Z[,APOS,BSTAGES]" overrides the tile
 // heuristic, CKS_IGEMM_KB caps the K-block bytes, CKS_EPI_STAGE=0 /
 // CKS_UNIFIED=0 disable the coalesced epilogue / unified stage barriers,
@@ -127,24 +130,24 @@ struct Knobs {
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
         gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1;
     Knobs() {
-        if (const char* e = getenv("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
-        if (const char* e = getenv("CKS_IGEMM_KB")) kb = atoi(e);
-        if (const char* e = getenv("CKS_EPI_STAGE")) epi = atoi(e) != 0;
-        if (const char* e = getenv("CKS_UNIFIED")) unified = atoi(e) != 0;
-        if (const char* e = getenv("CKS_MCAST")) mcast = atoi(e) == 1;
-        if (const char* e = getenv("CKS_WGRAD_KIMG")) kimg128 = atoi(e) == 128;
-        if (const char* e = getenv("CKS_IGEMM_ZC")) zc = atoi(e) != 0;  // 0: legacy global split-K
+        if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
+        if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
+        if (const char* e = cks_knob("CKS_EPI_STAGE")) epi = atoi(e) != 0;
+        if (const char* e = cks_knob("CKS_UNIFIED")) unified = atoi(e) != 0;
+        if (const char* e = cks_knob("CKS_MCAST")) mcast = atoi(e) == 1;
+        if (const char* e = cks_knob("CKS_WGRAD_KIMG")) kimg128 = atoi(e) == 128;
+        if (const char* e = cks_knob("CKS_IGEMM_ZC")) zc = atoi(e) != 0;  // 0: legacy global split-K
         // 1: 8 epilogue warps where free, 2: always (measured: no gain, tools/ab.sh) -- experiments
-        if (const char* e = getenv("CKS_EPI8")) epi8 = atoi(e);
-        if (const char* e = getenv("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
-        if (const char* e = getenv("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
-        if (const char* e = getenv("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
-        if (const char* e = getenv("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
+        if (const char* e = cks_knob("CKS_EPI8")) epi8 = atoi(e);
+        if (const char* e = cks_knob("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
+        if (const char* e = cks_knob("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
+        if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
+        if (const char* e = cks_knob("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
         // wave of clusters; 2 (default): also shrink G_Z (to >= 3/4) to a size that fits
-        if (const char* e = getenv("CKS_WGRAD_ZC")) wzc = atoi(e);
-        if (const char* e = getenv("CKS_EPI_BUFS")) epi_bufs = atoi(e) == 2 ? 2 : 1;  // TMA-store staging depth
-        if (const char* e = getenv("CKS_WGRAD_A1")) wa1 = atoi(e) != 0;  // O_C <= 64: one dY atom per stage
+        if (const char* e = cks_knob("CKS_WGRAD_ZC")) wzc = atoi(e);
+        if (const char* e = cks_knob("CKS_EPI_BUFS")) epi_bufs = atoi(e) == 2 ? 2 : 1;  // TMA-store staging depth
+        if (const char* e = cks_knob("CKS_WGRAD_A1")) wa1 = atoi(e) != 0;  // O_C <= 64: one dY atom per stage
     }
 };
 static const Knobs& knobs() {
@@ -334,13 +337,13 @@ static int64_t max_window(const std::vector<KRow>& rows) {
     return m;
 }
 
-IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms) {
+static IgemmCfg igemm_cfg_fwd_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
     Axis ah = axis_h(g), aw = axis_w(g);
     auto rh = krows_fwd(ah);
     return igemm_cfg(ah.O, {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt), max_window(rh), g.FW, g.sw, num_sms);
 }
 
-IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
+static IgemmCfg igemm_cfg_deconv_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
     Axis ah = axis_h(g), aw = axis_w(g);
     auto rh = krows_deconv(ah);
     std::vector<int64_t> cnt;
@@ -436,7 +439,7 @@ static void row_spread(std::vector<RowClassH>& cls, int64_t total, const std::ve
 
 // Narrow ConvV2: tile = R output rows x one column x 128 images x all OC,
 // the class's filter rows resident in shared memory.
-RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
+static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
     RowCfg c;
     if (!row_setup(g, dt, c) || g.OC > (dt == CKS_TF32 ? 128 : 256)) return c;  // instantiated BN range
     c.BN = 32;
@@ -526,7 +529,7 @@ int64_t row_wgrad_padding_macs(const cks_geom& g, cks_dtype dt) {
 // Narrow Sk-dilated: M = (fh, e) rows, 128/JB filter rows per M-block; N = OC
 // block; K = (oh, column, 64 images) of one column class, split into
 // segments; every segment of every class is one G_Z map-reduce partial.
-RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     RowCfg c;
     if (!row_setup(g, dt, c)) return c;
     if (dt == CKS_TF32) {  // MN-major tf32 needs the 128-byte (BASE32B) swizzle
@@ -609,7 +612,7 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
 // bounds it above by the SM count.  Here: enough segments that the
 // taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
 // with at least 4 K-blocks (256 images*positions) per segment.
-WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     WgradCfg c;
     RowCfg rc = row_cfg_wgrad(g, dt, gz_req, num_sms);
     if (rc.ok) {
@@ -717,7 +720,7 @@ size_t ks_split_bytes(const cks_geom& g, cks_dtype dt) {
 
 static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
-WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms) {
+static WsLayout ws_layout_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms) {
     WsLayout L;
     const int64_t eb = elem_bytes(dt);
     const int64_t Cp = pad_ch(g.C, dt), OCp = pad_ch(g.OC, dt);
@@ -756,4 +759,62 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
     return L;
 }
 
+}  // namespace cks
+
+// ---------------------------------------------------------------- plan cache
+// The paper pre-computes its index tables once; here every plan
+// decision (tile configuration, G_Z, workspace layout) is computed once per
+// (geometry, dtype, op, G_Z request, SM count) and served from a thread-safe
+// cache afterwards, so a training loop's repeated calls skip the planning.
+namespace cks {
+namespace {
+std::string plan_key(const cks_geom& g, int a, int b, int c, int d) {
+    const int64_t v[17] = {g.N, g.C, g.H, g.W, g.OC, g.FH, g.FW, g.sh, g.sw, g.ph, g.pw, g.dh, g.dw, a, b, c, d};
+    return std::string(reinterpret_cast<const char*>(v), sizeof(v));
+}
+template <class V>
+struct PlanMemo {
+    std::mutex mu;
+    std::unordered_map<std::string, V> m;
+    template <class F>
+    V get(const std::string& k, F&& make) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = m.find(k);
+            if (it != m.end()) return it->second;
+        }
+        V v = make();  // computed outside the lock (pure function of the key)
+        std::lock_guard<std::mutex> lk(mu);
+        if (m.size() >= 4096) m.clear();  // bounded
+        m.emplace(k, v);
+        return v;
+    }
+};
+}  // namespace
+
+IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms) {
+    static PlanMemo<IgemmCfg> memo;
+    return memo.get(plan_key(g, dt, 0, 0, num_sms), [&] { return igemm_cfg_fwd_plan(g, dt, num_sms); });
+}
+IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
+    static PlanMemo<IgemmCfg> memo;
+    return memo.get(plan_key(g, dt, 1, 0, num_sms), [&] { return igemm_cfg_deconv_plan(g, dt, num_sms); });
+}
+RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
+    static PlanMemo<RowCfg> memo;
+    return memo.get(plan_key(g, dt, 0, 0, 0), [&] { return row_cfg_fwd_plan(g, dt); });
+}
+RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+    static PlanMemo<RowCfg> memo;
+    return memo.get(plan_key(g, dt, 2, gz_req, num_sms), [&] { return row_cfg_wgrad_plan(g, dt, gz_req, num_sms); });
+}
+WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+    static PlanMemo<WgradCfg> memo;
+    return memo.get(plan_key(g, dt, 2, gz_req, num_sms), [&] { return wgrad_cfg_plan(g, dt, gz_req, num_sms); });
+}
+WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms) {
+    static PlanMemo<WsLayout> memo;
+    return memo.get(plan_key(g, dt, int(op), gz * 2 + (c_packed_given ? 1 : 0), num_sms),
+                    [&] { return ws_layout_plan(g, dt, op, gz, c_packed_given, num_sms); });
+}
 }  // namespace cks

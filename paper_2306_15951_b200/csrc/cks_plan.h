@@ -7,12 +7,21 @@
 // enumeration (tests/test_plan_abi.py).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "../../include/cks.h"
 
 namespace cks {
+
+// Experiment knob: getenv(name) in the experiments build (-DCKS_EXPERIMENTS,
+// libcks_exp.so), nullptr in the production library (no environment reads).
+#ifdef CKS_EXPERIMENTS
+inline const char* cks_knob(const char* name) { return getenv(name); }
+#else
+constexpr const char* cks_knob(const char*) { return nullptr; }
+#endif
 
 // Mathematical floor / ceil division (correct for negative numerators; C++
 // '/' truncates toward zero, and oh_s can be -1 -- SURVEY.md §7 hard part 6).

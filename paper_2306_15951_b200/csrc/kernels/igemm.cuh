@@ -71,8 +71,23 @@ struct KAxis {
     uint8_t phase[CKS_MAX_ROWS];
 };
 
+// Kernel-parameter form of an axis table: the trimmed windows per row and,
+// per phase, the affine row -> (A coordinate of tap 0, output coordinate) maps
+// (T1: a0 = o*s - p, out = o; T2 phase y: a0 = oh_s = u + a_y,
+// out = u*sh + ih_s).  Expanded into the KAxis table in shared memory at
+// kernel start; keeps the launch parameters (with the three tensor maps)
+// under the 4 KB classic kernel-parameter limit.
+constexpr int kMaxPhases = 16;
+struct KAxisC {
+    uint8_t ts[CKS_MAX_ROWS], te[CKS_MAX_ROWS];
+    int16_t row0[kMaxPhases + 1];  // run x (one phase) holds rows [row0[x], row0[x+1])
+    int16_t a00[kMaxPhases], a0st[kMaxPhases], out0[kMaxPhases], outst[kMaxPhases];
+    int16_t phid[kMaxPhases];      // phase index of run x (phases without rows have no run)
+    int16_t nph, nrows;
+};
+
 struct IgemmParams {
-    KAxis ah, aw;
+    KAxisC ah, aw;
     float* out;
     float* part;  // split-K partials [out_tiles][Z][PBW*BN/4][128 rows][4] (coalesced per warp)
     int* sem;     // split-K arrival counters [out_tiles] (zero on entry, left zero)
@@ -262,10 +277,19 @@ __global__ void __launch_bounds__(384, 1)
     int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));
     // epilogue staging (p.epi_stage): 4 x 4 KB, 1 KB aligned (128B-swizzled TMA-store source)
     float* epi = reinterpret_cast<float*>(smem + ((ptx::smem_u32(prog + 2 * kProgSlot) - ptx::smem_u32(smem) + 1023u) & ~1023u));
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(&p.ah);
-        uint4* dst = reinterpret_cast<uint4*>(tab);
-        for (int i = threadIdx.x; i < int(2 * sizeof(KAxis) / 16); i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < 2 * CKS_MAX_ROWS; i += blockDim.x) {
+        const KAxisC& ax = i < CKS_MAX_ROWS ? p.ah : p.aw;
+        KAxis& t = tab[i < CKS_MAX_ROWS ? 0 : 1];
+        const int r = i & (CKS_MAX_ROWS - 1);
+        int x = 0;
+        while (x + 1 < ax.nph && ax.row0[x + 1] <= r) ++x;
+        const int u = r - ax.row0[x];
+        const bool v = r < ax.nrows;
+        t.a0[r] = v ? int16_t(ax.a00[x] + u * ax.a0st[x]) : int16_t(0);
+        t.out[r] = v ? int16_t(ax.out0[x] + u * ax.outst[x]) : int16_t(0);
+        t.ts[r] = v ? ax.ts[r] : uint8_t(0);
+        t.te[r] = v ? ax.te[r] : uint8_t(0);
+        t.phase[r] = v ? uint8_t(ax.phid[x]) : uint8_t(0);
     }
 
     if (threadIdx.x == 0) trace_gt(p, 0);

@@ -1,6 +1,10 @@
+#!/bin/bash
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/g1_smi.txt
-timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/g1_pytest.log 2>&1
-timeout 300 python bench.py --config 2 --steps 20 --no-cpu-baseline --layers > gpurun_out/g1_c3.json 2> gpurun_out/g1_c3.err
-timeout 300 python bench.py --config 2 --dtype tf32 --steps 10 --no-cpu-baseline --layers > gpurun_out/g1_c3tf32.json 2> gpurun_out/g1_c3tf32.err
-timeout 300 python bench.py --steps 50 --no-cpu-baseline > gpurun_out/g1_c2.json 2> gpurun_out/g1_c2.err
+T=${1:-x}
+for v in eager g1 g2; do
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_probe_$v.csv \
+     python tools/ncu_graph_probe.py $v > gpurun_out/${T}_probe_$v.log 2>&1
+done
+timeout 300 ncu --graph-profiling graph --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_probe_g2graph.csv \
+     python tools/ncu_graph_probe.py g2 > gpurun_out/${T}_probe_g2graph.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_grid.py -q -x > gpurun_out/${T}_pytest.log 2>&1

@@ -8,12 +8,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from bench import LayerBufs  # noqa: E402
+from paper_2306_15951_b200 import build  # noqa: E402
 from cks_synth import get_config  # noqa: E402
 
 
 def main():
     cfg, name, op = int(sys.argv[1]), sys.argv[2], sys.argv[3]
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+    build.build()  # libcks.so, or libcks_exp.so under CKS_EXPERIMENTS=1 (knob sweeps)
     desc, layers = get_config(cfg)
     idx = [l.name for l in layers].index(name)
     b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0))

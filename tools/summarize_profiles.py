@@ -1,6 +1,8 @@
 """Summarise ncu artefacts from gpurun_out/ into committed profiles/.
 
-usage: python tools/summarize_profiles.py TAG
+usage: python tools/summarize_profiles.py TAG [WORKLOAD_KEY]
+  (WORKLOAD_KEY, e.g. config4/tf32: the bench workload the traffic list was
+   taken on; bench.py looks the dominant kernel's traffic up under it)
   reads  gpurun_out/launches_TAG.csv        (ncu --metrics gpu__time_duration.sum list)
          gpurun_out/traffic_TAG.csv         (optional: dram bytes per launch, all launches)
          gpurun_out/prof_TAG_*.ncu-rep      (ncu --set full captures)
@@ -85,7 +87,7 @@ def num(d, k):
     return x * scale.get(u, 1)
 
 
-def main(tag):
+def main(tag, key="config4/tf32"):
     os.makedirs(PROF, exist_ok=True)
     md = [f"# ncu summary -- round {tag}\n",
           "Captured on one B200 with `--clock-control none` (see tools/ncu_full.sh, bench.py).  ncu times are",
@@ -143,10 +145,17 @@ def main(tag):
     with open(os.path.join(PROF, f"ncu_summary_{tag}.md"), "w") as f:
         f.write("\n".join(md) + "\n")
     if traffic:
-        with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
-            json.dump({k.split("_kernel")[0] + "_kernel": v for k, v in traffic.items()}, f, indent=1)
+        tj = os.path.join(PROF, "ncu_traffic.json")
+        try:
+            allt = json.load(open(tj))
+        except Exception:
+            allt = {}
+        allt = {k: v for k, v in allt.items() if "/" in k}  # drop the round-1 flat layout
+        allt[key] = {k.split("_kernel")[0] + "_kernel": v for k, v in traffic.items()}
+        with open(tj, "w") as f:
+            json.dump(allt, f, indent=1)
     print("\n".join(md))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r02", *sys.argv[2:3])

@@ -1,4 +1,5 @@
 #!/bin/bash
+export CKS_EXPERIMENTS=1  # environment knobs live only in the experiments build (libcks_exp.so)
 # usage: tools/sweep_zc.sh CONFIG OP -- every layer: default plan, legacy split-K off/on,
 # and forced cluster split-K configs (CKS_IGEMM_CFG="BN,PBW,Z", 0 = default)
 echo "== default"; python tools/time_op.py $1 $2 all 20 2>&1 | awk '{print $1, $3}'

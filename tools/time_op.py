@@ -7,6 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from bench import LayerBufs  # noqa: E402
+from paper_2306_15951_b200 import build  # noqa: E402
 from cks_synth import get_config  # noqa: E402
 
 
@@ -14,6 +15,7 @@ def main():
     cfg, op = int(sys.argv[1]), sys.argv[2]
     names = sys.argv[3].split(",") if sys.argv[3] != "all" else None
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 50
+    build.build()  # libcks.so, or libcks_exp.so under CKS_EXPERIMENTS=1 (knob sweeps)
     desc, layers = get_config(cfg)
     s = torch.cuda.current_stream()
     for idx, lay in enumerate(layers):

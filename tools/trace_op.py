@@ -3,7 +3,12 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["CKS_EXPERIMENTS"] = "1"  # the debug timeline exists only in the experiments build
 import torch  # noqa: E402
+
+from paper_2306_15951_b200 import build  # noqa: E402
+
+build.build()
 
 from bench import LayerBufs  # noqa: E402
 from cks_synth import get_config  # noqa: E402
