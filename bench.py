@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--dtype", choices=("bf16", "tf32"), default="tf32",
                     help="headline: fp32 inputs multiplied as TF32 (the paper computes in fp32, P:262), or bf16 "
                          "inputs; fp32 accumulate and outputs either way")
+    ap.add_argument("--allreduce", choices=("nccl", "fused"), default="nccl",
+                    help="N > 1: dW sum by bucketed NCCL all_reduce in the step graph, or fused into the Sk-dilated "
+                         "G_Z reduce (KB-REDUCE-AR over NVLink peer memory, CUDA IPC)")
     ap.add_argument("--companion", choices=("bf16", "tf32", "none"), default="bf16",
                     help="also time the step in this input precision and report it beside the headline")
     return ap.parse_args()
@@ -278,8 +281,13 @@ class LayerBufs:
             "fwd": L.cks_launch_count(g, self.dt, L.CKS_OP_FWD),
             "split": 1,
             "deconv": L.cks_launch_count(g, self.dt, L.CKS_OP_DECONV, c_packed_given=True),
+            "deconv_w": L.cks_launch_count(g, self.dt, L.CKS_OP_DECONV),
             "wgrad": L.cks_launch_count(g, self.dt, L.CKS_OP_WGRAD),
         }
+        # KS-deconv without Stage1 (the GEMM reads W directly) where the library's
+        # policy takes it; eligible: W rows of a 16-byte multiple, sw <= 8
+        self.direct = "deconv" in lay.ops and L.plan_dict(g, self.dt, L.CKS_OP_DECONV).get("ks_direct") == "1"
+        self.direct_ok = "deconv" in lay.ops and (lay.C * eb) % 16 == 0 and lay.sw <= 8
 
     def run_split(self, stream_ptr):
         self.L.cks_ks_split(self.g, self.dt, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
@@ -288,6 +296,17 @@ class LayerBufs:
         L, g = self.L, self.g
         if op == "split":  # Stage1 alone
             L.cks_ks_split(g, self.dt, self.W.data_ptr(), self.cp.data_ptr(), stream_ptr)
+            return
+        if op in ("deconv_w", "deconv_free"):  # W given: library policy / forced Stage1-free
+            ws = self.ws["deconv"]
+            L.cks_deconv2d_ex(g, self.dt, self.G.data_ptr(), self.W.data_ptr(), None, self.dX.data_ptr(),
+                              ws.data_ptr(), ws.numel(), stream_ptr,
+                              L.CKS_KS_AUTO if op == "deconv_w" else L.CKS_KS_STAGE1_FREE)
+            return
+        if op == "wgrad_ar":  # Sk-dilated + G_Z and cross-rank reduce in one kernel (KB-REDUCE-AR)
+            ws = self.ws["wgrad_ar"]
+            L.cks_dilated_wgrad_allreduce(g, self.dt, self.X.data_ptr(), self.G.data_ptr(), self.dW.data_ptr(), 0,
+                                          ws.data_ptr(), ws.numel(), self.ar_grp, stream_ptr)
             return
         if op == "deconv_only":  # Stage2&3 from the already split sub-filters
             ws = self.ws["deconv"]
@@ -316,7 +335,7 @@ def op_kernel(b, op):
     op's time includes its staging kernels: G_Z reduce, channel padding)."""
     if op == "split":
         return "ks_split_kernel"
-    code = {"fwd": 0, "deconv_only": 1, "deconv": 1, "wgrad": 2}[op]
+    code = {"fwd": 0, "deconv_only": 1, "deconv": 1, "deconv_w": 1, "deconv_free": 1, "wgrad": 2, "wgrad_ar": 2}[op]
     kind = b.L.plan_dict(b.g, b.dt, code)["kind"]
     return KIND_KERNEL.get(kind, kind)
 
@@ -348,16 +367,34 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
     for b, s in zip(bufs, sizes):
         b.dW = flat[off:off + s].view(b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C)
         off += s
+    fused_ar = use_dist and args.allreduce == "fused"
+    if fused_ar:  # per-layer KB-REDUCE-AR groups: peers' buffers mapped over CUDA IPC
+        from paper_2306_15951_b200.dist import FusedWgradAllReduce
+        far = FusedWgradAllReduce([b.g for b in bufs], [b.dW for b in bufs], device)
+        for i, b in enumerate(bufs):
+            b.ar_grp = far.group(i)
+            n = b.L.cks_workspace_size(b.g, b.dt, b.L.CKS_OP_WGRAD_AR)
+            b.ws["wgrad_ar"] = torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+            b.launches["wgrad_ar"] = b.L.cks_launch_count(b.g, b.dt, b.L.CKS_OP_WGRAD_AR)
     ops_seq = []
     for i, b in enumerate(bufs):
         for op in ("fwd", "deconv", "wgrad"):
             if op in b.lay.ops:
+                if op == "wgrad" and fused_ar:
+                    ops_seq.append((i, "wgrad_ar"))
+                    continue
+                if op == "deconv" and b.direct:  # Stage1-free KS-deconv (no split)
+                    ops_seq.append((i, "deconv_w"))
+                    continue
                 if op == "deconv":
                     ops_seq.append((i, "split"))
                 ops_seq.append((i, "deconv_only" if op == "deconv" else op))
-    OPF = {"fwd": "fwd", "deconv_only": "deconv", "wgrad": "wgrad", "split": "split"}
+    OPF = {"fwd": "fwd", "deconv_only": "deconv", "deconv_w": "deconv", "wgrad": "wgrad", "wgrad_ar": "wgrad",
+           "split": "split"}
+    LKEY = {"fwd": "fwd", "deconv_only": "deconv", "deconv_w": "deconv_w", "wgrad": "wgrad", "wgrad_ar": "wgrad_ar",
+            "split": "split"}
     flops_step = sum(bufs[i].flops for i, op in ops_seq if op != "split")
-    launches_step = sum(bufs[i].launches[OPF[op]] for i, op in ops_seq)
+    launches_step = sum(bufs[i].launches[LKEY[op]] for i, op in ops_seq)
     kern = {(i, op): op_kernel(bufs[i], op) for i, op in ops_seq}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=device)  # 256 MB > 126 MB L2
     peaks = load_peaks()
@@ -421,8 +458,8 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
         buckets.append((offs[min(layers_k)], offs[max(layers_k) + 1]))
         k0 = k1 + 1
     last_of_bucket = {order[k1]: bi for bi, k1 in enumerate(cuts)}
-    ar_in_graph = os.environ.get("CKS_BENCH_AR_GRAPH", "1") == "1"
-    if use_dist:
+    ar_in_graph = os.environ.get("CKS_BENCH_AR_GRAPH", "1") == "1" or fused_ar
+    if use_dist and not fused_ar:
         s3.wait_stream(stream)
         with torch.cuda.stream(s3):  # communicator warm-up on the capture-side stream
             dist.all_reduce(flat)
@@ -458,7 +495,7 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
                 w.wait_event(fork)
             with torch.cuda.stream(s1):
                 for i, b in enumerate(bufs):
-                    if "deconv" in b.lay.ops:
+                    if "deconv" in b.lay.ops and not b.direct:
                         run(i, "split", s1)
                 split_done = torch.cuda.Event()
                 split_done.record(s1)
@@ -474,8 +511,8 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
                 if "wgrad" in b.lay.ops:
                     ws_k.wait_event(ev)
                     with torch.cuda.stream(ws_k):
-                        run(i, "wgrad", ws_k)
-                if use_dist and ar_graph and i in last_of_bucket:
+                        run(i, "wgrad_ar" if fused_ar else "wgrad", ws_k)
+                if use_dist and not fused_ar and ar_graph and i in last_of_bucket:
                     for w in wst:  # this bucket's dW is complete: NCCL all_reduce on s3
                         done = torch.cuda.Event()
                         done.record(w)
@@ -484,8 +521,8 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
                     with torch.cuda.stream(s3):
                         dist.all_reduce(flat[lo:hi])
                 if "deconv" in b.lay.ops:
-                    run(i, "deconv_only", main)
-            for w in wst + ([s3] if use_dist and ar_graph else []):
+                    run(i, "deconv_w" if b.direct else "deconv_only", main)
+            for w in wst + ([s3] if use_dist and not fused_ar and ar_graph else []):
                 join = torch.cuda.Event()
                 join.record(w)
                 main.wait_event(join)
@@ -507,7 +544,7 @@ def measure(args, torch, dist, device, rank, local, n_gpus, use_dist, dtype, hea
 
     def replay(g):
         g.replay()
-        if use_dist and not ar_in_graph:  # fallback: one all_reduce after the step
+        if use_dist and not fused_ar and not ar_in_graph:  # fallback: one all_reduce after the step
             dist.all_reduce(flat)
 
     t_start = torch.cuda.Event(enable_timing=True)
@@ -682,7 +719,9 @@ def run_gpu(args):
                    "parallelism": f"dp{n_gpus}",
                    "schedule": "fwd chain || KS Stage1 splits; reverse deconv chain || per-layer wgrad on %d "
                                "alternating streams (CUDA graph)" % m["nws"]
-                               + (("; dW all_reduce in %d buckets overlapping the backward (NCCL in the graph)"
+                               + (("; dW summed across ranks inside each layer's Sk-dilated G_Z reduce "
+                                   "(KB-REDUCE-AR, NVLink P2P, CUDA IPC)") if use_dist and args.allreduce == "fused" else
+                                  ("; dW all_reduce in %d buckets overlapping the backward (NCCL in the graph)"
                                    % m["buckets"] if m["ar_in_graph"] else "; dW all_reduce after the step graph")
                                   if use_dist else ""),
                    "serialized_step_ms_per_op_protocol": round(m["serialized_ms"], 5)},
@@ -692,6 +731,10 @@ def run_gpu(args):
     # ---- the zero-inserted / zero-padded formulation on the same kernels
     if not args.no_zins and n_gpus == 1:
         line["zins"] = run_zins(torch, bufs, max(3, min(args.steps, 20)), device, m["flush"], m["fam_ms"], args.layers)
+    # ---- Stage1-free vs Stage1 KS-deconv on every eligible layer
+    if not args.no_zins and n_gpus == 1:
+        line["ks_stage1_free"] = run_ks_compare(torch, bufs, max(3, min(args.steps, 20)), device, m["flush"],
+                                                args.layers)
     # ---- e2e through the public API with host buffers
     if not args.no_e2e:
         line["e2e"] = run_e2e(torch, dist, bufs, m["ops_seq"], m["flops_step"], n_gpus, max(2, min(args.steps, 10)),
@@ -709,6 +752,9 @@ def run_gpu(args):
                                 "clocks": c["clocks"],
                                 "per_layer": [{k: r[k] for k in ("layer", "op", "us", "tflops", "frac")}
                                               for r in c["per_layer"]]}
+        if not args.no_zins and n_gpus == 1:
+            line[args.companion]["ks_stage1_free"] = run_ks_compare(torch, c["bufs"], max(3, min(args.steps, 20)),
+                                                                    device, c["flush"], args.layers)
         del c
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
@@ -723,6 +769,56 @@ def run_gpu(args):
     if use_dist:
         dist.destroy_process_group()
     return 0
+
+
+def run_ks_compare(torch, bufs, steps, device, flush, per_layer):
+    """Stage1-free KS-deconv (the GEMM reads W directly)
+    against KB-SPLIT + KB-KS (Stage1 every step, then Stage2&3), per eligible
+    layer: one serialized graph with event nodes, L2 flushed per replay."""
+    seq = []
+    for i, b in enumerate(bufs):
+        if b.direct_ok:
+            seq += [(i, "split"), (i, "deconv_only"), (i, "deconv_free")]
+    if not seq:
+        return None
+    stream = torch.cuda.Stream(device)
+    with torch.cuda.stream(stream):
+        for i, op in seq:
+            bufs[i].run(op, stream.cuda_stream)
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(seq) + 1)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        sp = torch.cuda.current_stream().cuda_stream
+        for k, (i, op) in enumerate(seq):
+            evs[k].record()
+            bufs[i].run(op, sp)
+        evs[-1].record()
+    acc = [0.0] * len(seq)
+    with torch.cuda.stream(stream):
+        for it in range(steps + 2):
+            flush.fill_(float(it))
+            graph.replay()
+            stream.synchronize()
+            if it >= 2:
+                for k in range(len(seq)):
+                    acc[k] += evs[k].elapsed_time(evs[k + 1]) / steps
+    rows, tot_s1, tot_free = [], 0.0, 0.0
+    for k in range(0, len(seq), 3):
+        i = seq[k][0]
+        s1 = acc[k] + acc[k + 1]
+        fr = acc[k + 2]
+        tot_s1 += s1
+        tot_free += fr
+        rows.append({"layer": bufs[i].lay.name, "stage1_plus_ks_us": round(s1 * 1e3, 2),
+                     "split_us": round(acc[k] * 1e3, 2), "stage1_free_us": round(fr * 1e3, 2),
+                     "policy": "stage1_free" if bufs[i].direct else "stage1"})
+        if per_layer:
+            print(f"  ks {bufs[i].lay.name:22s} split+ks {s1 * 1e3:8.2f} us  stage1-free {fr * 1e3:8.2f} us"
+                  f"  ({rows[-1]['policy']})", file=sys.stderr)
+    return {"what": "KS-deconv with Stage1 (KB-SPLIT + KB-KS) vs Stage1-free (W read directly by the GEMM), "
+                    "serialized graph, L2 flushed", "ms_stage1_plus_ks": round(tot_s1, 5),
+            "ms_stage1_free": round(tot_free, 5), "layers": rows, "steps": steps}
 
 
 def run_zins(torch, bufs, steps, device, flush, cks_ms, per_layer):

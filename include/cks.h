@@ -126,6 +126,24 @@ cks_status cks_ks_split(const cks_geom* g, cks_dtype dt, const void* w, void* c_
 cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w,
                         const void* c_packed, float* dx, void* ws, size_t ws_bytes, void* stream);
 
+/* cks_deconv2d with an explicit Stage1 choice when w is given (c_packed NULL):
+ *   CKS_KS_AUTO          the library's policy (what cks_deconv2d does);
+ *   CKS_KS_STAGE1_FREE   no Stage1: the implicit GEMM reads W itself, per
+ *                        sub-filter row one TMA box of the taps
+ *                        fw = x, x+sw, ... of filter row
+ *                        fh = y + (CH_y-1-ch)*sh (the all-in-one variant of
+ *                        P:186); requires W rows of a
+ *                        16-byte multiple (C*elem % 16 == 0) and sw <= 8, else
+ *                        CKS_ERR_UNSUPPORTED;
+ *   CKS_KS_STAGE1        Stage1 (cks_ks_split) into ws, then Stage2&3.
+ * Same results in every mode (the same sums; only the B operand's source
+ * differs).  With c_packed given the mode must be AUTO or STAGE1.  ws as
+ * queried by cks_workspace_size(CKS_OP_DECONV) covers every mode. */
+typedef enum { CKS_KS_AUTO = 0, CKS_KS_STAGE1_FREE = 1, CKS_KS_STAGE1 = 2 } cks_ks_mode;
+cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, const void* w,
+                           const void* c_packed, float* dx, void* ws, size_t ws_bytes, void* stream,
+                           cks_ks_mode mode);
+
 /* Eq (3) via Sk-dilated-V2 (Alg. 3/3B P:445): dW[oc,fh,fw,ic] = sum over
  * n and the TRIMMED (oh, ow) range [oh_s, oh_e) x [ow_s, ow_e) of
  * X[n, oh*sh+fh-ph, ow*sw+fw-pw, ic] * dY[n,oh,ow,oc]: leaping access into X
@@ -215,6 +233,60 @@ cks_status cks_zins_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, co
                              void* ws, size_t ws_bytes, void* stream);
 cks_status cks_zins_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
                           void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------- fused wgrad + all-reduce
+ * Sk-dilated on this rank's batch shard followed by ONE kernel (KB-REDUCE-AR)
+ * that performs the G_Z aggregation AND the sum over the ranks of the
+ * data-parallel group through peer memory (NVLink P2P stores): the batch
+ * shard is the outermost segment of the paper's map-reduce over
+ * G_K = N*O_H*O_W.  Element i of dW is owned by rank
+ * i / slice (slice = ceil(n/4 / world) float4 vectors, n = OC*FH*FW*C):
+ * every rank pushes its aggregated partial of i to the owner's receive
+ * buffer, the owner sums the ranks' contributions in fixed order
+ * q = 0..world-1 and stores the result into every rank's dW.  Results are
+ * bit-identical on every rank and every run.
+ *
+ * cks_ar_group (all device pointers are valid in the CALLING process: peers'
+ * buffers mapped with cks_ipc_import, or plain pointers when every "rank" is
+ * on this device, e.g. tests):
+ *   recv[t]   rank t's receive buffer, cks_ar_recv_bytes() bytes;
+ *   out[t]    rank t's dW (out[rank] must equal dw);
+ *   flag[t]   rank t's two signal words (zeroed once; they count up);
+ *   count     this rank's three words: two CTA arrival counters and the
+ *             call sequence number (zeroed once; kept on the device, so a
+ *             CUDA graph that replays the call stays in step);
+ *   err       set to 1 (never cleared by the library) if a peer's signal did
+ *             not arrive within a bounded wait -- the kernel then finishes
+ *             (no hang) and dW is invalid.
+ * One (flag, count) set per call site: calls sharing them must be issued in
+ * the same order on every rank.
+ * Requires world <= CKS_AR_MAX_RANKS, n % 4 == 0.  ws: cks_workspace_size
+ * with op CKS_OP_WGRAD_AR.  Every rank must make the call (same geometry);
+ * the call returns once the kernels are queued. */
+#define CKS_AR_MAX_RANKS 8
+#define CKS_OP_WGRAD_AR 3
+typedef struct cks_ar_group {
+    int32_t world, rank;
+    int32_t ctas;  /* KB-REDUCE-AR grid cap (0: library choice); every CTA may spin at the barriers */
+    void* recv[CKS_AR_MAX_RANKS];
+    float* out[CKS_AR_MAX_RANKS];
+    uint32_t* flag[CKS_AR_MAX_RANKS];
+    uint32_t* count;
+    int32_t* err;
+} cks_ar_group;
+cks_status cks_ar_recv_bytes(const cks_geom* g, int32_t world, size_t* bytes);
+cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
+                                       int gz, void* ws, size_t ws_bytes, const cks_ar_group* grp, void* stream);
+
+/* CUDA IPC for the group's buffers (setup, not the hot path): export a
+ * device pointer of this process as an opaque 72-byte handle (64-byte
+ * cudaIpcMemHandle_t + 8-byte offset of ptr inside its allocation), import a
+ * peer process's handle as a pointer valid here (peer access enabled), and
+ * release it. */
+typedef struct cks_ipc_handle { unsigned char bytes[72]; } cks_ipc_handle;
+cks_status cks_ipc_export(const void* ptr, cks_ipc_handle* h);
+cks_status cks_ipc_import(const cks_ipc_handle* h, void** ptr);
+cks_status cks_ipc_close(void* ptr);
 
 const char* cks_status_string(cks_status s);
 int cks_version(void);

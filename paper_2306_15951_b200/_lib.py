@@ -23,8 +23,9 @@ STATUS = {0: "CKS_OK", 1: "CKS_ERR_NULL", 2: "CKS_ERR_GEOMETRY", 3: "CKS_ERR_UNS
 EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2d_fwd", "cks_ks_split_size",
            "cks_ks_split", "cks_deconv2d", "cks_dilated_wgrad", "cks_axis_table", "cks_op_counts",
            "cks_launch_count", "cks_status_string", "cks_version", "cks_zins_workspace_size",
-           "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad", "cks_plan_describe",
-           "cks_padding_macs")
+           "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad", "cks_plan_describe", "cks_deconv2d_ex",
+           "cks_padding_macs", "cks_ar_recv_bytes", "cks_dilated_wgrad_allreduce", "cks_ipc_export",
+           "cks_ipc_import", "cks_ipc_close")
 
 
 class CksError(RuntimeError):
@@ -37,6 +38,21 @@ class cks_geom(C.Structure):
     _fields_ = [("N", C.c_int64), ("C", C.c_int64), ("H", C.c_int64), ("W", C.c_int64), ("OC", C.c_int64),
                 ("FH", C.c_int64), ("FW", C.c_int64), ("sh", C.c_int32), ("sw", C.c_int32), ("ph", C.c_int32),
                 ("pw", C.c_int32), ("dh", C.c_int32), ("dw", C.c_int32)]
+
+
+CKS_AR_MAX_RANKS = 8
+CKS_OP_WGRAD_AR = 3
+
+
+class cks_ar_group(C.Structure):
+    """include/cks.h cks_ar_group: the peers' buffers of one fused wgrad + all-reduce."""
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("ctas", C.c_int32),
+                ("recv", C.c_void_p * CKS_AR_MAX_RANKS), ("out", C.c_void_p * CKS_AR_MAX_RANKS),
+                ("flag", C.c_void_p * CKS_AR_MAX_RANKS), ("count", C.c_void_p), ("err", C.c_void_p)]
+
+
+class cks_ipc_handle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 72)]
 
 
 def make_geom(N, C_, H, W, OC, FH, FW, sh, sw, ph, pw, dh=1, dw=1) -> cks_geom:
@@ -63,6 +79,7 @@ def lib():
             "cks_ks_split_size": (C.c_int, [G, C.c_int, C.POINTER(sz)]),
             "cks_ks_split": (C.c_int, [G, C.c_int, vp, vp, vp]),
             "cks_deconv2d": (C.c_int, [G, C.c_int, vp, vp, vp, vp, vp, sz, vp]),
+            "cks_deconv2d_ex": (C.c_int, [G, C.c_int, vp, vp, vp, vp, vp, sz, vp, C.c_int]),
             "cks_dilated_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, C.c_int, vp, sz, vp]),
             "cks_axis_table": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int,
                                          C.POINTER(C.c_int64), sz, C.POINTER(sz)]),
@@ -74,6 +91,12 @@ def lib():
             "cks_zins_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
             "cks_plan_describe": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.c_char_p, sz, C.POINTER(sz)]),
             "cks_padding_macs": (C.c_int, [G, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+            "cks_ar_recv_bytes": (C.c_int, [G, C.c_int32, C.POINTER(sz)]),
+            "cks_dilated_wgrad_allreduce": (C.c_int, [G, C.c_int, vp, vp, vp, C.c_int, vp, sz,
+                                                      C.POINTER(cks_ar_group), vp]),
+            "cks_ipc_export": (C.c_int, [vp, C.POINTER(cks_ipc_handle)]),
+            "cks_ipc_import": (C.c_int, [C.POINTER(cks_ipc_handle), C.POINTER(vp)]),
+            "cks_ipc_close": (C.c_int, [vp]),
             "cks_status_string": (C.c_char_p, [C.c_int]),
             "cks_version": (C.c_int, []),
         }
@@ -136,6 +159,43 @@ def cks_ks_split(g, dtype, w_ptr, c_ptr, stream):
 def cks_deconv2d(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream):
     _check(lib().cks_deconv2d(C.byref(g), dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream),
            "cks_deconv2d")
+
+
+CKS_KS_AUTO, CKS_KS_STAGE1_FREE, CKS_KS_STAGE1 = 0, 1, 2
+
+
+def cks_deconv2d_ex(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream, mode):
+    _check(lib().cks_deconv2d_ex(C.byref(g), dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream, mode),
+           "cks_deconv2d_ex")
+
+
+def cks_ar_recv_bytes(g: cks_geom, world: int) -> int:
+    v = C.c_size_t()
+    _check(lib().cks_ar_recv_bytes(C.byref(g), world, C.byref(v)), "cks_ar_recv_bytes")
+    return v.value
+
+
+def cks_dilated_wgrad_allreduce(g, dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, grp: cks_ar_group, stream):
+    _check(lib().cks_dilated_wgrad_allreduce(C.byref(g), dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes,
+                                             C.byref(grp), stream), "cks_dilated_wgrad_allreduce")
+
+
+def cks_ipc_export(ptr: int) -> bytes:
+    h = cks_ipc_handle()
+    _check(lib().cks_ipc_export(ptr, C.byref(h)), "cks_ipc_export")
+    return bytes(h.bytes)
+
+
+def cks_ipc_import(handle: bytes) -> int:
+    h = cks_ipc_handle()
+    C.memmove(h.bytes, handle, 72)
+    p = C.c_void_p()
+    _check(lib().cks_ipc_import(C.byref(h), C.byref(p)), "cks_ipc_import")
+    return p.value
+
+
+def cks_ipc_close(ptr: int):
+    _check(lib().cks_ipc_close(ptr), "cks_ipc_close")
 
 
 def cks_dilated_wgrad(g, dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, stream):

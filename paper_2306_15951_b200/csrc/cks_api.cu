@@ -14,6 +14,7 @@
 
 #include "../../include/cks.h"
 #include "cks_plan.h"
+#include "kernels/allreduce.cuh"
 #include "kernels/aux.cuh"
 #include "kernels/igemm.cuh"
 #include "kernels/narrow.cuh"
@@ -80,6 +81,23 @@ CUresult encode_cached(EncodeTiledFn enc, CUtensorMap* m, CUtensorMapDataType dt
     return r;
 }
 
+// cuMemGetAddressRange through the runtime's driver entry point (libcks.so
+// links the static runtime only, not libcuda)
+typedef CUresult (*MemRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+bool mem_range(const void* p, CUdeviceptr* base) {
+    static MemRangeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<MemRangeFn>(f);
+    });
+    size_t size = 0;
+    return fn && fn(base, &size, reinterpret_cast<CUdeviceptr>(p)) == CUDA_SUCCESS;
+}
+
 int device_sms() {
     int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return kPlanSMs;
@@ -89,13 +107,15 @@ int device_sms() {
 
 // rank-4 tiled tensor map, 128B swizzle, zero OOB fill
 bool make_tmap4(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t dims[4], const uint64_t strides_b[3],
-                const uint32_t box[4], int row_bytes = 128, bool atom32 = false) {
+                const uint32_t box[4], int row_bytes = 128, bool atom32 = false, const uint32_t* estr = nullptr) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
     cuuint64_t gs[3] = {strides_b[0], strides_b[1], strides_b[2]};
     cuuint32_t bd[4] = {box[0], box[1], box[2], box[3]};
     cuuint32_t es[4] = {1, 1, 1, 1};
+    if (estr)  // element strides: box[i] = count * estr[i] loads count elements at stride estr[i]
+        for (int i = 0; i < 4; ++i) es[i] = estr[i];
     CUresult r = encode_cached(enc, m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                      const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B  // MN-major tf32 (SWIZZLE_128B_BASE32B)
@@ -126,6 +146,21 @@ bool epi_tma_all() {
         return e ? atoi(e) != 0 : true;
     }();
     return on;
+}
+
+// rank-5 tiled tensor map with element strides (Stage1-free KS-deconv B operand)
+bool make_tmap5(CUtensorMap* m, cks_dtype dt, const void* base, const uint64_t dims[5], const uint64_t strides_b[4],
+                const uint32_t box[5], const uint32_t estr[5]) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t gd[5] = {dims[0], dims[1], dims[2], dims[3], dims[4]};
+    cuuint64_t gs[4] = {strides_b[0], strides_b[1], strides_b[2], strides_b[3]};
+    cuuint32_t bd[5] = {box[0], box[1], box[2], box[3], box[4]};
+    cuuint32_t es[5] = {estr[0], estr[1], estr[2], estr[3], estr[4]};
+    return encode_cached(enc, m, dt == CKS_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                         const_cast<void*>(base), gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         dt == CKS_TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // fp32 output map (TMA store), 128B swizzle
@@ -245,10 +280,10 @@ bool rows_ok(const std::vector<KRow>& rows) {
 }
 
 // ------------------------------------------------------------------ launchers
-template <int BN, bool TF, int KB, bool PAIR = false>
+template <int BN, bool TF, int KB, bool PAIR = false, bool BMN = false>
 cks_status launch_igemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y, const IgemmParams& p,
                           int smem, cudaStream_t st) {
-    auto kern = igemm_kernel<BN, TF, KB, PAIR>;
+    auto kern = igemm_kernel<BN, TF, KB, PAIR, BMN>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     // cluster split-K: one output tile per cluster of zsplit CTAs, one tile per CTA
     const int cl = p.zc ? p.zsplit : (p.pair ? 2 : p.cm);
@@ -273,8 +308,30 @@ cks_status launch_igemm_kb(int BN, const CUtensorMap& a, const CUtensorMap& b, c
     return CKS_ERR_UNSUPPORTED;
 }
 
+template <int BN, bool TF>
+cks_status launch_igemm_bmn(int KB, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y,
+                            const IgemmParams& p, int smem, cudaStream_t st) {
+    if (KB == 32) return launch_igemm_t<BN, TF, 32, false, true>(a, b, y, p, smem, st);
+    if (KB == 64) return launch_igemm_t<BN, TF, 64, false, true>(a, b, y, p, smem, st);
+    return launch_igemm_t<BN, TF, 128, false, true>(a, b, y, p, smem, st);
+}
+
 cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& y,
-                        const IgemmParams& p, int smem, cudaStream_t st) {
+                        const IgemmParams& p, int smem, cudaStream_t st, bool bmn = false) {
+    if (bmn) {  // Stage1-free KS-deconv: B = one 128-byte MN atom of W per tap (BN = 64 bf16 / 32 tf32)
+        if (p.pair || p.cm > 1) return CKS_ERR_UNSUPPORTED;
+        if (tf32) {
+            switch (BN) {
+                case 32: return launch_igemm_bmn<32, true>(KB, a, b, y, p, smem, st);
+                case 64: return launch_igemm_bmn<64, true>(KB, a, b, y, p, smem, st);
+                case 128: return launch_igemm_bmn<128, true>(KB, a, b, y, p, smem, st);
+            }
+            return CKS_ERR_UNSUPPORTED;
+        }
+        if (BN == 64) return launch_igemm_bmn<64, false>(KB, a, b, y, p, smem, st);
+        if (BN == 128) return launch_igemm_bmn<128, false>(KB, a, b, y, p, smem, st);
+        return CKS_ERR_UNSUPPORTED;
+    }
     if (p.pair) {  // CTA pairs: bf16, 128 B K blocks, 128 output channels per CTA (plan invariant)
         if (tf32 || KB != 128 || BN != 128) return CKS_ERR_UNSUPPORTED;
         return launch_igemm_t<128, false, 128, true>(a, b, y, p, smem, st);
@@ -292,7 +349,8 @@ cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const C
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
 cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRow>& rh, const std::vector<KRow>& rw,
                      const CUtensorMap& ta, const CUtensorMap& tb, float* out, int out_H, int out_W, int out_C,
-                     int N, int slot_stride, int phases_w, const WsLayout& L, void* ws, cudaStream_t st) {
+                     int N, int slot_stride, int phases_w, const WsLayout& L, void* ws, cudaStream_t st,
+                     const cks_geom* bmn = nullptr) {
     IgemmCfg cfg = cfg_in;
     if (debug_flags() & 16) {  // experiment: no split-K
         cfg.Z = 1;
@@ -382,7 +440,13 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
         uint32_t box[4] = {32, 1, 1, 32};
         if (make_tmap4_f32(&ty, out, d, sb, box)) p.tma_store = (cfg.epi && epi_tma_all()) ? 2 : 1;
     }
-    return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st);
+    if (bmn) {  // Stage1-free: per-phase filter-row origin and sub-filter widths (Alg. 2 Stage1's index map)
+        if (bmn->sh > kMaxPhases || bmn->sw > kMaxPhases) return CKS_ERR_UNSUPPORTED;
+        for (int y = 0; y < bmn->sh; ++y) p.bfh0[y] = int16_t(y + (cdiv(bmn->FH - y, bmn->sh) - 1) * bmn->sh);
+        for (int x = 0; x < bmn->sw; ++x) p.bcw[x] = int16_t(cdiv(bmn->FW - x, bmn->sw));
+        p.bsh = bmn->sh;
+    }
+    return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st, bmn != nullptr);
 }
 
 template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false>
@@ -644,6 +708,8 @@ struct ZinsLayout {
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+// fused wgrad + all-reduce: this rank's dW follows the wgrad scratch in the workspace
+size_t ar_local_offset(const WsLayout& L) { return al256(L.total); }
 
 ZinsLayout zins_layout(const cks_geom& g, cks_dtype dt, cks_op op) {
     ZinsLayout Z;
@@ -751,6 +817,11 @@ cks_status cks_workspace_size(const cks_geom* g, cks_dtype dt, cks_op op, int gz
     if (!g || !bytes) return CKS_ERR_NULL;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
+    if (int(op) == CKS_OP_WGRAD_AR) {  // wgrad scratch + this rank's dW (segments reduced by KB-REDUCE-AR)
+        const WsLayout L = ws_layout(*g, dt, CKS_OP_WGRAD, gz, false, kPlanSMs);
+        *bytes = ar_local_offset(L) + size_t(g->OC * g->FH * g->FW * g->C) * 4;
+        return CKS_OK;
+    }
     if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
     *bytes = ws_layout(*g, dt, op, gz, false, kPlanSMs).total;
     return CKS_OK;
@@ -826,8 +897,15 @@ cks_status cks_ks_split(const cks_geom* g, cks_dtype dt, const void* w, void* c_
 
 cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const void* w, const void* c_packed,
                         float* dx, void* ws, size_t ws_bytes, void* stream) {
+    return cks_deconv2d_ex(g, dt, dy, w, c_packed, dx, ws, ws_bytes, stream, CKS_KS_AUTO);
+}
+
+cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, const void* w, const void* c_packed,
+                           float* dx, void* ws, size_t ws_bytes, void* stream, cks_ks_mode mode) {
     if (!g || !dy || !dx) return CKS_ERR_NULL;
     if ((w == nullptr) == (c_packed == nullptr)) return CKS_ERR_NULL;
+    if (mode != CKS_KS_AUTO && mode != CKS_KS_STAGE1_FREE && mode != CKS_KS_STAGE1) return CKS_ERR_UNSUPPORTED;
+    if (c_packed && mode == CKS_KS_STAGE1_FREE) return CKS_ERR_UNSUPPORTED;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
     if (!aligned16(dy) || !aligned16(dx) || (w && !aligned16(w)) || (c_packed && !aligned16(c_packed)))
@@ -845,6 +923,38 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
         void* p = static_cast<uint8_t*>(ws) + L.dy_pad;
         if ((s = launch_pad(dt, dy, p, g->N * OH * OW, int(g->OC), int(OCp), st)) != CKS_OK) return s;
         dys = p;
+    }
+    const int64_t CWm0 = cdiv(g->FW, g->sw);
+    if (mode == CKS_KS_STAGE1_FREE && !ks_direct_eligible(*g, dt)) return CKS_ERR_UNSUPPORTED;
+    if (!c_packed && (mode == CKS_KS_STAGE1_FREE || (mode == CKS_KS_AUTO && ks_direct(*g, dt, kPlanSMs)))) {
+        // Stage1-free: B straight from W (OHWI) viewed as (IC, OC, FW, FH); one box = the
+        // CW taps fw = x, x+sw, ... (element stride sw) of one filter row, 128 B of IC x BK OC
+        IgemmCfg cfg = igemm_cfg_deconv_w(*g, dt, kPlanSMs);
+        const uint32_t BK = uint32_t(cfg.KB / eb);
+        CUtensorMap ta, tb;
+        {
+            uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
+            uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
+            uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
+            if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+        }
+        const int64_t atomw = 128 / eb;
+        if (cfg.BN > atomw) {  // (IC in atom, OC, IC atom, FW, FH): smem [tap][atom][BK][128 B]
+            uint64_t d[5] = {uint64_t(atomw), uint64_t(g->OC), uint64_t(g->C / atomw), uint64_t(g->FW), uint64_t(g->FH)};
+            uint64_t sb[4] = {uint64_t(g->FH * g->FW * g->C * eb), 128u, uint64_t(g->C * eb),
+                              uint64_t(g->FW * g->C * eb)};
+            uint32_t box[5] = {uint32_t(atomw), BK, uint32_t(cfg.BN / atomw), uint32_t(CWm0 * g->sw), 1};
+            uint32_t es[5] = {1, 1, 1, uint32_t(g->sw), 1};
+            if (g->C % atomw || !make_tmap5(&tb, dt, w, d, sb, box, es)) return CKS_ERR_CUDA;
+        } else {
+            uint64_t d[4] = {uint64_t(g->C), uint64_t(g->OC), uint64_t(g->FW), uint64_t(g->FH)};
+            uint64_t sb[3] = {uint64_t(g->FH * g->FW * g->C * eb), uint64_t(g->C * eb), uint64_t(g->FW * g->C * eb)};
+            uint32_t box[4] = {uint32_t(cfg.BN), BK, uint32_t(CWm0 * g->sw), 1};
+            uint32_t es[4] = {1, 1, uint32_t(g->sw), 1};
+            if (!make_tmap4(&tb, dt, w, d, sb, box, 128, dt == CKS_TF32, es)) return CKS_ERR_CUDA;
+        }
+        return run_igemm(cfg, dt, rh, rw, ta, tb, dx, int(g->H), int(g->W), int(g->C), int(g->N), int(CWm0), g->sw, L,
+                         ws, st, g);
     }
     const void* cp = c_packed;
     if (!cp) {  // Stage1 into the workspace
@@ -872,8 +982,13 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
                      st);
 }
 
-cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
-                             void* ws, size_t ws_bytes, void* stream) {
+// Sk-dilated (+ G_Z reduce).  ar != nullptr: the fused data-parallel variant --
+// the wgrad kernels write G_Z partials (or, for one segment / the in-cluster
+// reduce, this rank's dW) into the workspace, and KB-REDUCE-AR aggregates the
+// segments AND the ranks into every rank's dW.
+
+static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
+                             void* ws, size_t ws_bytes, void* stream, const cks_ar_group* ar) {
     if (!g || !x || !dy || !dw) return CKS_ERR_NULL;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
@@ -881,7 +996,14 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
     if (!aligned16(x) || !aligned16(dy) || !aligned16(dw)) return CKS_ERR_ALIGNMENT;
     if (g->OC > 65535 || g->C > 65535) return CKS_ERR_UNSUPPORTED;
     WsLayout L = ws_layout(*g, dt, CKS_OP_WGRAD, gz, false, kPlanSMs);
-    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    const long long n_dw = g->OC * g->FH * g->FW * g->C;
+    if (ar) {
+        WsLayout La = L;  // + this rank's dW (one segment / in-cluster reduce) after the wgrad scratch
+        La.total = ar_local_offset(L) + size_t(n_dw) * 4;
+        if ((s = check_ws(La, ws, ws_bytes)) != CKS_OK) return s;
+    } else if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) {
+        return s;
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Axis ah = axis_h(*g), aw = axis_w(*g);
     const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt), OCp = pad_ch(g->OC, dt);
@@ -905,7 +1027,9 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.row ? 64 : cfg.kimg)};
         if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
-    float* wout = (cfg.gz > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    const bool partials = cfg.gz > 1 && !cfg.zc;
+    float* wout = partials ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial)
+                           : (ar ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ar_local_offset(L)) : dw);
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
     if (cfg.row) {  // narrow channels: (fh, fw, c) rows as the GEMM M dimension
         s = run_wgrad_row(*g, dt, row_cfg_wgrad(*g, dt, gz, kPlanSMs), x, ta, wout, part_stride, st);
@@ -920,6 +1044,27 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
         s = run_wgrad_taps(*g, dt, cfg, ah, aw, ta, tb, wout, part_stride, st);
     }
     if (s != CKS_OK) return s;
+    if (ar) {  // KB-REDUCE-AR: segments and ranks in one kernel (fixed order)
+        ArParams q;
+        memset(&q, 0, sizeof(q));
+        q.part = reinterpret_cast<const float4*>(wout);
+        q.nv = n_dw / 4;
+        q.world = ar->world;
+        q.rank = ar->rank;
+        q.slice = (q.nv + ar->world - 1) / ar->world;
+        q.gz = partials ? cfg.gz : 1;
+        for (int t = 0; t < ar->world; ++t) {
+            q.recv[t] = static_cast<float4*>(ar->recv[t]);
+            q.out[t] = reinterpret_cast<float4*>(ar->out[t]);
+            q.flag[t] = ar->flag[t];
+        }
+        q.count = ar->count;
+        q.err = ar->err;
+        const long long need = std::max(q.nv, q.slice);
+        const long long cap = ar->ctas > 0 ? ar->ctas : 148;
+        const unsigned blocks = unsigned(std::max<long long>(1, std::min<long long>((need + 255) / 256, cap)));
+        return launch_pdl(reduce_allreduce_kernel, dim3(blocks), dim3(256), 0, st, q);
+    }
     if (cfg.gz > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
         const long long n = part_stride;
         const bool v4 = n % 4 == 0;
@@ -933,6 +1078,87 @@ cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, con
                           cfg.gz);
     }
     return CKS_OK;
+}
+
+cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
+                             void* ws, size_t ws_bytes, void* stream) {
+    return wgrad_impl(g, dt, x, dy, dw, gz, ws, ws_bytes, stream, nullptr);
+}
+
+cks_status cks_ar_recv_bytes(const cks_geom* g, int32_t world, size_t* bytes) {
+    if (!g || !bytes) return CKS_ERR_NULL;
+    cks_status s = validate(g);
+    if (s != CKS_OK) return s;
+    if (world < 1 || world > CKS_AR_MAX_RANKS) return CKS_ERR_UNSUPPORTED;
+    const long long nv = g->OC * g->FH * g->FW * g->C / 4;
+    *bytes = size_t(world) * size_t((nv + world - 1) / world) * 16;
+    return CKS_OK;
+}
+
+cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
+                                       int gz, void* ws, size_t ws_bytes, const cks_ar_group* grp, void* stream) {
+    if (!g || !grp || !grp->count || !grp->err) return CKS_ERR_NULL;
+    if (grp->world < 1 || grp->world > CKS_AR_MAX_RANKS || grp->rank < 0 || grp->rank >= grp->world)
+        return CKS_ERR_UNSUPPORTED;
+    if ((g->OC * g->FH * g->FW * g->C) % 4 != 0) return CKS_ERR_UNSUPPORTED;
+    for (int t = 0; t < grp->world; ++t) {
+        if (!grp->recv[t] || !grp->out[t] || !grp->flag[t]) return CKS_ERR_NULL;
+        if (!aligned16(grp->recv[t]) || !aligned16(grp->out[t])) return CKS_ERR_ALIGNMENT;
+    }
+    if (grp->out[grp->rank] != dw) return CKS_ERR_UNSUPPORTED;
+    return wgrad_impl(g, dt, x, dy, dw, gz, ws, ws_bytes, stream, grp);
+}
+
+cks_status cks_ipc_export(const void* ptr, cks_ipc_handle* h) {
+    if (!ptr || !h) return CKS_ERR_NULL;
+    CUdeviceptr base = 0;
+    if (!mem_range(ptr, &base)) return CKS_ERR_CUDA;
+    cudaIpcMemHandle_t mh;
+    if (cudaIpcGetMemHandle(&mh, reinterpret_cast<void*>(base)) != cudaSuccess) return last_cuda();
+    const uint64_t off = uint64_t(reinterpret_cast<CUdeviceptr>(ptr) - base);
+    static_assert(sizeof(mh) == 64, "cudaIpcMemHandle_t");
+    memcpy(h->bytes, &mh, 64);
+    memcpy(h->bytes + 64, &off, 8);
+    return CKS_OK;
+}
+
+// Imported allocations, by handle: a peer's buffers often live in one
+// allocation (the caching allocator's segments), and a handle may be opened
+// only once per process -- later imports reuse the mapping (refcounted).
+static std::mutex g_ipc_mu;
+static std::unordered_map<std::string, std::pair<void*, int>> g_ipc_open;
+
+cks_status cks_ipc_import(const cks_ipc_handle* h, void** ptr) {
+    if (!h || !ptr) return CKS_ERR_NULL;
+    cudaIpcMemHandle_t mh;
+    uint64_t off = 0;
+    memcpy(&mh, h->bytes, 64);
+    memcpy(&off, h->bytes + 64, 8);
+    const std::string key(reinterpret_cast<const char*>(h->bytes), 64);
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_open.find(key);
+    if (it == g_ipc_open.end()) {
+        void* base = nullptr;
+        if (cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return last_cuda();
+        it = g_ipc_open.emplace(key, std::make_pair(base, 0)).first;
+    }
+    ++it->second.second;
+    *ptr = static_cast<uint8_t*>(it->second.first) + off;
+    return CKS_OK;
+}
+
+cks_status cks_ipc_close(void* ptr) {
+    if (!ptr) return CKS_ERR_NULL;
+    CUdeviceptr base = 0;
+    if (!mem_range(ptr, &base)) return CKS_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    for (auto it = g_ipc_open.begin(); it != g_ipc_open.end(); ++it) {
+        if (reinterpret_cast<CUdeviceptr>(it->second.first) != base) continue;
+        if (--it->second.second > 0) return CKS_OK;
+        g_ipc_open.erase(it);
+        return cudaIpcCloseMemHandle(reinterpret_cast<void*>(base)) == cudaSuccess ? CKS_OK : last_cuda();
+    }
+    return CKS_ERR_UNSUPPORTED;  // not an imported pointer
 }
 
 cks_status cks_axis_table(int64_t I, int64_t F, int32_t s, int32_t p, int table, int64_t* out, size_t cap,
@@ -995,10 +1221,12 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     const bool cpad = pad_ch(g->C, dt) != g->C, ocpad = pad_ch(g->OC, dt) != g->OC;
     int n = 1;
     if (op == CKS_OP_FWD) n += (cpad && !row_cfg_fwd(*g, dt).ok) ? 2 : 0;
-    else if (op == CKS_OP_DECONV) n += (c_packed_given ? 0 : 1) + (ocpad ? 1 : 0);
-    else if (op == CKS_OP_WGRAD) {
+    else if (op == CKS_OP_DECONV) n += (c_packed_given || ks_direct(*g, dt, kPlanSMs) ? 0 : 1) + (ocpad ? 1 : 0);
+    else if (op == CKS_OP_WGRAD || int(op) == CKS_OP_WGRAD_AR) {
         const WgradCfg c = wgrad_cfg(*g, dt, gz, kPlanSMs);
-        n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) + (c.gz > 1 && !c.zc ? 1 : 0);
+        // + KB-REDUCE for G_Z partials; the fused variant always ends with KB-REDUCE-AR
+        n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) +
+             (int(op) == CKS_OP_WGRAD_AR ? 1 : (c.gz > 1 && !c.zc ? 1 : 0));
     }
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;

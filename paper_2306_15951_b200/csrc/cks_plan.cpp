@@ -167,7 +167,8 @@ bool epi_staging() { return knobs().epi != 0; }
 
 static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout,
                             int64_t kchan, int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms,
-                            int force_pbw, int epi_warps, bool pair = false, int epi_bufs = 1) {
+                            int force_pbw, int epi_warps, bool pair = false, int epi_bufs = 1, int force_bn = 0,
+                            int min_bn = 0) {
     IgemmCfg c;
     c.pair = pair ? 1 : 0;
     c.epi_bufs = epi_bufs;
@@ -182,6 +183,7 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     int ov_bn = 0, ov_pbw = 0, ov_z = 0;
     const bool ov = cfg_override(ov_bn, ov_pbw, ov_z);
     if (ov && ov_bn > 0) c.BN = ov_bn;
+    if (force_bn > 0) c.BN = force_bn;
     if (ov && ov_pbw > 0) force_pbw = ov_pbw;
     if (pair) {  // CTA pair: 2 x 128 images, 2 x 128 output channels, one pixel per tile
         c.BN = 128;
@@ -209,9 +211,13 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // (Z = 2) only for long K loops (>= 16 row steps) on grids of < 32 tiles.
     int pbw = int(std::min<int64_t>({256 / c.BN, 8, maxrow}));
     while (pbw > 1 && tiles_for(c.BN, pbw) < 120) --pbw;
-    if (!pair && tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0)) {
+    if (!pair && tiles_for(c.BN, pbw) < 64 && c.BN == 128 && !(ov && ov_bn > 0) && force_bn == 0) {
         c.BN = 64;
         pbw = 1;
+    }
+    if (min_bn > 0 && c.BN < min_bn) {  // Stage1-free KS-deconv: whole 128-byte MN atoms of B
+        c.BN = min_bn;
+        pbw = std::min<int>(pbw, int(std::min<int64_t>(256 / c.BN, 8)));
     }
     c.nbs = int((nout + c.BN * (pair ? 2 : 1) - 1) / (c.BN * (pair ? 2 : 1)));
     if (force_pbw > 0) pbw = std::min<int>(force_pbw, int(std::min<int64_t>(256 / c.BN, 8)));
@@ -297,7 +303,13 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
 // 8 epilogue warps (two per TMEM sub-partition, twice the output stores in
 // flight) when their 4 KB staging buffers cost no pipeline depth or tile width.
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
-                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw) {
+                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw,
+                   int force_bn) {
+    // Stage1-free KS-deconv: force_bn > 0 fixes the B width (one 128-byte MN atom per tap),
+    // force_bn < 0 asks for B widths of whole atoms of -force_bn channels; no CTA pairs
+    if (force_bn != 0)
+        return igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms, force_pbw, 4,
+                           false, 1, std::max(force_bn, 0), force_bn < 0 ? -force_bn : 0);
     // CTA pairs (cta_group::2, M = 256 images x N = 256 channels per MMA): the same
     // smem stage (this CTA's A slot + half the B row) feeds twice the MMA work of a
     // 128 x 128 tile, so the latency-bound 2-stage ring carries twice the math.
@@ -350,6 +362,35 @@ static IgemmCfg igemm_cfg_deconv_plan(const cks_geom& g, cks_dtype dt, int num_s
     for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
     return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
                      num_sms);
+}
+
+bool ks_direct_eligible(const cks_geom& g, cks_dtype dt) {
+    const int64_t eb = elem_bytes(dt);
+    return (g.C * eb) % 16 == 0 && g.sw <= 8 && g.sh <= 16 && cdiv(g.FW, g.sw) * g.sw <= 256 && g.FH <= 32767;
+}
+
+static IgemmCfg igemm_cfg_deconv_w_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
+    Axis ah = axis_h(g), aw = axis_w(g);
+    auto rh = krows_deconv(ah);
+    std::vector<int64_t> cnt;
+    for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
+    const int atomw = int(128 / elem_bytes(dt));  // channels of one 128-byte MN atom
+    // several atoms per tap need the IC axis split exactly into atoms (5-D map)
+    const int fb = g.C % atomw == 0 ? -atomw : atomw;
+    return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
+                     num_sms, 0, fb);
+}
+
+// Policy: Stage1-free where eligible and the W-direct plan keeps the packed
+// plan's tile (same BN, no CTA pairs): a narrower W-direct tile re-reads dY
+// more often (measured: TF32 C3 with BN forced to 32 was up to 1.4x slower)
+// (CKS_KS_DIRECT=0/1 forces it off / on where eligible; experiments build).
+bool ks_direct(const cks_geom& g, cks_dtype dt, int num_sms) {
+    if (!ks_direct_eligible(g, dt)) return false;
+    if (const char* e = cks_knob("CKS_KS_DIRECT")) return atoi(e) != 0;
+    const IgemmCfg c = igemm_cfg_deconv(g, dt, num_sms);
+    const IgemmCfg d = igemm_cfg_deconv_w(g, dt, num_sms);
+    return !c.pair && d.BN == c.BN;
 }
 
 // ---------------------------------------------------------------- narrow-channel row path
@@ -588,12 +629,14 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                 return std::string(b) + row_classes_str(r.cls);
             }
         }
-        const IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
+        const bool direct = op == CKS_OP_DECONV && ks_direct(g, dt, num_sms);
+        const IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms)
+                                            : (direct ? igemm_cfg_deconv_w(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms));
         snprintf(b, sizeof b,
                  "igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d out_tiles=%lld "
-                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d",
+                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d ks_direct=%d",
                  c.BN, c.pbw, c.KB, c.ntap, c.pa, c.apos, c.stages, c.a_stages, c.unified, (long long)c.out_tiles, c.Z,
-                 c.zc, c.kc_blocks, c.epi_warps, c.pair);
+                 c.zc, c.kc_blocks, c.epi_warps, c.pair, direct ? 1 : 0);
         return b;
     }
     const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);
@@ -743,13 +786,22 @@ static WsLayout ws_layout_plan(const cks_geom& g, cks_dtype dt, cks_op op, int g
     if (op == CKS_OP_DECONV || op == CKS_OP_WGRAD) {
         if (OCp != g.OC) take(size_t(g.N) * OH * OW * OCp * eb, L.dy_pad, L.dy_pad_bytes);
     }
+    // W given: room for Stage1's packed sub-filters whichever KS-deconv variant runs
+    // (cks_deconv2d_ex may force the Stage1 path); split-K scratch for both plans
     if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
     if ((op == CKS_OP_FWD && !row) || op == CKS_OP_DECONV) {
-        IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms);
-        if (c.Z > 1 && !c.zc) {
-            take(size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4, L.partial, L.partial_bytes);
-            take(size_t(c.out_tiles) * 4, L.sem, L.sem_bytes);
-        }
+        std::vector<IgemmCfg> cs;
+        if (op == CKS_OP_FWD) cs.push_back(igemm_cfg_fwd(g, dt, num_sms));
+        else cs.push_back(igemm_cfg_deconv(g, dt, num_sms));
+        if (op == CKS_OP_DECONV && !c_packed_given && ks_direct_eligible(g, dt)) cs.push_back(igemm_cfg_deconv_w(g, dt, num_sms));
+        size_t part = 0, sem = 0;
+        for (const IgemmCfg& c : cs)
+            if (c.Z > 1 && !c.zc) {
+                part = std::max(part, size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4);
+                sem = std::max(sem, size_t(c.out_tiles) * 4);
+            }
+        take(part, L.partial, L.partial_bytes);
+        take(sem, L.sem, L.sem_bytes);
     }
     if (op == CKS_OP_WGRAD) {
         WgradCfg c = wgrad_cfg(g, dt, gz, num_sms);
@@ -807,6 +859,10 @@ RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
 RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     static PlanMemo<RowCfg> memo;
     return memo.get(plan_key(g, dt, 2, gz_req, num_sms), [&] { return row_cfg_wgrad_plan(g, dt, gz_req, num_sms); });
+}
+IgemmCfg igemm_cfg_deconv_w(const cks_geom& g, cks_dtype dt, int num_sms) {
+    static PlanMemo<IgemmCfg> memo;
+    return memo.get(plan_key(g, dt, 3, 0, num_sms), [&] { return igemm_cfg_deconv_w_plan(g, dt, num_sms); });
 }
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     static PlanMemo<WgradCfg> memo;

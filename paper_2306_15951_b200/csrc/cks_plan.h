@@ -110,13 +110,22 @@ struct IgemmCfg {
     std::vector<int64_t> wph_cnt;  // rows per w phase
 };
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
-                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0);
+                   int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0,
+                   int force_bn = 0);
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 4160;  // minus alignment, barriers, tables, MMA programs
 constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
 constexpr int epi_stage_bytes(int epi_warps, int bufs = 1) { return epi_warps * bufs * 4096; }
 bool epi_staging();                       // coalesced-store epilogue (default on; CKS_EPI_STAGE=0 disables)
 IgemmCfg igemm_cfg_fwd(const cks_geom& g, cks_dtype dt, int num_sms);
 IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms);
+// Stage1-free KS-deconv: the implicit GEMM reads W
+// directly as an MN-major B operand (kernels/igemm.cuh BMN).  Eligible when
+// W rows are 16-byte multiples (IC * eb % 16 == 0), sw <= 8 (TMA element
+// stride) and the phases fit the kernel tables; ks_direct() is the policy the
+// library applies to a cks_deconv2d call given W (not packed sub-filters).
+bool ks_direct_eligible(const cks_geom& g, cks_dtype dt);
+bool ks_direct(const cks_geom& g, cks_dtype dt, int num_sms);
+IgemmCfg igemm_cfg_deconv_w(const cks_geom& g, cks_dtype dt, int num_sms);
 
 // Narrow-channel row path (kernels/narrow.cuh): one filter row's contiguous
 // (fw, c) run is one K-block of JB elements (ROWB = JB * element bytes).

@@ -28,6 +28,14 @@
 //                 (Stage1), a0 = oh_s = u + a_y, out = u*sh + ih_s (T2): the
 //                 epilogue is Stage3's phase-strided composition.
 //
+// Stage1-free KS-deconv (BMN, SURVEY §8(f) NEXT #4 -- the all-in-one variant
+// the paper tried and set aside): the B operand is read straight from
+// W [OC][FH][FW][IC] per sub-filter row -- one TMA box of taps fw = x, x+sw,
+// ... (element stride sw) of filter row fh = y + (CH_y-1-ch)*sh, IC innermost
+// -- as an MN-major operand (IC = N contiguous, OC = K); the rot180 of
+// Stage1 becomes the slot order (slot j <-> cw = CW_x-1-j), absorbed by keeping
+// accumulators in forward pixel order.  No packed sub-filters, no KB-SPLIT.
+//
 // Under-filled grids split the row steps into Z segments (split-K).  Cluster
 // split-K (zc, the default): the Z CTAs of one thread-block cluster compute
 // the Z segments of ONE output tile (one tile per CTA), stage their fp32
@@ -122,6 +130,11 @@ struct IgemmParams {
     int epi_bufs;         // 4 KB TMA-store staging buffers per epilogue warp (1 or 2)
     int epi_warps;        // epilogue warps: 4 (one per TMEM sub-partition) or 8 (two, alternate 32-column chunks)
     int dbg;              // experiment flags (0 in production): 1 skip stores, 2 skip MMA
+    // Stage1-free KS-deconv (BMN): per phase_h y the filter row of sub-filter row 0,
+    // fh0[y] = y + (CH_y - 1) * sh (row ch is fh0[y] - ch * sh); per phase_w x the
+    // sub-filter width CW_x; sh
+    int16_t bfh0[kMaxPhases], bcw[kMaxPhases];
+    int bsh;
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
 };
 
@@ -244,7 +257,7 @@ __device__ __forceinline__ uint32_t pos_mask(const Tile& c, int iw) {
     return m;
 }
 
-template <int BN, bool kTF32, int KB, bool PAIR = false>
+template <int BN, bool kTF32, int KB, bool PAIR = false, bool BMN = false>
 __global__ void __launch_bounds__(384, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmY, const __grid_constant__ IgemmParams p) {
@@ -369,6 +382,19 @@ __global__ void __launch_bounds__(384, 1)
                                                   c.ph);
                         } else if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
                             ptx::mbar_arrive(bf);  // experiment: B traffic removed (wrong results)
+                        } else if (BMN) {
+                            // W-direct: taps fw = x + j*sw (j = slot) of filter row fh, BN input channels
+                            // (BN / atom 128-byte N atoms: 5-D map, smem [tap][atom][BK rows][128 B]) x BK
+                            // output channels
+                            const int y = c.ph / p.phases_w, x = c.ph - y * p.phases_w;
+                            ptx::mbar_arrive_expect_tx(bf, btx);
+                            constexpr int ATOMW = 128 / S::EB;
+                            if (BN > ATOMW)
+                                ptx::tma_load_5d(bbuf + bs * p.b_stage_bytes, &tmB, bf, 0, kc * S::BK,
+                                                 c.nb * (BN / ATOMW), x, p.bfh0[y] - ch * p.bsh);
+                            else
+                                ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, bf, c.nb * BN, kc * S::BK, x,
+                                                 p.bfh0[y] - ch * p.bsh);
                         } else {
                             ptx::mbar_arrive_expect_tx(bf, btx);
                             ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, bf, kc * S::BK, c.nb * BN,
@@ -424,6 +450,13 @@ __global__ void __launch_bounds__(384, 1)
             // ---------------- MMA issuer (single thread)
             // K-major SW128 descriptor without the start address: LBO 16 B, SBO 1 KB
             const uint64_t dconst = ptx::smem_desc_kmajor(0, KB);
+            // B: K-major like A, or (BMN) MN-major: 128 B atoms of N laid out [tap][atom] (LBO = atom
+            // bytes, so N-merged MMAs walk consecutive taps), SBO = one K group (8 / 4 rows of 128 B)
+            constexpr uint32_t kAtomBytes = uint32_t(S::BK) * 128u;  // one 128-byte-wide N atom of BK K rows
+            const uint64_t bconst = !BMN ? dconst
+                                         : (kTF32 ? ptx::smem_desc_mn_b32(0, kAtomBytes, 512)
+                                                  : ptx::smem_desc_mn(0, kAtomBytes, 1024, 128));
+            constexpr uint32_t kBStep = BMN ? (S::UK * 128) >> 4 : 2;  // B descriptor advance per MMA K step
             uint32_t acc = 0, acc_ph = 0;
             uint32_t as = 0, aph = 0, bs = 0, bph = 0;  // ring slots / phases, stepped (no runtime division)
             const uint32_t na = uint32_t(p.a_stages), nb = uint32_t(p.b_stages);
@@ -441,12 +474,12 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::tc_fence_after();
                 const uint32_t dbase = tmem_base + acc * uint32_t(p.pbw * BNo);
                 __syncwarp();
-                const uint32_t idesc0 = ptx::instr_desc(kPair ? 256 : 128, 0, kTF32, false, false);
+                const uint32_t idesc0 = ptx::instr_desc(kPair ? 256 : 128, 0, kTF32, false, BMN);
                 bool first = true;
                 for (int ri = rs0; ri < rs1; ++ri) {
                     if (!p.unified) ptx::mbar_wait(&bfull[bs], bph);  // unified: covered by the A-slot wait
                     if (lane == 0) trace_ev(p, 1, ti, 1);
-                    const uint64_t bdesc0 = dconst | ptx::desc_addr(ptx::smem_u32(bbuf + bs * p.b_stage_bytes));
+                    const uint64_t bdesc0 = bconst | ptx::desc_addr(ptx::smem_u32(bbuf + bs * p.b_stage_bytes));
                     const int4* pl = pg + 2 + (first ? 0 : kProgEntries);
                     const int np = first ? np0 : np1;
                     first = false;
@@ -476,7 +509,7 @@ __global__ void __launch_bounds__(384, 1)
                                 } else {
 #pragma unroll
                                     for (int kk = 0; kk < S::BK / S::UK; ++kk)
-                                        ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2),
+                                        ptx::mma_ss<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * kBStep),
                                                            idesc, kk ? 1u : acc0);
                                 }
                             }
@@ -572,9 +605,16 @@ __global__ void __launch_bounds__(384, 1)
                                 }
                                 if (emit) {
                                     const int jhi = jlo + cnt - 1;
-                                    const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);
-                                    pg[2 + off + n] = make_int4(qa / p.apos, qa % p.apos, (p.pbw - 1 - jhi) * BN,
-                                                              cw_lo | (cnt << 8) | (int(st0) << 16));
+                                    if (BMN) {  // forward pixel order; slot of pixel jlo's tap, slots ascend with N
+                                        const int cw_hi = iw - (c.a0[0] + jlo * p.a0_step);
+                                        const int slot0 = p.bcw[tab[1].phase[c.j0]] - 1 - cw_hi;
+                                        pg[2 + off + n] = make_int4(qa / p.apos, qa % p.apos, jlo * BN,
+                                                                  slot0 | (cnt << 8) | (int(st0) << 16));
+                                    } else {
+                                        const int cw_lo = iw - (c.a0[0] + jhi * p.a0_step);
+                                        pg[2 + off + n] = make_int4(qa / p.apos, qa % p.apos, (p.pbw - 1 - jhi) * BN,
+                                                                  cw_lo | (cnt << 8) | (int(st0) << 16));
+                                    }
                                 }
                                 ++n;
                                 mm &= ~(((1u << cnt) - 1u) << jlo);
@@ -664,7 +704,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
                     for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
                         uint32_t r[32];
-                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
+                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN +
                                            c0, r);
                         ptx::tmem_ld_wait();
                         if (c0 >= cvalid) continue;
@@ -710,7 +750,7 @@ __global__ void __launch_bounds__(384, 1)
                     for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
                         const int k = j * (BNo / 32) + c0 / 32;
                         uint32_t r[32];
-                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN +
+                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN +
                                            c0, r);
                         ptx::tmem_ld_wait();
                         if (c0 >= cvalid) continue;
@@ -756,7 +796,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
                 for (int c0 = 32 * int(half); c0 < BNo; c0 += 32 * int(nhalf)) {
                     uint32_t r[32];
-                    ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (p.pbw - 1 - j) * BN + c0,
+                    ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN + c0,
                                    r);
                     ptx::tmem_ld_wait();
                     if (c0 >= lim || (p.dbg & 1) || (dst == nullptr && !stage)) continue;  // stage: warp-uniform

@@ -57,3 +57,92 @@ def sharded_layer_step(x_local, w, dy_local, stride, padding, grads_view, stream
     dx = K.deconv2d(dy_local, w, tuple(x_local.shape[1:3]), stride, padding, stream=stream)
     K.dilated_wgrad(x_local, dy_local, tuple(w.shape[1:3]), stride, padding, out=grads_view, stream=stream)
     return y, dx
+
+
+class FusedWgradAllReduce:
+    """Per-layer Sk-dilated + cross-rank dW sum in one kernel over peer memory
+    (cks_dilated_wgrad_allreduce, KB-REDUCE-AR): the
+    G_Z segments and the ranks' batch shards are reduced together in fixed
+    order, every rank receives the bit-identical dW, no NCCL call on the path.
+
+    Buffers per layer (allocated here, one flat tensor each): the receive
+    buffer (world x slice float4), two signal words, and three counter words
+    (CTA arrivals + the device-side call sequence number: the calls may be
+    captured in a CUDA graph and replayed).
+    Peers' buffers are mapped with CUDA IPC (handles exchanged over the
+    process group: gloo or NCCL), or, with ``virtual_world`` on ONE process,
+    the "ranks" are this process's own buffer sets (tests: every rank's kernel
+    on its own stream of the same GPU).
+    """
+
+    def __init__(self, geoms, dws, device, group=None, virtual_world=None, ctas=0):
+        from . import _lib as L
+        self.L = L
+        self.geoms = list(geoms)
+        self.device = device
+        self.ctas = int(ctas)
+        if virtual_world is not None:
+            self.world, self.ranks = int(virtual_world), list(range(int(virtual_world)))
+        else:
+            self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+            self.ranks = [dist.get_rank(group) if dist.is_initialized() else 0]
+        if not 1 <= self.world <= L.CKS_AR_MAX_RANKS:
+            raise ValueError("world size out of range for the fused all-reduce")
+        nl = len(self.geoms)
+        self.recv_off, off = [], 0
+        for g in self.geoms:
+            self.recv_off.append(off)
+            off += (L.cks_ar_recv_bytes(g, self.world) + 255) // 256 * 256
+        self.recv_bytes = max(off, 256)
+        # one buffer set per local rank (virtual ranks: several on this process)
+        self.sets = []
+        for r in self.ranks:
+            self.sets.append({
+                "recv": torch.empty(self.recv_bytes, dtype=torch.uint8, device=device),
+                "flags": torch.zeros(2 * nl, dtype=torch.int32, device=device),
+                "count": torch.zeros(4 * nl, dtype=torch.int32, device=device),
+                "err": torch.zeros(1, dtype=torch.int32, device=device),
+                "dws": dws[r] if virtual_world is not None else dws,
+            })
+        self._mapped = []
+        if virtual_world is not None:
+            peers = [(s["recv"].data_ptr(), [d.data_ptr() for d in s["dws"]], s["flags"].data_ptr())
+                     for s in self.sets]
+        else:
+            s = self.sets[0]
+            mine = (L.cks_ipc_export(s["recv"].data_ptr()), [L.cks_ipc_export(d.data_ptr()) for d in s["dws"]],
+                    L.cks_ipc_export(s["flags"].data_ptr()))
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+            peers = []
+            for t, (hr, hd, hf) in enumerate(allh):
+                if t == self.ranks[0]:
+                    peers.append((s["recv"].data_ptr(), [d.data_ptr() for d in s["dws"]], s["flags"].data_ptr()))
+                    continue
+                pr, pf = L.cks_ipc_import(hr), L.cks_ipc_import(hf)
+                pd = [L.cks_ipc_import(h) for h in hd]
+                self._mapped += [pr, pf] + pd
+                peers.append((pr, pd, pf))
+        self.peers = peers
+
+    def group(self, layer, local=0):
+        """cks_ar_group of `layer` for local buffer set `local`."""
+        L = self.L
+        s = self.sets[local]
+        grp = L.cks_ar_group()
+        grp.world, grp.rank, grp.ctas = self.world, self.ranks[local], self.ctas
+        for t, (pr, pd, pf) in enumerate(self.peers):
+            grp.recv[t] = pr + self.recv_off[layer]
+            grp.out[t] = pd[layer]
+            grp.flag[t] = pf + 8 * layer
+        grp.count = s["count"].data_ptr() + 16 * layer
+        grp.err = s["err"].data_ptr()
+        return grp
+
+    def errors(self):
+        return [int(s["err"].item()) for s in self.sets]
+
+    def close(self):
+        for p in self._mapped:
+            self.L.cks_ipc_close(p)
+        self._mapped = []

@@ -120,8 +120,13 @@ def test_workspace_and_launch_counts():
     # G_Z partials + KB-REDUCE, or the cluster reduce (neither): the launch count follows the workspace
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_WGRAD) == 1 + (L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD) > 0)
     g = L.make_geom(128, 64, 32, 32, 64, 3, 3, 2, 2, 1, 1)
-    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV) == 2
+    # W given: Stage1-free KS-deconv (one launch, no packed sub-filters in the
+    # workspace) where the plan takes it, else KB-SPLIT + KB-KS
+    direct = L.plan_dict(g, L.CKS_BF16, L.CKS_OP_DECONV)["ks_direct"] == "1"
+    assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV) == (1 if direct else 2)
     assert L.cks_launch_count(g, L.CKS_BF16, L.CKS_OP_DECONV, c_packed_given=True) == 1
+    g3 = L.make_geom(128, 3, 32, 32, 64, 3, 3, 2, 2, 1, 1)  # W rows of 6 bytes: not eligible
+    assert L.plan_dict(g3, L.CKS_BF16, L.CKS_OP_DECONV)["ks_direct"] == "0"
     gz = L.cks_choose_gz(g, L.CKS_BF16)
     assert 1 <= gz <= 64
     # G_Z partials + KB-REDUCE, or the cluster reduce (neither): the launch count follows the workspace

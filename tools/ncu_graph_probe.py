@@ -3,7 +3,8 @@ usage: python tools/ncu_graph_probe.py VARIANT   (run under ncu)
   eager   one igemm op launched eagerly
   g1      a graph holding that single op
   g2      a graph: wgrad op (row kernel + G_Z reduce) then the igemm op
-  g1nopdl a graph holding the single op, captured with CKS_NO_PDL=1 semantics
+  g2ev    as g2 with timing-event nodes between the ops (bench's serialized graph)
+  g3ev    three ops (stem fwd, stem wgrad, l1 fwd) with event nodes, after a flush fill
 """
 import os
 import sys
@@ -33,12 +34,25 @@ if v == "eager":
     with torch.cuda.stream(st):
         b.run("fwd", st.cuda_stream)
 else:
+    ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(4)]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):
         sp = torch.cuda.current_stream().cuda_stream
-        if v == "g2":
+        if v == "g3ev":
+            ev[0].record()
+            s0.run("fwd", sp)
+        if v in ("g2", "g2ev", "g3ev"):
+            if v != "g2":
+                ev[1].record()
             s0.run("wgrad", sp)
+        if v != "g2" and v != "g1":
+            ev[2].record()
         b.run("fwd", sp)
-    g.replay()
+        if v != "g2" and v != "g1":
+            ev[3].record()
+    with torch.cuda.stream(st):
+        flush.fill_(1.0)
+        g.replay()
 torch.cuda.synchronize()
 print("ok", v)
