@@ -234,6 +234,33 @@ cks_status cks_zins_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, co
 cks_status cks_zins_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
                           void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------ 3-D C-K-S
+ * The paper's operators with a depth axis ("stride^N and dilate^N times
+ * acceleration for N-dimensional deconvolution and dilated-convolution",
+ * P:407 "higher-dimensional versions ... analogized to its 2D counterpart";
+ * SURVEY §8(f) NEXT #3; reading c17): trimmed windows on all three axes
+ * (ConvV2), sd*sh*sw sub-filters (KS-deconv, Stage1-free: W is read directly),
+ * leaping access on all three axes (Sk-dilated).  Layouts: X [N][D][H][W][C],
+ * W [OC][FD][FH][FW][C], Y / dY [N][OD][OH][OW][OC], outputs fp32, overwritten.
+ * Validity as in 2-D per axis (O >= 1, p < F); FD, FH, FW <= 32, strides <= 8;
+ * OD*OH and D*H <= CKS_MAX_ROWS * 256.  KS-deconv needs W rows of a 16-byte
+ * multiple (C * elem % 16 == 0), else CKS_ERR_UNSUPPORTED.  Workspace:
+ * cks_workspace_size3 for the op (G_Z partials, channel padding). */
+typedef struct cks_geom3 {
+    int64_t N, C, D, H, W, OC, FD, FH, FW;
+    int32_t sd, sh, sw, pd, ph, pw;
+} cks_geom3;
+cks_status cks_output_shape3(const cks_geom3* g, int64_t* OD, int64_t* OH, int64_t* OW);
+cks_status cks_workspace_size3(const cks_geom3* g, cks_dtype dt, cks_op op, int gz, size_t* bytes);
+/* zero-free MACs N*C*OC*V_D*V_H*V_W (out[0]) and the per-axis V (out[1..3]) */
+cks_status cks_op_counts3(const cks_geom3* g, int64_t out[4]);
+cks_status cks_conv3d_fwd(const cks_geom3* g, cks_dtype dt, const void* x, const void* w, float* y, void* ws,
+                          size_t ws_bytes, void* stream);
+cks_status cks_deconv3d(const cks_geom3* g, cks_dtype dt, const void* dy, const void* w, float* dx, void* ws,
+                        size_t ws_bytes, void* stream);
+cks_status cks_dilated_wgrad3d(const cks_geom3* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------- fused wgrad + all-reduce
  * Sk-dilated on this rank's batch shard followed by ONE kernel (KB-REDUCE-AR)
  * that performs the G_Z aggregation AND the sum over the ranks of the

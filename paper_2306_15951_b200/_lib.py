@@ -24,7 +24,8 @@ EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2
            "cks_ks_split", "cks_deconv2d", "cks_dilated_wgrad", "cks_axis_table", "cks_op_counts",
            "cks_launch_count", "cks_status_string", "cks_version", "cks_zins_workspace_size",
            "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad", "cks_plan_describe", "cks_deconv2d_ex",
-           "cks_padding_macs", "cks_ar_recv_bytes", "cks_dilated_wgrad_allreduce", "cks_ipc_export",
+           "cks_padding_macs", "cks_output_shape3", "cks_workspace_size3", "cks_op_counts3", "cks_conv3d_fwd",
+           "cks_deconv3d", "cks_dilated_wgrad3d", "cks_ar_recv_bytes", "cks_dilated_wgrad_allreduce", "cks_ipc_export",
            "cks_ipc_import", "cks_ipc_close")
 
 
@@ -51,6 +52,16 @@ class cks_ar_group(C.Structure):
                 ("flag", C.c_void_p * CKS_AR_MAX_RANKS), ("count", C.c_void_p), ("err", C.c_void_p)]
 
 
+class cks_geom3(C.Structure):
+    """include/cks.h cks_geom3 (3-D C-K-S)."""
+    _fields_ = [(n, C.c_int64) for n in ("N", "C", "D", "H", "W", "OC", "FD", "FH", "FW")] + \
+               [(n, C.c_int32) for n in ("sd", "sh", "sw", "pd", "ph", "pw")]
+
+
+def make_geom3(N, C_, D, H, W, OC, FD, FH, FW, sd, sh, sw, pd, ph, pw) -> cks_geom3:
+    return cks_geom3(N, C_, D, H, W, OC, FD, FH, FW, sd, sh, sw, pd, ph, pw)
+
+
 class cks_ipc_handle(C.Structure):
     _fields_ = [("bytes", C.c_ubyte * 72)]
 
@@ -70,6 +81,7 @@ def lib():
                                "or __graft_entry__.build()")
         L = C.CDLL(LIB_PATH)
         G = C.POINTER(cks_geom)
+        G3 = C.POINTER(cks_geom3)
         vp, sz = C.c_void_p, C.c_size_t
         sig = {
             "cks_output_shape": (C.c_int, [G, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -91,6 +103,12 @@ def lib():
             "cks_zins_wgrad": (C.c_int, [G, C.c_int, vp, vp, vp, vp, sz, vp]),
             "cks_plan_describe": (C.c_int, [G, C.c_int, C.c_int, C.c_int, C.c_char_p, sz, C.POINTER(sz)]),
             "cks_padding_macs": (C.c_int, [G, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+            "cks_output_shape3": (C.c_int, [G3, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+            "cks_workspace_size3": (C.c_int, [G3, C.c_int, C.c_int, C.c_int, C.POINTER(sz)]),
+            "cks_op_counts3": (C.c_int, [G3, C.POINTER(C.c_int64)]),
+            "cks_conv3d_fwd": (C.c_int, [G3, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_deconv3d": (C.c_int, [G3, C.c_int, vp, vp, vp, vp, sz, vp]),
+            "cks_dilated_wgrad3d": (C.c_int, [G3, C.c_int, vp, vp, vp, C.c_int, vp, sz, vp]),
             "cks_ar_recv_bytes": (C.c_int, [G, C.c_int32, C.POINTER(sz)]),
             "cks_dilated_wgrad_allreduce": (C.c_int, [G, C.c_int, vp, vp, vp, C.c_int, vp, sz,
                                                       C.POINTER(cks_ar_group), vp]),
@@ -167,6 +185,38 @@ CKS_KS_AUTO, CKS_KS_STAGE1_FREE, CKS_KS_STAGE1 = 0, 1, 2
 def cks_deconv2d_ex(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream, mode):
     _check(lib().cks_deconv2d_ex(C.byref(g), dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream, mode),
            "cks_deconv2d_ex")
+
+
+# ------------------------------------------------------------------ 3-D C-K-S
+def cks_output_shape3(g: cks_geom3):
+    od, oh, ow = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().cks_output_shape3(C.byref(g), C.byref(od), C.byref(oh), C.byref(ow)), "cks_output_shape3")
+    return od.value, oh.value, ow.value
+
+
+def cks_workspace_size3(g: cks_geom3, dtype: int, op: int, gz: int = 0) -> int:
+    b = C.c_size_t()
+    _check(lib().cks_workspace_size3(C.byref(g), dtype, op, gz, C.byref(b)), "cks_workspace_size3")
+    return b.value
+
+
+def cks_op_counts3(g: cks_geom3) -> dict:
+    out = (C.c_int64 * 4)()
+    _check(lib().cks_op_counts3(C.byref(g), out), "cks_op_counts3")
+    return {"zero_free_macs": out[0], "VD": out[1], "VH": out[2], "VW": out[3]}
+
+
+def cks_conv3d_fwd(g, dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_conv3d_fwd(C.byref(g), dtype, x_ptr, w_ptr, y_ptr, ws_ptr, ws_bytes, stream), "cks_conv3d_fwd")
+
+
+def cks_deconv3d(g, dtype, dy_ptr, w_ptr, dx_ptr, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_deconv3d(C.byref(g), dtype, dy_ptr, w_ptr, dx_ptr, ws_ptr, ws_bytes, stream), "cks_deconv3d")
+
+
+def cks_dilated_wgrad3d(g, dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, stream):
+    _check(lib().cks_dilated_wgrad3d(C.byref(g), dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, stream),
+           "cks_dilated_wgrad3d")
 
 
 def cks_ar_recv_bytes(g: cks_geom, world: int) -> int:

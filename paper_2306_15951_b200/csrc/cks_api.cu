@@ -346,11 +346,21 @@ cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const C
     return launch_igemm_kb<false, 128>(BN, a, b, y, p, smem, st);
 }
 
+// Depth axis of a 3-D igemm launch (2-D: one trivial depth row).
+struct Depth3 {
+    std::vector<KRow> rd;  // depth rows (T1 / T2 of the d axis)
+    int a_rows_h = 0;      // A rows per depth slice
+    int out_rows_h = 0;    // output rows per depth slice
+    int b_rows_h = 0;      // filter rows per depth slice (packed / W row index = d * b_rows_h + h)
+    int FD = 1, sd = 1;    // W-direct: filter depth and depth stride
+};
+
 // Fill IgemmParams from the plan and launch (fwd and deconv share this).
+// out_H: output rows in total (3-D: OD * OH, flattened).
 cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRow>& rh, const std::vector<KRow>& rw,
                      const CUtensorMap& ta, const CUtensorMap& tb, float* out, int out_H, int out_W, int out_C,
                      int N, int slot_stride, int phases_w, const WsLayout& L, void* ws, cudaStream_t st,
-                     const cks_geom* bmn = nullptr) {
+                     const cks_geom* bmn = nullptr, const Depth3* d3 = nullptr) {
     IgemmCfg cfg = cfg_in;
     if (debug_flags() & 16) {  // experiment: no split-K
         cfg.Z = 1;
@@ -360,6 +370,15 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     IgemmParams p;
     memset(&p, 0, sizeof(p));
     if (!fill_axis(p.ah, rh) || !fill_axis(p.aw, rw)) return CKS_ERR_UNSUPPORTED;
+    {
+        static const std::vector<KRow> trivial = {KRow{0, 0, 1, 0, 0}};
+        if (!fill_axis(p.ad, d3 ? d3->rd : trivial)) return CKS_ERR_UNSUPPORTED;
+        p.a_rows_h = d3 ? d3->a_rows_h : 0;
+        p.out_rows_h = d3 ? d3->out_rows_h : 0;
+        p.b_rows_h = d3 ? d3->b_rows_h : 0;
+        p.phases_h = bmn ? bmn->sh : 1;
+        p.fd_rh = make_fastdiv(uint32_t(rh.size()));
+    }
     p.out = out;
     p.rows_h = int(rh.size());
     p.nph_w = int(cfg.wph_cnt.size());
@@ -420,7 +439,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.cm = cfg.cm;
     p.unified = cfg.unified;
     const int smem = 1024 + p.a_stages * p.apos * 128 * cfg.KB + p.b_stages * p.b_stage_bytes + 512 +
-                     int(2 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? epi_stage_bytes(cfg.epi_warps, cfg.epi_bufs) + 1024 : 0);
+                     int(3 * sizeof(KAxis)) + 2 * kProgSlot * 16 + (cfg.epi ? epi_stage_bytes(cfg.epi_warps, cfg.epi_bufs) + 1024 : 0);
     if (cfg.Z > 1 && !cfg.zc) {
         if (!L.partial_bytes || !L.sem_bytes) return CKS_ERR_WORKSPACE;
         p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial);
@@ -443,6 +462,11 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     if (bmn) {  // Stage1-free: per-phase filter-row origin and sub-filter widths (Alg. 2 Stage1's index map)
         if (bmn->sh > kMaxPhases || bmn->sw > kMaxPhases) return CKS_ERR_UNSUPPORTED;
         for (int y = 0; y < bmn->sh; ++y) p.bfh0[y] = int16_t(y + (cdiv(bmn->FH - y, bmn->sh) - 1) * bmn->sh);
+        const int FD = d3 ? d3->FD : 1, sd = d3 ? d3->sd : 1;
+        if (sd > kMaxPhases) return CKS_ERR_UNSUPPORTED;
+        for (int z = 0; z < sd; ++z) p.bfd0[z] = int16_t(z + (cdiv(FD - z, sd) - 1) * sd);
+        p.bsd = sd;
+        p.b_rows_h = int(bmn->FH);
         for (int x = 0; x < bmn->sw; ++x) p.bcw[x] = int16_t(cdiv(bmn->FW - x, bmn->sw));
         p.bsh = bmn->sh;
     }
@@ -625,10 +649,30 @@ cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, cons
 // per-tap Sk-dilated-V2 kernel (KB-WGRAD)
 cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, const Axis& ah, const Axis& aw,
                           const CUtensorMap& ta, const CUtensorMap& tb, float* wout, long long part_stride,
-                          cudaStream_t st) {
+                          cudaStream_t st, const Axis* ad = nullptr) {
     WgradParams p;
     memset(&p, 0, sizeof(p));
     auto th = table_t3(ah), tw = table_t3(aw);
+    if (th.size() > 32 || tw.size() > 32) return CKS_ERR_UNSUPPORTED;
+    if (ad) {  // 3-D: T3 of the depth axis
+        auto td = table_t3(*ad);
+        if (td.size() > 32) return CKS_ERR_UNSUPPORTED;
+        for (size_t i = 0; i < td.size(); ++i) {
+            p.od_s[i] = int16_t(td[i].oh_s);
+            p.od_e[i] = int16_t(td[i].oh_e);
+        }
+        p.FD = int(ad->F);
+        p.sd = int(ad->s);
+        p.pd = int(ad->p);
+    } else {
+        p.od_s[0] = 0;
+        p.od_e[0] = 1;
+        p.FD = 1;
+        p.sd = 1;
+        p.pd = 0;
+    }
+    p.OHr = int(ah.O);
+    p.Hr = int(ah.I);
     for (size_t i = 0; i < th.size(); ++i) {
         p.oh_s[i] = int16_t(th[i].oh_s);
         p.oh_e[i] = int16_t(th[i].oh_e);
@@ -1083,6 +1127,208 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
 cks_status cks_dilated_wgrad(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
                              void* ws, size_t ws_bytes, void* stream) {
     return wgrad_impl(g, dt, x, dy, dw, gz, ws, ws_bytes, stream, nullptr);
+}
+
+// ------------------------------------------------------------------ 3-D C-K-S
+cks_status cks_output_shape3(const cks_geom3* g, int64_t* OD, int64_t* OH, int64_t* OW) {
+    if (!g || !OD || !OH || !OW) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    const cks_geom g2 = plane_geom(*g);
+    *OD = axis_d(*g).O;
+    *OH = axis_h(g2).O;
+    *OW = axis_w(g2).O;
+    return CKS_OK;
+}
+
+cks_status cks_workspace_size3(const cks_geom3* g, cks_dtype dt, cks_op op, int gz, size_t* bytes) {
+    if (!g || !bytes) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    if (op < CKS_OP_FWD || op > CKS_OP_WGRAD) return CKS_ERR_UNSUPPORTED;
+    *bytes = ws_layout3(*g, dt, op, gz, kPlanSMs).total;
+    return CKS_OK;
+}
+
+cks_status cks_op_counts3(const cks_geom3* g, int64_t out[4]) {
+    if (!g || !out) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    const cks_geom g2 = plane_geom(*g);
+    const int64_t vd = axis_valid_pairs(axis_d(*g)), vh = axis_valid_pairs(axis_h(g2)),
+                  vw = axis_valid_pairs(axis_w(g2));
+    out[0] = g->N * g->C * g->OC * vd * vh * vw;
+    out[1] = vd;
+    out[2] = vh;
+    out[3] = vw;
+    return CKS_OK;
+}
+
+cks_status cks_conv3d_fwd(const cks_geom3* g, cks_dtype dt, const void* x, const void* w, float* y, void* ws,
+                          size_t ws_bytes, void* stream) {
+    if (!g || !x || !w || !y) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y)) return CKS_ERR_ALIGNMENT;
+    const cks_geom g2 = plane_geom(*g);
+    const Axis ad = axis_d(*g), ah = axis_h(g2), aw = axis_w(g2);
+    Depth3 d3;
+    d3.rd = krows_fwd(ad);
+    auto rh = krows_fwd(ah), rw = krows_fwd(aw);
+    if (!rows_ok(rh) || !rows_ok(rw) || !rows_ok(d3.rd)) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout3(*g, dt, CKS_OP_FWD, 0, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt);
+    const void* xs = x;
+    const void* wsrc = w;
+    if (Cp != g->C) {
+        void* xp = static_cast<uint8_t*>(ws) + L.x_pad;
+        void* wp = static_cast<uint8_t*>(ws) + L.w_pad;
+        if ((s = launch_pad(dt, x, xp, g->N * g->D * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        if ((s = launch_pad(dt, w, wp, g->OC * g->FD * g->FH * g->FW, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        xs = xp;
+        wsrc = wp;
+    }
+    IgemmCfg cfg = igemm_cfg_fwd3(*g, dt, kPlanSMs);
+    const uint32_t BK = uint32_t(cfg.KB / eb);
+    CUtensorMap ta, tb;
+    {   // X viewed as (C, N, W, D*H): depth and row flattened (a row step never crosses a depth slice)
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->D * g->H)};
+        uint64_t sb[3] = {uint64_t(g->D * g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
+        uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
+        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+    }
+    {   // W viewed as (C, OC, FD*FH*FW, 1): one box = the FW taps of filter row (fd, fh)
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->OC), uint64_t(g->FD * g->FH * g->FW), 1};
+        uint64_t sb[3] = {uint64_t(g->FD * g->FH * g->FW * Cp * eb), uint64_t(Cp * eb),
+                          uint64_t(g->OC * g->FD * g->FH * g->FW * Cp * eb)};
+        uint32_t box[4] = {BK, uint32_t(cfg.BN), uint32_t(g->FW), 1};
+        if (!make_tmap4(&tb, dt, wsrc, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+    }
+    d3.a_rows_h = int(g->H);
+    d3.out_rows_h = int(ah.O);
+    d3.b_rows_h = int(g->FH);
+    return run_igemm(cfg, dt, rh, rw, ta, tb, y, int(ad.O * ah.O), int(aw.O), int(g->OC), int(g->N), int(g->FW), 1,
+                     L, ws, st, nullptr, &d3);
+}
+
+cks_status cks_deconv3d(const cks_geom3* g, cks_dtype dt, const void* dy, const void* w, float* dx, void* ws,
+                        size_t ws_bytes, void* stream) {
+    if (!g || !dy || !w || !dx) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    if (!aligned16(dy) || !aligned16(dx) || !aligned16(w)) return CKS_ERR_ALIGNMENT;
+    const cks_geom g2 = plane_geom(*g);
+    if (!ks_direct_eligible(g2, dt)) return CKS_ERR_UNSUPPORTED;  // Stage1-free only: 16-byte W rows
+    const Axis ad = axis_d(*g), ah = axis_h(g2), aw = axis_w(g2);
+    Depth3 d3;
+    d3.rd = krows_deconv(ad);
+    auto rh = krows_deconv(ah), rw = krows_deconv(aw);
+    if (!rows_ok(rh) || !rows_ok(rw) || !rows_ok(d3.rd)) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout3(*g, dt, CKS_OP_DECONV, 0, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t eb = elem_bytes(dt), OCp = pad_ch(g->OC, dt);
+    const int64_t OD = ad.O, OH = ah.O, OW = aw.O;
+    const void* dys = dy;
+    if (OCp != g->OC) {
+        void* p = static_cast<uint8_t*>(ws) + L.dy_pad;
+        if ((s = launch_pad(dt, dy, p, g->N * OD * OH * OW, int(g->OC), int(OCp), st)) != CKS_OK) return s;
+        dys = p;
+    }
+    IgemmCfg cfg = igemm_cfg_deconv3(*g, dt, kPlanSMs);
+    const uint32_t BK = uint32_t(cfg.KB / eb);
+    const int64_t CWm0 = cdiv(g->FW, g->sw), atomw = 128 / eb;
+    CUtensorMap ta, tb;
+    {   // dY viewed as (OC, N, OW, OD*OH)
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OD * OH)};
+        uint64_t sb[3] = {uint64_t(OD * OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
+        uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+    }
+    // W (OHWI) read directly: filter rows (fd, fh) flattened to FD*FH
+    if (cfg.BN > atomw) {
+        uint64_t d[5] = {uint64_t(atomw), uint64_t(g->OC), uint64_t(g->C / atomw), uint64_t(g->FW),
+                         uint64_t(g->FD * g->FH)};
+        uint64_t sb[4] = {uint64_t(g->FD * g->FH * g->FW * g->C * eb), 128u, uint64_t(g->C * eb),
+                          uint64_t(g->FW * g->C * eb)};
+        uint32_t box[5] = {uint32_t(atomw), BK, uint32_t(cfg.BN / atomw), uint32_t(CWm0 * g->sw), 1};
+        uint32_t es[5] = {1, 1, 1, uint32_t(g->sw), 1};
+        if (g->C % atomw || !make_tmap5(&tb, dt, w, d, sb, box, es)) return CKS_ERR_CUDA;
+    } else {
+        uint64_t d[4] = {uint64_t(g->C), uint64_t(g->OC), uint64_t(g->FW), uint64_t(g->FD * g->FH)};
+        uint64_t sb[3] = {uint64_t(g->FD * g->FH * g->FW * g->C * eb), uint64_t(g->C * eb),
+                          uint64_t(g->FW * g->C * eb)};
+        uint32_t box[4] = {uint32_t(cfg.BN), BK, uint32_t(CWm0 * g->sw), 1};
+        uint32_t es[4] = {1, 1, uint32_t(g->sw), 1};
+        if (!make_tmap4(&tb, dt, w, d, sb, box, 128, dt == CKS_TF32, es)) return CKS_ERR_CUDA;
+    }
+    d3.a_rows_h = int(OH);
+    d3.out_rows_h = int(g->H);
+    d3.FD = int(g->FD);
+    d3.sd = g->sd;
+    return run_igemm(cfg, dt, rh, rw, ta, tb, dx, int(g->D * g->H), int(g->W), int(g->C), int(g->N), int(CWm0), g->sw,
+                     L, ws, st, &g2, &d3);
+}
+
+cks_status cks_dilated_wgrad3d(const cks_geom3* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
+                               void* ws, size_t ws_bytes, void* stream) {
+    if (!g || !x || !dy || !dw) return CKS_ERR_NULL;
+    cks_status s = validate3(g);
+    if (s != CKS_OK) return s;
+    if (gz < 0) return CKS_ERR_UNSUPPORTED;
+    if (!aligned16(x) || !aligned16(dy) || !aligned16(dw)) return CKS_ERR_ALIGNMENT;
+    if (g->OC > 65535 || g->C > 65535) return CKS_ERR_UNSUPPORTED;
+    WsLayout L = ws_layout3(*g, dt, CKS_OP_WGRAD, gz, kPlanSMs);
+    if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const cks_geom g2 = plane_geom(*g);
+    const Axis ad = axis_d(*g), ah = axis_h(g2), aw = axis_w(g2);
+    const int64_t eb = elem_bytes(dt), Cp = pad_ch(g->C, dt), OCp = pad_ch(g->OC, dt);
+    const void* xs = x;
+    const void* dys = dy;
+    const WgradCfg cfg = wgrad_cfg3(*g, dt, gz, kPlanSMs);
+    if (Cp != g->C) {
+        void* p = static_cast<uint8_t*>(ws) + L.x_pad;
+        if ((s = launch_pad(dt, x, p, g->N * g->D * g->H * g->W, int(g->C), int(Cp), st)) != CKS_OK) return s;
+        xs = p;
+    }
+    if (OCp != g->OC) {
+        void* p = static_cast<uint8_t*>(ws) + L.dy_pad;
+        if ((s = launch_pad(dt, dy, p, g->N * ad.O * ah.O * aw.O, int(g->OC), int(OCp), st)) != CKS_OK) return s;
+        dys = p;
+    }
+    CUtensorMap ta, tb;
+    {   // dY viewed as (OC, OW, OD*OH, N)
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ad.O * ah.O), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ad.O * ah.O * aw.O * OCp * eb)};
+        uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.kimg)};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
+    }
+    {   // X viewed as (C, W, D*H, N): leaping rows (id, ih) flattened
+        uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->D * g->H), uint64_t(g->N)};
+        uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->D * g->H * g->W * Cp * eb)};
+        uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.kimg)};
+        if (!make_tmap4(&tb, dt, xs, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
+    }
+    const long long part_stride = g->OC * g->FD * g->FH * g->FW * g->C;
+    float* wout = (cfg.gz > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    s = run_wgrad_taps(g2, dt, cfg, ah, aw, ta, tb, wout, part_stride, st, &ad);
+    if (s != CKS_OK) return s;
+    if (cfg.gz > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
+        const long long n = part_stride;
+        const bool v4 = n % 4 == 0;
+        const long long nv = v4 ? n / 4 : n;
+        const unsigned G = unsigned(std::min(16, cfg.gz));
+        const unsigned blocks = unsigned(std::min<long long>((nv + 31) / 32, 148LL * 16));
+        if (v4)
+            return launch_pdl(reduce_partials_kernel<float4>, dim3(blocks), dim3(32, G), 0, st,
+                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, cfg.gz);
+        return launch_pdl(reduce_partials_kernel<float>, dim3(blocks), dim3(32, G), 0, st, (const float*)wout, dw, nv,
+                          cfg.gz);
+    }
+    return CKS_OK;
 }
 
 cks_status cks_ar_recv_bytes(const cks_geom* g, int32_t world, size_t* bytes) {

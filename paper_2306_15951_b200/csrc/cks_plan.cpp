@@ -655,9 +655,11 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
 // bounds it above by the SM count.  Here: enough segments that the
 // taps x OC-blocks x IC-blocks x G_Z tiles cover the 148 SMs about once,
 // with at least 4 K-blocks (256 images*positions) per segment.
-static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+// ad: the depth axis of a 3-D Sk-dilated (per-tap kernel only; every tap's K
+// range is the product of its trimmed d, h and w ranges)
+static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms, const Axis* ad = nullptr) {
     WgradCfg c;
-    RowCfg rc = row_cfg_wgrad(g, dt, gz_req, num_sms);
+    RowCfg rc = ad ? RowCfg() : row_cfg_wgrad(g, dt, gz_req, num_sms);
     if (rc.ok) {
         c.row = true;
         c.BN = rc.BN;
@@ -680,18 +682,25 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
     c.mt = (dt == CKS_BF16 && c.BN == 64 && g.FW == 3 && knobs().wmt) ? 3 : 1;
     Axis ah = axis_h(g), aw = axis_w(g);
     auto th = table_t3(ah), tw = table_t3(aw);
+    int64_t dmul = 1;  // 3-D: taps x depth windows (the smallest depth window for lmin)
+    if (ad) {
+        int64_t dmin = INT64_MAX;
+        for (auto& d : table_t3(*ad))
+            if (d.oh_e > d.oh_s) dmin = std::min(dmin, d.oh_e - d.oh_s);
+        dmul = dmin == INT64_MAX ? 0 : dmin;
+    }
     int64_t uws = INT64_MAX, uwe = INT64_MIN;
     for (auto& b : tw)
         if (b.oh_e > b.oh_s) { uws = std::min(uws, b.oh_s); uwe = std::max(uwe, b.oh_e); }
     int64_t lmin = INT64_MAX, ntaps = 0;
     for (auto& a : th) {
         if (c.mt > 1) {
-            int64_t L = (a.oh_e - a.oh_s) * std::max<int64_t>(uwe - uws, 0) * c.nblk64;
+            int64_t L = dmul * (a.oh_e - a.oh_s) * std::max<int64_t>(uwe - uws, 0) * c.nblk64;
             if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
             continue;
         }
         for (auto& b : tw) {
-            int64_t L = (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
+            int64_t L = dmul * (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
             if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
         }
     }
@@ -702,12 +711,12 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
         ntaps = 0;
         for (auto& a : th)
             for (auto& b : tw) {
-                int64_t L = (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
+                int64_t L = dmul * (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
                 if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
             }
         if (ntaps == 0) lmin = 1;
     }
-    c.base_tiles = int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
+    c.base_tiles = (ad ? ad->F : 1) * int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
     if (gz_req > 0) {
         c.gz = gz_req;
     } else {
@@ -873,4 +882,102 @@ WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_pa
     return memo.get(plan_key(g, dt, int(op), gz * 2 + (c_packed_given ? 1 : 0), num_sms),
                     [&] { return ws_layout_plan(g, dt, op, gz, c_packed_given, num_sms); });
 }
+
+// ---------------------------------------------------------------- 3-D plans
+cks_status validate3(const cks_geom3* g) {
+    if (!g) return CKS_ERR_NULL;
+    if (g->D < 1 || g->FD < 1 || g->sd < 1 || g->pd < 0) return CKS_ERR_GEOMETRY;
+    if (g->pd >= g->FD || g->D + 2 * g->pd - g->FD < 0) return CKS_ERR_GEOMETRY;
+    if (g->FD > 32 || g->sd > 8) return CKS_ERR_UNSUPPORTED;
+    const cks_geom g2 = plane_geom(*g);
+    cks_status s = validate(&g2);
+    if (s != CKS_OK) return s;
+    const Axis ad = axis_d(*g), ah = axis_h(g2);
+    if (ad.O * ah.O > int64_t(CKS_MAX_ROWS) * 256 || g->D * g->H > int64_t(CKS_MAX_ROWS) * 256 ||
+        ad.O > CKS_MAX_ROWS || g->D > CKS_MAX_ROWS)
+        return CKS_ERR_UNSUPPORTED;
+    return CKS_OK;
+}
+
+cks_geom plane_geom(const cks_geom3& g) {
+    cks_geom p;
+    p.N = g.N, p.C = g.C, p.H = g.H, p.W = g.W, p.OC = g.OC, p.FH = g.FH, p.FW = g.FW;
+    p.sh = g.sh, p.sw = g.sw, p.ph = g.ph, p.pw = g.pw, p.dh = 1, p.dw = 1;
+    return p;
+}
+
+Axis axis_d(const cks_geom3& g) { return Axis{g.D, g.FD, g.sd, g.pd, out_extent(g.D, g.FD, g.sd, g.pd)}; }
+
+static std::string plan_key3(const cks_geom3& g, int a, int b, int c, int d) {
+    const int64_t v[19] = {g.N, g.C, g.D, g.H, g.W, g.OC, g.FD, g.FH, g.FW, g.sd, g.sh, g.sw, g.pd, g.ph, g.pw,
+                           a, b, c, d};
+    return std::string(reinterpret_cast<const char*>(v), sizeof(v));
+}
+
+IgemmCfg igemm_cfg_fwd3(const cks_geom3& g, cks_dtype dt, int num_sms) {
+    static PlanMemo<IgemmCfg> memo;
+    return memo.get(plan_key3(g, dt, 0, 0, num_sms), [&] {
+        const cks_geom g2 = plane_geom(g);
+        const Axis ad = axis_d(g), ah = axis_h(g2), aw = axis_w(g2);
+        return igemm_cfg(ad.O * ah.O, {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt),
+                         max_window(krows_fwd(ah)) * max_window(krows_fwd(ad)), g.FW, g.sw, num_sms);
+    });
+}
+
+IgemmCfg igemm_cfg_deconv3(const cks_geom3& g, cks_dtype dt, int num_sms) {
+    static PlanMemo<IgemmCfg> memo;
+    return memo.get(plan_key3(g, dt, 1, 0, num_sms), [&] {
+        const cks_geom g2 = plane_geom(g);
+        const Axis ad = axis_d(g), ah = axis_h(g2), aw = axis_w(g2);
+        std::vector<int64_t> cnt;
+        for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
+        const int atomw = int(128 / elem_bytes(dt));
+        const int fb = g.C % atomw == 0 ? -atomw : atomw;  // Stage1-free: whole 128-byte MN atoms of W
+        return igemm_cfg(ad.I * ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt),
+                         max_window(krows_deconv(ah)) * max_window(krows_deconv(ad)), cdiv(g.FW, g.sw), 1, num_sms,
+                         0, fb);
+    });
+}
+
+WgradCfg wgrad_cfg3(const cks_geom3& g, cks_dtype dt, int gz_req, int num_sms) {
+    static PlanMemo<WgradCfg> memo;
+    return memo.get(plan_key3(g, dt, 2, gz_req, num_sms), [&] {
+        const Axis ad = axis_d(g);
+        return wgrad_cfg_plan(plane_geom(g), dt, gz_req, num_sms, &ad);
+    });
+}
+
+WsLayout ws_layout3(const cks_geom3& g, cks_dtype dt, cks_op op, int gz, int num_sms) {
+    WsLayout L;
+    const int64_t eb = elem_bytes(dt), Cp = pad_ch(g.C, dt), OCp = pad_ch(g.OC, dt);
+    const Axis ad = axis_d(g);
+    const cks_geom g2 = plane_geom(g);
+    const int64_t OH = axis_h(g2).O, OW = axis_w(g2).O;
+    size_t off = 0;
+    auto take = [&](size_t bytes, size_t& at, size_t& sz) {
+        if (!bytes) return;
+        at = off;
+        sz = bytes;
+        off += align256(bytes);
+    };
+    if ((op == CKS_OP_FWD || op == CKS_OP_WGRAD) && Cp != g.C)
+        take(size_t(g.N) * g.D * g.H * g.W * Cp * eb, L.x_pad, L.x_pad_bytes);
+    if (op == CKS_OP_FWD && Cp != g.C) take(size_t(g.OC) * g.FD * g.FH * g.FW * Cp * eb, L.w_pad, L.w_pad_bytes);
+    if ((op == CKS_OP_DECONV || op == CKS_OP_WGRAD) && OCp != g.OC)
+        take(size_t(g.N) * ad.O * OH * OW * OCp * eb, L.dy_pad, L.dy_pad_bytes);
+    if (op == CKS_OP_FWD || op == CKS_OP_DECONV) {
+        const IgemmCfg c = op == CKS_OP_FWD ? igemm_cfg_fwd3(g, dt, num_sms) : igemm_cfg_deconv3(g, dt, num_sms);
+        if (c.Z > 1 && !c.zc) {
+            take(size_t(c.out_tiles) * c.Z * 128 * c.pbw * c.BN * 4, L.partial, L.partial_bytes);
+            take(size_t(c.out_tiles) * 4, L.sem, L.sem_bytes);
+        }
+    }
+    if (op == CKS_OP_WGRAD) {
+        const WgradCfg c = wgrad_cfg3(g, dt, gz, num_sms);
+        if (c.gz > 1 && !c.zc) take(size_t(c.gz) * g.OC * g.FD * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+    }
+    L.total = off;
+    return L;
+}
+
 }  // namespace cks

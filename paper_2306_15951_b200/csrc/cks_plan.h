@@ -112,7 +112,7 @@ struct IgemmCfg {
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0,
                    int force_bn = 0);
-constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 3584 - 4160;  // minus alignment, barriers, tables, MMA programs
+constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 5376 - 4160;  // minus alignment, barriers, 3 axis tables, MMA programs
 constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
 constexpr int epi_stage_bytes(int epi_warps, int bufs = 1) { return epi_warps * bufs * 4096; }
 bool epi_staging();                       // coalesced-store epilogue (default on; CKS_EPI_STAGE=0 disables)
@@ -180,6 +180,15 @@ struct WsLayout {
 };
 WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms);
 size_t ks_split_bytes(const cks_geom& g, cks_dtype dt);
+
+// 3-D (cks_geom3): the (H, W) plane as a 2-D geometry, the depth axis, plans.
+cks_status validate3(const cks_geom3* g);
+cks_geom plane_geom(const cks_geom3& g);
+Axis axis_d(const cks_geom3& g);
+IgemmCfg igemm_cfg_fwd3(const cks_geom3& g, cks_dtype dt, int num_sms);
+IgemmCfg igemm_cfg_deconv3(const cks_geom3& g, cks_dtype dt, int num_sms);
+WgradCfg wgrad_cfg3(const cks_geom3& g, cks_dtype dt, int gz_req, int num_sms);
+WsLayout ws_layout3(const cks_geom3& g, cks_dtype dt, cks_op op, int gz, int num_sms);
 
 // Text form of the plan the library uses for (g, dt, op, gz) -- kernel kind
 // and tile configuration as key=value pairs (tests, tools/plan_dump.py).

@@ -96,6 +96,17 @@ struct KAxisC {
 
 struct IgemmParams {
     KAxisC ah, aw;
+    // 3-D: the depth axis is a third table; an output
+    // "row" is (d row, h row), its row steps run over the (filter depth, filter
+    // row) pairs of both trimmed windows.  A / output / B rows are flattened
+    // (d * rows_per_depth + h); 2-D = one trivial depth row (a0 0, window [0,1)).
+    KAxisC ad;
+    int a_rows_h;      // A tensor rows per depth slice (X: H, dY: OH)
+    int out_rows_h;    // output rows per depth slice
+    int b_rows_h;      // B filter rows per depth slice (fwd: FH; packed KS: CHm; W-direct: FH)
+    int phases_h;      // phase = (phase_d * phases_h + phase_h) * phases_w + phase_w
+    int bsd;           // W-direct: filter depth of sub-filter depth row cd is bfd0[z] - cd * bsd
+    int16_t bfd0[kMaxPhases];
     float* out;
     float* part;  // split-K partials [out_tiles][Z][PBW*BN/4][128 rows][4] (coalesced per warp)
     int* sem;     // split-K arrival counters [out_tiles] (zero on entry, left zero)
@@ -118,7 +129,7 @@ struct IgemmParams {
     int zc;  // cluster split-K: cluster = the zsplit segments of one output tile, DSMEM reduction
     int pair;  // CTA pair (cta_group::2): the even/odd CTA of a cluster hold image blocks 2q / 2q+1 of one
                // tile (M = 256) and B columns [0, BN) / [BN, 2 BN) of its 2 BN outputs; nblk counts pairs
-    FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc;  // divisors of the tile / row-step decode
+    FastDiv fd_z, fd_nbs, fd_nblk, fd_wb, fd_kc, fd_rh;  // divisors of the tile / row-step decode
     long long num_tiles;  // output tiles x zsplit
     int cm;               // cluster size along the O_C blocks: the A tile of a pixel is multicast (1 = off)
     int unified;          // one A slot per row step: A slot + B row share one full/empty barrier pair
@@ -174,6 +185,9 @@ struct IgemmShape {
 // size arrays that are only indexed inside fully unrolled loops (registers).
 struct Tile {
     int z, nb, nblk, rh, j0, len, ph;
+    int rd, cds, nh;      // depth row, first filter depth of its window, filter rows of the h window
+    int orow;             // output row (flattened d * out_rows_h + h)
+    int a0d;              // A depth coordinate of filter depth 0
     int rs0, rs1;         // row-step range [rs0, rs1) of this split
     int rot;              // per-CTA rotation of the row-step order (spreads weight reads over L2)
     int chs;              // first filter row of the h window
@@ -183,7 +197,8 @@ struct Tile {
     long long out_tile;
 };
 
-__device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p, const KAxis& ah, const KAxis& aw) {
+__device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p, const KAxis& ah, const KAxis& aw,
+                                            const KAxis& ad) {
     // 32-bit decode (tile counts < 2^31; 64-bit div/mod is a slow software routine)
     Tile c;
     uint32_t t = uint32_t(t64);
@@ -200,13 +215,23 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
     t = q;
     q = fdivu(t, p.fd_wb);
     const int wb = int(t - q * uint32_t(p.wblocks));
-    c.rh = int(q);
+    {
+        const uint32_t r3 = q;  // (depth row, h row)
+        const uint32_t rd = fdivu(r3, p.fd_rh);
+        c.rd = int(rd);
+        c.rh = int(r3 - rd * uint32_t(p.rows_h));
+    }
     int x = 0;
     while (x + 1 < p.nph_w && p.wb_cum[x + 1] <= wb) ++x;
     c.j0 = p.wph_off[x] + (wb - p.wb_cum[x]) * p.pbw;
     c.len = min(p.pbw, p.wph_off[x] + p.wph_cnt[x] - c.j0);
-    c.ph = ah.phase[c.rh] * p.phases_w + aw.phase[c.j0];
+    c.ph = (ad.phase[c.rd] * p.phases_h + ah.phase[c.rh]) * p.phases_w + aw.phase[c.j0];
     const int chs = ah.ts[c.rh], che = ah.te[c.rh];
+    const int cds = ad.ts[c.rd], cde = ad.te[c.rd];
+    c.cds = cds;
+    c.nh = che - chs;
+    c.a0d = ad.a0[c.rd];
+    c.orow = ad.out[c.rd] * p.out_rows_h + ah.out[c.rh];
     c.chs = chs;
     int lo = 1 << 20, hi = -(1 << 20), plo = 1 << 20, phi = -(1 << 20);
 #pragma unroll
@@ -226,12 +251,12 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
             }
         }
     }
-    const bool empty = (hi <= lo) || (che <= chs);
+    const bool empty = (hi <= lo) || (che <= chs) || (cde <= cds);
     c.cwlo = empty ? 0 : lo;
     c.cwhi = empty ? 0 : hi;
     c.pos_lo = empty ? 0 : plo;
     c.pos_hi = empty ? 0 : phi;
-    const int rs = empty ? 0 : (che - chs) * p.kc_blocks;
+    const int rs = empty ? 0 : (che - chs) * (cde - cds) * p.kc_blocks;
     c.rs0 = p.zsplit == 1 ? 0 : int(fdivu(uint32_t(rs) * uint32_t(c.z), p.fd_z));
     c.rs1 = p.zsplit == 1 ? rs : int(fdivu(uint32_t(rs) * uint32_t(c.z + 1), p.fd_z));
     c.rot = c.rs1 > c.rs0 ? int(((blockIdx.x >> (p.pair ? 1 : 0)) / unsigned(p.cm)) % unsigned(c.rs1 - c.rs0))
@@ -287,12 +312,13 @@ __global__ void __launch_bounds__(384, 1)
     // constant loads instead of dependent cold loads in every role's decode)
     KAxis* tab = reinterpret_cast<KAxis*>(reinterpret_cast<uint8_t*>(bars) + 512);
     // 2 program slots x (2 header + 2 x 64 entries)
-    int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 2 * sizeof(KAxis));
+    int4* prog = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(tab) + 3 * sizeof(KAxis));
     // epilogue staging (p.epi_stage): 4 x 4 KB, 1 KB aligned (128B-swizzled TMA-store source)
     float* epi = reinterpret_cast<float*>(smem + ((ptx::smem_u32(prog + 2 * kProgSlot) - ptx::smem_u32(smem) + 1023u) & ~1023u));
-    for (int i = threadIdx.x; i < 2 * CKS_MAX_ROWS; i += blockDim.x) {
-        const KAxisC& ax = i < CKS_MAX_ROWS ? p.ah : p.aw;
-        KAxis& t = tab[i < CKS_MAX_ROWS ? 0 : 1];
+    for (int i = threadIdx.x; i < 3 * CKS_MAX_ROWS; i += blockDim.x) {
+        const int which = i / CKS_MAX_ROWS;  // 0: h, 1: w, 2: d
+        const KAxisC& ax = which == 0 ? p.ah : (which == 1 ? p.aw : p.ad);
+        KAxis& t = tab[which];
         const int r = i & (CKS_MAX_ROWS - 1);
         int x = 0;
         while (x + 1 < ax.nph && ax.row0[x + 1] <= r) ++x;
@@ -362,12 +388,16 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) trace_ev(p, trole, ti, 0);
         const uint32_t btx = uint32_t(p.ntap * S::TILE_B);
         for (long long t = t0; t < p.num_tiles; t += tstep) {
-            const Tile c = decode_tile(t, p, tab[0], tab[1]);
+            const Tile c = decode_tile(t, p, tab[0], tab[1], tab[2]);
             const int a0h = tab[0].a0[c.rh];
             for (int ri = c.rs0; ri < c.rs1; ++ri) {
                 const int r = row_step(c, ri);
                 const int rq = int(fdivu(uint32_t(r), p.fd_kc));
-                const int ch = c.chs + rq, kc = r - rq * p.kc_blocks;
+                const int kc = r - rq * p.kc_blocks;
+                const int rdq = rq / c.nh;  // (filter depth, filter row) of this row step
+                const int cd = c.cds + rdq, ch = c.chs + (rq - rdq * c.nh);
+                const int arow = (c.a0d + cd) * p.a_rows_h + a0h + ch;  // flattened A row
+                const int brow = cd * p.b_rows_h + ch;                   // flattened filter row
                 if (is_b) {
                     uint64_t* bf = p.unified ? &afull[bs] : &bfull[bs];
                     ptx::mbar_wait(p.unified ? &aempty[bs] : &bempty[bs], bph ^ 1);
@@ -378,7 +408,7 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t bfc = ptx::mapa(ptx::smem_u32(bf), 0);
                             if (leader) ptx::mbar_arrive_expect_tx_cluster(bfc, 2 * btx);
                             ptx::tma_load_4d_pair(bbuf + bs * p.b_stage_bytes, &tmB, bfc, kc * S::BK,
-                                                  c.nb * 2 * BN + int(blockIdx.x & 1u) * BN, ch * p.slot_stride,
+                                                  c.nb * 2 * BN + int(blockIdx.x & 1u) * BN, brow * p.slot_stride,
                                                   c.ph);
                         } else if ((p.dbg & 4) && bq >= uint32_t(p.b_stages)) {
                             ptx::mbar_arrive(bf);  // experiment: B traffic removed (wrong results)
@@ -386,19 +416,21 @@ __global__ void __launch_bounds__(384, 1)
                             // W-direct: taps fw = x + j*sw (j = slot) of filter row fh, BN input channels
                             // (BN / atom 128-byte N atoms: 5-D map, smem [tap][atom][BK rows][128 B]) x BK
                             // output channels
-                            const int y = c.ph / p.phases_w, x = c.ph - y * p.phases_w;
+                            const int zy = c.ph / p.phases_w, x = c.ph - zy * p.phases_w;
+                            const int z = zy / p.phases_h, y = zy - z * p.phases_h;
+                            const int wrow = (p.bfd0[z] - cd * p.bsd) * p.b_rows_h + p.bfh0[y] - ch * p.bsh;
                             ptx::mbar_arrive_expect_tx(bf, btx);
                             constexpr int ATOMW = 128 / S::EB;
                             if (BN > ATOMW)
                                 ptx::tma_load_5d(bbuf + bs * p.b_stage_bytes, &tmB, bf, 0, kc * S::BK,
-                                                 c.nb * (BN / ATOMW), x, p.bfh0[y] - ch * p.bsh);
+                                                 c.nb * (BN / ATOMW), x, wrow);
                             else
                                 ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, bf, c.nb * BN, kc * S::BK, x,
-                                                 p.bfh0[y] - ch * p.bsh);
+                                                 wrow);
                         } else {
                             ptx::mbar_arrive_expect_tx(bf, btx);
                             ptx::tma_load_4d(bbuf + bs * p.b_stage_bytes, &tmB, bf, kc * S::BK, c.nb * BN,
-                                             ch * p.slot_stride, c.ph);
+                                             brow * p.slot_stride, c.ph);
                         }
                     }
                     __syncwarp();
@@ -419,7 +451,7 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t afc = ptx::mapa(ptx::smem_u32(&afull[as]), 0);
                             if (leader) ptx::mbar_arrive_expect_tx_cluster(afc, 2 * a_slot);
                             ptx::tma_load_4d_pair(abuf + as * a_slot, &tmA, afc, kc * S::BK, c.nblk * 128, iw0,
-                                                  a0h + ch);
+                                                  arow);
                         } else if ((p.dbg & 8) && aq > uint32_t(p.a_stages)) {
                             ptx::mbar_arrive(&afull[as]);  // experiment: A traffic removed (wrong results)
                         } else if (p.cm > 1) {
@@ -429,11 +461,11 @@ __global__ void __launch_bounds__(384, 1)
                             for (int col = 0; col < p.apos; ++col)
                                 ptx::tma_load_4d_mc(abuf + as * a_slot + col * S::A_BYTES + crank * rows * KB, &tmA,
                                                     &afull[as], kc * S::BK, c.nblk * 128 + int(crank) * rows,
-                                                    iw0 + col, a0h + ch, cmask);
+                                                    iw0 + col, arow, cmask);
                         } else {
                             ptx::mbar_arrive_expect_tx(&afull[as], a_slot);
                             ptx::tma_load_4d(abuf + as * a_slot, &tmA, &afull[as], kc * S::BK, c.nblk * 128, iw0,
-                                             a0h + ch);
+                                             arow);
                         }
                     }
                     __syncwarp();
@@ -563,7 +595,7 @@ __global__ void __launch_bounds__(384, 1)
         {
             uint32_t ps = 0, pph = 0;
             for (long long t = t0; t < p.num_tiles && leader; t += tstep) {
-                const Tile c = decode_tile(t, p, tab[0], tab[1]);
+                const Tile c = decode_tile(t, p, tab[0], tab[1], tab[2]);
                 ptx::mbar_wait(&pempty[ps], pph ^ 1);
                 int4* pg = prog + ps * kProgSlot;
                 // ---- MMA program of this tile, built by this warp ahead of the MMA warp: entry =
@@ -680,7 +712,7 @@ __global__ void __launch_bounds__(384, 1)
         int ti = 0;
         if (et == 0) trace_ev(p, 2, ti, 0);
         for (long long t = t0; t < p.num_tiles; t += tstep) {
-            const Tile c = decode_tile(t, p, tab[0], tab[1]);
+            const Tile c = decode_tile(t, p, tab[0], tab[1], tab[2]);
             ptx::mbar_wait(&tfull[acc], acc_ph);
             if (et == 0) trace_ev(p, 2, ti, 1);
             ptx::tc_fence_after();
@@ -727,7 +759,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (ptx::elect_one()) {
-                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], tab[0].out[c.rh], nrow0);
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], c.orow, nrow0);
                             ptx::bulk_commit();
                         }
                         __syncwarp();
@@ -765,7 +797,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (ptx::elect_one()) {
-                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], tab[0].out[c.rh], nrow0);
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], c.orow, nrow0);
                             ptx::bulk_commit();
                         }
                         __syncwarp();
@@ -790,7 +822,7 @@ __global__ void __launch_bounds__(384, 1)
                 else if (split)  // column group q = (j*BN + c)/4 of row `row`
                     dst = p.part + ((c.out_tile * p.zsplit + c.z) * (pw_cols / 4) + j * (BN / 4)) * 512LL + row * 4;
                 else if (n < p.N)
-                    dst = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                    dst = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
                                    tab[1].out[c.j0 + j]) * p.out_C + cbase;
                 const int lim = split ? BN : cvalid;
 #pragma unroll 1
@@ -823,7 +855,7 @@ __global__ void __launch_bounds__(384, 1)
                             const int cc = c0 + 4 * cq;
                             if (nn < p.N && cc < lim)
                                 *reinterpret_cast<float4*>(p.out + ((static_cast<long long>(nn) * p.out_H +
-                                                                     tab[0].out[c.rh]) * p.out_W +
+                                                                     c.orow) * p.out_W +
                                                                     tab[1].out[c.j0 + j]) * p.out_C + cbase + cc) = v;
                         }
                         __syncwarp();
@@ -873,7 +905,7 @@ __global__ void __launch_bounds__(384, 1)
                                          (c.out_tile * p.zsplit) * (pw_cols / 4) * 128LL + row;
                     const long long zs = (pw_cols / 4) * 128LL;
                     for (int j = 0; j < c.len; ++j) {
-                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
                                                tab[1].out[c.j0 + j]) * p.out_C + cbase;
                         for (int c0 = 0; c0 < cvalid; c0 += 32) {
                             const float4* src = base + (j * BN + c0) / 4 * 128LL;
@@ -917,7 +949,7 @@ __global__ void __launch_bounds__(384, 1)
         // cluster split-K reduce: every rank's segment is staged in its smem
         ptx::cluster_sync();
         if (warp >= 4 && warp < 8 && blockIdx.x < p.num_tiles && !(p.dbg & 1)) {
-            const Tile c = decode_tile(blockIdx.x, p, tab[0], tab[1]);
+            const Tile c = decode_tile(blockIdx.x, p, tab[0], tab[1], tab[2]);
             const int row = int(threadIdx.x) - 128;  // accumulator row = image
             const int n = c.nblk * 128 + row;
             const int G = c.len * (BN / 4);  // float4 column groups of the tile
@@ -956,7 +988,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int gg = gq + h;
                         const int j = gg / (BN / 4), cc = (gg % (BN / 4)) * 4;
                         if (cc >= cvalid) continue;
-                        float* o = p.out + ((static_cast<long long>(n) * p.out_H + tab[0].out[c.rh]) * p.out_W +
+                        float* o = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
                                             tab[1].out[c.j0 + j]) * p.out_C + cbase + cc;
                         if ((p.out_C % 4) == 0 && cc + 4 <= cvalid) {
                             *reinterpret_cast<float4*>(o) = v;

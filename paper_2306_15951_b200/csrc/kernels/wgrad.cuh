@@ -32,6 +32,11 @@ namespace cks {
 
 struct WgradParams {
     int16_t oh_s[32], oh_e[32], ow_s[32], ow_e[32];  // T3 per tap row / column
+    // 3-D: T3 of the depth axis per filter depth, and the
+    // row extents per depth slice of dY (OH) and X (H): rows are flattened
+    // d * rows + h.  2-D: FD = 1, [od_s, od_e) = [0, 1), sd = 1, pd = 0.
+    int16_t od_s[32], od_e[32];
+    int FD, sd, pd, OHr, Hr;
     int ouw_s, ouw_e;       // row tiles: union of the taps' ow ranges
     float* out;             // dW (gz == 1) or partials [gz][OC][FH*FW][C]
     int FH, FW, sh, sw, ph, pw;
@@ -68,10 +73,10 @@ struct WgradShape {
 };
 
 struct WTile {
-    int nb, mb, z, fh, fw;
+    int nb, mb, z, fh, fw, fd;
     int kb0, kb1;  // k-block range of this segment
-    int wn;        // ow extent
-    int ohs, ows;
+    int wn, hn;    // ow / oh extents
+    int ohs, ows, ods;
 };
 
 template <int MT>
@@ -91,13 +96,18 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
         t /= uint32_t(p.gz);
     }
     const int tap = int(t);
-    c.fh = MT > 1 ? tap : tap / p.FW;
+    const int fdh = MT > 1 ? tap : tap / p.FW;  // filter (depth, row)
+    c.fd = fdh / p.FH;
+    c.fh = fdh - c.fd * p.FH;
     c.fw = MT > 1 ? 0 : tap % p.FW;
     c.ohs = p.oh_s[c.fh];
+    c.ods = p.od_s[c.fd];
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
     const int hn = p.oh_e[c.fh] - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
+    const int dn = p.od_e[c.fd] - c.ods;
     c.wn = wn;
-    const uint32_t L = uint32_t(hn) * uint32_t(wn) * uint32_t(p.nblk64);
+    c.hn = hn;
+    const uint32_t L = uint32_t(max(dn, 0)) * uint32_t(max(hn, 0)) * uint32_t(max(wn, 0)) * uint32_t(p.nblk64);
     c.kb0 = int(uint64_t(L) * uint32_t(c.z) / uint32_t(p.gz));
     c.kb1 = int(uint64_t(L) * uint32_t(c.z + 1) / uint32_t(p.gz));
     return c;
@@ -165,7 +175,10 @@ __global__ void __launch_bounds__(256, 1)
             for (int kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = kb % p.nblk64;
                 const int pos = kb / p.nblk64;
-                const int oh = c.ohs + pos / c.wn, ow = c.ows + pos % c.wn;
+                const int pq = pos / c.wn;
+                const int ow = c.ows + (pos - pq * c.wn);
+                const int dq = pq / c.hn;
+                const int oh = c.ohs + (pq - dq * c.hn), od = c.ods + dq;
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * S::STAGE_BYTES;
                 if (ptx::elect_one()) {
@@ -174,10 +187,11 @@ __global__ void __launch_bounds__(256, 1)
                         const int a_atoms = min(128 / S::CH, (p.OC - c.mb * 128 + S::CH - 1) / S::CH);
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(a_atoms * S::ATOM));
                         for (int j = 0; j < a_atoms; ++j)
-                            ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow, oh,
-                                             n64 * KIMG);
+                            ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow,
+                                             od * p.OHr + oh, n64 * KIMG);
                     } else {
-                        const int ih = oh * p.sh + c.fh - p.ph;  // leaping access (Fig. 7)
+                        // leaping access (Fig. 7) on every axis: flattened X row of (id, ih)
+                        const int ih = (od * p.sd + c.fd - p.pd) * p.Hr + oh * p.sh + c.fh - p.ph;
                         uint32_t nv = 0;
 #pragma unroll
                         for (int f = 0; f < MT; ++f) nv += (MT == 1 || (ow >= p.ow_s[f] && ow < p.ow_e[f])) ? 1u : 0u;
@@ -248,7 +262,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp >= 4) {
         const uint32_t sub = warp & 3;
         const int row = int(sub * 32 + lane);
-        const int taps = p.FH * p.FW;
+        const int taps = p.FD * p.FH * p.FW;
         const bool vec4 = (p.C % 4) == 0;
         uint32_t acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
@@ -267,7 +281,8 @@ __global__ void __launch_bounds__(256, 1)
                 dst = reinterpret_cast<float*>(smem) + (f * (BN / 4)) * 512 + row * 4;
             else if (oc < p.OC)
                 dst = p.out + c.z * p.part_stride +
-                      (static_cast<long long>(oc) * taps + c.fh * p.FW + (MT > 1 ? f : c.fw)) * p.C + cbase;
+                      (static_cast<long long>(oc) * taps + (c.fd * p.FH + c.fh) * p.FW + (MT > 1 ? f : c.fw)) * p.C +
+                      cbase;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r[32];
@@ -322,7 +337,7 @@ __global__ void __launch_bounds__(256, 1)
             const int G = MT * BN / 4;
             const int g0 = (c.z * G) / p.gz, g1 = ((c.z + 1) * G) / p.gz;
             const uint32_t sbase = ptx::smem_u32(smem) + uint32_t(row) * 16u;
-            const int taps = p.FH * p.FW;
+            const int taps = p.FD * p.FH * p.FW;
             if (oc < p.OC) {
 #pragma unroll 1
                 for (int gq = g0; gq < g1; gq += 2) {
@@ -353,7 +368,8 @@ __global__ void __launch_bounds__(256, 1)
                         const int gg = gq + h;
                         const int f = gg / (BN / 4), ic = c.nb * BN + (gg % (BN / 4)) * 4;
                         if (ic >= p.C) continue;
-                        float* o = p.out + (static_cast<long long>(oc) * taps + c.fh * p.FW + (MT > 1 ? f : c.fw)) * p.C + ic;
+                        float* o = p.out + (static_cast<long long>(oc) * taps + (c.fd * p.FH + c.fh) * p.FW +
+                                            (MT > 1 ? f : c.fw)) * p.C + ic;
                         if ((p.C % 4) == 0) {
                             *reinterpret_cast<float4*>(o) = v;
                         } else {

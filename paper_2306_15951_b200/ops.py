@@ -166,6 +166,66 @@ def dilated_wgrad(x, dy, filter_hw, stride=1, padding=0, gz=0, out=None, stream=
     return out
 
 
+# --------------------------------------------------------------- 3-D C-K-S
+# NDHWC activations, OIDHW-as-[OC][FD][FH][FW][C] filters.
+def _triple(v):
+    return (v, v, v) if isinstance(v, int) else tuple(v)
+
+
+def _geom3(x_shape, w_shape, stride, padding):
+    N, D, H, W, C = x_shape
+    OC, FD, FH, FW, C2 = w_shape
+    if C != C2:
+        raise ValueError("X channels != W in-channels")
+    (sd, sh, sw), (pd, ph, pw) = _triple(stride), _triple(padding)
+    return L.make_geom3(N, C, D, H, W, OC, FD, FH, FW, sd, sh, sw, pd, ph, pw)
+
+
+def conv3d_fwd(x, w, stride=1, padding=0, out=None, stream=None):
+    """Y = conv3D(X, W) by ConvV2 with trimmed windows on all three axes."""
+    _check_dev(x, w, out)
+    dt = _dtype_code(x)
+    g = _geom3(tuple(x.shape), tuple(w.shape), stride, padding)
+    OD, OH, OW = L.cks_output_shape3(g)
+    if out is None:
+        out = _empty((g.N, OD, OH, OW, g.OC), torch.float32, x.device, stream)
+    ws = workspace(L.cks_workspace_size3(g, dt, L.CKS_OP_FWD), x.device, stream)
+    L.cks_conv3d_fwd(g, dt, x.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out
+
+
+def deconv3d(dy, w, x_dhw, stride=1, padding=0, out=None, stream=None):
+    """dX = deconv3D(dY, W^rot180) by Stage1-free KS-deconv (sd*sh*sw phases)."""
+    _check_dev(dy, w, out)
+    dt = _dtype_code(dy)
+    N = dy.shape[0]
+    D, H, W = x_dhw
+    g = _geom3((N, D, H, W, w.shape[4]), tuple(w.shape), stride, padding)
+    if L.cks_output_shape3(g) != tuple(dy.shape[1:4]):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = _empty((N, D, H, W, g.C), torch.float32, dy.device, stream)
+    ws = workspace(L.cks_workspace_size3(g, dt, L.CKS_OP_DECONV), dy.device, stream)
+    L.cks_deconv3d(g, dt, dy.data_ptr(), w.data_ptr(), out.data_ptr(), *_ws_args(ws), _stream_ptr(stream))
+    return out
+
+
+def dilated_wgrad3d(x, dy, filter_dhw, stride=1, padding=0, gz=0, out=None, stream=None):
+    """dW = dilated_conv3D(X, dY) by Sk-dilated with leaping access on all axes."""
+    _check_dev(x, dy, out)
+    dt = _dtype_code(x)
+    FD, FH, FW = filter_dhw
+    g = _geom3(tuple(x.shape), (dy.shape[4], FD, FH, FW, x.shape[4]), stride, padding)
+    if L.cks_output_shape3(g) != tuple(dy.shape[1:4]):
+        raise ValueError("dY spatial shape does not match the geometry")
+    if out is None:
+        out = _empty((g.OC, FD, FH, FW, g.C), torch.float32, x.device, stream)
+    ws = workspace(L.cks_workspace_size3(g, dt, L.CKS_OP_WGRAD, gz), x.device, stream)
+    L.cks_dilated_wgrad3d(g, dt, x.data_ptr(), dy.data_ptr(), out.data_ptr(), gz, *_ws_args(ws),
+                          _stream_ptr(stream))
+    return out
+
+
 # ----------------------------------------------------------------- KB-ZINS
 # The zero-inserting / zero-padding formulation (include/cks.h KB-ZINS), on the
 # same tensor-core kernels: a measurement baseline for the zeros C-K-S skips.

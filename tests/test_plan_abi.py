@@ -7,6 +7,7 @@ import os
 import re
 import sys
 
+import numpy as np
 import pytest
 
 import oracle as O
@@ -284,3 +285,26 @@ def test_mma_program_capacity_bound():
                 d = L.plan_dict(g, dt, op)
                 if d["kind"] == "igemm":
                     assert int(d["pbw"]) * int(d["ntap"]) <= 64, (geo, dt, op, d)
+
+
+def test_op_counts3_match_oracle():
+    """3-D zero-free MAC counts: library (closed forms per axis) == oracle
+    (enumeration of the valid (o, f) pairs), bit-exact."""
+    from oracle import cks_oracle3d as O3
+    rng = np.random.default_rng(12)
+    n = 0
+    while n < 200:
+        f = [int(rng.integers(1, 6)) for _ in range(3)]
+        s = [int(rng.integers(1, 5)) for _ in range(3)]
+        p = [int(rng.integers(0, ff)) for ff in f]
+        dhw = [int(rng.integers(1, 14)) for _ in range(3)]
+        if any(i + 2 * pp - ff < 0 for i, ff, pp in zip(dhw, f, p)):
+            continue
+        N, C, OC = int(rng.integers(1, 5)), int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        g = L.make_geom3(N, C, *dhw, OC, *f, *s, *p)
+        got = L.cks_op_counts3(g)
+        ref = O3.op_counts3d(N, C, OC, dhw, f, s, p)
+        assert got["zero_free_macs"] == ref["zero_free_macs"]
+        assert [got["VD"], got["VH"], got["VW"]] == ref["V"]
+        assert list(L.cks_output_shape3(g)) == ref["O"]
+        n += 1

@@ -1,4 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
 T=${1:-x}
-timeout 600 python -m pytest tests/test_gpu_allreduce.py -q -x > gpurun_out/${T}_ar.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_3d.py -q -x > gpurun_out/${T}_3d.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/${T}_pytest.log 2>&1
