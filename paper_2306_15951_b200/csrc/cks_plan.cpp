@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -148,6 +148,8 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_ZC")) wzc = atoi(e);
         if (const char* e = cks_knob("CKS_EPI_BUFS")) epi_bufs = atoi(e) == 2 ? 2 : 1;  // TMA-store staging depth
         if (const char* e = cks_knob("CKS_WGRAD_A1")) wa1 = atoi(e) != 0;  // O_C <= 64: one dY atom per stage
+        if (const char* e = cks_knob("CKS_WGRAD_MT_TF32")) wmt_tf32 = atoi(e) != 0;  // TF32 row tiles
+        if (const char* e = cks_knob("CKS_WGRAD_A1_TF32")) wa1_tf32 = atoi(e) != 0;  // TF32: 64 OC of dY per stage
     }
 };
 static const Knobs& knobs() {
@@ -679,7 +681,8 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
     c.nblk64 = int((g.N + c.kimg - 1) / c.kimg);
     // row tiles (all F_W = 3 taps of a filter row per tile, the dY block shared):
     // bf16, IC <= 64 (three double-buffered 64-column accumulators fit TMEM)
-    c.mt = (dt == CKS_BF16 && c.BN == 64 && g.FW == 3 && knobs().wmt) ? 3 : 1;
+    // TF32 row tiles keep 64-image k-blocks (3 x 16 KB X blocks + 2 dY atoms per stage)
+    c.mt = (c.BN == 64 && g.FW == 3 && knobs().wmt && (dt == CKS_BF16 || knobs().wmt_tf32)) ? 3 : 1;
     Axis ah = axis_h(g), aw = axis_w(g);
     auto th = table_t3(ah), tw = table_t3(aw);
     int64_t dmul = 1;  // 3-D: taps x depth windows (the smallest depth window for lmin)
@@ -716,6 +719,11 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
             }
         if (ntaps == 0) lmin = 1;
     }
+    if (dt == CKS_TF32 && c.mt > 1) {  // TF32 row tiles: 64-image k-blocks (the k range shrinks with them)
+        if (c.kimg == 128) lmin *= 2;
+        c.kimg = 64;
+        c.nblk64 = int((g.N + 63) / 64);
+    }
     c.base_tiles = (ad ? ad->F : 1) * int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
     if (gz_req > 0) {
         c.gz = gz_req;
@@ -727,11 +735,11 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
     // cluster reduce (zc): gz <= 8 segments of a tile as one thread-block cluster,
     // one tile per CTA (one wave), the tile's fp32 sums staged in the idle ring
     // (same stage arithmetic as WgradShape) -- no partials in HBM, no KB-REDUCE launch
-    c.a1 = (dt == CKS_BF16 && c.BN == 64 && g.OC <= 64 && knobs().wa1) ? 1 : 0;
+    c.a1 = (c.BN == 64 && g.OC <= 64 && knobs().wa1 && (dt == CKS_BF16 || knobs().wa1_tf32)) ? 1 : 0;
     {
         const int eb = dt == CKS_TF32 ? 4 : 2, ch = 128 / eb;
         const int64_t atom = int64_t(c.kimg) * 128;
-        const int64_t stage = (c.a1 ? 1 : 128 / ch) * atom + int64_t(c.mt) * (c.BN / ch) * atom;
+        const int64_t stage = (c.a1 ? 64 / ch : 128 / ch) * atom + int64_t(c.mt) * (c.BN / ch) * atom;
         const int64_t stages = std::min<int64_t>(8, 200 * 1024 / stage);
         const bool fits = int64_t(128) * c.mt * c.BN * 4 <= stages * stage;
         // every cluster must be resident at once (one tile per CTA): B200 GPCs hold

@@ -71,6 +71,7 @@ __device__ __forceinline__ void ar_barrier(const ArParams& p, int k, unsigned ep
             __nanosleep(64);
         }
     }
+    __syncwarp();
     __syncthreads();
 }
 
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(256) reduce_allreduce_kernel(const __grid_cons
     ptx::pdl_wait();
     __shared__ unsigned s_epoch;
     if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(p.count + 2) + 1u;  // this call's number
+    __syncwarp();
     __syncthreads();
     const unsigned epoch = s_epoch;
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;

@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         ptx::fence_barrier_init();
     }
+    __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) {
         if (kPair)
             ptx::tmem_alloc_pair(tmem_slot, tmem_cols);
@@ -896,6 +897,7 @@ __global__ void __launch_bounds__(384, 1)
                     *red_flag = last;
                     __threadfence();
                 }
+                __syncwarp();
                 asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");
                 if (et == 0) trace_ev(p, 2, ti, 3);
                 if (*red_flag && n < p.N && half == 0) {
@@ -939,6 +941,7 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                 }
+                __syncwarp();
                 asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");  // red_flag reuse guard
                 if (et == 0) trace_ev(p, 2, ti, 4);
             }

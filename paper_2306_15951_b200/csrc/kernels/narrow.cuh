@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::fence_barrier_init();
     }
+    __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
     ptx::pdl_wait();  // W and X may come from the previous kernel
     {   // all threads: this class's filter rows in the K-major swizzled B layout,
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_init(tempty, 128);
         ptx::fence_barrier_init();
     }
+    __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
     ptx::tc_fence_before();
     __syncthreads();

@@ -52,9 +52,10 @@ struct WgradParams {
 // an MN-major swizzle atom column.  BF16: SWIZZLE_128B (16 B chunks, 8-row
 // K groups, SBO 1 KB).  TF32: SWIZZLE_128B_BASE32B (32 B chunks, 4-row K
 // groups, SBO 512 B) -- the MN-major layout tcgen05 kind::tf32 requires.
-// A1: O_C <= 64 -- the stage holds ONE dY atom; the MMA's other 64 A rows read
-// the stage's first X block (garbage rows of D, never stored), so the ring
-// carries one more stage instead of a zero-filled atom.
+// A1: O_C <= 64 -- the stage holds only the dY atoms of 64 channels (one bf16
+// atom, two tf32 atoms); the MMA's other 64 A rows read the stage's first X
+// block (garbage rows of D, never stored), so the ring carries one more stage
+// instead of zero-filled atoms.
 template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false>
 struct WgradShape {
     static constexpr int EB = kTF32 ? 4 : 2;
@@ -64,7 +65,7 @@ struct WgradShape {
     static constexpr int B_BYTES = (BN / CH) * ATOM;    // BN IC x KIMG images
     static constexpr int UK = 32 / EB;                  // K (images) per MMA
     static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
-    static constexpr int A_STAGE = A1 ? ATOM : A_BYTES;  // dY bytes reserved per stage
+    static constexpr int A_STAGE = A1 ? (64 / CH) * ATOM : A_BYTES;  // dY bytes reserved per stage (A1: 64 OC)
     static constexpr int STAGE_BYTES = A_STAGE + MT * B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::fence_barrier_init();
     }
+    __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, S::TMEM_COLS);
     ptx::tc_fence_before();
     __syncthreads();

@@ -36,3 +36,25 @@ def test_reference_arm_non_zero_rank_is_silent():
                           "--warmup", "0", "--config", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT,
                          env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_gpus_n_self_launches_ranks(monkeypatch):
+    """--gpus N without torchrun re-launches bench.py under torch.distributed.run
+    with N processes on 127.0.0.1 (the driver may call it either way)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+
+    import subprocess as sp
+    monkeypatch.setattr(sp, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    assert bench.main() == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"] and cmd[-5].endswith("bench.py")

@@ -476,15 +476,17 @@ def test_autograd_generator_layer(torch_cuda, dtype):
                                     (Layer("rt3", 130, 64, 40, 40, 64, 3, 3, 1, 1, 0, 0), 7),
                                     (Layer("rt4", 130, 64, 40, 40, 64, 5, 3, 1, 1, 2, 1), 1)],
                          ids=lambda v: v.name if isinstance(v, Layer) else f"gz{v}")
-def test_wgrad_row_tiles(torch_cuda, lay, gz):
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_wgrad_row_tiles(torch_cuda, lay, gz, dtype):
     """Large-map 3-wide filters with I_C <= 64 take the row-tile Sk-dilated
     kernel (one filter row's F_W taps per tile share the dY block, per-tap
-    trimmed ow ranges, O_C < 128 loads only the valid dY rows): against the
-    oracle, for several G_Z segmentations, deterministic on repeat."""
-    a, got = run_all(torch_cuda, lay, "bf16", config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)
+    trimmed ow ranges, O_C <= 64 loads only the valid dY rows -- one bf16 /
+    two tf32 atoms): against the oracle, for several G_Z segmentations,
+    deterministic on repeat."""
+    a, got = run_all(torch_cuda, lay, dtype, config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)
     ref = O.wgrad_ref(a["X"], a["dY"], lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
-    check(got["wgrad"], ref, "bf16", f"{lay} row-tile wgrad gz={gz}", red_len(lay, "wgrad"))
-    again = run_all(torch_cuda, lay, "bf16", config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)[1]["wgrad"]
+    check(got["wgrad"], ref, dtype, f"{lay} row-tile wgrad gz={gz}", red_len(lay, "wgrad"))
+    again = run_all(torch_cuda, lay, dtype, config=15, idx=int(lay.name[2:]), ops=("wgrad",), gz=gz)[1]["wgrad"]
     np.testing.assert_array_equal(got["wgrad"], again)
 
 

@@ -18,7 +18,8 @@ def main():
     build.build()  # libcks.so, or libcks_exp.so under CKS_EXPERIMENTS=1 (knob sweeps)
     desc, layers = get_config(cfg)
     idx = [l.name for l in layers].index(name)
-    b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0))
+    b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0),
+                  os.environ.get("CKS_DTYPE", "bf16"))
     b.dW = torch.empty((b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C), dtype=torch.float32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(reps):

@@ -106,10 +106,10 @@ def main(tag, key="config4/tf32"):
         rows = read_ncu_csv(tp)
         by = defaultdict(lambda: defaultdict(float))
         for r in rows:
-            key = (r["ID"], r["Kernel Name"])
+            lk = (r["ID"], r["Kernel Name"])
             v = float(r["Metric Value"].replace(",", ""))
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r["Metric Unit"], 1)
-            by[key][r["Metric Name"]] += v * mult
+            by[lk][r["Metric Name"]] += v * mult
         agg = defaultdict(list)
         for (i, name), m in by.items():
             b = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)

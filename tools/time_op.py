@@ -22,7 +22,7 @@ def main():
         base = "deconv" if op in ("split", "deconv_only") else op
         if names and lay.name not in names or base not in lay.ops:
             continue
-        b = LayerBufs(torch, lay, cfg, idx, 0, torch.device("cuda", 0))
+        b = LayerBufs(torch, lay, cfg, idx, 0, torch.device("cuda", 0), os.environ.get("CKS_DTYPE", "bf16"))
         b.dW = torch.empty((lay.OC, lay.FH, lay.FW, lay.C), dtype=torch.float32, device="cuda")
         for _ in range(3):
             b.run(op, s.cuda_stream)
