@@ -482,6 +482,11 @@ cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const Wgra
         if (p.gz > 8) return CKS_ERR_UNSUPPORTED;
         return launch_pdl_cluster(kern, dim3(unsigned(p.num_tiles)), dim3(256), S::SMEM_BYTES, st, p.gz, a, b, p);
     }
+    if (p.tcmc) {  // filter-row clusters: tc consecutive tiles (the filter rows of one segment) per cluster
+        long long grid = std::min<long long>(p.num_tiles, device_sms() / p.tc * p.tc);
+        if (grid < p.tc || p.num_tiles % p.tc) return CKS_ERR_UNSUPPORTED;
+        return launch_pdl_cluster(kern, dim3(unsigned(grid)), dim3(256), S::SMEM_BYTES, st, p.tc, a, b, p);
+    }
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
     return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), S::SMEM_BYTES, st, a, b, p);
@@ -698,6 +703,16 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.num_tiles = cfg.base_tiles * cfg.gz;
     p.part_stride = part_stride;
     p.zc = cfg.zc;
+    p.tc = cfg.tc;
+    p.tcmc = cfg.tcmc;
+    p.ouh_s = 1 << 20;
+    p.ouh_e = -(1 << 20);
+    for (auto& a : th)
+        if (a.oh_e > a.oh_s) {
+            p.ouh_s = std::min<int>(p.ouh_s, int(a.oh_s));
+            p.ouh_e = std::max<int>(p.ouh_e, int(a.oh_e));
+        }
+    if (p.ouh_e < p.ouh_s) p.ouh_e = p.ouh_s = 0;
     p.ouw_s = 1 << 20;
     p.ouw_e = -(1 << 20);
     for (auto& b : tw)

@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -150,6 +150,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_A1")) wa1 = atoi(e) != 0;  // O_C <= 64: one dY atom per stage
         if (const char* e = cks_knob("CKS_WGRAD_MT_TF32")) wmt_tf32 = atoi(e) != 0;  // TF32 row tiles
         if (const char* e = cks_knob("CKS_WGRAD_A1_TF32")) wa1_tf32 = atoi(e) != 0;  // TF32: 64 OC of dY per stage
+        if (const char* e = cks_knob("CKS_WGRAD_TC")) wtc = atoi(e);  // filter-row groups (2: multicast clusters)
     }
 };
 static const Knobs& knobs() {
@@ -648,8 +649,8 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                  r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, (long long)r.tiles, int(r.cls.size()));
         return std::string(b) + row_classes_str(r.cls);
     }
-    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d base_tiles=%lld", w.BN, w.nbs,
-             w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, (long long)w.base_tiles);
+    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d tc=%d base_tiles=%lld", w.BN, w.nbs,
+             w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, w.tc, (long long)w.base_tiles);
     return b;
 }
 
@@ -769,6 +770,13 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
                 c.zc = 1;
             }
         }
+    }
+    // filter-row clusters (row tiles, no in-cluster G_Z reduce): the F_H row tiles of a segment share
+    // each dY block by multicast and walk the union of their oh ranges in lockstep
+    // (CKS_WGRAD_TC: 0 off, 1 aligned groups, 2 aligned groups as multicast clusters)
+    if (knobs().wtc && c.mt > 1 && !c.zc && g.FH >= 2 && g.FH <= 8) {
+        c.tc = int(g.FH);
+        c.tcmc = knobs().wtc == 2 ? 1 : 0;
     }
     return c;
 }

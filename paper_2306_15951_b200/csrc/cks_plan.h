@@ -170,6 +170,8 @@ struct WgradCfg {
     int mt = 1;        // taps per tile along w: 1, or F_W (row tiles sharing the dY block)
     int zc = 0;        // cluster reduce: the gz segments of a tile form one cluster (DSMEM sum, no partials)
     int a1 = 0;        // O_C <= 64 (bf16, BN = 64): one dY atom per ring stage
+    int tc = 0;        // filter-row group (row tiles: the F_H filter rows of a segment walk the same k-blocks)
+    int tcmc = 0;      // the group is a cluster with dY multicast
 };
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tmem_alloc(tmem_slot, tmem_cols);
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    ptx::block_sync();
     if (p.cm > 1 || kPair) ptx::cluster_sync();  // peers' barriers exist before the first multicast / pair op
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     }
-    __syncthreads();
+    ptx::block_sync();
     if (p.zc) {
         // cluster split-K reduce: every rank's segment is staged in its smem
         ptx::cluster_sync();

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    ptx::block_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int ci = int(blockIdx.x) - cl.base;
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, 1)
         if (p.tma_store && ptx::elect_one()) ptx::bulk_wait_read0();
         __syncwarp();
     }
-    __syncthreads();
+    ptx::block_sync();
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, tmem_cols);
     ptx::tc_fence_before();
-    __syncthreads();
+    ptx::block_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     ptx::pdl_wait();
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(256, 1)
             tph ^= 1u;
         }
     }
-    __syncthreads();
+    ptx::block_sync();
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, tmem_cols);

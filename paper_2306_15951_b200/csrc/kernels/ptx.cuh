@@ -89,6 +89,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// Block-wide barrier that tolerates warps arriving divergently (non-.aligned
+// barrier.sync): the role-specialised kernels reach their join / post-init
+// barriers from per-lane code paths (elected issuers, single-lane barrier
+// initialisation), where __syncthreads' barrier.sync.aligned would require
+// converged warps (compute-sanitizer synccheck).
+__device__ __forceinline__ void block_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -25,6 +25,16 @@
 // outside its own range [ow_s(fw), ow_e(fw)) (T3) neither loads nor multiplies
 // (trimming stays exact).  Only the valid rows of the dY block (O_C channels)
 // are loaded; accumulator rows >= O_C are never stored.
+//
+// Filter-row clusters (TC = F_H row tiles, round 2): the F_H row tiles of one
+// segment form a thread-block cluster that walks the UNION of the filter rows'
+// trimmed oh ranges in lockstep; cluster rank 0 loads each dY block once and
+// multicasts it to the F_H CTAs (a filter row outside its own oh range neither
+// loads X nor multiplies, so trimming stays exact), and every CTA's MMA commit
+// releases the stage in all of them.  dY then crosses L2 -> SM once per
+// segment instead of F_H times and the CTAs that share it stay in step (DRAM
+// re-reads of dY / X between filter rows: ncu showed 2.7x the algorithmic
+// bytes on the ResNet l1 layers without it).
 #pragma once
 #include "ptx.cuh"
 
@@ -46,6 +56,10 @@ struct WgradParams {
     long long part_stride;  // OC*FH*FW*C
     int zc;                 // cluster reduce: the gz segments of one tile are the gz CTAs of one cluster;
                             // partials staged in smem, summed in fixed order through DSMEM into dW
+    int tc;                 // filter-row group size (F_H; 0/1 = off), row tiles only: the group's tiles walk
+                            // the union oh range with identical segments (adjacent tiles)
+    int tcmc;               // 1: the group is a cluster and rank 0 multicasts each dY block
+    int ouh_s, ouh_e;       // filter-row clusters: union of the filter rows' oh ranges
 };
 
 // One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
@@ -84,6 +98,11 @@ template <int MT>
 __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     WTile c;
     uint32_t t = uint32_t(t64);  // 32-bit decode (64-bit div/mod is slow)
+    int tcr = 0;                 // filter-row cluster: rank = filter row (fastest)
+    if (p.tc > 1) {
+        tcr = int(t % uint32_t(p.tc));
+        t /= uint32_t(p.tc);
+    }
     if (p.zc) {  // segments fastest: the gz CTAs of a cluster share (tap, mb, nb)
         c.z = int(t % uint32_t(p.gz));
         t /= uint32_t(p.gz);
@@ -96,15 +115,15 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
         c.z = int(t % uint32_t(p.gz));
         t /= uint32_t(p.gz);
     }
-    const int tap = int(t);
+    const int tap = p.tc > 1 ? int(t) * p.tc + tcr : int(t);
     const int fdh = MT > 1 ? tap : tap / p.FW;  // filter (depth, row)
     c.fd = fdh / p.FH;
     c.fh = fdh - c.fd * p.FH;
     c.fw = MT > 1 ? 0 : tap % p.FW;
-    c.ohs = p.oh_s[c.fh];
+    c.ohs = p.tc > 1 ? p.ouh_s : p.oh_s[c.fh];
     c.ods = p.od_s[c.fd];
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
-    const int hn = p.oh_e[c.fh] - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
+    const int hn = (p.tc > 1 ? p.ouh_e : p.oh_e[c.fh]) - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     const int dn = p.od_e[c.fd] - c.ods;
     c.wn = wn;
     c.hn = hn;
@@ -117,6 +136,15 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
 // row tiles: does tap fw see any k-block of the segment (else its partial is 0)?
 __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& p, int fw) {
     if (c.kb1 <= c.kb0 || c.wn <= 0) return false;
+    if (p.tc > 1) {  // union oh range: walk the segment's positions (this filter row's oh, the tap's ow)
+        const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
+        for (int q = p0; q <= p1; ++q) {
+            const int pq = q / c.wn;
+            const int oh = c.ohs + (pq % c.hn), ow = c.ows + (q - pq * c.wn);
+            if (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh] && ow >= p.ow_s[fw] && ow < p.ow_e[fw]) return true;
+        }
+        return false;
+    }
     const int s = p.ow_s[fw] - c.ows, e = p.ow_e[fw] - c.ows;  // tap range, relative to the union start
     if (e <= s) return false;
     const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
@@ -150,7 +178,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < S::STAGES; ++i) {
             ptx::mbar_init(&full[i], 2);  // A producer + B producer
-            ptx::mbar_init(&empty[i], 1);
+            ptx::mbar_init(&empty[i], p.tcmc ? p.tc : 1);  // filter-row cluster: every CTA's MMA commit
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&tfull[i], 1);
@@ -161,9 +189,12 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, S::TMEM_COLS);
     ptx::tc_fence_before();
-    __syncthreads();
+    ptx::block_sync();
+    if (p.tcmc) ptx::cluster_sync();  // peers' barriers exist before the first multicast / remote commit
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tcrank = p.tc > 1 ? blockIdx.x % uint32_t(p.tc) : 0u;
+    const uint16_t tcmask = uint16_t((1u << (p.tcmc ? p.tc : 1)) - 1u);
     ptx::pdl_wait();  // inputs of this op may come from the previous kernel
 
     if (warp == 0 || warp == 3) {
@@ -181,6 +212,8 @@ __global__ void __launch_bounds__(256, 1)
                 const int ow = c.ows + (pos - pq * c.wn);
                 const int dq = pq / c.hn;
                 const int oh = c.ohs + (pq - dq * c.hn), od = c.ods + dq;
+                // filter-row clusters walk the union oh range: rows outside this filter row's own range
+                const bool ohok = p.tc <= 1 || (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh]);
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * S::STAGE_BYTES;
                 if (ptx::elect_one()) {
@@ -188,19 +221,27 @@ __global__ void __launch_bounds__(256, 1)
                         // only the atoms holding valid O_C rows (the rest of the MMA's M rows are never stored)
                         const int a_atoms = min(128 / S::CH, (p.OC - c.mb * 128 + S::CH - 1) / S::CH);
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(a_atoms * S::ATOM));
-                        for (int j = 0; j < a_atoms; ++j)
-                            ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow,
-                                             od * p.OHr + oh, n64 * KIMG);
+                        if (p.tcmc) {  // rank 0 loads the dY block once for the cluster (multicast)
+                            if (tcrank == 0)
+                                for (int j = 0; j < a_atoms; ++j)
+                                    ptx::tma_load_4d_mc(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH,
+                                                        ow, od * p.OHr + oh, n64 * KIMG, tcmask);
+                        } else {
+                            for (int j = 0; j < a_atoms; ++j)
+                                ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow,
+                                                 od * p.OHr + oh, n64 * KIMG);
+                        }
                     } else {
                         // leaping access (Fig. 7) on every axis: flattened X row of (id, ih)
                         const int ih = (od * p.sd + c.fd - p.pd) * p.Hr + oh * p.sh + c.fh - p.ph;
                         uint32_t nv = 0;
 #pragma unroll
-                        for (int f = 0; f < MT; ++f) nv += (MT == 1 || (ow >= p.ow_s[f] && ow < p.ow_e[f])) ? 1u : 0u;
+                        for (int f = 0; f < MT; ++f)
+                            nv += (ohok && (MT == 1 || (ow >= p.ow_s[f] && ow < p.ow_e[f]))) ? 1u : 0u;
                         ptx::mbar_arrive_expect_tx(&full[stage], nv * S::B_BYTES);
 #pragma unroll
                         for (int f = 0; f < MT; ++f) {
-                            if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
+                            if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) continue;  // trimmed tap
                             const int iw = ow * p.sw + (MT > 1 ? f : c.fw) - p.pw;
 #pragma unroll
                             for (int j = 0; j < BN / S::CH; ++j)
@@ -234,10 +275,15 @@ __global__ void __launch_bounds__(256, 1)
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
                 const uint64_t ad = dconst | ptx::desc_addr(a_addr);
                 const int ow = c.ows + (kb / p.nblk64) % max(c.wn, 1);
+                bool ohok = true;
+                if (p.tc > 1) {
+                    const int oh = c.ohs + ((kb / p.nblk64) / max(c.wn, 1)) % max(c.hn, 1);
+                    ohok = oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh];
+                }
                 if (ptx::elect_one()) {
 #pragma unroll
                     for (int f = 0; f < MT; ++f) {
-                        if (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f])) continue;  // trimmed tap
+                        if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) continue;  // trimmed tap
                         const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_STAGE + f * S::B_BYTES);
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
 #pragma unroll
@@ -246,7 +292,10 @@ __global__ void __launch_bounds__(256, 1)
                                                bd + uint64_t(kk * (S::KSTEP >> 4)), idesc, (acc0 | uint32_t(kk)) != 0);
                         started |= 1u << f;
                     }
-                    ptx::mma_commit(&empty[stage]);
+                    if (p.tcmc)
+                        ptx::mma_commit_mc(&empty[stage], tcmask);  // the stage's dY is every cluster CTA's
+                    else
+                        ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
                 if (++stage == S::STAGES) {
@@ -327,7 +376,7 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
     }
-    __syncthreads();
+    ptx::block_sync();
     if (p.zc) {
         // G_Z map-reduce inside the cluster: CTA z sums column slice z of the
         // tile over the gz segments in fixed order z' = 0..gz-1 and writes dW
@@ -383,6 +432,8 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         ptx::cluster_sync();  // peers finished reading this CTA's staging
+    } else if (p.tcmc) {
+        ptx::cluster_sync();  // no CTA leaves while peers may still multicast into it / commit to it
     }
     if (warp == 2) {
         ptx::tc_fence_after();
