@@ -332,9 +332,10 @@ cks_status launch_igemm(int BN, int KB, bool tf32, const CUtensorMap& a, const C
         if (BN == 128) return launch_igemm_bmn<128, false>(KB, a, b, y, p, smem, st);
         return CKS_ERR_UNSUPPORTED;
     }
-    if (p.pair) {  // CTA pairs: bf16, 128 B K blocks, 128 output channels per CTA (plan invariant)
-        if (tf32 || KB != 128 || BN != 128) return CKS_ERR_UNSUPPORTED;
-        return launch_igemm_t<128, false, 128, true>(a, b, y, p, smem, st);
+    if (p.pair) {  // CTA pairs: 128 B K blocks, 128 output channels per CTA (plan invariant)
+        if (KB != 128 || BN != 128) return CKS_ERR_UNSUPPORTED;
+        return tf32 ? launch_igemm_t<128, true, 128, true>(a, b, y, p, smem, st)
+                    : launch_igemm_t<128, false, 128, true>(a, b, y, p, smem, st);
     }
     if (tf32) {
         if (KB == 32) return launch_igemm_kb<true, 32>(BN, a, b, y, p, smem, st);

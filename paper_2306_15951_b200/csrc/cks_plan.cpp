@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -141,6 +141,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_EPI8")) epi8 = atoi(e);
         if (const char* e = cks_knob("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
         if (const char* e = cks_knob("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
+        if (const char* e = cks_knob("CKS_PAIR_TF32")) pair_tf32 = atoi(e) != 0;  // 0: BF16-only CTA pairs
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = cks_knob("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
@@ -331,7 +332,8 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
             c2.unified == c4.unified && c2.BN == c4.BN && c2.Z == c4.Z && c2.zc == c4.zc)
             c4 = c2;
     }
-    if (knobs().pair && eb == 2 && nout >= 256 && N > 128 && kchan * eb >= 128 && force_pbw == 0 && c4.pbw == 1 &&
+    if (knobs().pair && (eb == 2 || knobs().pair_tf32) && nout >= 256 && N > 128 && kchan * eb >= 128 &&
+        force_pbw == 0 && c4.pbw == 1 &&
         c4.nbs >= 2 && c4.Z == 1) {
         const IgemmCfg cp = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
                                         0, 4, true);

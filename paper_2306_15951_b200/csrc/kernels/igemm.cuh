@@ -534,11 +534,11 @@ __global__ void __launch_bounds__(384, 1)
                             const uint32_t d = dbase + uint32_t(en.z);
                             const uint32_t acc0 = uint32_t(en.w >> 16) & 1u;
                             if (!(p.dbg & 2) && ptx::elect_one()) {
-                                if (!kTF32 && kPair) {
+                                if (kPair) {
 #pragma unroll
                                     for (int kk = 0; kk < S::BK / S::UK; ++kk)
-                                        ptx::mma_ss_pair(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2), idesc,
-                                                         kk ? 1u : acc0);
+                                        ptx::mma_ss_pair<kTF32>(d, adesc + uint64_t(kk * 2), bdesc + uint64_t(kk * 2),
+                                                                idesc, kk ? 1u : acc0);
                                 } else {
 #pragma unroll
                                     for (int kk = 0; kk < S::BK / S::UK; ++kk)

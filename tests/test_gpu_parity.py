@@ -496,9 +496,10 @@ def test_wgrad_row_tiles(torch_cuda, lay, gz, dtype):
                                  Layer("pr2", 260, 128, 15, 14, 512, 3, 3, 2, 2, 1, 1),
                                  Layer("pr3", 384, 512, 8, 8, 256, 4, 4, 2, 2, 1, 1)],
                          ids=lambda l: l.name)
-def test_pair_tiles(torch_cuda, lay):
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_pair_tiles(torch_cuda, lay, dtype):
     """>= 256 output channels and > 128 images: 2-CTA tiles (M = 256 images of one
     pixel across a CTA pair, N = 256 channels, each CTA holding half of B); odd
     image-block counts leave the last pair's second CTA out of range.  Forward
     and KS-deconv (whose output channels are I_C) against the oracle."""
-    check_full(torch_cuda, lay, "bf16", config=16, idx=int(lay.name[2:]), ops=("fwd", "deconv"))
+    check_full(torch_cuda, lay, dtype, config=16, idx=int(lay.name[2:]), ops=("fwd", "deconv"))

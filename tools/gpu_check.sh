@@ -1,12 +1,11 @@
 #!/bin/bash
 mkdir -p gpurun_out
 T=${1:-x}
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_3d.py -q -x -k "row_tiles or 3d_layers or c1" > gpurun_out/${T}_tests.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "pair_tiles or full_size" > gpurun_out/${T}_tests.log 2>&1
 export CKS_EXPERIMENTS=1
-for dt in tf32 bf16; do
-  for tc in 1 0 2; do
-    echo "== $dt tc=$tc" >> gpurun_out/${T}_time.txt
-    CKS_DTYPE=$dt CKS_WGRAD_TC=$tc python tools/time_op.py 2 wgrad l1_0 20 >> gpurun_out/${T}_time.txt 2>&1
-    CKS_DTYPE=$dt CKS_WGRAD_TC=$tc timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:wgrad_kernel -c 1 python tools/prof_layer.py 2 l1_0 wgrad 1 2>&1 | grep -E "dram|duration" >> gpurun_out/${T}_time.txt
+for op in fwd deconv; do
+  for pt in 1 0; do
+    echo "== $op pair_tf32=$pt" >> gpurun_out/${T}_time.txt
+    CKS_DTYPE=tf32 CKS_PAIR_TF32=$pt python tools/time_op.py 2 $op l3a,l3_0,l3ds,l4a,l4_0 20 >> gpurun_out/${T}_time.txt 2>&1
   done
 done
