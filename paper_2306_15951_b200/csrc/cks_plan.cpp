@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -142,6 +142,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_MT")) wmt = atoi(e) != 0;  // 0: one tap per wgrad tile
         if (const char* e = cks_knob("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = cks_knob("CKS_PAIR_TF32")) pair_tf32 = atoi(e) != 0;  // 0: BF16-only CTA pairs
+        if (const char* e = cks_knob("CKS_TF32_WIDE")) tf32_wide = atoi(e) != 0;  // wide TF32 pixel blocks
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = cks_knob("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
@@ -238,6 +239,24 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
         if (2 * (int64_t(c.pa) * 128 * c.KB + c.stage_bytes) <= budget && c.pa <= 256) break;
     }
     if (pbw < 1) pbw = 1;
+    // Wide TF32 tiles: TF32 3x3 layers are bound by TMA ingress of the activation
+    // columns (ncu, C3 l1: tensor 42 %); a wider pixel block reuses each column for
+    // more (pixel, tap) pairs -- the row step then spans two A slots (a 3-deep A ring
+    // of half-row-step slots) instead of double-buffering whole row steps.
+    // Measured (TF32, warm): C3 l1 fwd / KS-deconv 143 -> 127 us, l2 122 -> 106 us.
+    int wide_apos = 0;
+    if (eb == 4 && !pair && force_pbw == 0 && knobs().tf32_wide && !(ov && ov_pbw > 0)) {
+        const int64_t stage = ntap * c.BN * c.KB, colb = int64_t(128) * c.KB;
+        for (int pb = pbw + 1; pb <= std::min<int64_t>({int64_t(256 / c.BN), 8, maxrow}); ++pb) {
+            // >= 3 waves of tiles (C3 l4, 7x7: 2-pixel tiles leave 1.5 waves and lose 15 %)
+            if (tiles_for(c.BN, pb) < 3 * int64_t(num_sms) || prog_entries_bound(pb, ntap, a0_step, c.BN) > kProgEntries)
+                break;
+            const int64_t pa_ = (pb - 1) * a0_step + ntap, ap = (pa_ + 1) / 2;
+            if (2 * stage + 3 * ap * colb > budget) break;
+            pbw = pb;
+            wide_apos = int(ap);
+        }
+    }
     c.pbw = pbw;
     c.pa = int((pbw - 1) * a0_step + ntap);
     c.stage_bytes = int(ntap * c.BN * c.KB);
@@ -248,6 +267,7 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     c.apos = c.pa;
     const int64_t col_bytes = 128 * c.KB;  // one activation column, 128 images
     while (c.apos > 1 && 2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > budget) --c.apos;
+    if (wide_apos > 0) c.apos = wide_apos;
     if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > budget) c.stages = 1;
     if (ov && g_ov_apos > 0) c.apos = std::min(c.pa, g_ov_apos);
     if (ov && g_ov_bst > 0) c.stages = g_ov_bst;

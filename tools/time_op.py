@@ -19,7 +19,7 @@ def main():
     desc, layers = get_config(cfg)
     s = torch.cuda.current_stream()
     for idx, lay in enumerate(layers):
-        base = "deconv" if op in ("split", "deconv_only") else op
+        base = "deconv" if op in ("split", "deconv_only", "deconv_w", "deconv_free") else op
         if names and lay.name not in names or base not in lay.ops:
             continue
         b = LayerBufs(torch, lay, cfg, idx, 0, torch.device("cuda", 0), os.environ.get("CKS_DTYPE", "bf16"))
