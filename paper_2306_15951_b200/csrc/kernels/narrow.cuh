@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0 || warp == 3) {
         // ---------------- producers: warp 0 = X rows (A, leaping access), warp 3 = dY (B)
         const bool is_b = warp == 3;
+        const uint64_t pol = is_b ? ptx::l2_policy_evict_first() : ptx::l2_policy_evict_last();
         uint32_t stage = 0, phase = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const RowWTile c(t, p);
@@ -404,16 +405,19 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::mbar_wait(&empty[stage], phase ^ 1u);
                 uint8_t* st = smem + stage * stage_bytes;
                 if (ptx::elect_one()) {
+                    // X boxes overlap across neighbouring columns and rows (FW*C-wide runs at
+                    // stride sw*C, FH rows at stride sh) and are re-read: keep them in L2 ahead of
+                    // dY, which is read once (L2 eviction priorities)
                     if (!is_b) {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(p.FH * 64 * ROWB));
-                        ptx::tma_load_4d(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
-                                         oh * p.sh - p.ph, 0);
+                        ptx::tma_load_4d_hint(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
+                                              oh * p.sh - p.ph, 0, pol);
                     } else {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(B_BYTES));
 #pragma unroll
                         for (int j = 0; j < BN / CH; ++j)
-                            ptx::tma_load_4d(st + p.a_bytes + j * 8192, &tmDY, &full[stage], c.nb * BN + j * CH, ow, oh,
-                                             n64 * 64);
+                            ptx::tma_load_4d_hint(st + p.a_bytes + j * 8192, &tmDY, &full[stage], c.nb * BN + j * CH,
+                                                  ow, oh, n64 * 64, pol);
                     }
                 }
                 __syncwarp();
