@@ -474,10 +474,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st, bmn != nullptr);
 }
 
-template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false>
+template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false, bool PP = false>
 cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
-    using S = WgradShape<BN, TF, KIMG, MT, A1>;
-    auto kern = wgrad_kernel<BN, TF, KIMG, MT, A1>;
+    using S = WgradShape<BN, TF, KIMG, MT, A1, PP>;
+    auto kern = wgrad_kernel<BN, TF, KIMG, MT, A1, PP>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     if (p.zc) {  // one tile per CTA, the gz segments of a tile are one cluster
         if (p.gz > 8) return CKS_ERR_UNSUPPORTED;
@@ -706,6 +706,8 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.zc = cfg.zc;
     p.tc = cfg.tc;
     p.tcmc = cfg.tcmc;
+    p.pp = cfg.pp;
+    p.Wx = int(g.W);
     p.ouh_s = 1 << 20;
     p.ouh_e = -(1 << 20);
     for (auto& a : th)
@@ -724,6 +726,12 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     if (p.ouw_e < p.ouw_s) p.ouw_e = p.ouw_s = 0;
     const bool tf = dt == CKS_TF32;
     const bool k128 = cfg.kimg == 128;
+    if (cfg.pp && cfg.BN == 64) {  // position pairs: two positions' dY on M, four X columns per k-block
+        if (tf) return k128 ? launch_wgrad_t<64, true, 128, 4, true, true>(ta, tb, p, st)
+                            : launch_wgrad_t<64, true, 64, 4, true, true>(ta, tb, p, st);
+        return k128 ? launch_wgrad_t<64, false, 128, 4, true, true>(ta, tb, p, st)
+                    : launch_wgrad_t<64, false, 64, 4, true, true>(ta, tb, p, st);
+    }
     if (cfg.a1 && !tf && cfg.BN == 64) {  // O_C <= 64: one dY atom per stage
         if (cfg.mt == 3)
             return k128 ? launch_wgrad_t<64, false, 128, 3, true>(ta, tb, p, st)
@@ -1093,7 +1101,7 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.row ? 64 : cfg.kimg)};
         if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
-    const bool partials = cfg.gz > 1 && !cfg.zc;
+    const bool partials = cfg.npart() > 1 && !cfg.zc;
     float* wout = partials ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial)
                            : (ar ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ar_local_offset(L)) : dw);
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
@@ -1118,7 +1126,7 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         q.world = ar->world;
         q.rank = ar->rank;
         q.slice = (q.nv + ar->world - 1) / ar->world;
-        q.gz = partials ? cfg.gz : 1;
+        q.gz = partials ? cfg.npart() : 1;
         for (int t = 0; t < ar->world; ++t) {
             q.recv[t] = static_cast<float4*>(ar->recv[t]);
             q.out[t] = reinterpret_cast<float4*>(ar->out[t]);
@@ -1131,17 +1139,18 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         const unsigned blocks = unsigned(std::max<long long>(1, std::min<long long>((need + 255) / 256, cap)));
         return launch_pdl(reduce_allreduce_kernel, dim3(blocks), dim3(256), 0, st, q);
     }
-    if (cfg.gz > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
+    if (cfg.npart() > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
         const long long n = part_stride;
         const bool v4 = n % 4 == 0;
         const long long nv = v4 ? n / 4 : n;
-        const unsigned G = unsigned(std::min(16, cfg.gz));
+        const int np = cfg.npart();
+        const unsigned G = unsigned(std::min(16, np));
         const unsigned blocks = unsigned(std::min<long long>((nv + 31) / 32, 148LL * 16));
         if (v4)
             return launch_pdl(reduce_partials_kernel<float4>, dim3(blocks), dim3(32, G), 0, st,
-                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, cfg.gz);
+                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, np);
         return launch_pdl(reduce_partials_kernel<float>, dim3(blocks), dim3(32, G), 0, st, (const float*)wout, dw, nv,
-                          cfg.gz);
+                          np);
     }
     return CKS_OK;
 }
@@ -1335,20 +1344,21 @@ cks_status cks_dilated_wgrad3d(const cks_geom3* g, cks_dtype dt, const void* x, 
         if (!make_tmap4(&tb, dt, xs, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
     }
     const long long part_stride = g->OC * g->FD * g->FH * g->FW * g->C;
-    float* wout = (cfg.gz > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
+    float* wout = (cfg.npart() > 1 && !cfg.zc) ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.partial) : dw;
     s = run_wgrad_taps(g2, dt, cfg, ah, aw, ta, tb, wout, part_stride, st, &ad);
     if (s != CKS_OK) return s;
-    if (cfg.gz > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
+    if (cfg.npart() > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
         const long long n = part_stride;
         const bool v4 = n % 4 == 0;
         const long long nv = v4 ? n / 4 : n;
-        const unsigned G = unsigned(std::min(16, cfg.gz));
+        const int np = cfg.npart();
+        const unsigned G = unsigned(std::min(16, np));
         const unsigned blocks = unsigned(std::min<long long>((nv + 31) / 32, 148LL * 16));
         if (v4)
             return launch_pdl(reduce_partials_kernel<float4>, dim3(blocks), dim3(32, G), 0, st,
-                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, cfg.gz);
+                              reinterpret_cast<const float4*>(wout), reinterpret_cast<float4*>(dw), nv, np);
         return launch_pdl(reduce_partials_kernel<float>, dim3(blocks), dim3(32, G), 0, st, (const float*)wout, dw, nv,
-                          cfg.gz);
+                          np);
     }
     return CKS_OK;
 }
@@ -1494,7 +1504,7 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
         const WgradCfg c = wgrad_cfg(*g, dt, gz, kPlanSMs);
         // + KB-REDUCE for G_Z partials; the fused variant always ends with KB-REDUCE-AR
         n += (cpad && !c.row ? 1 : 0) + (ocpad ? 1 : 0) +
-             (int(op) == CKS_OP_WGRAD_AR ? 1 : (c.gz > 1 && !c.zc ? 1 : 0));
+             (int(op) == CKS_OP_WGRAD_AR ? 1 : (c.npart() > 1 && !c.zc ? 1 : 0));
     }
     else return CKS_ERR_UNSUPPORTED;
     *launches = n;

@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -143,6 +143,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = cks_knob("CKS_PAIR_TF32")) pair_tf32 = atoi(e) != 0;  // 0: BF16-only CTA pairs
         if (const char* e = cks_knob("CKS_TF32_WIDE")) tf32_wide = atoi(e) != 0;  // wide TF32 pixel blocks
+        if (const char* e = cks_knob("CKS_WGRAD_PP")) wpp = atoi(e) != 0;  // Sk-dilated position pairs
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = cks_knob("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
@@ -671,8 +672,8 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                  r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, (long long)r.tiles, int(r.cls.size()));
         return std::string(b) + row_classes_str(r.cls);
     }
-    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d tc=%d base_tiles=%lld", w.BN, w.nbs,
-             w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, w.tc, (long long)w.base_tiles);
+    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d tc=%d pp=%d base_tiles=%lld",
+             w.BN, w.nbs, w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, w.tc, w.pp, (long long)w.base_tiles);
     return b;
 }
 
@@ -800,6 +801,15 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
         c.tc = int(g.FH);
         c.tcmc = knobs().wtc == 2 ? 1 : 0;
     }
+    // position pairs: O_C <= 64 row tiles with unit column stride and an even union ow range
+    if (knobs().wpp && c.mt == 3 && c.a1 && c.BN == 64 && g.sw == 1 && !c.zc && !c.tcmc && uwe > uws &&
+        (uwe - uws) % 2 == 0) {
+        c.pp = 1;
+        if (c.kimg == 128) {  // 64-image k-blocks: 48 / 96 KB stages (bf16 / tf32), a deeper ring
+            c.kimg = 64;
+            c.nblk64 = int((g.N + 63) / 64);
+        }
+    }
     return c;
 }
 
@@ -852,7 +862,7 @@ static WsLayout ws_layout_plan(const cks_geom& g, cks_dtype dt, cks_op op, int g
     }
     if (op == CKS_OP_WGRAD) {
         WgradCfg c = wgrad_cfg(g, dt, gz, num_sms);
-        if (c.gz > 1 && !c.zc) take(size_t(c.gz) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+        if (c.npart() > 1 && !c.zc) take(size_t(c.npart()) * g.OC * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
     }
     L.total = off;
     return L;
@@ -1012,7 +1022,8 @@ WsLayout ws_layout3(const cks_geom3& g, cks_dtype dt, cks_op op, int gz, int num
     }
     if (op == CKS_OP_WGRAD) {
         const WgradCfg c = wgrad_cfg3(g, dt, gz, num_sms);
-        if (c.gz > 1 && !c.zc) take(size_t(c.gz) * g.OC * g.FD * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
+        if (c.npart() > 1 && !c.zc)
+            take(size_t(c.npart()) * g.OC * g.FD * g.FH * g.FW * g.C * 4, L.partial, L.partial_bytes);
     }
     L.total = off;
     return L;

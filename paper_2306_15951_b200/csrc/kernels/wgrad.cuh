@@ -35,6 +35,17 @@
 // segment instead of F_H times and the CTAs that share it stay in step (DRAM
 // re-reads of dY / X between filter rows: ncu showed 2.7x the algorithmic
 // bytes on the ResNet l1 layers without it).
+//
+// Position pairs (PP, round 2; F_W = 3, s_w = 1, O_C <= 64, I_C <= 64): the
+// MMA's M = 128 holds the dY of TWO neighbouring output positions (ow, ow+1,
+// 64 channels each) and each of the four X columns iw = ow - pw + j
+// (j = 0..3) is ONE MMA: rows 0-63 accumulate tap j of position ow, rows
+// 64-127 tap j-1 of position ow+1 -- every X column that both positions
+// read is multiplied once, and no A row is idle (the plain row tile leaves
+// the 64 upper M rows unused with O_C = 64).  Tap fw's sum is then
+// D_fw[0:64] + D_{fw+1}[64:128]; the two halves are written as two G_Z
+// partials (slots 2z, 2z+1) that KB-REDUCE adds in fixed order.  A column
+// outside X is skipped for both halves (exact trimming).
 #pragma once
 #include "ptx.cuh"
 
@@ -59,6 +70,8 @@ struct WgradParams {
     int tc;                 // filter-row group size (F_H; 0/1 = off), row tiles only: the group's tiles walk
                             // the union oh range with identical segments (adjacent tiles)
     int tcmc;               // 1: the group is a cluster and rank 0 multicasts each dY block
+    int pp;                 // position pairs (MT = 4 X columns per k-block of two positions)
+    int Wx;                 // X width (position pairs: column range check)
     int ouh_s, ouh_e;       // filter-row clusters: union of the filter rows' oh ranges
 };
 
@@ -70,7 +83,7 @@ struct WgradParams {
 // atom, two tf32 atoms); the MMA's other 64 A rows read the stage's first X
 // block (garbage rows of D, never stored), so the ring carries one more stage
 // instead of zero-filled atoms.
-template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false>
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false, bool PP = false>
 struct WgradShape {
     static constexpr int EB = kTF32 ? 4 : 2;
     static constexpr int CH = 128 / EB;                 // channels per box
@@ -79,7 +92,8 @@ struct WgradShape {
     static constexpr int B_BYTES = (BN / CH) * ATOM;    // BN IC x KIMG images
     static constexpr int UK = 32 / EB;                  // K (images) per MMA
     static constexpr int KSTEP = UK * 128;              // bytes per MMA K step
-    static constexpr int A_STAGE = A1 ? (64 / CH) * ATOM : A_BYTES;  // dY bytes reserved per stage (A1: 64 OC)
+    // dY bytes reserved per stage (A1: 64 OC; position pairs: 64 OC of two positions = M 128)
+    static constexpr int A_STAGE = PP ? 2 * (64 / CH) * ATOM : (A1 ? (64 / CH) * ATOM : A_BYTES);
     static constexpr int STAGE_BYTES = A_STAGE + MT * B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
@@ -125,9 +139,9 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
     const int hn = (p.tc > 1 ? p.ouh_e : p.oh_e[c.fh]) - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     const int dn = p.od_e[c.fd] - c.ods;
-    c.wn = wn;
+    c.wn = p.pp ? wn / 2 : wn;  // position pairs: the k index runs over pairs (host: wn even)
     c.hn = hn;
-    const uint32_t L = uint32_t(max(dn, 0)) * uint32_t(max(hn, 0)) * uint32_t(max(wn, 0)) * uint32_t(p.nblk64);
+    const uint32_t L = uint32_t(max(dn, 0)) * uint32_t(max(hn, 0)) * uint32_t(max(c.wn, 0)) * uint32_t(p.nblk64);
     c.kb0 = int(uint64_t(L) * uint32_t(c.z) / uint32_t(p.gz));
     c.kb1 = int(uint64_t(L) * uint32_t(c.z + 1) / uint32_t(p.gz));
     return c;
@@ -156,11 +170,25 @@ __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& 
     return false;
 }
 
-template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false>
+// position pairs: does X column j (iw = ow0 - pw + j) of any k-block of the segment lie in X?
+__device__ __forceinline__ bool pp_col_has_work(const WTile& c, const WgradParams& p, int j) {
+    if (c.kb1 <= c.kb0 || c.wn <= 0) return false;
+    const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
+    for (int q = p0; q <= p1; ++q) {
+        const int pq = q / c.wn;
+        const int ow0 = c.ows + 2 * (q - pq * c.wn), oh = c.ohs + (pq % c.hn);
+        const int iw = ow0 - p.pw + j;
+        if (iw >= 0 && iw < p.Wx && (p.tc <= 1 || (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh]))) return true;
+    }
+    return false;
+}
+
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false, bool PP = false>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
-    using S = WgradShape<BN, kTF32, KIMG, MT, A1>;
+    using S = WgradShape<BN, kTF32, KIMG, MT, A1, PP>;
+    static_assert(!PP || (MT == 4 && A1 && BN == 64), "position pairs: 4 X columns, 64 OC, 64 IC");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::STAGES * S::STAGE_BYTES);
@@ -209,7 +237,7 @@ __global__ void __launch_bounds__(256, 1)
                 const int n64 = kb % p.nblk64;
                 const int pos = kb / p.nblk64;
                 const int pq = pos / c.wn;
-                const int ow = c.ows + (pos - pq * c.wn);
+                const int ow = c.ows + (PP ? 2 : 1) * (pos - pq * c.wn);  // position pairs: first position
                 const int dq = pq / c.hn;
                 const int oh = c.ohs + (pq - dq * c.hn), od = c.ods + dq;
                 // filter-row clusters walk the union oh range: rows outside this filter row's own range
@@ -217,7 +245,30 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * S::STAGE_BYTES;
                 if (ptx::elect_one()) {
-                    if (!is_b) {
+                    if (PP && !is_b) {  // dY of positions ow, ow+1: 64 channels each (M rows 0-63, 64-127)
+                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(S::A_STAGE));
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+#pragma unroll
+                            for (int j = 0; j < 64 / S::CH; ++j)
+                                ptx::tma_load_4d(sa + (q * (64 / S::CH) + j) * S::ATOM, &tmDY, &full[stage], j * S::CH,
+                                                 ow + q, od * p.OHr + oh, n64 * KIMG);
+                    } else if (PP) {  // X columns iw = ow - pw + j, j = 0..3 (outside X: neither loaded nor used)
+                        const int ih = (od * p.sd + c.fd - p.pd) * p.Hr + oh * p.sh + c.fh - p.ph;
+                        uint32_t nv = 0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) nv += (ohok && ow - p.pw + j >= 0 && ow - p.pw + j < p.Wx) ? 1u : 0u;
+                        ptx::mbar_arrive_expect_tx(&full[stage], nv * S::B_BYTES);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int iw = ow - p.pw + j;
+                            if (!ohok || iw < 0 || iw >= p.Wx) continue;
+#pragma unroll
+                            for (int jj = 0; jj < BN / S::CH; ++jj)
+                                ptx::tma_load_4d(sa + S::A_STAGE + j * S::B_BYTES + jj * S::ATOM, &tmX, &full[stage],
+                                                 c.nb * BN + jj * S::CH, iw, ih, n64 * KIMG);
+                        }
+                    } else if (!is_b) {
                         // only the atoms holding valid O_C rows (the rest of the MMA's M rows are never stored)
                         const int a_atoms = min(128 / S::CH, (p.OC - c.mb * 128 + S::CH - 1) / S::CH);
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(a_atoms * S::ATOM));
@@ -274,7 +325,7 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::tc_fence_after();
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
                 const uint64_t ad = dconst | ptx::desc_addr(a_addr);
-                const int ow = c.ows + (kb / p.nblk64) % max(c.wn, 1);
+                const int ow = c.ows + (PP ? 2 : 1) * ((kb / p.nblk64) % max(c.wn, 1));
                 bool ohok = true;
                 if (p.tc > 1) {
                     const int oh = c.ohs + ((kb / p.nblk64) / max(c.wn, 1)) % max(c.hn, 1);
@@ -283,7 +334,11 @@ __global__ void __launch_bounds__(256, 1)
                 if (ptx::elect_one()) {
 #pragma unroll
                     for (int f = 0; f < MT; ++f) {
-                        if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) continue;  // trimmed tap
+                        if (PP) {  // X column f: one MMA for tap f of ow (rows 0-63) and tap f-1 of ow+1 (64-127)
+                            if (!ohok || ow - p.pw + f < 0 || ow - p.pw + f >= p.Wx) continue;
+                        } else if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) {
+                            continue;  // trimmed tap
+                        }
                         const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_STAGE + f * S::B_BYTES);
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
 #pragma unroll
@@ -324,6 +379,50 @@ __global__ void __launch_bounds__(256, 1)
             const int oc = c.mb * 128 + row;
             const int cbase = c.nb * BN;
             const int cvalid = min(BN, p.C - cbase);
+            if constexpr (PP) {
+                // tap fw = D_fw[0:64] (position ow, warps 0-1) + D_{fw+1}[64:128] (ow+1, warps 2-3):
+                // the halves go to G_Z partial slots 2z and 2z+1 (summed by KB-REDUCE)
+                const int h = sub >= 2 ? 1 : 0;
+                const int ocr = row - 64 * h;
+#pragma unroll 1
+                for (int fw = 0; fw < 3; ++fw) {
+                    const int j = fw + h;
+                    const bool live = !zero && pp_col_has_work(c, p, j);
+                    float* dst = ocr < p.OC ? p.out + (2 * c.z + h) * p.part_stride +
+                                                  (static_cast<long long>(ocr) * taps + (c.fd * p.FH + c.fh) * p.FW + fw) *
+                                                      p.C + cbase
+                                            : nullptr;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * (MT * BN) + j * BN + c0, r);
+                        ptx::tmem_ld_wait();
+                        if (dst == nullptr || c0 >= cvalid) continue;
+                        if (!live) {
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) r[q] = 0u;
+                        }
+                        if (vec4 && c0 + 32 <= cvalid) {
+#pragma unroll
+                            for (int q = 0; q < 32; q += 4)
+                                *reinterpret_cast<float4*>(dst + c0 + q) =
+                                    make_float4(__uint_as_float(r[q]), __uint_as_float(r[q + 1]),
+                                                __uint_as_float(r[q + 2]), __uint_as_float(r[q + 3]));
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 32; ++q)
+                                if (c0 + q < cvalid) dst[c0 + q] = __uint_as_float(r[q]);
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                continue;
+            } else {
 #pragma unroll 1
             for (int f = 0; f < MT; ++f) {
             const bool fzero = zero || (MT > 1 && !tap_has_work(c, p, f));
@@ -368,6 +467,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             }
+            }  // generic taps
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
             if (++acc == 2) {
