@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -143,7 +143,9 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_PAIR")) pair = atoi(e) != 0;      // 0: no 2-CTA igemm tiles
         if (const char* e = cks_knob("CKS_PAIR_TF32")) pair_tf32 = atoi(e) != 0;  // 0: BF16-only CTA pairs
         if (const char* e = cks_knob("CKS_TF32_WIDE")) tf32_wide = atoi(e) != 0;  // wide TF32 pixel blocks
+        if (const char* e = cks_knob("CKS_BF16_WIDE")) bf16_wide = atoi(e) != 0;  // the same for BF16
         if (const char* e = cks_knob("CKS_WGRAD_PP")) wpp = atoi(e) != 0;  // Sk-dilated position pairs
+        if (const char* e = cks_knob("CKS_PAIR_WAVES_TF32")) pair_waves_tf32 = atoi(e);  // TF32 pair grid (1/10 waves)
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
         if (const char* e = cks_knob("CKS_GZ_MAX")) gz_max = std::max(1, atoi(e));  // G_Z cap (experiments)
         // 0: G_Z partials + KB-REDUCE; 1: in-cluster reduce when the plan's G_Z fits one
@@ -244,9 +246,10 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     // columns (ncu, C3 l1: tensor 42 %); a wider pixel block reuses each column for
     // more (pixel, tap) pairs -- the row step then spans two A slots (a 3-deep A ring
     // of half-row-step slots) instead of double-buffering whole row steps.
-    // Measured (TF32, warm): C3 l1 fwd / KS-deconv 143 -> 127 us, l2 122 -> 106 us.
+    // Measured (warm): TF32 C3 l1 fwd / KS-deconv 143 -> 127 us, l2 122 -> 106 us;
+    // BF16 l1 81 -> 73 us, l2 64 -> 57 us (C2's small maps keep < 3 waves: unchanged).
     int wide_apos = 0;
-    if (eb == 4 && !pair && force_pbw == 0 && knobs().tf32_wide && !(ov && ov_pbw > 0)) {
+    if ((eb == 4 ? knobs().tf32_wide : knobs().bf16_wide) && !pair && force_pbw == 0 && !(ov && ov_pbw > 0)) {
         const int64_t stage = ntap * c.BN * c.KB, colb = int64_t(128) * c.KB;
         for (int pb = pbw + 1; pb <= std::min<int64_t>({int64_t(256 / c.BN), 8, maxrow}); ++pb) {
             // >= 3 waves of tiles (C3 l4, 7x7: 2-pixel tiles leave 1.5 waves and lose 15 %)
@@ -358,7 +361,11 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
         c4.nbs >= 2 && c4.Z == 1) {
         const IgemmCfg cp = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
                                         0, 4, true);
-        if (cp.unified && cp.stages >= 2 && cp.KB == 128 && cp.out_tiles * 2 * 2 >= int64_t(num_sms) * 5) return cp;
+        // pair grid of >= 2.5 waves (BF16); TF32 layers are ingress-bound and gain from the pair's
+        // halved activation traffic on shorter grids too (knob: tenths of a wave)
+        const int64_t waves10 = eb == 4 ? knobs().pair_waves_tf32 : 25;
+        if (cp.unified && cp.stages >= 2 && cp.KB == 128 && cp.out_tiles * 2 * 2 * 10 >= int64_t(num_sms) * waves10)
+            return cp;
     }
     if (knobs().epi8 == 0) return c4;
     const IgemmCfg c8 = igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms,
@@ -513,7 +520,7 @@ static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
     while (c.BN < g.OC) c.BN *= 2;
     const int wbytes = int((g.FH * c.BN * c.ROWB + 1023) / 1024 * 1024);
     const int stage = 128 * c.ROWB;
-    const int staging = 4 * 2 * 4096;
+    const int staging = 4 * 2 * 4096;  // kernels/narrow.cuh RowFwdShape::STAGING
     const int budget = 227 * 1024 - 1024 - 512;
     c.stages = std::min(16, (budget - wbytes - staging) / stage);
     if (c.stages < 3) return c;

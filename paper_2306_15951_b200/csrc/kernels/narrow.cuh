@@ -73,7 +73,10 @@ struct RowFwdShape {
     static constexpr int EB = TF ? 4 : 2;
     static constexpr int JB = ROWB / EB;           // elements per box row
     static constexpr int STAGE = 128 * ROWB;       // one X row of 128 images
-    static constexpr int STAGING = 4 * 2 * 4096;   // 4 epilogue warps x 2 x (32 rows x 128 B)
+    // 4 epilogue warps x 2 x (32 rows x 128 B): two TMA stores in flight per warp
+    // (four measured no faster on the stem: the stores are not what bounds it)
+    static constexpr int EPI_BUFS = 2;
+    static constexpr int STAGING = 4 * EPI_BUFS * 4096;
     static constexpr int RMAX = 256 / BN < 8 ? 256 / BN : 8;  // 2 x R x BN TMEM columns <= 512
 };
 
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp >= 4) {
         // ---------------- epilogue: TMEM -> registers -> (swizzled staging -> TMA store | direct stores)
         const uint32_t sub = warp & 3u;
-        uint8_t* my = stg + sub * 2 * 4096;
+        uint8_t* my = stg + sub * S::EPI_BUFS * 4096;
         uint32_t i = 0, q = 0;
         for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
             const RowFwdTile tl(t, cl, p);
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(256, 1)
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(S::RMAX * BN) + uint32_t(r * BN + c0), v);
                     ptx::tmem_ld_wait();
                     if (p.tma_store) {
-                        uint8_t* buf = my + (q++ & 1u) * 4096;
+                        uint8_t* buf = my + (q++ & uint32_t(S::EPI_BUFS - 1)) * 4096;
                         if (ptx::elect_one()) ptx::bulk_wait_read1();  // buffer of chunk q-2 drained
                         __syncwarp();
 #pragma unroll
