@@ -364,7 +364,7 @@ IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t 
         // pair grid of >= 2.5 waves (BF16); TF32 layers are ingress-bound and gain from the pair's
         // halved activation traffic on shorter grids too (knob: tenths of a wave)
         const int64_t waves10 = eb == 4 ? knobs().pair_waves_tf32 : 25;
-        if (cp.unified && cp.stages >= 2 && cp.KB == 128 && cp.out_tiles * 2 * 2 * 10 >= int64_t(num_sms) * waves10)
+        if (cp.unified && cp.stages >= 2 && cp.KB == 128 && cp.out_tiles * 2 * 10 >= int64_t(num_sms) * waves10)
             return cp;
     }
     if (knobs().epi8 == 0) return c4;
