@@ -745,6 +745,8 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
                     : launch_wgrad_t<64, true, 64, 1, true>(ta, tb, p, st);
     }
     if (cfg.mt == 3 && tf && cfg.BN == 64) return launch_wgrad_t<64, true, 64, 3>(ta, tb, p, st);
+    if (cfg.mt == 3 && cfg.BN == 128)  // BN = 128 row tiles (one accumulator buffer)
+        return tf ? launch_wgrad_t<128, true, 32, 3>(ta, tb, p, st) : launch_wgrad_t<128, false, 64, 3>(ta, tb, p, st);
     if (cfg.mt == 3 && !tf && cfg.BN == 64)  // row tiles: the F_W = 3 taps of a filter row share the dY block
         return k128 ? launch_wgrad_t<64, false, 128, 3>(ta, tb, p, st) : launch_wgrad_t<64, false, 64, 3>(ta, tb, p, st);
 #define CKS_WG(BN_)                                                                                   \

@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -144,6 +144,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_PAIR_TF32")) pair_tf32 = atoi(e) != 0;  // 0: BF16-only CTA pairs
         if (const char* e = cks_knob("CKS_TF32_WIDE")) tf32_wide = atoi(e) != 0;  // wide TF32 pixel blocks
         if (const char* e = cks_knob("CKS_BF16_WIDE")) bf16_wide = atoi(e) != 0;  // the same for BF16
+        if (const char* e = cks_knob("CKS_WGRAD_MT128")) wmt128 = atoi(e) != 0;  // BN = 128 row tiles
         if (const char* e = cks_knob("CKS_WGRAD_PP")) wpp = atoi(e) != 0;  // Sk-dilated position pairs
         if (const char* e = cks_knob("CKS_PAIR_WAVES_TF32")) pair_waves_tf32 = atoi(e);  // TF32 pair grid (1/10 waves)
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
@@ -713,7 +714,9 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
     // row tiles (all F_W = 3 taps of a filter row per tile, the dY block shared):
     // bf16, IC <= 64 (three double-buffered 64-column accumulators fit TMEM)
     // TF32 row tiles keep 64-image k-blocks (3 x 16 KB X blocks + 2 dY atoms per stage)
-    c.mt = (c.BN == 64 && g.FW == 3 && knobs().wmt && (dt == CKS_BF16 || knobs().wmt_tf32)) ? 3 : 1;
+    // BN = 128 row tiles (I_C <= 128): one TMEM accumulator buffer (3 x 128 columns)
+    c.mt = ((c.BN == 64 || (c.BN == 128 && knobs().wmt128)) && g.FW == 3 && knobs().wmt &&
+            (dt == CKS_BF16 || knobs().wmt_tf32)) ? 3 : 1;
     Axis ah = axis_h(g), aw = axis_w(g);
     auto th = table_t3(ah), tw = table_t3(aw);
     int64_t dmul = 1;  // 3-D: taps x depth windows (the smallest depth window for lmin)
@@ -750,10 +753,11 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
             }
         if (ntaps == 0) lmin = 1;
     }
-    if (dt == CKS_TF32 && c.mt > 1) {  // TF32 row tiles: 64-image k-blocks (the k range shrinks with them)
-        if (c.kimg == 128) lmin *= 2;
-        c.kimg = 64;
-        c.nblk64 = int((g.N + 63) / 64);
+    if (dt == CKS_TF32 && c.mt > 1) {  // TF32 row tiles: 64-image (BN = 128: 32-image) k-blocks
+        const int k = c.BN == 128 ? 32 : 64;
+        lmin = lmin * c.kimg / k;
+        c.kimg = k;
+        c.nblk64 = int((g.N + k - 1) / k);
     }
     c.base_tiles = (ad ? ad->F : 1) * int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
     if (gz_req > 0) {

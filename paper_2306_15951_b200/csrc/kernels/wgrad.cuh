@@ -97,8 +97,11 @@ struct WgradShape {
     static constexpr int STAGE_BYTES = A_STAGE + MT * B_BYTES;
     static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * MT * BN <= 128 ? 128 : 2 * MT * BN <= 256 ? 256 : 512;
-    static_assert(2 * MT * BN <= 512, "two accumulator buffers of MT taps must fit TMEM");
+    // accumulator buffers: two (the epilogue of a tile overlaps the next tile's MMAs) when
+    // they fit TMEM, else one (BN = 128 row tiles: long K loops, the epilogue is short)
+    static constexpr int NACC = 2 * MT * BN <= 512 ? 2 : 1;
+    static constexpr uint32_t TMEM_COLS = NACC * MT * BN <= 128 ? 128 : NACC * MT * BN <= 256 ? 256 : 512;
+    static_assert(MT * BN <= 512, "the accumulators of MT taps must fit TMEM");
 };
 
 struct WTile {
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
             __syncwarp();
-            if (++acc == 2) {
+            if (++acc == uint32_t(S::NACC)) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tempty[acc]);
-                if (++acc == 2) {
+                if (++acc == uint32_t(S::NACC)) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(256, 1)
             }  // generic taps
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
-            if (++acc == 2) {
+            if (++acc == uint32_t(S::NACC)) {
                 acc = 0;
                 acc_phase ^= 1;
             }

@@ -474,7 +474,9 @@ def test_autograd_generator_layer(torch_cuda, dtype):
                                     (Layer("rt1", 130, 40, 40, 37, 64, 3, 3, 1, 1, 1, 1), 3),
                                     (Layer("rt2", 200, 64, 81, 80, 24, 3, 3, 2, 2, 1, 1), 0),
                                     (Layer("rt3", 130, 64, 40, 40, 64, 3, 3, 1, 1, 0, 0), 7),
-                                    (Layer("rt4", 130, 64, 40, 40, 64, 5, 3, 1, 1, 2, 1), 1)],
+                                    (Layer("rt4", 130, 64, 40, 40, 64, 5, 3, 1, 1, 2, 1), 1),
+                                    (Layer("rt5", 130, 128, 30, 30, 96, 3, 3, 1, 1, 1, 1), 0),   # BN = 128 row tiles
+                                    (Layer("rt6", 140, 112, 29, 31, 128, 3, 3, 1, 1, 1, 1), 5)],
                          ids=lambda v: v.name if isinstance(v, Layer) else f"gz{v}")
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
 def test_wgrad_row_tiles(torch_cuda, lay, gz, dtype):

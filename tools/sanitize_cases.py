@@ -30,12 +30,15 @@ CASES = [
     ("narrow", 70, 3, 20, 16, 64, 7, 2, 3),          # filter-row kernels (fwd_row / wgrad_row + reduce)
     ("rowtiles", 130, 64, 40, 40, 64, 3, 1, 1),      # Sk-dilated row tiles, A1 (O_C <= 64)
     ("pad", 9, 3, 12, 13, 5, 3, 2, 1),               # channel padding (KB-PAD), odd pitches
+    ("pospairs", 130, 64, 28, 28, 64, 3, 1, 1),      # Sk-dilated position pairs + filter-row groups
+    ("wide", 256, 64, 28, 28, 64, 3, 1, 1),          # wide pixel blocks (two A slots per row step)
+    ("pair256", 260, 256, 14, 14, 256, 3, 1, 1),     # CTA pairs (both dtypes)
 ]
 
 for dtype in ("bf16", "tf32"):
     for name, N, C, H, W, OC, F, s, p in CASES:
         if name == "pair" and dtype == "tf32":
-            continue
+            continue  # pair256 covers TF32 pairs
         X = t((N, H, W, C), dtype)
         Wt = t((OC, F, F, C), dtype)
         OH, OW = (H + 2 * p - F) // s + 1, (W + 2 * p - F) // s + 1

@@ -67,14 +67,14 @@ int main() {
     // X: N=256 images x H=32 x W=32 x C=8 bf16 viewed (W*C, N, H, 1)  (4 MB, L2 resident)
     const int N = 256, H = 32, W = 32, C = 8;
     void* d;
-    cudaMalloc(&d, (size_t)N * H * W * C * 2);
+    cudaMalloc(&d, (size_t)N * H * W * C * 2 * 4);
     cudaMemset(d, 0, (size_t)N * H * W * C * 2);
     unsigned long long* cyc;
     cudaMalloc(&cyc, sms * 8);
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     printf("ctas contig RB R T S nw  B/clk/SM\n");
-    for (int ctas : {148, 64, 16})
-    for (int contig : {0, 1})
+    for (int ctas : {148})
+    for (int contig : {0, 1, 2})
     for (int RB : {64, 128})
         for (int R : {128})
             for (int T : {1, 4})
@@ -86,8 +86,10 @@ int main() {
                         cuuint64_t dims[4] = {(cuuint64_t)W * C, (cuuint64_t)N, (cuuint64_t)H, 1};
                         cuuint64_t str[3] = {(cuuint64_t)H * W * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)N * H * W * C * 2};
                         if (contig) {  // rows of one box contiguous: (W*C, N) with N stride = RB bytes... use a dense [H][N][RB] view
+                            // contig 2: rows at a 2*RB pitch (image-innermost layout with twice the channels)
+                            const cuuint64_t pitch = (cuuint64_t)RB * contig;
                             dims[0] = RB / 2; dims[1] = N; dims[2] = H; dims[3] = 1;
-                            str[0] = RB; str[1] = (cuuint64_t)N * RB; str[2] = (cuuint64_t)N * H * RB;
+                            str[0] = pitch; str[1] = (cuuint64_t)N * pitch; str[2] = (cuuint64_t)N * H * pitch;
                         }
                         cuuint32_t box[4] = {(cuuint32_t)RB / 2, (cuuint32_t)R, (cuuint32_t)T, 1}, es[4] = {1, 1, 1, 1};
                         CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, d, dims, str, box, es,
