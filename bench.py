@@ -286,7 +286,9 @@ class LayerBufs:
         }
         # KS-deconv without Stage1 (the GEMM reads W directly) where the library's
         # policy takes it; eligible: W rows of a 16-byte multiple, sw <= 8
-        self.direct = "deconv" in lay.ops and L.plan_dict(g, self.dt, L.CKS_OP_DECONV).get("ks_direct") == "1"
+        pd = L.plan_dict(g, self.dt, L.CKS_OP_DECONV) if "deconv" in lay.ops else {}
+        # W given: Stage1-free, or (narrow outputs) the multi-phase tile -- no separate Stage1 either way
+        self.direct = pd.get("ks_direct") == "1" or pd.get("ks_mp") == "1"
         self.direct_ok = "deconv" in lay.ops and (lay.C * eb) % 16 == 0 and lay.sw <= 8
 
     def run_split(self, stream_ptr):

@@ -139,7 +139,19 @@ cks_status cks_deconv2d(const cks_geom* g, cks_dtype dt, const void* dy, const v
  * Same results in every mode (the same sums; only the B operand's source
  * differs).  With c_packed given the mode must be AUTO or STAGE1.  ws as
  * queried by cks_workspace_size(CKS_OP_DECONV) covers every mode. */
-typedef enum { CKS_KS_AUTO = 0, CKS_KS_STAGE1_FREE = 1, CKS_KS_STAGE1 = 2 } cks_ks_mode;
+/*   CKS_KS_MULTIPHASE    narrow outputs (I_C <= 8, F_H % sh == F_W % sw == 0,
+ *                        every phase with >= 1 row): the sh*sw phases are
+ *                        stacked on the GEMM N dimension -- with each phase's
+ *                        row index shifted by its a_y (T2) all phases read the
+ *                        same CH x CW window of dY, so the deconvolution is
+ *                        one unit-stride ConvV2 over dY with the stacked
+ *                        sub-filters, then a phase-strided scatter to dX
+ *                        (CKS_ERR_UNSUPPORTED if not eligible).  AUTO picks it
+ *                        where eligible.  At the first / last window row and
+ *                        column the GEMM also forms the products of the phases
+ *                        whose dX row / column does not exist there; they are
+ *                        discarded (never stored). */
+typedef enum { CKS_KS_AUTO = 0, CKS_KS_STAGE1_FREE = 1, CKS_KS_STAGE1 = 2, CKS_KS_MULTIPHASE = 3 } cks_ks_mode;
 cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, const void* w,
                            const void* c_packed, float* dx, void* ws, size_t ws_bytes, void* stream,
                            cks_ks_mode mode);

@@ -179,7 +179,7 @@ def cks_deconv2d(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, strea
            "cks_deconv2d")
 
 
-CKS_KS_AUTO, CKS_KS_STAGE1_FREE, CKS_KS_STAGE1 = 0, 1, 2
+CKS_KS_AUTO, CKS_KS_STAGE1_FREE, CKS_KS_STAGE1, CKS_KS_MULTIPHASE = 0, 1, 2, 3
 
 
 def cks_deconv2d_ex(g, dtype, dy_ptr, w_ptr, c_ptr, dx_ptr, ws_ptr, ws_bytes, stream, mode):

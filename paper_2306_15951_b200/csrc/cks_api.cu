@@ -980,8 +980,9 @@ cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, cons
                            float* dx, void* ws, size_t ws_bytes, void* stream, cks_ks_mode mode) {
     if (!g || !dy || !dx) return CKS_ERR_NULL;
     if ((w == nullptr) == (c_packed == nullptr)) return CKS_ERR_NULL;
-    if (mode != CKS_KS_AUTO && mode != CKS_KS_STAGE1_FREE && mode != CKS_KS_STAGE1) return CKS_ERR_UNSUPPORTED;
-    if (c_packed && mode == CKS_KS_STAGE1_FREE) return CKS_ERR_UNSUPPORTED;
+    if (mode != CKS_KS_AUTO && mode != CKS_KS_STAGE1_FREE && mode != CKS_KS_STAGE1 && mode != CKS_KS_MULTIPHASE)
+        return CKS_ERR_UNSUPPORTED;
+    if (c_packed && (mode == CKS_KS_STAGE1_FREE || mode == CKS_KS_MULTIPHASE)) return CKS_ERR_UNSUPPORTED;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
     if (!aligned16(dy) || !aligned16(dx) || (w && !aligned16(w)) || (c_packed && !aligned16(c_packed)))
@@ -992,6 +993,36 @@ cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, cons
     WsLayout L = ws_layout(*g, dt, CKS_OP_DECONV, 0, c_packed != nullptr, kPlanSMs);
     if ((s = check_ws(L, ws, ws_bytes)) != CKS_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!c_packed && (mode == CKS_KS_MULTIPHASE || mode == CKS_KS_AUTO)) {
+        const MpPlan m = mp_plan(*g, dt);
+        if (m.ok) {  // narrow outputs: the phases stacked on N of one unit-stride ConvV2 over dY
+            void* wm = static_cast<uint8_t*>(ws) + L.mp_w;
+            float* yp = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + L.mp_y);
+            const long long np = (long long)m.NP * m.CH * m.CW * g->OC;
+            const unsigned pb = unsigned(std::min<long long>((np + 255) / 256, 1024));
+            if (dt == CKS_BF16)
+                s = launch_pdl(ks_mp_pack_kernel<uint16_t>, dim3(pb), dim3(256), 0, st,
+                               static_cast<const uint16_t*>(w), static_cast<uint16_t*>(wm), int(g->OC), int(g->FH),
+                               int(g->FW), int(g->C), int(g->sh), int(g->sw), m.CH, m.CW, m.NP, int(g->OC));
+            else
+                s = launch_pdl(ks_mp_pack_kernel<uint32_t>, dim3(pb), dim3(256), 0, st,
+                               static_cast<const uint32_t*>(w), static_cast<uint32_t*>(wm), int(g->OC), int(g->FH),
+                               int(g->FW), int(g->C), int(g->sh), int(g->sw), m.CH, m.CW, m.NP, int(g->OC));
+            if (s != CKS_OK) return s;
+            s = cks_conv2d_fwd(&m.pg, dt, dy, wm, yp, static_cast<uint8_t*>(ws) + L.mp_inner, L.mp_inner_bytes, stream);
+            if (s != CKS_OK) return s;
+            MpPhase t;
+            memset(&t, 0, sizeof(t));
+            for (int i = 0; i < 8; ++i) t.ih_s[i] = m.ih_s[i], t.a_y[i] = m.a_y[i], t.iw_s[i] = m.iw_s[i], t.a_x[i] = m.a_x[i];
+            const int64_t MH = out_extent(m.pg.H, m.pg.FH, 1, m.pg.ph), MW = out_extent(m.pg.W, m.pg.FW, 1, m.pg.pw);
+            const long long tot = g->N * g->H * g->W * g->C;
+            const unsigned sb = unsigned(std::min<long long>((tot + 255) / 256, 148LL * 16));
+            return launch_pdl(ks_mp_scatter_kernel, dim3(sb), dim3(256), 0, st, (const float*)yp, dx, (long long)g->N,
+                              int(g->H), int(g->W), int(g->C), int(g->sh), int(g->sw), int(MH), int(MW), m.NP, m.ph2,
+                              m.pw2, t);
+        }
+        if (mode == CKS_KS_MULTIPHASE) return CKS_ERR_UNSUPPORTED;
+    }
     const int64_t eb = elem_bytes(dt), OCp = pad_ch(g->OC, dt);
     const int64_t OH = ah.O, OW = aw.O;
     const void* dys = dy;
@@ -1501,7 +1532,17 @@ cks_status cks_launch_count(const cks_geom* g, cks_dtype dt, cks_op op, int gz, 
     const bool cpad = pad_ch(g->C, dt) != g->C, ocpad = pad_ch(g->OC, dt) != g->OC;
     int n = 1;
     if (op == CKS_OP_FWD) n += (cpad && !row_cfg_fwd(*g, dt).ok) ? 2 : 0;
-    else if (op == CKS_OP_DECONV) n += (c_packed_given || ks_direct(*g, dt, kPlanSMs) ? 0 : 1) + (ocpad ? 1 : 0);
+    else if (op == CKS_OP_DECONV) {
+        const MpPlan m = c_packed_given ? MpPlan() : mp_plan(*g, dt);
+        if (m.ok) {  // pack + the pseudo ConvV2 + scatter
+            int inner = 0;
+            const cks_status s2 = cks_launch_count(&m.pg, dt, CKS_OP_FWD, 0, 0, &inner);
+            if (s2 != CKS_OK) return s2;
+            n = 2 + inner;
+        } else {
+            n += (c_packed_given || ks_direct(*g, dt, kPlanSMs) ? 0 : 1) + (ocpad ? 1 : 0);
+        }
+    }
     else if (op == CKS_OP_WGRAD || int(op) == CKS_OP_WGRAD_AR) {
         const WgradCfg c = wgrad_cfg(*g, dt, gz, kPlanSMs);
         // + KB-REDUCE for G_Z partials; the fused variant always ends with KB-REDUCE-AR

@@ -128,7 +128,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -145,6 +145,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_TF32_WIDE")) tf32_wide = atoi(e) != 0;  // wide TF32 pixel blocks
         if (const char* e = cks_knob("CKS_BF16_WIDE")) bf16_wide = atoi(e) != 0;  // the same for BF16
         if (const char* e = cks_knob("CKS_WGRAD_MT128")) wmt128 = atoi(e) != 0;  // BN = 128 row tiles
+        if (const char* e = cks_knob("CKS_KS_MP")) ks_mp = atoi(e) != 0;  // multi-phase narrow-output KS-deconv
         if (const char* e = cks_knob("CKS_WGRAD_PP")) wpp = atoi(e) != 0;  // Sk-dilated position pairs
         if (const char* e = cks_knob("CKS_PAIR_WAVES_TF32")) pair_waves_tf32 = atoi(e);  // TF32 pair grid (1/10 waves)
         if (const char* e = cks_knob("CKS_SMEM_CAP")) smem_cap = atoi(e);    // KB of ring budget (experiments)
@@ -396,6 +397,47 @@ static IgemmCfg igemm_cfg_deconv_plan(const cks_geom& g, cks_dtype dt, int num_s
     for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
     return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
                      num_sms);
+}
+
+MpPlan mp_plan(const cks_geom& g, cks_dtype dt) {
+    MpPlan m;
+    if (knobs().ks_mp == 0) return m;
+    // stride > 1 (a single phase is the KS path itself), narrow outputs, equal sub-filters
+    if (g.sh * g.sw < 2 || g.C > 8 || g.FH % g.sh || g.FW % g.sw || g.sh > 8 || g.sw > 8) return m;
+    const int64_t NP = (int64_t(g.sh) * g.sw * g.C + 3) / 4 * 4;  // stacked channels, 16-byte fp32 rows
+    if (NP > 64) return m;
+    const Axis ah = axis_h(g), aw = axis_w(g);
+    const auto th = table_t2(ah), tw = table_t2(aw);
+    int64_t amin_h = 0, amax_h = INT64_MIN, amin_w = 0, amax_w = INT64_MIN;
+    for (auto& ph : th) {
+        if (ph.CH != g.FH / g.sh || ph.U <= 0) return m;  // every phase the full sub-filter, >= 1 row
+        amin_h = std::min(amin_h, ph.a);
+        amax_h = std::max(amax_h, ph.a + ph.U);
+    }
+    for (auto& ph : tw) {
+        if (ph.CH != g.FW / g.sw || ph.U <= 0) return m;
+        amin_w = std::min(amin_w, ph.a);
+        amax_w = std::max(amax_w, ph.a + ph.U);
+    }
+    m.CH = int(g.FH / g.sh);
+    m.CW = int(g.FW / g.sw);
+    m.ph2 = int(-amin_h);
+    m.pw2 = int(-amin_w);
+    if (m.ph2 >= m.CH || m.pw2 >= m.CW) return m;  // ConvV2 validity (p < F)
+    m.NP = int(NP);
+    cks_geom pg;
+    pg.N = g.N, pg.C = g.OC, pg.H = ah.O, pg.W = aw.O, pg.OC = NP, pg.FH = m.CH, pg.FW = m.CW;
+    pg.sh = 1, pg.sw = 1, pg.ph = m.ph2, pg.pw = m.pw2, pg.dh = 1, pg.dw = 1;
+    if (validate(&pg) != CKS_OK) return m;
+    // the pseudo output must reach every phase row / column: o = u + a + p' < O'
+    if (amax_h - 1 + m.ph2 >= out_extent(pg.H, pg.FH, 1, pg.ph) || amax_w - 1 + m.pw2 >= out_extent(pg.W, pg.FW, 1, pg.pw))
+        return m;
+    for (auto& ph : th) m.ih_s[ph.y] = int16_t(ph.ih_s), m.a_y[ph.y] = int16_t(ph.a);
+    for (auto& ph : tw) m.iw_s[ph.y] = int16_t(ph.ih_s), m.a_x[ph.y] = int16_t(ph.a);
+    m.pg = pg;
+    m.ok = true;
+    (void)dt;
+    return m;
 }
 
 bool ks_direct_eligible(const cks_geom& g, cks_dtype dt) {
@@ -668,9 +710,10 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                                             : (direct ? igemm_cfg_deconv_w(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms));
         snprintf(b, sizeof b,
                  "igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d out_tiles=%lld "
-                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d ks_direct=%d",
+                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d ks_direct=%d ks_mp=%d",
                  c.BN, c.pbw, c.KB, c.ntap, c.pa, c.apos, c.stages, c.a_stages, c.unified, (long long)c.out_tiles, c.Z,
-                 c.zc, c.kc_blocks, c.epi_warps, c.pair, direct ? 1 : 0);
+                 c.zc, c.kc_blocks, c.epi_warps, c.pair, direct ? 1 : 0,
+                 op == CKS_OP_DECONV && mp_plan(g, dt).ok ? 1 : 0);
         return b;
     }
     const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);
@@ -857,6 +900,15 @@ static WsLayout ws_layout_plan(const cks_geom& g, cks_dtype dt, cks_op op, int g
     // W given: room for Stage1's packed sub-filters whichever KS-deconv variant runs
     // (cks_deconv2d_ex may force the Stage1 path); split-K scratch for both plans
     if (op == CKS_OP_DECONV && !c_packed_given) take(ks_split_bytes(g, dt), L.c_packed, L.c_packed_bytes);
+    if (op == CKS_OP_DECONV && !c_packed_given) {  // multi-phase KS-deconv (narrow outputs)
+        const MpPlan m = mp_plan(g, dt);
+        if (m.ok) {
+            const int64_t OHp = out_extent(m.pg.H, m.pg.FH, 1, m.pg.ph), OWp = out_extent(m.pg.W, m.pg.FW, 1, m.pg.pw);
+            take(size_t(m.NP) * m.CH * m.CW * pad_ch(g.OC, dt) * eb, L.mp_w, L.mp_w_bytes);
+            take(size_t(g.N) * OHp * OWp * m.NP * 4, L.mp_y, L.mp_y_bytes);
+            take(ws_layout(m.pg, dt, CKS_OP_FWD, 0, false, num_sms).total, L.mp_inner, L.mp_inner_bytes);
+        }
+    }
     if ((op == CKS_OP_FWD && !row) || op == CKS_OP_DECONV) {
         std::vector<IgemmCfg> cs;
         if (op == CKS_OP_FWD) cs.push_back(igemm_cfg_fwd(g, dt, num_sms));

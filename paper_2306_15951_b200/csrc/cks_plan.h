@@ -181,7 +181,20 @@ WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
 struct WsLayout {
     size_t x_pad = 0, w_pad = 0, dy_pad = 0, c_packed = 0, partial = 0, sem = 0, total = 0;
     size_t x_pad_bytes = 0, w_pad_bytes = 0, dy_pad_bytes = 0, c_packed_bytes = 0, partial_bytes = 0, sem_bytes = 0;
+    size_t mp_w = 0, mp_y = 0, mp_inner = 0;  // multi-phase KS-deconv: stacked filter, pseudo output, inner ws
+    size_t mp_w_bytes = 0, mp_y_bytes = 0, mp_inner_bytes = 0;
 };
+
+// Multi-phase KS-deconv for narrow outputs (kernels/aux.cuh ks_mp_*): the
+// phases stacked on N of one unit-stride ConvV2 over dY (pseudo geometry
+// `pg`: X := dY, OC := NP stacked channels, F := CH x CW, padding ph2, pw2).
+struct MpPlan {
+    bool ok = false;
+    int CH = 0, CW = 0, NP = 0, ph2 = 0, pw2 = 0;
+    int16_t ih_s[8], a_y[8], iw_s[8], a_x[8];
+    cks_geom pg;
+};
+MpPlan mp_plan(const cks_geom& g, cks_dtype dt);
 WsLayout ws_layout(const cks_geom& g, cks_dtype dt, cks_op op, int gz, bool c_packed_given, int num_sms);
 size_t ks_split_bytes(const cks_geom& g, cks_dtype dt);
 

@@ -128,6 +128,72 @@ __global__ void __launch_bounds__(256) zero_insert_kernel(const V* __restrict__ 
     }
 }
 
+// Multi-phase KS-deconv for narrow outputs (I_C <= 8, F % s == 0 on both
+// axes, so every phase has the same CH x CW sub-filter): the sh*sw phases are
+// stacked on the GEMM N dimension.  With the phase row index shifted by a_y
+// (T2), every phase reads the SAME CH x CW window of dY at window origin r, so
+// the deconvolution is one unit-stride ConvV2 over dY with the stacked filter
+//   Wm[n = (y*sw + x)*IC + ic][ch][cw][oc] = C_{y,x}[oc,ch,cw,ic]
+//                                          = W[oc, y+(CH-1-ch)*sh, x+(CW-1-cw)*sw, ic]
+// (zeros for n >= sh*sw*IC, oc >= OC) and a phase-strided scatter of its
+// output Y'[n][o][q][.] to dX rows u*sh + ih_s(y), u = o - ph' - a_y.
+template <typename T>
+__global__ void __launch_bounds__(256) ks_mp_pack_kernel(const T* __restrict__ W, T* __restrict__ out, int OC,
+                                                         int FH, int FW, int IC, int sh, int sw, int CH, int CW,
+                                                         int NP, int OCp) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    const long long total = static_cast<long long>(NP) * CH * CW * OCp;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += gridDim.x * 256LL) {
+        const int oc = int(i % OCp);
+        long long r = i / OCp;
+        const int cw = int(r % CW);
+        r /= CW;
+        const int ch = int(r % CH);
+        const int n = int(r / CH);
+        const int pidx = n / IC, ic = n % IC;
+        T v = T(0);
+        if (pidx < sh * sw && oc < OC) {
+            const int y = pidx / sw, x = pidx % sw;
+            const int fh = y + (CH - 1 - ch) * sh, fw = x + (CW - 1 - cw) * sw;
+            v = W[((static_cast<long long>(oc) * FH + fh) * FW + fw) * IC + ic];
+        }
+        out[i] = v;
+    }
+}
+
+// dX[n][u*sh + ih_s(y)][v*sw + iw_s(x)][ic] = Y'[n][u + a_y + ph'][v + a_x + pw'][(y*sw+x)*IC + ic]
+// for every phase and row / column of the phase (the phases partition dX, so
+// every element of dX is written exactly once).  Thread = one dX element.
+struct MpPhase {
+    int16_t ih_s[8], a_y[8], iw_s[8], a_x[8];
+};
+__global__ void __launch_bounds__(256) ks_mp_scatter_kernel(const float* __restrict__ yp, float* __restrict__ dx,
+                                                            long long N, int H, int W, int IC, int sh, int sw, int MH,
+                                                            int MW, int NP, int ph2, int pw2, MpPhase t) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    const long long total = N * H * W * IC;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += gridDim.x * 256LL) {
+        const int ic = int(i % IC);
+        long long r = i / IC;
+        const int iw = int(r % W);
+        r /= W;
+        const int ih = int(r % H);
+        const long long n = r / H;
+        // phase of this element: ih = u*sh + ih_s(y) with ih_s(y) in [0, sh)
+        int y = 0, x = 0;
+        while (y + 1 < sh && t.ih_s[y] != ih % sh) ++y;
+        while (x + 1 < sw && t.iw_s[x] != iw % sw) ++x;
+        const int u = (ih - t.ih_s[y]) / sh, v = (iw - t.iw_s[x]) / sw;
+        const int o = u + t.a_y[y] + ph2, q = v + t.a_x[x] + pw2;
+        float val = 0.f;
+        if (o >= 0 && o < MH && q >= 0 && q < MW)
+            val = yp[((n * MH + o) * MW + q) * NP + (y * sw + x) * IC + ic];
+        dx[i] = val;
+    }
+}
+
 // out[i] = sum_{z = 0..gz-1} part[z][i] with a FIXED association
 // (deterministic): z-group g = threadIdx.y sums z = g, g+G, g+2G, ... in
 // increasing z, then the G group sums are added in order g = 0..G-1.

@@ -119,7 +119,8 @@ def deconv2d(dy, w, x_hw, stride=1, padding=0, c_packed=None, in_channels=None, 
     Pass ``c_packed`` (from ks_split) to skip Stage1; then ``w`` may be a
     shape-only tensor and is not read.  ``ks_mode`` (W given): "auto" (the
     library's choice), "stage1_free" (the GEMM reads W directly, no packed
-    sub-filters) or "stage1" (Stage1 into the workspace, then Stage2&3)."""
+    sub-filters), "stage1" (Stage1 into the workspace, then Stage2&3) or
+    "multiphase" (narrow outputs: the phases stacked on the GEMM N dimension)."""
     _check_dev(dy, c_packed, out)
     dt = _dtype_code(dy)
     N, OH_, OW_, OC = dy.shape
@@ -141,7 +142,8 @@ def deconv2d(dy, w, x_hw, stride=1, padding=0, c_packed=None, in_channels=None, 
     else:
         ws = workspace(L.cks_workspace_size(g, dt, L.CKS_OP_DECONV), dy.device, stream)
         wp, cp = 0, c_packed.data_ptr()
-    mode = {"auto": L.CKS_KS_AUTO, "stage1_free": L.CKS_KS_STAGE1_FREE, "stage1": L.CKS_KS_STAGE1}[ks_mode]
+    mode = {"auto": L.CKS_KS_AUTO, "stage1_free": L.CKS_KS_STAGE1_FREE, "stage1": L.CKS_KS_STAGE1,
+            "multiphase": L.CKS_KS_MULTIPHASE}[ks_mode]
     L.cks_deconv2d_ex(g, dt, dy.data_ptr(), wp or None, cp or None, out.data_ptr(), *_ws_args(ws),
                       _stream_ptr(stream), mode)
     return out
