@@ -15,7 +15,8 @@ EXPERIMENTS = os.environ.get("CKS_EXPERIMENTS") == "1"
 LIB = os.path.join(PKG, "libcks_exp.so" if EXPERIMENTS else "libcks.so")
 SOURCES = [os.path.join(CSRC, "cks_api.cu"), os.path.join(CSRC, "cks_plan.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("cks_plan.h", "kernels/ptx.cuh", "kernels/igemm.cuh",
-                                                  "kernels/wgrad.cuh", "kernels/aux.cuh", "kernels/narrow.cuh")] + \
+                                                  "kernels/wgrad.cuh", "kernels/aux.cuh", "kernels/narrow.cuh",
+                                                  "kernels/allreduce.cuh")] + \
     [os.path.join(os.path.dirname(PKG), "include", "cks.h")]
 
 

@@ -246,25 +246,29 @@ FastDiv make_fastdiv(uint32_t d) {
 // the kernel reproduces the KRow table exactly.
 bool fill_axis(KAxisC& k, const std::vector<KRow>& rows) {
     memset(&k, 0, sizeof(k));
-    int nph = 0;
-    for (size_t i = 0; i < rows.size(); ++i) {
-        const KRow& r = rows[i];
-        if (i == 0 || r.phase != rows[i - 1].phase) {  // a new run (phase) starts here
-            if (nph == kMaxPhases || r.phase > 255) return false;
-            k.row0[nph] = int16_t(i);
-            k.phid[nph] = int16_t(r.phase);
-            k.a00[nph] = int16_t(r.a0);
-            k.out0[nph] = int16_t(r.out);
-            if (i + 1 < rows.size() && rows[i + 1].phase == r.phase) {
-                k.a0st[nph] = int16_t(rows[i + 1].a0 - r.a0);
-                k.outst[nph] = int16_t(rows[i + 1].out - r.out);
-            }
-            ++nph;
+    const std::vector<int> st = run_starts(rows);  // affine runs (one phase, one group length)
+    if (st.size() > size_t(kMaxPhases)) return false;
+    const int nph = int(st.size());
+    for (int x = 0; x < nph; ++x) {
+        const KRow& r = rows[st[x]];
+        const int e = x + 1 < nph ? st[x + 1] : int(rows.size());
+        if (r.phase > 255 || r.glen < 1 || r.glen > 16 || (r.glen > 1 && r.phase > 15)) return false;
+        k.row0[x] = int16_t(st[x]);
+        k.phid[x] = int16_t(r.phase);
+        k.rlen[x] = int8_t(r.glen);
+        k.a00[x] = int16_t(r.a0);
+        k.out0[x] = int16_t(r.out);
+        if (st[x] + 1 < e) {
+            k.a0st[x] = int16_t(rows[st[x] + 1].a0 - r.a0);
+            k.outst[x] = int16_t(rows[st[x] + 1].out - r.out);
         }
-        const int x = nph - 1, u = int(i) - k.row0[x];
-        if (r.a0 != k.a00[x] + int64_t(u) * k.a0st[x] || r.out != k.out0[x] + int64_t(u) * k.outst[x]) return false;
-        k.ts[i] = uint8_t(r.ts);
-        k.te[i] = uint8_t(r.te);
+        for (int i = st[x]; i < e; ++i) {
+            const int u = i - st[x];
+            if (rows[i].a0 != k.a00[x] + int64_t(u) * k.a0st[x] || rows[i].out != k.out0[x] + int64_t(u) * k.outst[x])
+                return false;
+            k.ts[i] = uint8_t(rows[i].ts);
+            k.te[i] = uint8_t(rows[i].te);
+        }
     }
     k.row0[nph] = int16_t(rows.size());
     k.nph = int16_t(nph);
@@ -408,6 +412,12 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.zsplit = cfg.Z;
     p.zc = cfg.zc;
     p.pair = cfg.pair;
+    if (cfg.rg_ni > 0) {  // row groups: M row r = (group row r / rg_ni, image r % rg_ni)
+        if (cfg.rg_ni != 32 && cfg.rg_ni != 64) return CKS_ERR_UNSUPPORTED;
+        p.rg_ni = cfg.rg_ni;
+        p.rg_shift = cfg.rg_ni == 32 ? 5 : 6;
+        p.rg_ostep = cfg.rg_ostep;
+    }
     p.epi_warps = cfg.epi ? cfg.epi_warps : 4;
     p.epi_bufs = cfg.epi ? cfg.epi_bufs : 1;
     {
@@ -945,13 +955,20 @@ cks_status cks_conv2d_fwd(const cks_geom* g, cks_dtype dt, const void* x, const 
         wsrc = wp;
     }
     IgemmCfg cfg = igemm_cfg_fwd(*g, dt, kPlanSMs);
+    if (cfg.rg_ni > 0) rh = igemm_rows_fwd(*g, cfg.rg_ni);  // row groups (N <= 64)
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
-    {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile
+    {   // X viewed as (C, N, W, H): one box = apos columns x 128 images, each column a canonical tile;
+        // row groups: one column x rg_ni images x rg_ph rows (element stride s_h) = 128 tile rows
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->H)};
         uint64_t sb[3] = {uint64_t(g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
         uint32_t box[4] = {BK, 128u / uint32_t(cfg.cm), cfg.cm > 1 ? 1u : uint32_t(cfg.apos), 1};
-        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+        uint32_t es[4] = {1, 1, 1, uint32_t(cfg.rg_es)};
+        if (cfg.rg_ni > 0) {
+            box[1] = uint32_t(cfg.rg_ni);
+            box[3] = uint32_t(cfg.rg_ph * cfg.rg_es);
+        }
+        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB, false, cfg.rg_ni > 0 ? es : nullptr)) return CKS_ERR_CUDA;
     }
     {   // W viewed as (C, OC, FH*FW, 1): one box = the FW taps of a filter row x BN filters
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->OC), uint64_t(g->FH * g->FW), 1};
@@ -1037,12 +1054,17 @@ cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, cons
         // Stage1-free: B straight from W (OHWI) viewed as (IC, OC, FW, FH); one box = the
         // CW taps fw = x, x+sw, ... (element stride sw) of one filter row, 128 B of IC x BK OC
         IgemmCfg cfg = igemm_cfg_deconv_w(*g, dt, kPlanSMs);
+        if (cfg.rg_ni > 0) rh = igemm_rows_deconv(*g, cfg.rg_ni);  // row groups (N <= 64)
         const uint32_t BK = uint32_t(cfg.KB / eb);
         CUtensorMap ta, tb;
         {
             uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
             uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
             uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
+            if (cfg.rg_ni > 0) {  // one column x rg_ni images x rg_ph consecutive dY rows
+                box[1] = uint32_t(cfg.rg_ni);
+                box[3] = uint32_t(cfg.rg_ph);
+            }
             if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
         }
         const int64_t atomw = 128 / eb;
@@ -1071,12 +1093,18 @@ cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, cons
     }
     const int64_t CHm = cdiv(g->FH, g->sh), CWm = cdiv(g->FW, g->sw), P = int64_t(g->sh) * g->sw;
     IgemmCfg cfg = igemm_cfg_deconv(*g, dt, kPlanSMs);
+    if (cfg.rg_ni > 0) rh = igemm_rows_deconv(*g, cfg.rg_ni);  // row groups (N <= 64)
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
-    {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images
+    {   // dY viewed as (OC, N, OW, OH): one box = apos columns x 128 images (row groups: one
+        // column x rg_ni images x rg_ph consecutive dY rows)
         uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OH)};
         uint64_t sb[3] = {uint64_t(OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
         uint32_t box[4] = {BK, 128u / uint32_t(cfg.cm), cfg.cm > 1 ? 1u : uint32_t(cfg.apos), 1};
+        if (cfg.rg_ni > 0) {
+            box[1] = uint32_t(cfg.rg_ni);
+            box[3] = uint32_t(cfg.rg_ph);
+        }
         if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     {   // packed C_{y,x} viewed as (OCp, C, CHm*CWm, P): one box = the CWm taps of sub-filter row ch

@@ -118,6 +118,47 @@ std::vector<KRow> krows_deconv(const Axis& a) {
     return r;
 }
 
+std::vector<KRow> group_rows(const std::vector<KRow>& rows, int ph, int64_t es, int64_t ostep) {
+    std::vector<KRow> g;
+    for (size_t i = 0; i < rows.size();) {
+        KRow r = rows[i];
+        size_t j = i + 1;
+        while (j < rows.size() && int(j - i) < ph && rows[j].phase == r.phase && rows[j].ts == r.ts &&
+               rows[j].te == r.te && rows[j].a0 == r.a0 + int64_t(j - i) * es &&
+               rows[j].out == r.out + int64_t(j - i) * ostep)
+            ++j;
+        r.glen = int64_t(j - i);
+        g.push_back(r);
+        i = j;
+    }
+    return g;
+}
+
+std::vector<int> run_starts(const std::vector<KRow>& rows) {
+    std::vector<int> st;
+    size_t s = 0;
+    int64_t a0st = 0, outst = 0;
+    for (size_t i = 0; i < rows.size(); ++i) {
+        const KRow& r = rows[i];
+        bool start = i == 0 || r.phase != rows[i - 1].phase || r.glen != rows[i - 1].glen;
+        if (!start) {
+            const int64_t u = int64_t(i - s);
+            if (u == 1) {
+                a0st = r.a0 - rows[s].a0;
+                outst = r.out - rows[s].out;
+            } else if (r.a0 != rows[s].a0 + u * a0st || r.out != rows[s].out + u * outst) {
+                start = true;
+            }
+        }
+        if (start) {
+            st.push_back(int(i));
+            s = i;
+            a0st = outst = 0;
+        }
+    }
+    return st;
+}
+
 // Experiment knobs (tools/ sweeps only; compiled in only with -DCKS_EXPERIMENTS,
 // i.e. the separate libcks_exp.so that CKS_EXPERIMENTS=1 builds and loads), read once
 // per process: CKS_IGEMM_CFG="BN,PBW,Z[,APOS,BSTAGES]" overrides the tile
@@ -128,7 +169,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -158,6 +199,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_MT_TF32")) wmt_tf32 = atoi(e) != 0;  // TF32 row tiles
         if (const char* e = cks_knob("CKS_WGRAD_A1_TF32")) wa1_tf32 = atoi(e) != 0;  // TF32: 64 OC of dY per stage
         if (const char* e = cks_knob("CKS_WGRAD_TC")) wtc = atoi(e);  // filter-row groups (2: multicast clusters)
+        if (const char* e = cks_knob("CKS_RG")) rg = atoi(e) != 0;  // 0: batch-as-M tiles at any N
     }
 };
 static const Knobs& knobs() {
@@ -178,8 +220,9 @@ bool epi_staging() { return knobs().epi != 0; }
 static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout,
                             int64_t kchan, int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms,
                             int force_pbw, int epi_warps, bool pair = false, int epi_bufs = 1, int force_bn = 0,
-                            int min_bn = 0) {
+                            int min_bn = 0, int rg_ni = 0) {
     IgemmCfg c;
+    if (rg_ni > 0) pair = false;  // row groups: one M tile holds the whole batch
     c.pair = pair ? 1 : 0;
     c.epi_bufs = epi_bufs;
     // coalesced-store epilogue staging only where the output rows allow 16 B vectors
@@ -189,6 +232,11 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     if (knobs().smem_cap > 0) budget = std::min<int64_t>(budget, int64_t(knobs().smem_cap) * 1024);  // experiments
     c.wph_cnt = wph_cnt;
     c.nblk = int((N + 127) / 128);
+    if (rg_ni > 0) {
+        c.rg_ni = rg_ni;
+        c.rg_ph = 128 / rg_ni;
+        c.nblk = 1;
+    }
     c.BN = nout <= 32 ? 32 : (nout <= 64 ? 64 : 128);
     int ov_bn = 0, ov_pbw = 0, ov_z = 0;
     const bool ov = cfg_override(ov_bn, ov_pbw, ov_z);
@@ -277,6 +325,9 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
     if (2 * c.stage_bytes + 2 * int64_t(c.apos) * col_bytes > budget) c.stages = 1;
     if (ov && g_ov_apos > 0) c.apos = std::min(c.pa, g_ov_apos);
     if (ov && g_ov_bst > 0) c.stages = g_ov_bst;
+    // row groups: one activation column per A slot (a box of rg_ph rows x rg_ni
+    // images is one 128-row K-major tile only for a single column)
+    if (c.rg_ni > 0) c.apos = 1;
     c.a_stages = int(std::min<int64_t>(8, (budget - c.stages * c.stage_bytes) / (int64_t(c.apos) * col_bytes)));
     // one A slot per row step: A slot and B row form one stage (one barrier pair,
     // one commit per row step); as many stages as fit
@@ -334,7 +385,10 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
 // flight) when their 4 KB staging buffers cost no pipeline depth or tile width.
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw,
-                   int force_bn) {
+                   int force_bn, int rg_ni) {
+    if (rg_ni > 0)  // row groups (N <= 64): single-CTA tiles, one wave model as below
+        return igemm_cfg_w(rows_h, wph_cnt, N, nout, kchan, eb, max_taps_h, ntap, a0_step, num_sms, force_pbw, 4,
+                           false, 1, std::max(force_bn, 0), force_bn < 0 ? -force_bn : 0, rg_ni);
     // Stage1-free KS-deconv: force_bn > 0 fixes the B width (one 128-byte MN atom per tap),
     // force_bn < 0 asks for B widths of whole atoms of -force_bn channels; no CTA pairs
     if (force_bn != 0)
@@ -384,19 +438,52 @@ static int64_t max_window(const std::vector<KRow>& rows) {
     return m;
 }
 
+int rg_images(int64_t N) {
+    if (!knobs().rg || N > 64) return 0;
+    return N <= 32 ? 32 : 64;
+}
+
+std::vector<KRow> igemm_rows_fwd(const cks_geom& g, int rg_ni) {
+    auto rh = krows_fwd(axis_h(g));
+    return rg_ni > 0 ? group_rows(rh, 128 / rg_ni, g.sh, 1) : rh;
+}
+
+std::vector<KRow> igemm_rows_deconv(const cks_geom& g, int rg_ni) {
+    auto rh = krows_deconv(axis_h(g));
+    return rg_ni > 0 ? group_rows(rh, 128 / rg_ni, 1, g.sh) : rh;
+}
+
+int rg_plan(const cks_geom& g, bool deconv) {
+    const int ni = rg_images(g.N);
+    if (ni == 0 || (!deconv && g.sh > 8)) return 0;  // TMA element strides <= 8
+    const auto rows = deconv ? igemm_rows_deconv(g, ni) : igemm_rows_fwd(g, ni);
+    for (auto& r : rows)
+        if (r.phase > 15) return 0;  // the kernel packs (phase, group length) into one byte
+    return run_starts(rows).size() <= 16 ? ni : 0;  // kernels/igemm.cuh kMaxPhases runs
+}
+
 static IgemmCfg igemm_cfg_fwd_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
-    Axis ah = axis_h(g), aw = axis_w(g);
-    auto rh = krows_fwd(ah);
-    return igemm_cfg(ah.O, {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt), max_window(rh), g.FW, g.sw, num_sms);
+    Axis aw = axis_w(g);
+    const int rg = rg_plan(g, false);
+    auto rh = igemm_rows_fwd(g, rg);
+    IgemmCfg c = igemm_cfg(int64_t(rh.size()), {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt), max_window(rh),
+                           g.FW, g.sw, num_sms, 0, 0, rg);
+    c.rg_es = int(g.sh);
+    c.rg_ostep = 1;
+    return c;
 }
 
 static IgemmCfg igemm_cfg_deconv_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
-    Axis ah = axis_h(g), aw = axis_w(g);
-    auto rh = krows_deconv(ah);
+    Axis aw = axis_w(g);
+    const int rg = rg_plan(g, true);
+    auto rh = igemm_rows_deconv(g, rg);
     std::vector<int64_t> cnt;
     for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
-    return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
-                     num_sms);
+    IgemmCfg c = igemm_cfg(int64_t(rh.size()), cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh),
+                           cdiv(g.FW, g.sw), 1, num_sms, 0, 0, rg);
+    c.rg_es = 1;
+    c.rg_ostep = int(g.sh);
+    return c;
 }
 
 MpPlan mp_plan(const cks_geom& g, cks_dtype dt) {
@@ -446,15 +533,19 @@ bool ks_direct_eligible(const cks_geom& g, cks_dtype dt) {
 }
 
 static IgemmCfg igemm_cfg_deconv_w_plan(const cks_geom& g, cks_dtype dt, int num_sms) {
-    Axis ah = axis_h(g), aw = axis_w(g);
-    auto rh = krows_deconv(ah);
+    Axis aw = axis_w(g);
+    const int rg = rg_plan(g, true);
+    auto rh = igemm_rows_deconv(g, rg);
     std::vector<int64_t> cnt;
     for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
     const int atomw = int(128 / elem_bytes(dt));  // channels of one 128-byte MN atom
     // several atoms per tap need the IC axis split exactly into atoms (5-D map)
     const int fb = g.C % atomw == 0 ? -atomw : atomw;
-    return igemm_cfg(ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh), cdiv(g.FW, g.sw), 1,
-                     num_sms, 0, fb);
+    IgemmCfg c = igemm_cfg(int64_t(rh.size()), cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt), max_window(rh),
+                           cdiv(g.FW, g.sw), 1, num_sms, 0, fb, rg);
+    c.rg_es = 1;
+    c.rg_ostep = int(g.sh);
+    return c;
 }
 
 // Policy: Stage1-free where eligible and the W-direct plan keeps the packed
@@ -710,10 +801,10 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                                             : (direct ? igemm_cfg_deconv_w(g, dt, num_sms) : igemm_cfg_deconv(g, dt, num_sms));
         snprintf(b, sizeof b,
                  "igemm BN=%d pbw=%d KB=%d ntap=%d pa=%d apos=%d stages=%d a_stages=%d unified=%d out_tiles=%lld "
-                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d ks_direct=%d ks_mp=%d",
+                 "Z=%d zc=%d kc=%d epi_warps=%d pair=%d ks_direct=%d ks_mp=%d rg=%d",
                  c.BN, c.pbw, c.KB, c.ntap, c.pa, c.apos, c.stages, c.a_stages, c.unified, (long long)c.out_tiles, c.Z,
                  c.zc, c.kc_blocks, c.epi_warps, c.pair, direct ? 1 : 0,
-                 op == CKS_OP_DECONV && mp_plan(g, dt).ok ? 1 : 0);
+                 op == CKS_OP_DECONV && mp_plan(g, dt).ok ? 1 : 0, c.rg_ni);
         return b;
     }
     const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);

@@ -60,9 +60,23 @@ int64_t axis_valid_pairs(const Axis& a);         // V
 // Row r: A-operand coordinate of tap 0 (a0), trimmed tap window [ts, te),
 // output coordinate, phase index.  Fwd: one row per output o (T1).  Deconv:
 // the T2 rows of all phases in phase order.
-struct KRow { int64_t a0, ts, te, out, phase; };
+// glen: row groups (below) -- the group holds rows [this, this + glen) of the
+// ungrouped table, all with this row's window and phase.
+struct KRow { int64_t a0, ts, te, out, phase; int64_t glen = 1; };
 std::vector<KRow> krows_fwd(const Axis& a);
 std::vector<KRow> krows_deconv(const Axis& a);
+
+// Row groups for small per-GPU batches (N <= 64): the implicit GEMM's M = 128
+// rows become rg_ph = 128 / rg_ni consecutive output rows x rg_ni images
+// (rg_ni = 32 or 64), so a batch of 32 images fills the tensor-core tile
+// instead of a quarter of it.  A group is a run of <= ph rows of one phase
+// with the SAME trimmed window (trim-homogeneous), A coordinates a0
+// stepping by es (the TMA element stride of the A box) and outputs by ostep.
+std::vector<KRow> group_rows(const std::vector<KRow>& rows, int ph, int64_t es, int64_t ostep);
+// Start indices of the affine runs of a row table (one phase, one group
+// length, a0 and out affine in the run index): the kernel's compact axis form.
+std::vector<int> run_starts(const std::vector<KRow>& rows);
+int rg_images(int64_t N);  // 32 / 64 images per M tile (row groups), 0 = batch-as-M (N > 64)
 
 // MMA-program capacity of the implicit GEMM (kernels/igemm.cuh): entries per
 // list.  Every entry is one MMA group covering >= 1 (pixel, tap) pair of the
@@ -108,10 +122,22 @@ struct IgemmCfg {
     int a0_step = 1;                  // tap-0 column step between consecutive pixels
     int64_t out_tiles = 0, tiles = 0;
     std::vector<int64_t> wph_cnt;  // rows per w phase
+    int rg_ni = 0;                 // row groups: images per M tile (0 = off: M = 128 images)
+    int rg_ph = 1;                 // row groups: output rows per M tile (128 / rg_ni)
+    int rg_es = 1;                 // row groups: A-row step inside a group (TMA element stride)
+    int rg_ostep = 1;              // row groups: output-row step inside a group
 };
 IgemmCfg igemm_cfg(int64_t rows_h, const std::vector<int64_t>& wph_cnt, int64_t N, int64_t nout, int64_t kchan,
                    int64_t eb, int64_t max_taps_h, int64_t ntap, int64_t a0_step, int num_sms, int force_pbw = 0,
-                   int force_bn = 0);
+                   int force_bn = 0, int rg_ni = 0);
+// Row groups of a 2-D layer: rg_ni for the forward / KS-deconv h axis (0 when
+// N > 64 or the grouped table does not fit the kernel's compact axis form),
+// and the h-axis rows the igemm runs over (grouped when rg_ni > 0).  A forward
+// group's A rows step by s_h (TMA element stride), its outputs by 1; a
+// KS-deconv group's A rows step by 1 (one phase), its outputs by s_h.
+int rg_plan(const cks_geom& g, bool deconv);
+std::vector<KRow> igemm_rows_fwd(const cks_geom& g, int rg_ni);
+std::vector<KRow> igemm_rows_deconv(const cks_geom& g, int rg_ni);
 constexpr int kSmemBudget = 227 * 1024 - 1024 - 512 - 5376 - 4160;  // minus alignment, barriers, 3 axis tables, MMA programs
 constexpr int kEpiStageBytes = 4 * 4096;  // epilogue transpose staging: 4 warps x (32 x 32 fp32)
 constexpr int epi_stage_bytes(int epi_warps, int bufs = 1) { return epi_warps * bufs * 4096; }

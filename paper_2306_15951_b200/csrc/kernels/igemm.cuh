@@ -91,6 +91,7 @@ struct KAxisC {
     int16_t row0[kMaxPhases + 1];  // run x (one phase) holds rows [row0[x], row0[x+1])
     int16_t a00[kMaxPhases], a0st[kMaxPhases], out0[kMaxPhases], outst[kMaxPhases];
     int16_t phid[kMaxPhases];      // phase index of run x (phases without rows have no run)
+    int8_t rlen[kMaxPhases];       // row groups: output rows per table row of run x (1 = ungrouped)
     int16_t nph, nrows;
 };
 
@@ -147,6 +148,9 @@ struct IgemmParams {
     int16_t bfh0[kMaxPhases], bcw[kMaxPhases];
     int bsh;
     unsigned long long* trace;  // debug timeline (nullptr in production): [cta<4][role<5][1024]
+    // Row groups (small batches, N <= 64): M row r of a tile = image r % rg_ni of output row
+    // orow + (r / rg_ni) * rg_ostep (valid for r / rg_ni < the group length); 0 = batch-as-M
+    int rg_ni, rg_shift, rg_ostep;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -189,6 +193,7 @@ struct Tile {
     int orow;             // output row (flattened d * out_rows_h + h)
     int a0d;              // A depth coordinate of filter depth 0
     int rs0, rs1;         // row-step range [rs0, rs1) of this split
+    int glen;             // row groups: output rows of this tile's group
     int rot;              // per-CTA rotation of the row-step order (spreads weight reads over L2)
     int chs;              // first filter row of the h window
     int cwlo, cwhi;       // union of the pixels' w windows
@@ -225,7 +230,8 @@ __device__ __forceinline__ Tile decode_tile(long long t64, const IgemmParams& p,
     while (x + 1 < p.nph_w && p.wb_cum[x + 1] <= wb) ++x;
     c.j0 = p.wph_off[x] + (wb - p.wb_cum[x]) * p.pbw;
     c.len = min(p.pbw, p.wph_off[x] + p.wph_cnt[x] - c.j0);
-    c.ph = (ad.phase[c.rd] * p.phases_h + ah.phase[c.rh]) * p.phases_w + aw.phase[c.j0];
+    c.ph = (ad.phase[c.rd] * p.phases_h + (ah.phase[c.rh] & 15)) * p.phases_w + aw.phase[c.j0];
+    c.glen = (ah.phase[c.rh] >> 4) + 1;
     const int chs = ah.ts[c.rh], che = ah.te[c.rh];
     const int cds = ad.ts[c.rd], cde = ad.te[c.rd];
     c.cds = cds;
@@ -328,7 +334,8 @@ __global__ void __launch_bounds__(384, 1)
         t.out[r] = v ? int16_t(ax.out0[x] + u * ax.outst[x]) : int16_t(0);
         t.ts[r] = v ? ax.ts[r] : uint8_t(0);
         t.te[r] = v ? ax.te[r] : uint8_t(0);
-        t.phase[r] = v ? uint8_t(ax.phid[x]) : uint8_t(0);
+        // phase, and (row groups, h axis) the group length - 1 in bits 4..7
+        t.phase[r] = v ? uint8_t(ax.phid[x] | ((ax.rlen[x] - 1) << 4)) : uint8_t(0);
     }
 
     if (threadIdx.x == 0) trace_gt(p, 0);
@@ -717,7 +724,13 @@ __global__ void __launch_bounds__(384, 1)
             ptx::mbar_wait(&tfull[acc], acc_ph);
             if (et == 0) trace_ev(p, 2, ti, 1);
             ptx::tc_fence_after();
-            const int nrow0 = c.nblk * 128 + int(sub) * 32;  // image of lane 0
+            // M row -> (image, output row).  Batch-as-M: image nblk*128 + row of output row orow.
+            // Row groups (rg_ni >= 32): the warp's 32 rows are images of ONE group row wgr,
+            // output row orow + wgr * rg_ostep, stored only if wgr < the group length.
+            const int wgr = p.rg_ni ? (int(sub * 32) >> p.rg_shift) : 0;
+            const bool wlive_row = wgr < c.glen;
+            const int orow_w = c.orow + wgr * p.rg_ostep;
+            const int nrow0 = p.rg_ni ? (int(sub * 32) & (p.rg_ni - 1)) : c.nblk * 128 + int(sub) * 32;  // image of lane 0
             const int n = nrow0 + int(lane);
             const int cbase = c.nb * BNo;
             const int cvalid = min(BNo, p.out_C - cbase);
@@ -740,7 +753,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN +
                                            c0, r);
                         ptx::tmem_ld_wait();
-                        if (c0 >= cvalid) continue;
+                        if (c0 >= cvalid || !wlive_row) continue;
                         float* blk = epi + (ew * nbuf + (ebuf & (nbuf - 1u))) * 1024;
                         ++ebuf;
                         if (ptx::elect_one()) {  // the store that last used this buffer has read it
@@ -760,7 +773,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (ptx::elect_one()) {
-                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], c.orow, nrow0);
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], orow_w, nrow0);
                             ptx::bulk_commit();
                         }
                         __syncwarp();
@@ -786,7 +799,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN +
                                            c0, r);
                         ptx::tmem_ld_wait();
-                        if (c0 >= cvalid) continue;
+                        if (c0 >= cvalid || !wlive_row) continue;
                         float* blk = reinterpret_cast<float*>(stg + k * 4096);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
@@ -798,7 +811,7 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (ptx::elect_one()) {
-                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], c.orow, nrow0);
+                            ptx::tma_store_4d(&tmY, blk, cbase + c0, tab[1].out[c.j0 + j], orow_w, nrow0);
                             ptx::bulk_commit();
                         }
                         __syncwarp();
@@ -822,8 +835,8 @@ __global__ void __launch_bounds__(384, 1)
                     dst = reinterpret_cast<float*>(smem) + (j * (BN / 4)) * 512 + row * 4;
                 else if (split)  // column group q = (j*BN + c)/4 of row `row`
                     dst = p.part + ((c.out_tile * p.zsplit + c.z) * (pw_cols / 4) + j * (BN / 4)) * 512LL + row * 4;
-                else if (n < p.N)
-                    dst = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
+                else if (n < p.N && wlive_row)
+                    dst = p.out + ((static_cast<long long>(n) * p.out_H + orow_w) * p.out_W +
                                    tab[1].out[c.j0 + j]) * p.out_C + cbase;
                 const int lim = split ? BN : cvalid;
 #pragma unroll 1
@@ -832,7 +845,8 @@ __global__ void __launch_bounds__(384, 1)
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(pw_cols) + (BMN ? j : p.pbw - 1 - j) * BN + c0,
                                    r);
                     ptx::tmem_ld_wait();
-                    if (c0 >= lim || (p.dbg & 1) || (dst == nullptr && !stage)) continue;  // stage: warp-uniform
+                    if (c0 >= lim || (p.dbg & 1) || (dst == nullptr && !stage) || (stage && !wlive_row))
+                        continue;  // stage: warp-uniform
                     if (!live) {
 #pragma unroll
                         for (int q = 0; q < 32; ++q) r[q] = 0u;
@@ -856,7 +870,7 @@ __global__ void __launch_bounds__(384, 1)
                             const int cc = c0 + 4 * cq;
                             if (nn < p.N && cc < lim)
                                 *reinterpret_cast<float4*>(p.out + ((static_cast<long long>(nn) * p.out_H +
-                                                                     c.orow) * p.out_W +
+                                                                     orow_w) * p.out_W +
                                                                     tab[1].out[c.j0 + j]) * p.out_C + cbase + cc) = v;
                         }
                         __syncwarp();
@@ -900,14 +914,14 @@ __global__ void __launch_bounds__(384, 1)
                 __syncwarp();
                 asm volatile("bar.sync 1, %0;" ::"r"(32 * p.epi_warps) : "memory");
                 if (et == 0) trace_ev(p, 2, ti, 3);
-                if (*red_flag && n < p.N && half == 0) {
+                if (*red_flag && n < p.N && wlive_row && half == 0) {
                     // last segment: sum the Z partials in order z = 0..Z-1; thread = row,
                     // 8 column groups x Z vector loads in flight, coalesced 512 B per warp load
                     const float4* base = reinterpret_cast<const float4*>(p.part) +
                                          (c.out_tile * p.zsplit) * (pw_cols / 4) * 128LL + row;
                     const long long zs = (pw_cols / 4) * 128LL;
                     for (int j = 0; j < c.len; ++j) {
-                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
+                        float* orow = p.out + ((static_cast<long long>(n) * p.out_H + orow_w) * p.out_W +
                                                tab[1].out[c.j0 + j]) * p.out_C + cbase;
                         for (int c0 = 0; c0 < cvalid; c0 += 32) {
                             const float4* src = base + (j * BN + c0) / 4 * 128LL;
@@ -953,14 +967,15 @@ __global__ void __launch_bounds__(384, 1)
         ptx::cluster_sync();
         if (warp >= 4 && warp < 8 && blockIdx.x < p.num_tiles && !(p.dbg & 1)) {
             const Tile c = decode_tile(blockIdx.x, p, tab[0], tab[1], tab[2]);
-            const int row = int(threadIdx.x) - 128;  // accumulator row = image
-            const int n = c.nblk * 128 + row;
+            const int row = int(threadIdx.x) - 128;  // accumulator row = image (row groups: see epilogue)
+            const int gr = p.rg_ni ? (row >> p.rg_shift) : 0;
+            const int n = p.rg_ni ? (row & (p.rg_ni - 1)) : c.nblk * 128 + row;
             const int G = c.len * (BN / 4);  // float4 column groups of the tile
             const int g0 = (c.z * G) / p.zsplit, g1 = ((c.z + 1) * G) / p.zsplit;
             const int cbase = c.nb * BN;
             const int cvalid = min(BN, p.out_C - cbase);
             const uint32_t sbase = ptx::smem_u32(smem) + uint32_t(row) * 16u;
-            if (n < p.N) {
+            if (n < p.N && gr < c.glen) {
                 // two column groups x Z ranks of DSMEM loads in flight, then the fixed-order sums
 #pragma unroll 1
                 for (int gq = g0; gq < g1; gq += 2) {
@@ -991,7 +1006,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int gg = gq + h;
                         const int j = gg / (BN / 4), cc = (gg % (BN / 4)) * 4;
                         if (cc >= cvalid) continue;
-                        float* o = p.out + ((static_cast<long long>(n) * p.out_H + c.orow) * p.out_W +
+                        float* o = p.out + ((static_cast<long long>(n) * p.out_H + c.orow + gr * p.rg_ostep) * p.out_W +
                                             tab[1].out[c.j0 + j]) * p.out_C + cbase + cc;
                         if ((p.out_C % 4) == 0 && cc + 4 <= cvalid) {
                             *reinterpret_cast<float4*>(o) = v;

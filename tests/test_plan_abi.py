@@ -308,3 +308,18 @@ def test_op_counts3_match_oracle():
         assert [got["VD"], got["VH"], got["VW"]] == ref["V"]
         assert list(L.cks_output_shape3(g)) == ref["O"]
         n += 1
+
+
+def test_row_group_plans():
+    """Small per-GPU batches (N <= 64, e.g. C5 strong scaling: 256 / 8 = 32 images per GPU) tile M as
+    128 / rg_ni output rows x rg_ni images (row groups) instead of 128 images of one pixel."""
+    for N, want in [(1, 32), (20, 32), (32, 32), (33, 64), (64, 64), (65, 0), (128, 0), (256, 0)]:
+        for geo in [(N, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1), (N, 128, 28, 28, 256, 3, 3, 2, 2, 1, 1),
+                    (N, 64, 56, 56, 128, 1, 1, 2, 2, 0, 0)]:
+            g = L.make_geom(*geo)
+            for dt in (L.CKS_BF16, L.CKS_TF32):
+                for op in (L.CKS_OP_FWD, L.CKS_OP_DECONV):
+                    d = L.plan_dict(g, dt, op)
+                    assert d["kind"] == "igemm" and int(d["rg"]) == want, (geo, dt, op, d)
+                    if want:  # one activation column per A slot, no CTA pairs
+                        assert d["apos"] == "1" and d["pair"] == "0", d
