@@ -717,6 +717,8 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.tc = cfg.tc;
     p.tcmc = cfg.tcmc;
     p.pp = cfg.pp;
+    p.rg = cfg.rg;
+    p.rg_pk = cfg.rg ? cfg.rg_pk : 1;
     p.Wx = int(g.W);
     p.ouh_s = 1 << 20;
     p.ouh_e = -(1 << 20);
@@ -1156,7 +1158,12 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         dys = p;
     }
     CUtensorMap ta;  // dY viewed as (OC, OW, OH, N): boxes of 128 B of channels x 64 / 128 images
-    {
+    if (cfg.rg && !cfg.row) {  // row groups: (OC, N, OW, OH), boxes of rg images x rg_pk positions
+        uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(aw.O), uint64_t(ah.O)};
+        uint64_t sb[3] = {uint64_t(ah.O * aw.O * OCp * eb), uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb)};
+        uint32_t box[4] = {uint32_t(128 / eb), uint32_t(cfg.rg), uint32_t(cfg.rg_pk), 1};
+        if (!make_tmap4(&ta, dt, dys, d, sb, box, 128, dt == CKS_TF32)) return CKS_ERR_CUDA;
+    } else {
         uint64_t d[4] = {uint64_t(OCp), uint64_t(aw.O), uint64_t(ah.O), uint64_t(g->N)};
         uint64_t sb[3] = {uint64_t(OCp * eb), uint64_t(aw.O * OCp * eb), uint64_t(ah.O * aw.O * OCp * eb)};
         uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.row ? 64 : cfg.kimg)};
@@ -1170,7 +1177,13 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         s = run_wgrad_row(*g, dt, row_cfg_wgrad(*g, dt, gz, kPlanSMs), x, ta, wout, part_stride, st);
     } else {
         CUtensorMap tb;  // X viewed as (C, W, H, N): leaping rows ih = oh*sh + fh - ph
-        {
+        if (cfg.rg) {  // row groups: (C, N, W, H), rg images x rg_pk leaping columns (element stride s_w)
+            uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->H)};
+            uint64_t sb[3] = {uint64_t(g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
+            uint32_t box[4] = {uint32_t(128 / eb), uint32_t(cfg.rg), uint32_t(cfg.rg_pk * g->sw), 1};
+            uint32_t es[4] = {1, 1, uint32_t(g->sw), 1};
+            if (!make_tmap4(&tb, dt, xs, d, sb, box, 128, dt == CKS_TF32, es)) return CKS_ERR_CUDA;
+        } else {
             uint64_t d[4] = {uint64_t(Cp), uint64_t(g->W), uint64_t(g->H), uint64_t(g->N)};
             uint64_t sb[3] = {uint64_t(Cp * eb), uint64_t(g->W * Cp * eb), uint64_t(g->H * g->W * Cp * eb)};
             uint32_t box[4] = {uint32_t(128 / eb), 1, 1, uint32_t(cfg.kimg)};

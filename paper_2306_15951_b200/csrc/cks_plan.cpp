@@ -814,8 +814,10 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
                  r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, (long long)r.tiles, int(r.cls.size()));
         return std::string(b) + row_classes_str(r.cls);
     }
-    snprintf(b, sizeof b, "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d tc=%d pp=%d base_tiles=%lld",
-             w.BN, w.nbs, w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, w.tc, w.pp, (long long)w.base_tiles);
+    snprintf(b, sizeof b,
+             "wgrad BN=%d nbs=%d mblocks=%d kimg=%d mt=%d gz=%d zc=%d a1=%d tc=%d pp=%d base_tiles=%lld rg=%d rg_pk=%d",
+             w.BN, w.nbs, w.mblocks, w.kimg, w.mt, w.gz, w.zc, w.a1, w.tc, w.pp, (long long)w.base_tiles, w.rg,
+             w.rg_pk);
     return b;
 }
 
@@ -863,35 +865,47 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
     int64_t uws = INT64_MAX, uwe = INT64_MIN;
     for (auto& b : tw)
         if (b.oh_e > b.oh_s) { uws = std::min(uws, b.oh_s); uwe = std::max(uwe, b.oh_e); }
+    // k-blocks of the shortest tap (segment sizing): positions (row groups: chunks of
+    // rg_pk positions) x image blocks
+    auto kbw = [&](int64_t wn) { return c.rg ? (wn + c.rg_pk - 1) / c.rg_pk : wn; };
     int64_t lmin = INT64_MAX, ntaps = 0;
-    for (auto& a : th) {
-        if (c.mt > 1) {
-            int64_t L = dmul * (a.oh_e - a.oh_s) * std::max<int64_t>(uwe - uws, 0) * c.nblk64;
-            if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
-            continue;
-        }
-        for (auto& b : tw) {
-            int64_t L = dmul * (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
-            if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
-        }
-    }
-    if (ntaps == 0) lmin = 1;
-    if (c.mt > 1 && lmin < 2048) {  // small maps: row tiles cost parallelism (C2 sweep slower); one tap per tile
-        c.mt = 1;
+    auto compute_lmin = [&] {
         lmin = INT64_MAX;
         ntaps = 0;
-        for (auto& a : th)
+        for (auto& a : th) {
+            if (c.mt > 1) {
+                int64_t L = dmul * (a.oh_e - a.oh_s) * kbw(std::max<int64_t>(uwe - uws, 0)) * c.nblk64;
+                if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
+                continue;
+            }
             for (auto& b : tw) {
-                int64_t L = dmul * (a.oh_e - a.oh_s) * (b.oh_e - b.oh_s) * c.nblk64;
+                int64_t L = dmul * (a.oh_e - a.oh_s) * kbw(b.oh_e - b.oh_s) * c.nblk64;
                 if (L > 0) { lmin = std::min(lmin, L); ++ntaps; }
             }
+        }
         if (ntaps == 0) lmin = 1;
+    };
+    compute_lmin();
+    if (c.mt > 1 && lmin < 2048) {  // small maps: row tiles cost parallelism (C2 sweep slower); one tap per tile
+        c.mt = 1;
+        compute_lmin();
     }
     if (dt == CKS_TF32 && c.mt > 1) {  // TF32 row tiles: 64-image (BN = 128: 32-image) k-blocks
         const int k = c.BN == 128 ? 32 : 64;
         lmin = lmin * c.kimg / k;
         c.kimg = k;
         c.nblk64 = int((g.N + k - 1) / k);
+    }
+    // Row groups (position chunks) for small batches: a k-block of kimg K rows holds
+    // rg_pk consecutive output positions x rg = kimg / rg_pk images (position-major), so
+    // N <= kimg / 2 images do not leave half the k-block as TMA zero fill.  2-D only
+    // (the depth axis keeps image blocks), column stride <= 8 (TMA element stride of
+    // the X box).
+    if (!ad && knobs().rg && g.sw <= 8 && 2 * g.N <= c.kimg) {
+        c.rg = g.N <= 16 ? 16 : 32;
+        c.rg_pk = c.kimg / c.rg;
+        c.nblk64 = 1;
+        compute_lmin();
     }
     c.base_tiles = (ad ? ad->F : 1) * int64_t(g.FH) * (c.mt > 1 ? 1 : g.FW) * c.mblocks * c.nbs;
     if (gz_req > 0) {
@@ -947,7 +961,7 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
         c.tcmc = knobs().wtc == 2 ? 1 : 0;
     }
     // position pairs: O_C <= 64 row tiles with unit column stride and an even union ow range
-    if (knobs().wpp && c.mt == 3 && c.a1 && c.BN == 64 && g.sw == 1 && !c.zc && !c.tcmc && uwe > uws &&
+    if (knobs().wpp && !c.rg && c.mt == 3 && c.a1 && c.BN == 64 && g.sw == 1 && !c.zc && !c.tcmc && uwe > uws &&
         (uwe - uws) % 2 == 0) {
         c.pp = 1;
         if (c.kimg == 128) {  // 64-image k-blocks: 48 / 96 KB stages (bf16 / tf32), a deeper ring

@@ -199,6 +199,8 @@ struct WgradCfg {
     int tc = 0;        // filter-row group (row tiles: the F_H filter rows of a segment walk the same k-blocks)
     int tcmc = 0;      // the group is a cluster with dY multicast
     int pp = 0;        // position pairs (M = two positions' dY; halves written as 2 G_Z partials per segment)
+    int rg = 0;        // row groups (N <= kimg / 2): images per k-block position chunk (16 / 32), 0 = off
+    int rg_pk = 1;     // row groups: output positions per k-block (kimg / rg)
     int npart() const { return pp ? 2 * gz : gz; }  // fp32 partials the segments write (>1: KB-REDUCE)
 };
 WgradCfg wgrad_cfg(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);

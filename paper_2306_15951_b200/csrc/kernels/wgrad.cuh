@@ -73,6 +73,10 @@ struct WgradParams {
     int pp;                 // position pairs (MT = 4 X columns per k-block of two positions)
     int Wx;                 // X width (position pairs: column range check)
     int ouh_s, ouh_e;       // filter-row clusters: union of the filter rows' oh ranges
+    // Row groups (small batches): a k-block is rg_pk consecutive output positions x rg images
+    // (position-major K rows; boxes over (C, N, W, H) maps); a tap multiplies only the K rows of
+    // its valid positions.  rg = 0: k-blocks of KIMG images at one position (rg_pk = 1).
+    int rg, rg_pk;
 };
 
 // One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
@@ -107,7 +111,8 @@ struct WgradShape {
 struct WTile {
     int nb, mb, z, fh, fw, fd;
     int kb0, kb1;  // k-block range of this segment
-    int wn, hn;    // ow / oh extents
+    int wn, hn;    // ow / oh extents (wn: k-block columns -- positions, pairs or position chunks)
+    int wr;        // ow positions of the tile's (union) range
     int ohs, ows, ods;
 };
 
@@ -142,7 +147,8 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
     const int hn = (p.tc > 1 ? p.ouh_e : p.oh_e[c.fh]) - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     const int dn = p.od_e[c.fd] - c.ods;
-    c.wn = p.pp ? wn / 2 : wn;  // position pairs: the k index runs over pairs (host: wn even)
+    c.wn = p.pp ? wn / 2 : (p.rg ? (wn + p.rg_pk - 1) / p.rg_pk : wn);  // pairs (host: wn even) / chunks
+    c.wr = wn;
     c.hn = hn;
     const uint32_t L = uint32_t(max(dn, 0)) * uint32_t(max(hn, 0)) * uint32_t(max(c.wn, 0)) * uint32_t(p.nblk64);
     c.kb0 = int(uint64_t(L) * uint32_t(c.z) / uint32_t(p.gz));
@@ -157,8 +163,8 @@ __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& 
         const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
         for (int q = p0; q <= p1; ++q) {
             const int pq = q / c.wn;
-            const int oh = c.ohs + (pq % c.hn), ow = c.ows + (q - pq * c.wn);
-            if (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh] && ow >= p.ow_s[fw] && ow < p.ow_e[fw]) return true;
+            const int oh = c.ohs + (pq % c.hn), ow = c.ows + p.rg_pk * (q - pq * c.wn);
+            if (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh] && ow < p.ow_e[fw] && ow + p.rg_pk > p.ow_s[fw]) return true;
         }
         return false;
     }
@@ -167,8 +173,8 @@ __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& 
     const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
     if (p1 - p0 + 1 >= c.wn) return true;  // the segment covers every ow
     for (int q = p0; q <= p1; ++q) {
-        const int w = q % c.wn;
-        if (w >= s && w < e) return true;
+        const int w = (q % c.wn) * p.rg_pk;  // first position of the k-block (row groups: of the chunk)
+        if (w < e && w + p.rg_pk > s) return true;
     }
     return false;
 }
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(256, 1)
                 const int n64 = kb % p.nblk64;
                 const int pos = kb / p.nblk64;
                 const int pq = pos / c.wn;
-                const int ow = c.ows + (PP ? 2 : 1) * (pos - pq * c.wn);  // position pairs: first position
+                const int ow = c.ows + (PP ? 2 : p.rg_pk) * (pos - pq * c.wn);  // pairs / chunks: first position
                 const int dq = pq / c.hn;
                 const int oh = c.ohs + (pq - dq * c.hn), od = c.ods + dq;
                 // filter-row clusters walk the union oh range: rows outside this filter row's own range
@@ -280,6 +286,10 @@ __global__ void __launch_bounds__(256, 1)
                                 for (int j = 0; j < a_atoms; ++j)
                                     ptx::tma_load_4d_mc(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH,
                                                         ow, od * p.OHr + oh, n64 * KIMG, tcmask);
+                        } else if (p.rg) {  // rg_pk positions x rg images, (C, N, W, H) map
+                            for (int j = 0; j < a_atoms; ++j)
+                                ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, 0, ow,
+                                                 od * p.OHr + oh);
                         } else {
                             for (int j = 0; j < a_atoms; ++j)
                                 ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, ow,
@@ -291,16 +301,22 @@ __global__ void __launch_bounds__(256, 1)
                         uint32_t nv = 0;
 #pragma unroll
                         for (int f = 0; f < MT; ++f)
-                            nv += (ohok && (MT == 1 || (ow >= p.ow_s[f] && ow < p.ow_e[f]))) ? 1u : 0u;
+                            nv += (ohok && (MT == 1 || (ow < p.ow_e[f] && ow + p.rg_pk > p.ow_s[f]))) ? 1u : 0u;
                         ptx::mbar_arrive_expect_tx(&full[stage], nv * S::B_BYTES);
 #pragma unroll
                         for (int f = 0; f < MT; ++f) {
-                            if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) continue;  // trimmed tap
+                            // trimmed tap (row groups: no valid position in the chunk)
+                            if (!ohok || (MT > 1 && !(ow < p.ow_e[f] && ow + p.rg_pk > p.ow_s[f]))) continue;
                             const int iw = ow * p.sw + (MT > 1 ? f : c.fw) - p.pw;
 #pragma unroll
-                            for (int j = 0; j < BN / S::CH; ++j)
-                                ptx::tma_load_4d(sa + S::A_STAGE + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
-                                                 c.nb * BN + j * S::CH, iw, ih, n64 * KIMG);
+                            for (int j = 0; j < BN / S::CH; ++j) {
+                                if (p.rg)  // rg_pk leaping columns (element stride s_w) x rg images
+                                    ptx::tma_load_4d(sa + S::A_STAGE + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
+                                                     c.nb * BN + j * S::CH, 0, iw, ih);
+                                else
+                                    ptx::tma_load_4d(sa + S::A_STAGE + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
+                                                     c.nb * BN + j * S::CH, iw, ih, n64 * KIMG);
+                            }
                         }
                     }
                 }
@@ -328,7 +344,7 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::tc_fence_after();
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
                 const uint64_t ad = dconst | ptx::desc_addr(a_addr);
-                const int ow = c.ows + (PP ? 2 : 1) * ((kb / p.nblk64) % max(c.wn, 1));
+                const int ow = c.ows + (PP ? 2 : p.rg_pk) * ((kb / p.nblk64) % max(c.wn, 1));
                 bool ohok = true;
                 if (p.tc > 1) {
                     const int oh = c.ohs + ((kb / p.nblk64) / max(c.wn, 1)) % max(c.hn, 1);
@@ -337,8 +353,17 @@ __global__ void __launch_bounds__(256, 1)
                 if (ptx::elect_one()) {
 #pragma unroll
                     for (int f = 0; f < MT; ++f) {
+                        int kk0 = 0, kk1 = KIMG / S::UK;  // K steps of this tap in the k-block
                         if (PP) {  // X column f: one MMA for tap f of ow (rows 0-63) and tap f-1 of ow+1 (64-127)
                             if (!ohok || ow - p.pw + f < 0 || ow - p.pw + f >= p.Wx) continue;
+                        } else if (p.rg) {
+                            // row groups: only the K rows (q * rg + image) of the tap's valid positions q of
+                            // the chunk are multiplied -- exact trimming at the range ends
+                            const int lo = MT > 1 ? p.ow_s[f] : c.ows, hi = MT > 1 ? p.ow_e[f] : c.ows + c.wr;
+                            const int q0 = max(lo - ow, 0), q1 = min(hi - ow, p.rg_pk);
+                            if (!ohok || q1 <= q0) continue;
+                            kk0 = q0 * p.rg / S::UK;
+                            kk1 = q1 * p.rg / S::UK;
                         } else if (!ohok || (MT > 1 && !(ow >= p.ow_s[f] && ow < p.ow_e[f]))) {
                             continue;  // trimmed tap
                         }
@@ -346,8 +371,10 @@ __global__ void __launch_bounds__(256, 1)
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
 #pragma unroll
                         for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
-                            ptx::mma_ss<kTF32>(d + uint32_t(f * BN), ad + uint64_t(kk * (S::KSTEP >> 4)),
-                                               bd + uint64_t(kk * (S::KSTEP >> 4)), idesc, (acc0 | uint32_t(kk)) != 0);
+                            if (kk >= kk0 && kk < kk1)
+                                ptx::mma_ss<kTF32>(d + uint32_t(f * BN), ad + uint64_t(kk * (S::KSTEP >> 4)),
+                                                   bd + uint64_t(kk * (S::KSTEP >> 4)), idesc,
+                                                   (acc0 | uint32_t(kk - kk0)) != 0);
                         started |= 1u << f;
                     }
                     if (p.tcmc)

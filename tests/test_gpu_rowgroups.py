@@ -141,3 +141,17 @@ def test_row_groups_leave_other_rows_untouched(torch_cuda, N):
     assert not torch.isnan(y).any()
     assert torch.isnan(buf[n:]).all()
     check(y.cpu().numpy(), O.conv_ref(a["X"], a["W"], 1, 1, 1, 1), "bf16", "rg guard", red_len(lay, "fwd"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("gz", [0, 1, 5])
+@pytest.mark.parametrize("lay", [Layer("rgw0", 16, 64, 57, 45, 64, 3, 3, 1, 1, 1, 1),    # row tiles, odd widths
+                                 Layer("rgw1", 32, 64, 41, 39, 64, 3, 3, 1, 2, 1, 1),    # s_w = 2 leaping chunks
+                                 Layer("rgw2", 7, 128, 20, 23, 96, 3, 3, 2, 2, 1, 1),    # BN = 128, s = 2
+                                 Layer("rgw3", 24, 96, 13, 17, 136, 5, 4, 1, 3, 2, 1),   # wide taps, s_w = 3
+                                 Layer("rgw4", 3, 256, 9, 9, 256, 3, 3, 1, 1, 1, 1)],    # BN = 256, tiny batch
+                         ids=lambda l: l.name)
+def test_row_group_wgrad(torch_cuda, lay, gz, dtype):
+    """Sk-dilated with position chunks: every tap multiplies only the K rows of its valid positions
+    (chunks cut by the T3 ranges at both ends), G_Z segments split the chunk sequence."""
+    check_full(torch_cuda, lay, dtype, config=15, idx=int(lay.name[3:]), ops=("wgrad",), gz=gz)

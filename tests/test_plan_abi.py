@@ -323,3 +323,17 @@ def test_row_group_plans():
                     assert d["kind"] == "igemm" and int(d["rg"]) == want, (geo, dt, op, d)
                     if want:  # one activation column per A slot, no CTA pairs
                         assert d["apos"] == "1" and d["pair"] == "0", d
+
+
+def test_row_group_wgrad_plans():
+    """Sk-dilated at N <= kimg / 2: k-blocks of rg_pk output positions x rg images (position chunks)."""
+    for N, rg in [(1, 16), (16, 16), (17, 32), (32, 32), (33, 0), (64, 0), (256, 0)]:
+        for geo in [(N, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1), (N, 128, 28, 28, 256, 3, 3, 2, 2, 1, 1),
+                    (N, 256, 14, 14, 256, 3, 3, 1, 1, 1, 1)]:
+            for dt in (L.CKS_BF16, L.CKS_TF32):
+                d = L.plan_dict(L.make_geom(*geo), dt, L.CKS_OP_WGRAD)
+                assert d["kind"] == "wgrad", d
+                want = rg if 2 * N <= int(d["kimg"]) else 0
+                assert int(d["rg"]) == want, (geo, dt, d)
+                if want:
+                    assert int(d["rg_pk"]) * want == int(d["kimg"]) and d["pp"] == "0", d
