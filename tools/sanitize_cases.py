@@ -33,6 +33,10 @@ CASES = [
     ("pospairs", 130, 64, 28, 28, 64, 3, 1, 1),      # Sk-dilated position pairs + filter-row groups
     ("wide", 256, 64, 28, 28, 64, 3, 1, 1),          # wide pixel blocks (two A slots per row step)
     ("pair256", 260, 256, 14, 14, 256, 3, 1, 1),     # CTA pairs (both dtypes)
+    ("rg32", 32, 64, 23, 19, 64, 3, 1, 1),           # row groups: 4 rows x 32 images, position chunks
+    ("rg_s2", 20, 64, 17, 15, 128, 3, 2, 1),         # row groups, element-strided A box, KS phases
+    ("rg64", 50, 128, 9, 11, 96, 3, 1, 1),           # row groups of 2 rows x 64 images
+    ("rg_zc", 16, 512, 4, 4, 256, 3, 2, 1),          # row groups + cluster split-K, 16-image chunks
 ]
 
 for dtype in ("bf16", "tf32"):

@@ -16,7 +16,7 @@ from cks_synth import get_config  # noqa: E402
 cfg, name, op = int(sys.argv[1]), sys.argv[2], sys.argv[3]
 desc, layers = get_config(cfg)
 idx = [l.name for l in layers].index(name)
-b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0))
+b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0), os.environ.get("CKS_DTYPE", "bf16"))
 b.dW = torch.empty((b.lay.OC, b.lay.FH, b.lay.FW, b.lay.C), dtype=torch.float32, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 b.run(op, s)
