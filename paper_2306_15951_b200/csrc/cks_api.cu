@@ -636,7 +636,8 @@ cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, cons
                          float* wout, long long part_stride, cudaStream_t st) {
     const bool tf = dt == CKS_TF32;
     CUtensorMap tx;
-    if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 64, uint32_t(g.FH), tf)) return CKS_ERR_CUDA;
+    const int xrows = int(g.FH) + g.sh * (rc.q - 1);  // one X box serves q output rows
+    if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 64, uint32_t(xrows), tf)) return CKS_ERR_CUDA;
     RowWgradParams q;
     memset(&q, 0, sizeof(q));
     q.out = wout;
@@ -652,7 +653,9 @@ cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, cons
     q.nblk64 = rc.nblk;
     q.num_tiles = int(rc.tiles);
     q.stages = rc.stages;
-    q.a_bytes = rc.mb * 128 * 64 * int(elem_bytes(dt));
+    q.q = rc.q;
+    q.xrows = xrows;
+    q.a_bytes = ((rc.q - 1) * g.sh + rc.mb * (128 / rc.JB)) * 64 * rc.ROWB;
     if (tf) return rc.ROWB == 128 ? launch_wgrad_row_rb<128, true>(rc.BN, tx, tdy, q, rc.smem, st) : CKS_ERR_UNSUPPORTED;
     switch (rc.ROWB) {
         case 32: return launch_wgrad_row_rb<32, false>(rc.BN, tx, tdy, q, rc.smem, st);

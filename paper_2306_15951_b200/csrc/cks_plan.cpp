@@ -169,7 +169,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1, wrow_q = 0;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -200,6 +200,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_A1_TF32")) wa1_tf32 = atoi(e) != 0;  // TF32: 64 OC of dY per stage
         if (const char* e = cks_knob("CKS_WGRAD_TC")) wtc = atoi(e);  // filter-row groups (2: multicast clusters)
         if (const char* e = cks_knob("CKS_RG")) rg = atoi(e) != 0;  // 0: batch-as-M tiles at any N
+        if (const char* e = cks_knob("CKS_WROW_Q")) wrow_q = atoi(e);  // narrow Sk-dilated: output rows per k-block
     }
 };
 static const Knobs& knobs() {
@@ -755,16 +756,41 @@ static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, in
     c.nbs = int((pad_ch(g.OC, dt) + c.BN - 1) / c.BN);
     c.nblk = int((g.N + 63) / 64);
     const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    // Output rows per k-block q: one X box of FH + sh*(q-1) rows serves q output rows.  Measured
+    // (tools/time_op.py, CKS_WROW_Q): ResNet stem TF32 407 -> 329 us (q = 2), BF16 252 -> 206 (2)
+    // -> 190 us (3); DCGAN G32to64 BF16 45 -> 38 us; small maps lose parallelism (C2 vgg32 s2:
+    // 12 -> 15 us).  Policy: q = 2 where it saves >= 20 % of the X rows per output row and
+    // leaves >= 4 k-blocks per SM; q = 3 only with >= 16 k-blocks per SM; always a >= 2-deep ring.
+    {
+        const int64_t atom = int64_t(64) * c.ROWB;
+        const int64_t ow_cols = out_extent(g.W, g.FW, g.sw, g.pw);
+        const int qmax = knobs().wrow_q > 0 ? knobs().wrow_q : 3;
+        for (int q = qmax; q >= 1; --q) {
+            if (q == 1) {
+                c.q = 1;
+                break;
+            }
+            const int64_t stage = ((q - 1) * g.sh + int64_t(c.mb) * R) * atom + int64_t(q) * c.BN * 64 * eb;
+            const int64_t kblocks = ((OH + q - 1) / q) * ow_cols * c.nblk;
+            const bool forced = knobs().wrow_q > 0;
+            const bool saves = 5 * (g.FH + g.sh * (q - 1)) <= 4 * q * g.FH;  // <= 80 % of the rows
+            const bool enough = kblocks >= int64_t(q == 2 ? 4 : 16) * num_sms;
+            if ((227 * 1024 - 2048) / stage >= 2 && (q - 1) * g.sh + g.FH <= 256 && (forced || (saves && enough))) {
+                c.q = q;
+                break;
+            }
+        }
+    }
     std::vector<int64_t> segcap;
     for (auto& k : c.cls) {
-        k.work = OH * k.ncols * c.nblk;
+        k.work = ((OH + c.q - 1) / c.q) * k.ncols * c.nblk;
         segcap.push_back(gz_req > 0 ? k.work : std::max<int64_t>(1, k.work / 8));  // >= 8 k-blocks per segment
     }
     const int64_t want = gz_req > 0 ? gz_req : std::max<int64_t>(1, num_sms / c.nbs);
     row_spread(c.cls, std::max<int64_t>(want, int64_t(c.cls.size())), segcap);
     c.gz = 0;
     for (auto& k : c.cls) c.gz += k.cnt;
-    const int stage = int(c.mb * 128 * 64 * eb + c.BN * 64 * eb);
+    const int stage = int(((c.q - 1) * g.sh + c.mb * R) * 64 * c.ROWB + c.q * c.BN * 64 * eb);
     c.stages = std::min(8, (227 * 1024 - 2048) / stage);
     if (c.stages < 2) return c;
     c.smem = 1024 + c.stages * stage + 256;
@@ -810,8 +836,8 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
     const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);
     if (w.row) {
         const RowCfg r = row_cfg_wgrad(g, dt, gz, num_sms);
-        snprintf(b, sizeof b, "row_wgrad ROWB=%d JB=%d BN=%d mb=%d nbs=%d gz=%d stages=%d tiles=%lld classes=%d cls=",
-                 r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, (long long)r.tiles, int(r.cls.size()));
+        snprintf(b, sizeof b, "row_wgrad ROWB=%d JB=%d BN=%d mb=%d nbs=%d gz=%d stages=%d q=%d tiles=%lld classes=%d cls=",
+                 r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, r.q, (long long)r.tiles, int(r.cls.size()));
         return std::string(b) + row_classes_str(r.cls);
     }
     snprintf(b, sizeof b,

@@ -175,6 +175,7 @@ struct RowCfg {
     int stages = 0;      // pipeline depth
     int smem = 0;        // dynamic shared memory bytes
     int mb = 1, nbs = 1, gz = 1, nblk = 1;  // wgrad: M-blocks, OC blocks, G_Z (total partials), 64-image blocks
+    int q = 1;           // wgrad: output rows per k-block (one X box of FH + sh * (q - 1) rows)
     std::vector<RowClassH> cls;
     int grid = 1;        // CTAs
     int64_t tiles = 0;

@@ -320,7 +320,11 @@ struct RowWgradParams {
     int nblk64;   // ceil(N / 64)
     int num_tiles;  // nbs * gz
     int stages;
-    int a_bytes;  // mb * 128 * 64 * eb
+    int a_bytes;  // A region: ((q - 1) * sh + mb * R) filter-row atoms of 64 images
+    // q output rows per k-block (round 2): ONE X box of xrows = FH + sh * (q - 1) rows serves the
+    // q rows' M-blocks (row oh0 + i starts at atom i * sh), so the X rows shared by neighbouring
+    // output rows cross L2 -> SM once per k-block instead of once per output row
+    int q, xrows;
 };
 
 // Tile t -> OC block nb, segment (partial) part of class k, its k-block range
@@ -333,7 +337,7 @@ struct RowWTile {
         part = t / p.nbs;
         k = row_class_of(p.cls, p.ncls, part);
         const int z = part - p.cls[k].base, gzc = p.cls[k].cnt;
-        const uint32_t L = uint32_t(p.OH) * uint32_t(p.cls[k].ncols) * uint32_t(p.nblk64);
+        const uint32_t L = uint32_t((p.OH + p.q - 1) / p.q) * uint32_t(p.cls[k].ncols) * uint32_t(p.nblk64);
         kb0 = uint32_t(uint64_t(L) * uint32_t(z) / uint32_t(gzc));
         kb1 = uint32_t(uint64_t(L) * uint32_t(z + 1) / uint32_t(gzc));
     }
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(256, 1)
     static_assert(!TF || ROWB == 128, "TF32 MN-major operands use the 128-byte (BASE32B) swizzle");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int stage_bytes = p.a_bytes + B_BYTES;
+    const int stage_bytes = p.a_bytes + p.q * B_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * stage_bytes);
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
@@ -404,7 +408,8 @@ __global__ void __launch_bounds__(256, 1)
             for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = int(kb % uint32_t(p.nblk64));
                 const int pos = int(kb / uint32_t(p.nblk64));
-                const int oh = pos / cl.ncols, ow = cl.col0 + cl.cstep * (pos % cl.ncols);
+                const int oh0 = (pos / cl.ncols) * p.q, ow = cl.col0 + cl.cstep * (pos % cl.ncols);
+                const int nq = min(p.q, p.OH - oh0);
                 ptx::mbar_wait(&empty[stage], phase ^ 1u);
                 uint8_t* st = smem + stage * stage_bytes;
                 if (ptx::elect_one()) {
@@ -412,15 +417,16 @@ __global__ void __launch_bounds__(256, 1)
                     // stride sw*C, FH rows at stride sh) and are re-read: keep them in L2 ahead of
                     // dY, which is read once (L2 eviction priorities)
                     if (!is_b) {
-                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(p.FH * 64 * ROWB));
+                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(p.xrows * 64 * ROWB));
                         ptx::tma_load_4d_hint(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
-                                              oh * p.sh - p.ph, 0, pol);
+                                              oh0 * p.sh - p.ph, 0, pol);
                     } else {
-                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(B_BYTES));
+                        ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(nq * B_BYTES));
+                        for (int i = 0; i < nq; ++i)
 #pragma unroll
-                        for (int j = 0; j < BN / CH; ++j)
-                            ptx::tma_load_4d_hint(st + p.a_bytes + j * 8192, &tmDY, &full[stage], c.nb * BN + j * CH,
-                                                  ow, oh, n64 * 64, pol);
+                            for (int j = 0; j < BN / CH; ++j)
+                                ptx::tma_load_4d_hint(st + p.a_bytes + i * B_BYTES + j * 8192, &tmDY, &full[stage],
+                                                      c.nb * BN + j * CH, ow, oh0 + i, n64 * 64, pol);
                     }
                 }
                 __syncwarp();
@@ -441,34 +447,43 @@ __global__ void __launch_bounds__(256, 1)
             ptx::tc_fence_after();
             uint32_t started = 0;
             for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
-                const int oh = int(kb / uint32_t(p.nblk64)) / cl.ncols;
-                const uint32_t mm = row_wgrad_mmask(oh, R, p);
+                const int oh0 = (int(kb / uint32_t(p.nblk64)) / cl.ncols) * p.q;
+                const int nq = min(p.q, p.OH - oh0);
+                uint32_t mmq = 0;  // M-blocks issued in this k-block (any of its output rows)
+                for (int i = 0; i < nq; ++i) mmq |= row_wgrad_mmask(oh0 + i, R, p);
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::tc_fence_after();
                 const uint32_t sa = ptx::smem_u32(smem + stage * stage_bytes);
                 const uint32_t sb = sa + uint32_t(p.a_bytes);
                 if (ptx::elect_one()) {
-                    for (int m = 0; m < p.mb; ++m) {
-                        if (!((mm >> m) & 1u)) continue;  // all filter rows of the block outside X
-                        const uint32_t acc0 = (started >> m) & 1u;
+                    uint32_t st_loc = started;
+                    for (int i = 0; i < nq; ++i) {
+                        const uint32_t mm = row_wgrad_mmask(oh0 + i, R, p);
+                        for (int m = 0; m < p.mb; ++m) {
+                            if (!((mm >> m) & 1u)) continue;  // all filter rows of the block outside X
+                            const uint32_t acc0 = (st_loc >> m) & 1u;
+                            // output row oh0 + i: filter row fh = X box row i*sh + fh
+                            const uint32_t arow = uint32_t((i * p.sh + m * R) * 64 * ROWB);
 #pragma unroll
-                        for (int kk = 0; kk < 64 / UK; ++kk) {
-                            uint64_t ad, bd;
-                            if constexpr (TF) {
-                                ad = ptx::smem_desc_mn_b32(sa + uint32_t(m * R * 64 * ROWB + kk * UK * ROWB), 64 * ROWB, 512);
-                                bd = ptx::smem_desc_mn_b32(sb + uint32_t(kk * UK * 128), 8192, 512);
-                            } else {
-                                ad = ptx::smem_desc_mn(sa + uint32_t(m * R * 64 * ROWB + kk * UK * ROWB), 64 * ROWB,
-                                                       8 * ROWB, ROWB);
-                                bd = ptx::smem_desc_sw128(sb + uint32_t(kk * UK * 128), 8192, 1024);
+                            for (int kk = 0; kk < 64 / UK; ++kk) {
+                                uint64_t ad, bd;
+                                if constexpr (TF) {
+                                    ad = ptx::smem_desc_mn_b32(sa + arow + uint32_t(kk * UK * ROWB), 64 * ROWB, 512);
+                                    bd = ptx::smem_desc_mn_b32(sb + uint32_t(i * B_BYTES + kk * UK * 128), 8192, 512);
+                                } else {
+                                    ad = ptx::smem_desc_mn(sa + arow + uint32_t(kk * UK * ROWB), 64 * ROWB, 8 * ROWB,
+                                                           ROWB);
+                                    bd = ptx::smem_desc_sw128(sb + uint32_t(i * B_BYTES + kk * UK * 128), 8192, 1024);
+                                }
+                                ptx::mma_ss<TF>(tmem_base + uint32_t(m * BN), ad, bd, idesc, (acc0 | uint32_t(kk)) != 0);
                             }
-                            ptx::mma_ss<TF>(tmem_base + uint32_t(m * BN), ad, bd, idesc, (acc0 | uint32_t(kk)) != 0);
                         }
+                        st_loc |= mm;
                     }
                     ptx::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
-                started |= mm;
+                started |= mmq;
                 if (++stage == uint32_t(p.stages)) {
                     stage = 0;
                     phase ^= 1u;
@@ -491,7 +506,8 @@ __global__ void __launch_bounds__(256, 1)
             uint32_t started = 0;  // M-blocks that received an MMA (the same walk as the issuer)
             for (uint32_t kb = c.kb0; kb < c.kb1;) {
                 const int pos = int(kb / uint32_t(p.nblk64));
-                started |= row_wgrad_mmask(pos / cl.ncols, R, p);
+                const int oh0 = (pos / cl.ncols) * p.q;
+                for (int i = 0; i < p.q && oh0 + i < p.OH; ++i) started |= row_wgrad_mmask(oh0 + i, R, p);
                 kb = uint32_t(pos + 1) * uint32_t(p.nblk64);  // next position
             }
             ptx::mbar_wait(tfull, tph);

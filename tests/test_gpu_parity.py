@@ -505,3 +505,17 @@ def test_pair_tiles(torch_cuda, lay, dtype):
     image-block counts leave the last pair's second CTA out of range.  Forward
     and KS-deconv (whose output channels are I_C) against the oracle."""
     check_full(torch_cuda, lay, dtype, config=16, idx=int(lay.name[2:]), ops=("fwd", "deconv"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("lay", [Layer("wq0", 128, 3, 125, 128, 64, 7, 7, 2, 2, 3, 3),   # stem-like, odd O_H
+                                 Layer("wq1", 128, 3, 33, 40, 64, 3, 3, 1, 1, 1, 1)],    # 3x3 s1, odd O_H
+                         ids=lambda l: l.name)
+def test_narrow_wgrad_multi_row_kblocks(torch_cuda, lay, dtype):
+    """KB-WGRAD-ROW with q > 1 output rows per k-block (one X box of F_H + s_h(q-1) rows shared by
+    the q rows' M-blocks; the last k-block of an odd O_H carries fewer rows)."""
+    from paper_2306_15951_b200 import _lib as L
+    g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+    d = L.plan_dict(g, L.CKS_BF16 if dtype == "bf16" else L.CKS_TF32, L.CKS_OP_WGRAD)
+    assert d["kind"] == "row_wgrad" and int(d["q"]) >= 2, d
+    check_full(torch_cuda, lay, dtype, config=16, idx=int(lay.name[2:]), ops=("wgrad",))
