@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(256, 1)
         // K chunks [kc0, kc1) only
         constexpr uint32_t idesc = ptx::instr_desc(128, BN, TF, false, false);
         const uint32_t a0 = ptx::smem_u32(abuf), w0 = ptx::smem_u32(wsm);
+        const int nkc = cl.kc1 - cl.kc0;
+        const uint64_t adesc0 = ptx::smem_desc_kmajor(a0 + 32u * uint32_t(cl.kc0), ROWB);
+        const uint64_t bdesc0 = ptx::smem_desc_kmajor(w0 + 32u * uint32_t(cl.kc0), ROWB);
         uint32_t s = 0, ph = 0, i = 0;
         for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
             const RowFwdTile tl(t, cl, p);
@@ -230,14 +233,19 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::mbar_wait(&full[s], ph);
                 ptx::tc_fence_after();
                 if (ptx::elect_one()) {
-                    const uint32_t sa = a0 + s * uint32_t(S::STAGE);
+                    // descriptors built once per stage / filter row and advanced by adds (the single
+                    // issuing thread's scalar work per MMA bounds this kernel: ncu, TF32 stem)
+                    const uint64_t ad = adesc0 + uint64_t((s * uint32_t(S::STAGE)) >> 4);
                     for (int r = r0; r < r1; ++r) {
                         const int fh = ih - ih0 - r * p.sh;
-                        const uint32_t sb = w0 + uint32_t(fh * BN * ROWB);
-                        for (int kc = cl.kc0; kc < cl.kc1; ++kc)
-                            ptx::mma_ss<TF>(dbase + uint32_t(r * BN), ptx::smem_desc_kmajor(sa + 32u * kc, ROWB),
-                                            ptx::smem_desc_kmajor(sb + 32u * kc, ROWB), idesc,
-                                            (((started >> r) & 1u) || kc > cl.kc0) ? 1u : 0u);
+                        const uint64_t bd = bdesc0 + uint64_t(uint32_t(fh * BN * ROWB) >> 4);
+                        const uint32_t d = dbase + uint32_t(r * BN);
+                        const uint32_t acc0 = (started >> r) & 1u;
+#pragma unroll
+                        for (int k = 0; k < ROWB / 32; ++k)  // 32-byte K chunks [kc0, kc1) of the class
+                            if (k < nkc)
+                                ptx::mma_ss<TF>(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                                (acc0 | uint32_t(k)) != 0);
                         started |= 1u << r;  // (elected lane's copy; all lanes update below)
                     }
                     ptx::mma_commit(&empty[s]);
@@ -439,6 +447,9 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer
         constexpr uint32_t idesc = ptx::instr_desc(128, BN, TF, true, true);
+        const uint32_t s0 = ptx::smem_u32(smem);
+        const uint64_t adesc0 = TF ? ptx::smem_desc_mn_b32(s0, 64 * ROWB, 512) : ptx::smem_desc_mn(s0, 64 * ROWB, 8 * ROWB, ROWB);
+        const uint64_t bdesc0 = TF ? ptx::smem_desc_mn_b32(s0, 8192, 512) : ptx::smem_desc_sw128(s0, 8192, 1024);
         uint32_t stage = 0, phase = 0, tph = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
             const RowWTile c(t, p);
@@ -463,20 +474,13 @@ __global__ void __launch_bounds__(256, 1)
                             if (!((mm >> m) & 1u)) continue;  // all filter rows of the block outside X
                             const uint32_t acc0 = (st_loc >> m) & 1u;
                             // output row oh0 + i: filter row fh = X box row i*sh + fh
-                            const uint32_t arow = uint32_t((i * p.sh + m * R) * 64 * ROWB);
+                            // descriptors advanced by adds (start-address field, 16-byte units)
+                            const uint64_t ad = adesc0 + uint64_t((sa - s0 + uint32_t((i * p.sh + m * R) * 64 * ROWB)) >> 4);
+                            const uint64_t bd = bdesc0 + uint64_t((sb - s0 + uint32_t(i * B_BYTES)) >> 4);
 #pragma unroll
-                            for (int kk = 0; kk < 64 / UK; ++kk) {
-                                uint64_t ad, bd;
-                                if constexpr (TF) {
-                                    ad = ptx::smem_desc_mn_b32(sa + arow + uint32_t(kk * UK * ROWB), 64 * ROWB, 512);
-                                    bd = ptx::smem_desc_mn_b32(sb + uint32_t(i * B_BYTES + kk * UK * 128), 8192, 512);
-                                } else {
-                                    ad = ptx::smem_desc_mn(sa + arow + uint32_t(kk * UK * ROWB), 64 * ROWB, 8 * ROWB,
-                                                           ROWB);
-                                    bd = ptx::smem_desc_sw128(sb + uint32_t(i * B_BYTES + kk * UK * 128), 8192, 1024);
-                                }
-                                ptx::mma_ss<TF>(tmem_base + uint32_t(m * BN), ad, bd, idesc, (acc0 | uint32_t(kk)) != 0);
-                            }
+                            for (int kk = 0; kk < 64 / UK; ++kk)
+                                ptx::mma_ss<TF>(tmem_base + uint32_t(m * BN), ad + uint64_t((kk * UK * ROWB) >> 4),
+                                                bd + uint64_t((kk * UK * 128) >> 4), idesc, (acc0 | uint32_t(kk)) != 0);
                         }
                         st_loc |= mm;
                     }
