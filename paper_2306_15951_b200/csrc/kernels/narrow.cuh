@@ -102,13 +102,17 @@ struct RowFwdTile {
     }
 };
 
-// accumulators r of a tile that X row ih feeds: fh = ih - ((oh0 + r)*sh - ph) in [0, FH)
-__device__ __forceinline__ void row_users(int ih, int oh0, int rn, const RowFwdParams& p, int& r0, int& r1) {
-    const int d = ih - oh0 * p.sh + p.ph;  // = fh + r*sh
-    r1 = min(rn, d / p.sh + 1);            // r <= d / sh
-    const int lo = d - p.FH + 1;           // r*sh >= d - FH + 1
-    r0 = lo <= 0 ? 0 : (lo + p.sh - 1) / p.sh;
+// Shared-memory row slot of filter row fh in KB-CONV-ROW's B operand: filter rows are grouped by
+// fh mod sh, each group in DECREASING fh, so the filter rows fh, fh - sh, fh - 2 sh, ... that one X
+// row meets in consecutive accumulators r, r + 1, ... are consecutive BN-row blocks -- one
+// N-merged MMA (N = cnt * BN) serves them all.
+__host__ __device__ __forceinline__ int row_fwd_slot(int fh, int FH, int sh) {
+    const int c = fh % sh;
+    const int base = c * (FH / sh) + min(c, FH % sh);  // filter rows with a smaller residue
+    const int nc = (FH - c + sh - 1) / sh;              // filter rows with residue c
+    return base + (nc - 1 - fh / sh);
 }
+
 
 template <int ROWB, int BN, bool TF>
 __global__ void __launch_bounds__(256, 1)
@@ -126,6 +130,10 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tfull = empty + 16;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // per-CTA tables (no runtime divisions by s_h in the issue loops): filter-row smem slots, and
+    // for d = ih - (oh0*sh - ph) the accumulator range [r0, r1) that X row ih feeds ((r0 << 4) | r1)
+    uint8_t* stab = reinterpret_cast<uint8_t*>(tmem_slot + 1);  // [32]
+    uint8_t* rut = stab + 32;                                    // [128]
     constexpr uint32_t TMEM_COLS = 2 * S::RMAX * BN <= 64 ? 64 : (2 * S::RMAX * BN <= 128 ? 128 : (2 * S::RMAX * BN <= 256 ? 256 : 512));
 
     ptx::pdl_launch_dependents();
@@ -149,6 +157,16 @@ __global__ void __launch_bounds__(256, 1)
     }
     __syncwarp();  // reconverge the initialising lane's warp before the block barrier
     if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+    for (int i = threadIdx.x; i < 32 + 128; i += blockDim.x) {
+        if (i < 32) {
+            stab[i] = uint8_t(i < p.FH ? row_fwd_slot(i, p.FH, p.sh) : 0);
+        } else {
+            const int d = i - 32;
+            const int r1 = min(15, d / p.sh + 1), lo = d - p.FH + 1;
+            const int r0 = lo <= 0 ? 0 : min(15, (lo + p.sh - 1) / p.sh);
+            rut[d] = uint8_t((r0 << 4) | r1);
+        }
+    }
     ptx::pdl_wait();  // W and X may come from the previous kernel
     {   // all threads: this class's filter rows in the K-major swizzled B layout,
         // row r = fh*BN + oc, K = box element e <-> run element off + e (zero outside [0, FW*C))
@@ -158,6 +176,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int q = threadIdx.x; q < chunks; q += blockDim.x) {
             const int r = q / (ROWB / 16), c16 = q % (ROWB / 16);
             const int fh = r / BN, oc = r % BN;
+            const int rs = row_fwd_slot(fh, p.FH, p.sh) * BN + oc;  // smem row of (fh, oc)
             uint32_t v[4] = {0u, 0u, 0u, 0u};
             if (oc < p.OC) {
 #pragma unroll
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
             }
-            const uint32_t off = ptx::swz(uint32_t(r * ROWB + c16 * 16), ROWB);
+            const uint32_t off = ptx::swz(uint32_t(rs * ROWB + c16 * 16), ROWB);
             *reinterpret_cast<uint4*>(wsm + off) = make_uint4(v[0], v[1], v[2], v[3]);
         }
         ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05
@@ -193,8 +212,8 @@ __global__ void __launch_bounds__(256, 1)
             const int rl = max(ih0, 0), rh = min(p.H, ih0 + p.sh * (tl.rn - 1) + p.FH);
             const int origin = (tl.ow * p.sw - p.pw) * p.C + cl.off;
             for (int ih = rl; ih < rh; ++ih) {
-                int r0, r1;
-                row_users(ih, tl.oh0, tl.rn, p, r0, r1);
+                const int ru = rut[ih - ih0];
+                const int r0 = ru >> 4, r1 = min(tl.rn, ru & 15);
                 if (r0 >= r1) continue;  // stride gap: no output uses this row
                 ptx::mbar_wait(&empty[s], ph ^ 1u);
                 if (ptx::elect_one()) {
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer: each loaded row into every accumulator that uses it,
         // K chunks [kc0, kc1) only
-        constexpr uint32_t idesc = ptx::instr_desc(128, BN, TF, false, false);
+        constexpr uint32_t idesc0 = ptx::instr_desc(128, 0, TF, false, false);  // N set per MMA group
         const uint32_t a0 = ptx::smem_u32(abuf), w0 = ptx::smem_u32(wsm);
         const int nkc = cl.kc1 - cl.kc0;
         const uint64_t adesc0 = ptx::smem_desc_kmajor(a0 + 32u * uint32_t(cl.kc0), ROWB);
@@ -227,8 +246,8 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t dbase = tmem_base + acc * uint32_t(S::RMAX * BN);
             uint32_t started = 0;
             for (int ih = rl; ih < rh; ++ih) {
-                int r0, r1;
-                row_users(ih, tl.oh0, tl.rn, p, r0, r1);
+                const int ru = rut[ih - ih0];
+                const int r0 = ru >> 4, r1 = min(tl.rn, ru & 15);
                 if (r0 >= r1) continue;
                 ptx::mbar_wait(&full[s], ph);
                 ptx::tc_fence_after();
@@ -236,17 +255,24 @@ __global__ void __launch_bounds__(256, 1)
                     // descriptors built once per stage / filter row and advanced by adds (the single
                     // issuing thread's scalar work per MMA bounds this kernel: ncu, TF32 stem)
                     const uint64_t ad = adesc0 + uint64_t((s * uint32_t(S::STAGE)) >> 4);
-                    for (int r = r0; r < r1; ++r) {
-                        const int fh = ih - ih0 - r * p.sh;
-                        const uint64_t bd = bdesc0 + uint64_t(uint32_t(fh * BN * ROWB) >> 4);
-                        const uint32_t d = dbase + uint32_t(r * BN);
-                        const uint32_t acc0 = (started >> r) & 1u;
+                    // accumulators [r0, r1) meet filter rows fh0, fh0 - sh, ...: consecutive B blocks
+                    // (row_fwd_slot).  The started ones form a prefix (outputs start in row order):
+                    // at most two N-merged MMA groups per K chunk, accumulate / overwrite.
+                    const int slot0 = stab[ih - ih0 - r0 * p.sh];
+                    int rsd = r0;
+                    while (rsd < r1 && ((started >> rsd) & 1u)) ++rsd;
+#pragma unroll
+                    for (int grp = 0; grp < 2; ++grp) {
+                        const int ga = grp == 0 ? r0 : rsd, gb = grp == 0 ? rsd : r1;
+                        if (gb <= ga) continue;
+                        const uint64_t bd = bdesc0 + uint64_t(uint32_t((slot0 + ga - r0) * BN * ROWB) >> 4);
+                        const uint32_t d = dbase + uint32_t(ga * BN);
+                        const uint32_t idesc = idesc0 | ((uint32_t((gb - ga) * BN) >> 3) << 17);
 #pragma unroll
                         for (int k = 0; k < ROWB / 32; ++k)  // 32-byte K chunks [kc0, kc1) of the class
                             if (k < nkc)
                                 ptx::mma_ss<TF>(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
-                                                (acc0 | uint32_t(k)) != 0);
-                        started |= 1u << r;  // (elected lane's copy; all lanes update below)
+                                                (grp == 0 || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(&empty[s]);
                 }
