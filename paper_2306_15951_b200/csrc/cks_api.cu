@@ -484,10 +484,10 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     return launch_igemm(cfg.BN, cfg.KB, dt == CKS_TF32, ta, tb, ty, p, smem, st, bmn != nullptr);
 }
 
-template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false, bool PP = false>
-cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
+template <int BN, bool TF, int KIMG, int MT, bool A1, bool PP, bool RG>
+cks_status launch_wgrad_k(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
     using S = WgradShape<BN, TF, KIMG, MT, A1, PP>;
-    auto kern = wgrad_kernel<BN, TF, KIMG, MT, A1, PP>;
+    auto kern = wgrad_kernel<BN, TF, KIMG, MT, A1, PP, RG>;
     if (set_smem(kern, S::SMEM_BYTES) != CKS_OK) return CKS_ERR_CUDA;
     if (p.zc) {  // one tile per CTA, the gz segments of a tile are one cluster
         if (p.gz > 8) return CKS_ERR_UNSUPPORTED;
@@ -501,6 +501,19 @@ cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const Wgra
     long long grid = std::min<long long>(p.num_tiles, device_sms());
     if (grid < 1) grid = 1;
     return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), S::SMEM_BYTES, st, a, b, p);
+}
+
+// row-group (position-chunk) k-blocks are a separate instantiation: the batch-as-K kernels keep
+// their exact issue sequence (a runtime flag in the MMA loop cost up to 14 %: C6 5x5 64->64)
+template <int BN, bool TF, int KIMG, int MT = 1, bool A1 = false, bool PP = false>
+cks_status launch_wgrad_t(const CUtensorMap& a, const CUtensorMap& b, const WgradParams& p, cudaStream_t st) {
+    if constexpr (PP) {
+        if (p.rg) return CKS_ERR_UNSUPPORTED;
+        return launch_wgrad_k<BN, TF, KIMG, MT, A1, PP, false>(a, b, p, st);
+    } else {
+        return p.rg ? launch_wgrad_k<BN, TF, KIMG, MT, A1, PP, true>(a, b, p, st)
+                    : launch_wgrad_k<BN, TF, KIMG, MT, A1, PP, false>(a, b, p, st);
+    }
 }
 
 cks_status launch_pad(cks_dtype dt, const void* src, void* dst, long long rows, int C, int Cp, cudaStream_t st) {

@@ -116,7 +116,7 @@ struct WTile {
     int ohs, ows, ods;
 };
 
-template <int MT>
+template <int MT, bool RG = false>
 __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     WTile c;
     uint32_t t = uint32_t(t64);  // 32-bit decode (64-bit div/mod is slow)
@@ -147,7 +147,7 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
     const int hn = (p.tc > 1 ? p.ouh_e : p.oh_e[c.fh]) - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     const int dn = p.od_e[c.fd] - c.ods;
-    c.wn = p.pp ? wn / 2 : (p.rg ? (wn + p.rg_pk - 1) / p.rg_pk : wn);  // pairs (host: wn even) / chunks
+    c.wn = p.pp ? wn / 2 : (RG ? (wn + p.rg_pk - 1) / p.rg_pk : wn);  // pairs (host: wn even) / chunks
     c.wr = wn;
     c.hn = hn;
     const uint32_t L = uint32_t(max(dn, 0)) * uint32_t(max(hn, 0)) * uint32_t(max(c.wn, 0)) * uint32_t(p.nblk64);
@@ -157,14 +157,16 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
 }
 
 // row tiles: does tap fw see any k-block of the segment (else its partial is 0)?
+template <bool RG>
 __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& p, int fw) {
+    const int rpk = RG ? p.rg_pk : 1;  // positions per k-block
     if (c.kb1 <= c.kb0 || c.wn <= 0) return false;
     if (p.tc > 1) {  // union oh range: walk the segment's positions (this filter row's oh, the tap's ow)
         const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
         for (int q = p0; q <= p1; ++q) {
             const int pq = q / c.wn;
-            const int oh = c.ohs + (pq % c.hn), ow = c.ows + p.rg_pk * (q - pq * c.wn);
-            if (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh] && ow < p.ow_e[fw] && ow + p.rg_pk > p.ow_s[fw]) return true;
+            const int oh = c.ohs + (pq % c.hn), ow = c.ows + rpk * (q - pq * c.wn);
+            if (oh >= p.oh_s[c.fh] && oh < p.oh_e[c.fh] && ow < p.ow_e[fw] && ow + rpk > p.ow_s[fw]) return true;
         }
         return false;
     }
@@ -173,8 +175,8 @@ __device__ __forceinline__ bool tap_has_work(const WTile& c, const WgradParams& 
     const int p0 = c.kb0 / p.nblk64, p1 = (c.kb1 - 1) / p.nblk64;
     if (p1 - p0 + 1 >= c.wn) return true;  // the segment covers every ow
     for (int q = p0; q <= p1; ++q) {
-        const int w = (q % c.wn) * p.rg_pk;  // first position of the k-block (row groups: of the chunk)
-        if (w < e && w + p.rg_pk > s) return true;
+        const int w = (q % c.wn) * rpk;  // first position of the k-block (row groups: of the chunk)
+        if (w < e && w + rpk > s) return true;
     }
     return false;
 }
@@ -192,11 +194,14 @@ __device__ __forceinline__ bool pp_col_has_work(const WTile& c, const WgradParam
     return false;
 }
 
-template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false, bool PP = false>
+template <int BN, bool kTF32 = false, int KIMG = 64, int MT = 1, bool A1 = false, bool PP = false, bool RG = false>
 __global__ void __launch_bounds__(256, 1)
     wgrad_kernel(const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmX,
                  const __grid_constant__ WgradParams p) {
     using S = WgradShape<BN, kTF32, KIMG, MT, A1, PP>;
+    static_assert(!(PP && RG), "position pairs and row groups exclude each other");
+    // row groups (compile-time: the batch-as-K kernels keep their exact issue sequence)
+    const int rpk = RG ? p.rg_pk : 1;
     static_assert(!PP || (MT == 4 && A1 && BN == 64), "position pairs: 4 X columns, 64 OC, 64 IC");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -241,12 +246,12 @@ __global__ void __launch_bounds__(256, 1)
         const bool is_b = warp == 3;
         uint32_t stage = 0, phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode<MT>(t, p);
+            const WTile c = wdecode<MT, RG>(t, p);
             for (int kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = kb % p.nblk64;
                 const int pos = kb / p.nblk64;
                 const int pq = pos / c.wn;
-                const int ow = c.ows + (PP ? 2 : p.rg_pk) * (pos - pq * c.wn);  // pairs / chunks: first position
+                const int ow = c.ows + (PP ? 2 : rpk) * (pos - pq * c.wn);  // pairs / chunks: first position
                 const int dq = pq / c.hn;
                 const int oh = c.ohs + (pq - dq * c.hn), od = c.ods + dq;
                 // filter-row clusters walk the union oh range: rows outside this filter row's own range
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(256, 1)
                                 for (int j = 0; j < a_atoms; ++j)
                                     ptx::tma_load_4d_mc(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH,
                                                         ow, od * p.OHr + oh, n64 * KIMG, tcmask);
-                        } else if (p.rg) {  // rg_pk positions x rg images, (C, N, W, H) map
+                        } else if (RG) {  // rg_pk positions x rg images, (C, N, W, H) map
                             for (int j = 0; j < a_atoms; ++j)
                                 ptx::tma_load_4d(sa + j * S::ATOM, &tmDY, &full[stage], c.mb * 128 + j * S::CH, 0, ow,
                                                  od * p.OHr + oh);
@@ -301,16 +306,16 @@ __global__ void __launch_bounds__(256, 1)
                         uint32_t nv = 0;
 #pragma unroll
                         for (int f = 0; f < MT; ++f)
-                            nv += (ohok && (MT == 1 || (ow < p.ow_e[f] && ow + p.rg_pk > p.ow_s[f]))) ? 1u : 0u;
+                            nv += (ohok && (MT == 1 || (ow < p.ow_e[f] && ow + rpk > p.ow_s[f]))) ? 1u : 0u;
                         ptx::mbar_arrive_expect_tx(&full[stage], nv * S::B_BYTES);
 #pragma unroll
                         for (int f = 0; f < MT; ++f) {
                             // trimmed tap (row groups: no valid position in the chunk)
-                            if (!ohok || (MT > 1 && !(ow < p.ow_e[f] && ow + p.rg_pk > p.ow_s[f]))) continue;
+                            if (!ohok || (MT > 1 && !(ow < p.ow_e[f] && ow + rpk > p.ow_s[f]))) continue;
                             const int iw = ow * p.sw + (MT > 1 ? f : c.fw) - p.pw;
 #pragma unroll
                             for (int j = 0; j < BN / S::CH; ++j) {
-                                if (p.rg)  // rg_pk leaping columns (element stride s_w) x rg images
+                                if (RG)  // rg_pk leaping columns (element stride s_w) x rg images
                                     ptx::tma_load_4d(sa + S::A_STAGE + f * S::B_BYTES + j * S::ATOM, &tmX, &full[stage],
                                                      c.nb * BN + j * S::CH, 0, iw, ih);
                                 else
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t dconst = kTF32 ? ptx::smem_desc_mn_b32(0, S::ATOM, 512) : ptx::smem_desc_sw128(0, S::ATOM, 1024);
         uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode<MT>(t, p);
+            const WTile c = wdecode<MT, RG>(t, p);
             ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
             ptx::tc_fence_after();
             const uint32_t d = tmem_base + acc * (MT * BN);
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::tc_fence_after();
                 const uint32_t a_addr = ptx::smem_u32(smem + stage * S::STAGE_BYTES);
                 const uint64_t ad = dconst | ptx::desc_addr(a_addr);
-                const int ow = c.ows + (PP ? 2 : p.rg_pk) * ((kb / p.nblk64) % max(c.wn, 1));
+                const int ow = c.ows + (PP ? 2 : rpk) * ((kb / p.nblk64) % max(c.wn, 1));
                 bool ohok = true;
                 if (p.tc > 1) {
                     const int oh = c.ohs + ((kb / p.nblk64) / max(c.wn, 1)) % max(c.hn, 1);
@@ -356,11 +361,11 @@ __global__ void __launch_bounds__(256, 1)
                         int kk0 = 0, kk1 = KIMG / S::UK;  // K steps of this tap in the k-block
                         if (PP) {  // X column f: one MMA for tap f of ow (rows 0-63) and tap f-1 of ow+1 (64-127)
                             if (!ohok || ow - p.pw + f < 0 || ow - p.pw + f >= p.Wx) continue;
-                        } else if (p.rg) {
+                        } else if (RG) {
                             // row groups: only the K rows (q * rg + image) of the tap's valid positions q of
                             // the chunk are multiplied -- exact trimming at the range ends
                             const int lo = MT > 1 ? p.ow_s[f] : c.ows, hi = MT > 1 ? p.ow_e[f] : c.ows + c.wr;
-                            const int q0 = max(lo - ow, 0), q1 = min(hi - ow, p.rg_pk);
+                            const int q0 = max(lo - ow, 0), q1 = min(hi - ow, rpk);
                             if (!ohok || q1 <= q0) continue;
                             kk0 = q0 * p.rg / S::UK;
                             kk1 = q1 * p.rg / S::UK;
@@ -369,12 +374,19 @@ __global__ void __launch_bounds__(256, 1)
                         }
                         const uint64_t bd = dconst | ptx::desc_addr(a_addr + S::A_STAGE + f * S::B_BYTES);
                         const uint32_t acc0 = MT > 1 ? ((started >> f) & 1u) : uint32_t(kb > c.kb0);
+                        if (RG) {  // row groups: the K steps of the tap's valid positions only
 #pragma unroll
-                        for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
-                            if (kk >= kk0 && kk < kk1)
+                            for (int kk = 0; kk < KIMG / S::UK; ++kk)
+                                if (kk >= kk0 && kk < kk1)
+                                    ptx::mma_ss<kTF32>(d + uint32_t(f * BN), ad + uint64_t(kk * (S::KSTEP >> 4)),
+                                                       bd + uint64_t(kk * (S::KSTEP >> 4)), idesc,
+                                                       (acc0 | uint32_t(kk - kk0)) != 0);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < KIMG / S::UK; ++kk)  // KIMG images in K16 (bf16) / K8 (tf32) steps
                                 ptx::mma_ss<kTF32>(d + uint32_t(f * BN), ad + uint64_t(kk * (S::KSTEP >> 4)),
-                                                   bd + uint64_t(kk * (S::KSTEP >> 4)), idesc,
-                                                   (acc0 | uint32_t(kk - kk0)) != 0);
+                                                   bd + uint64_t(kk * (S::KSTEP >> 4)), idesc, (acc0 | uint32_t(kk)) != 0);
+                        }
                         started |= 1u << f;
                     }
                     if (p.tcmc)
@@ -402,7 +414,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool vec4 = (p.C % 4) == 0;
         uint32_t acc = 0, acc_phase = 0;
         for (long long t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const WTile c = wdecode<MT>(t, p);
+            const WTile c = wdecode<MT, RG>(t, p);
             const bool zero = c.kb1 <= c.kb0;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
@@ -455,7 +467,7 @@ __global__ void __launch_bounds__(256, 1)
             } else {
 #pragma unroll 1
             for (int f = 0; f < MT; ++f) {
-            const bool fzero = zero || (MT > 1 && !tap_has_work(c, p, f));
+            const bool fzero = zero || (MT > 1 && !tap_has_work<RG>(c, p, f));
             float* dst = nullptr;
             if (p.zc)  // own smem (the ring is idle: one tile per CTA): column group q = (f*BN + c)/4, [q][128 rows]
                 dst = reinterpret_cast<float*>(smem) + (f * (BN / 4)) * 512 + row * 4;
@@ -512,7 +524,7 @@ __global__ void __launch_bounds__(256, 1)
         // tile over the gz segments in fixed order z' = 0..gz-1 and writes dW
         ptx::cluster_sync();
         if (warp >= 4 && blockIdx.x < p.num_tiles) {
-            const WTile c = wdecode<MT>(blockIdx.x, p);
+            const WTile c = wdecode<MT, RG>(blockIdx.x, p);
             const int row = int(threadIdx.x) - 128;
             const int oc = c.mb * 128 + row;
             const int G = MT * BN / 4;
