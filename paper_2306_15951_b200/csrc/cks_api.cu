@@ -422,6 +422,7 @@ cks_status run_igemm(const IgemmCfg& cfg_in, cks_dtype dt, const std::vector<KRo
     p.epi_bufs = cfg.epi ? cfg.epi_bufs : 1;
     {
         const int need = cfg.acc_stages * cfg.pbw * cfg.BN * (cfg.pair ? 2 : 1);
+        if (need > 512) return CKS_ERR_UNSUPPORTED;  // TMEM holds 512 fp32 columns per SM
         int cols = 32;
         while (cols < need) cols *= 2;
         p.tmem_cols = tmem_full() ? 512 : cols;

@@ -169,7 +169,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1, wrow_q = 0;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1, wrow_q = 0, acc1 = 0;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -201,6 +201,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_WGRAD_TC")) wtc = atoi(e);  // filter-row groups (2: multicast clusters)
         if (const char* e = cks_knob("CKS_RG")) rg = atoi(e) != 0;  // 0: batch-as-M tiles at any N
         if (const char* e = cks_knob("CKS_WROW_Q")) wrow_q = atoi(e);  // narrow Sk-dilated: output rows per k-block
+        if (const char* e = cks_knob("CKS_ACC1")) acc1 = atoi(e) != 0;  // single TMEM accumulator buffer (experiments)
     }
 };
 static const Knobs& knobs() {
@@ -340,6 +341,9 @@ static IgemmCfg igemm_cfg_w(int64_t rows_h, const std::vector<int64_t>& wph_cnt,
         }
     }
     c.acc_stages = 2;
+    // experiments: one TMEM accumulator buffer for pixel blocks whose two buffers would exceed
+    // the 512 TMEM columns (CKS_ACC1 with a forced CKS_IGEMM_CFG pixel block)
+    if (knobs().acc1 && int64_t(2) * c.pbw * c.BN * (pair ? 2 : 1) > 512) c.acc_stages = 1;
     c.wblocks = 0;
     for (auto v : wph_cnt) c.wblocks += int((v + c.pbw - 1) / c.pbw);
     c.out_tiles = rows_h * c.wblocks * c.nblk * c.nbs;
