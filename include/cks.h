@@ -317,6 +317,24 @@ cks_status cks_ar_recv_bytes(const cks_geom* g, int32_t world, size_t* bytes);
 cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
                                        int gz, void* ws, size_t ws_bytes, const cks_ar_group* grp, void* stream);
 
+/* cks_dilated_wgrad_allreduce_emulated -- the same operation for `world`
+ * ranks that share ONE GPU (tests; any setup with fewer GPUs than ranks).
+ * Per-rank arrays of length world: g[r] (the rank's batch shard), x[r],
+ * dy[r], dw[r], ws[r] / ws_bytes[r] (cks_workspace_size, CKS_OP_WGRAD_AR),
+ * grps[r] (world = world, rank = r; every pointer valid in this process --
+ * peers' buffers imported with cks_ipc_import or local).  Every rank's
+ * Sk-dilated is queued on `stream`, then ONE cooperative KB-REDUCE-AR launch
+ * covers all ranks (grid.y = rank): the CTAs that spin at the cross-rank
+ * barriers are co-resident with the CTAs they wait for.  Separate launches
+ * (streams, threads or processes) that wait on one another are not
+ * guaranteed to run concurrently on one GPU, so the single-rank entry point
+ * above must only be used with one rank per GPU.  Results are bit-identical
+ * to the one-rank-per-GPU form (same kernels, same fixed order). */
+cks_status cks_dilated_wgrad_allreduce_emulated(int32_t world, const cks_geom* g, cks_dtype dt,
+                                                const void* const* x, const void* const* dy, float* const* dw,
+                                                int gz, void* const* ws, const size_t* ws_bytes,
+                                                const cks_ar_group* grps, void* stream);
+
 /* CUDA IPC for the group's buffers (setup, not the hot path): export a
  * device pointer of this process as an opaque 72-byte handle (64-byte
  * cudaIpcMemHandle_t + 8-byte offset of ptr inside its allocation), import a

@@ -26,7 +26,7 @@ EXPORTS = ("cks_output_shape", "cks_workspace_size", "cks_choose_gz", "cks_conv2
            "cks_zins_conv2d_fwd", "cks_zins_deconv2d", "cks_zins_wgrad", "cks_plan_describe", "cks_deconv2d_ex",
            "cks_padding_macs", "cks_output_shape3", "cks_workspace_size3", "cks_op_counts3", "cks_conv3d_fwd",
            "cks_deconv3d", "cks_dilated_wgrad3d", "cks_ar_recv_bytes", "cks_dilated_wgrad_allreduce", "cks_ipc_export",
-           "cks_ipc_import", "cks_ipc_close")
+           "cks_ipc_import", "cks_ipc_close", "cks_dilated_wgrad_allreduce_emulated")
 
 
 class CksError(RuntimeError):
@@ -112,6 +112,9 @@ def lib():
             "cks_ar_recv_bytes": (C.c_int, [G, C.c_int32, C.POINTER(sz)]),
             "cks_dilated_wgrad_allreduce": (C.c_int, [G, C.c_int, vp, vp, vp, C.c_int, vp, sz,
                                                       C.POINTER(cks_ar_group), vp]),
+            "cks_dilated_wgrad_allreduce_emulated": (C.c_int, [C.c_int32, G, C.c_int, C.POINTER(vp), C.POINTER(vp),
+                                                               C.POINTER(vp), C.c_int, C.POINTER(vp), C.POINTER(sz),
+                                                               C.POINTER(cks_ar_group), vp]),
             "cks_ipc_export": (C.c_int, [vp, C.POINTER(cks_ipc_handle)]),
             "cks_ipc_import": (C.c_int, [C.POINTER(cks_ipc_handle), C.POINTER(vp)]),
             "cks_ipc_close": (C.c_int, [vp]),
@@ -228,6 +231,16 @@ def cks_ar_recv_bytes(g: cks_geom, world: int) -> int:
 def cks_dilated_wgrad_allreduce(g, dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes, grp: cks_ar_group, stream):
     _check(lib().cks_dilated_wgrad_allreduce(C.byref(g), dtype, x_ptr, dy_ptr, dw_ptr, gz, ws_ptr, ws_bytes,
                                              C.byref(grp), stream), "cks_dilated_wgrad_allreduce")
+
+
+def cks_dilated_wgrad_allreduce_emulated(geoms, dtype, x_ptrs, dy_ptrs, dw_ptrs, gz, ws_ptrs, ws_bytes, grps,
+                                         stream):
+    """All `len(geoms)` ranks on this GPU: per-rank lists; one cooperative reduce launch."""
+    w = len(geoms)
+    GA, PA, SA, RA = cks_geom * w, C.c_void_p * w, C.c_size_t * w, cks_ar_group * w
+    _check(lib().cks_dilated_wgrad_allreduce_emulated(w, GA(*geoms), dtype, PA(*x_ptrs), PA(*dy_ptrs), PA(*dw_ptrs),
+                                                      gz, PA(*ws_ptrs), SA(*ws_bytes), RA(*grps), stream),
+           "cks_dilated_wgrad_allreduce_emulated")
 
 
 def cks_ipc_export(ptr: int) -> bytes:

@@ -1142,7 +1142,8 @@ cks_status cks_deconv2d_ex(const cks_geom* g, cks_dtype dt, const void* dy, cons
 // segments AND the ranks into every rank's dW.
 
 static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw, int gz,
-                             void* ws, size_t ws_bytes, void* stream, const cks_ar_group* ar) {
+                             void* ws, size_t ws_bytes, void* stream, const cks_ar_group* ar,
+                             ArParams* defer = nullptr, long long* defer_blocks = nullptr) {
     if (!g || !x || !dy || !dw) return CKS_ERR_NULL;
     cks_status s = validate(g);
     if (s != CKS_OK) return s;
@@ -1228,6 +1229,11 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
         const long long need = std::max(q.nv, q.slice);
         const long long cap = ar->ctas > 0 ? ar->ctas : 148;
         const unsigned blocks = unsigned(std::max<long long>(1, std::min<long long>((need + 255) / 256, cap)));
+        if (defer) {  // emulated ranks: the caller launches every rank's reduce in one cooperative grid
+            *defer = q;
+            *defer_blocks = blocks;
+            return CKS_OK;
+        }
         return launch_pdl(reduce_allreduce_kernel, dim3(blocks), dim3(256), 0, st, q);
     }
     if (cfg.npart() > 1 && !cfg.zc) {  // fixed-order aggregation of the G_Z segments
@@ -1464,8 +1470,7 @@ cks_status cks_ar_recv_bytes(const cks_geom* g, int32_t world, size_t* bytes) {
     return CKS_OK;
 }
 
-cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
-                                       int gz, void* ws, size_t ws_bytes, const cks_ar_group* grp, void* stream) {
+static cks_status ar_check(const cks_geom* g, const float* dw, const cks_ar_group* grp) {
     if (!g || !grp || !grp->count || !grp->err) return CKS_ERR_NULL;
     if (grp->world < 1 || grp->world > CKS_AR_MAX_RANKS || grp->rank < 0 || grp->rank >= grp->world)
         return CKS_ERR_UNSUPPORTED;
@@ -1475,7 +1480,52 @@ cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const vo
         if (!aligned16(grp->recv[t]) || !aligned16(grp->out[t])) return CKS_ERR_ALIGNMENT;
     }
     if (grp->out[grp->rank] != dw) return CKS_ERR_UNSUPPORTED;
+    return CKS_OK;
+}
+
+cks_status cks_dilated_wgrad_allreduce(const cks_geom* g, cks_dtype dt, const void* x, const void* dy, float* dw,
+                                       int gz, void* ws, size_t ws_bytes, const cks_ar_group* grp, void* stream) {
+    const cks_status s = ar_check(g, dw, grp);
+    if (s != CKS_OK) return s;
     return wgrad_impl(g, dt, x, dy, dw, gz, ws, ws_bytes, stream, grp);
+}
+
+cks_status cks_dilated_wgrad_allreduce_emulated(int32_t world, const cks_geom* g, cks_dtype dt,
+                                                const void* const* x, const void* const* dy, float* const* dw,
+                                                int gz, void* const* ws, const size_t* ws_bytes,
+                                                const cks_ar_group* grps, void* stream) {
+    if (!g || !x || !dy || !dw || !ws || !ws_bytes || !grps) return CKS_ERR_NULL;
+    if (world < 1 || world > CKS_AR_MAX_RANKS) return CKS_ERR_UNSUPPORTED;
+    ArGroupParams P;
+    memset(&P, 0, sizeof(P));
+    long long blocks = 1;
+    for (int r = 0; r < world; ++r) {
+        if (grps[r].world != world || grps[r].rank != r) return CKS_ERR_UNSUPPORTED;
+        cks_status s = ar_check(&g[r], dw[r], &grps[r]);
+        if (s != CKS_OK) return s;
+        long long b = 1;
+        s = wgrad_impl(&g[r], dt, x[r], dy[r], dw[r], gz, ws[r], ws_bytes[r], stream, &grps[r], &P.r[r], &b);
+        if (s != CKS_OK) return s;
+        blocks = std::max(blocks, b);  // every rank's barrier counts gridDim.x CTAs
+    }
+    // all world x blocks CTAs must be co-resident (they spin at the cross-rank barriers)
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reduce_allreduce_emul_kernel, 256, 0) != cudaSuccess)
+        return last_cuda();
+    const long long resident = (long long)per_sm * device_sms();
+    blocks = std::max<long long>(1, std::min<long long>(blocks, resident / world));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(unsigned(blocks), unsigned(world));
+    cfg.blockDim = dim3(256);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, reduce_allreduce_emul_kernel, P) != cudaSuccess) return last_cuda();
+    return CKS_OK;
 }
 
 cks_status cks_ipc_export(const void* ptr, cks_ipc_handle* h) {

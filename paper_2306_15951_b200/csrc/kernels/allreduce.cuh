@@ -75,9 +75,8 @@ __device__ __forceinline__ void ar_barrier(const ArParams& p, int k, unsigned ep
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) reduce_allreduce_kernel(const __grid_constant__ ArParams p) {
-    ptx::pdl_launch_dependents();
-    ptx::pdl_wait();
+// One rank's KB-REDUCE-AR (every CTA of the rank runs it; gridDim.x = the rank's CTAs).
+__device__ __forceinline__ void ar_run(const ArParams& p) {
     __shared__ unsigned s_epoch;
     if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(p.count + 2) + 1u;  // this call's number
     __syncwarp();
@@ -114,6 +113,22 @@ __global__ void __launch_bounds__(256) reduce_allreduce_kernel(const __grid_cons
         for (int t = 0; t < p.world; ++t) p.out[t][lo + j] = v;
     }
     ar_barrier(p, 1, epoch);
+}
+
+__global__ void __launch_bounds__(256) reduce_allreduce_kernel(const __grid_constant__ ArParams p) {
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    ar_run(p);
+}
+
+// Single-GPU emulation of `world` ranks: ONE cooperative launch, blockIdx.y = rank, so every
+// CTA that spins at a cross-rank barrier is co-resident with the CTAs it waits for (separate
+// launches that wait on one another are not guaranteed to run at the same time).
+struct ArGroupParams {
+    ArParams r[kArMaxRanks];
+};
+__global__ void __launch_bounds__(256) reduce_allreduce_emul_kernel(const __grid_constant__ ArGroupParams g) {
+    ar_run(g.r[blockIdx.y]);
 }
 
 }  // namespace cks

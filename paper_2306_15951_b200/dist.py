@@ -71,8 +71,10 @@ class FusedWgradAllReduce:
     captured in a CUDA graph and replayed).
     Peers' buffers are mapped with CUDA IPC (handles exchanged over the
     process group: gloo or NCCL), or, with ``virtual_world`` on ONE process,
-    the "ranks" are this process's own buffer sets (tests: every rank's kernel
-    on its own stream of the same GPU).
+    the "ranks" are this process's own buffer sets, run together by
+    ``run_emulated`` (every rank's Sk-dilated, then ONE cooperative reduce
+    launch over all ranks: kernels that wait on one another must never be
+    separate launches on one GPU).
     """
 
     def __init__(self, geoms, dws, device, group=None, virtual_world=None, ctas=0):
@@ -138,6 +140,15 @@ class FusedWgradAllReduce:
         grp.count = s["count"].data_ptr() + 16 * layer
         grp.err = s["err"].data_ptr()
         return grp
+
+    def run_emulated(self, layer, geoms, dtype, xs, dys, gz, wss, stream):
+        """Virtual ranks: Sk-dilated of every rank's shard (geoms[r], xs[r], dys[r]: device pointers,
+        wss[r]: workspace tensors) + the fused G_Z / cross-rank reduce in one cooperative launch."""
+        grps = [self.group(layer, r) for r in range(self.world)]
+        dw = [self.sets[r]["dws"][layer].data_ptr() for r in range(self.world)]
+        self.L.cks_dilated_wgrad_allreduce_emulated(list(geoms), dtype, list(xs), list(dys), dw, gz,
+                                                    [w.data_ptr() for w in wss], [w.numel() for w in wss], grps,
+                                                    stream)
 
     def errors(self):
         return [int(s["err"].item()) for s in self.sets]

@@ -6,11 +6,16 @@ partials through peer memory (the paper's map-reduce over G_K = N*O_H*O_W,
 P:210, with the shard as the outermost segment).  Every rank must hold the
 full-batch dW of the fp64 oracle, bit-identical across ranks and repeats.
 
-* virtual ranks: W buffer sets in one process, each rank's kernels on its own
-  stream of the one GPU (the peers' "remote" stores are plain device stores);
-* two processes on one GPU: the buffers are exchanged as CUDA IPC handles over
-  a gloo group (cks_ipc_export / cks_ipc_import), the exact multi-process
-  setup of an 8-GPU node, with the processes time-sliced on one device.
+* virtual ranks: W buffer sets in one process, run by
+  cks_dilated_wgrad_allreduce_emulated: every rank's Sk-dilated, then ONE
+  cooperative KB-REDUCE-AR launch over all ranks (grid.y = rank).  Kernels that
+  wait on one another are never separate launches on one GPU -- nothing
+  guarantees they are co-scheduled (B200_PROFILING.md: Xid 109 with 2-4 such
+  ranks as processes on one GPU);
+* two processes: rank 1's receive buffer, dW and signal words are exported as
+  CUDA IPC handles over a gloo group and imported by rank 0, which runs both
+  ranks' reduce in its one cooperative launch -- the cross-process P2P stores
+  and the handle exchange of an 8-GPU node, without cross-process waits.
 """
 import os
 import subprocess
@@ -53,11 +58,8 @@ def _run_virtual(torch, world, dtype, reps=2):
     for l in LAYERS:
         geoms.append(L.make_geom(shard_range(l.N, world, 0)[1], l.C, l.H, l.W, l.OC, l.FH, l.FW, l.sh, l.sw,
                                  l.ph, l.pw))
-    # the virtual ranks share one GPU: a rank's KB-REDUCE-AR CTAs spin at the barriers
-    # while the other ranks' wgrad grids still need SMs, so the test caps the AR grid
-    # (8 CTAs) and the wgrad grids (G_Z = 2); on a real node every rank has its own GPU
     fused = FusedWgradAllReduce(geoms, dws, dev0, virtual_world=world, ctas=8)
-    streams = [torch.cuda.Stream() for _ in range(world)]
+    stream = torch.cuda.Stream()
     wss = []
     for r in range(world):
         per = []
@@ -70,12 +72,11 @@ def _run_virtual(torch, world, dtype, reps=2):
     for _ in range(reps):
         torch.cuda.synchronize()
         for i, l in enumerate(LAYERS):
-            for r in range(world):  # every rank's call queued before any is waited on
-                X, G, n = shards[i][r]
-                g = L.make_geom(n, l.C, l.H, l.W, l.OC, l.FH, l.FW, l.sh, l.sw, l.ph, l.pw)
-                grp = fused.group(i, r)
-                L.cks_dilated_wgrad_allreduce(g, dt, X.data_ptr(), G.data_ptr(), dws[r][i].data_ptr(), 2,
-                                              wss[r][i].data_ptr(), wss[r][i].numel(), grp, streams[r].cuda_stream)
+            gs = [L.make_geom(shards[i][r][2], l.C, l.H, l.W, l.OC, l.FH, l.FW, l.sh, l.sw, l.ph, l.pw)
+                  for r in range(world)]
+            fused.run_emulated(i, gs, dt, [shards[i][r][0].data_ptr() for r in range(world)],
+                               [shards[i][r][1].data_ptr() for r in range(world)], 2,
+                               [wss[r][i] for r in range(world)], stream.cuda_stream)
         torch.cuda.synchronize()
         assert fused.errors() == [0] * world, "a cross-rank wait timed out"
         results.append([[d.cpu().numpy() for d in dws[r]] for r in range(world)])

@@ -68,18 +68,16 @@ for dtype in ("bf16", "tf32"):
     torch.cuda.synchronize()
     print("ok", dtype, "3d", flush=True)
 
-# fused Sk-dilated + all-reduce, two virtual ranks on two streams
+# fused Sk-dilated + all-reduce, two virtual ranks in one cooperative reduce launch
 from paper_2306_15951_b200.dist import FusedWgradAllReduce  # noqa: E402
 g = L.make_geom(33, 64, 9, 9, 64, 3, 3, 2, 2, 1, 1)
 dws = [[torch.empty((64, 3, 3, 64), device=dev)] for _ in range(2)]
 fused = FusedWgradAllReduce([g], dws, dev, virtual_world=2, ctas=4)
-streams = [torch.cuda.Stream() for _ in range(2)]
 Xs = [t((33, 9, 9, 64), "bf16") for _ in range(2)]
 Gs = [t((33, 5, 5, 64), "bf16") for _ in range(2)]
 wss = [torch.empty(L.cks_workspace_size(g, L.CKS_BF16, L.CKS_OP_WGRAD_AR, 2), dtype=torch.uint8, device=dev)
        for _ in range(2)]
-for r in range(2):
-    L.cks_dilated_wgrad_allreduce(g, L.CKS_BF16, Xs[r].data_ptr(), Gs[r].data_ptr(), dws[r][0].data_ptr(), 2,
-                                  wss[r].data_ptr(), wss[r].numel(), fused.group(0, r), streams[r].cuda_stream)
+fused.run_emulated(0, [g, g], L.CKS_BF16, [x.data_ptr() for x in Xs], [y.data_ptr() for y in Gs], 2, wss,
+                   torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
 print("ok allreduce errors", fused.errors(), flush=True)
