@@ -16,7 +16,7 @@ def main():
     cfg, name, op = int(sys.argv[1]), sys.argv[2], sys.argv[3]
     reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
     build.build()  # libcks.so, or libcks_exp.so under CKS_EXPERIMENTS=1 (knob sweeps)
-    desc, layers = get_config(cfg)
+    desc, layers = get_config(cfg, int(os.environ["CKS_BATCH"]) if os.environ.get("CKS_BATCH") else None)
     idx = [l.name for l in layers].index(name)
     b = LayerBufs(torch, layers[idx], cfg, idx, 0, torch.device("cuda", 0),
                   os.environ.get("CKS_DTYPE", "bf16"))
