@@ -49,6 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             tmp = f"{LIB}.{os.getpid()}.tmp"
             cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
                    "-Xcompiler", "-fPIC", "-shared", "-o", tmp] + (["-DCKS_EXPERIMENTS"] if EXPERIMENTS else []) + SOURCES
+            if EXPERIMENTS and os.environ.get("CKS_NVCC_DEFS"):  # compile-time variants (experiments build only)
+                cmd += os.environ["CKS_NVCC_DEFS"].split()
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
                 print(" ".join(cmd), file=sys.stderr)

@@ -659,7 +659,7 @@ static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
     while (c.BN < g.OC) c.BN *= 2;
     const int wbytes = int((g.FH * c.BN * c.ROWB + 1023) / 1024 * 1024);
     const int stage = 128 * c.ROWB;
-    const int staging = 4 * 2 * 4096;  // kernels/narrow.cuh RowFwdShape::STAGING
+    const int staging = 4 * CKS_ROW_EPI_BUFS * 4096;  // kernels/narrow.cuh RowFwdShape::STAGING
     const int budget = 227 * 1024 - 1024 - 512;
     c.stages = std::min(16, (budget - wbytes - staging) / stage);
     if (c.stages < 3) return c;

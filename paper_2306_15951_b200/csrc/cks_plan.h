@@ -158,6 +158,9 @@ IgemmCfg igemm_cfg_deconv_w(const cks_geom& g, cks_dtype dt, int num_sms);
 // Eligible for FW*C small enough that a run (+ its alignment shift) fits a
 // 64-element bf16 / 32-element fp32 row, C <= 16 (bf16) / 8 (fp32), and a
 // 16-byte X row pitch (W*C*eb % 16 == 0).
+#ifndef CKS_ROW_EPI_BUFS
+#define CKS_ROW_EPI_BUFS 2  // KB-CONV-ROW TMA-store staging buffers per epilogue warp (kernels/narrow.cuh)
+#endif
 constexpr int kRowClasses = 24;  // column classes per launch (kernels/narrow.cuh RowClass table)
 struct RowClassH {
     int col0 = 0, cstep = 1, ncols = 0;  // output columns col0 + cstep * i

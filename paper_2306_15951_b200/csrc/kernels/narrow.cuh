@@ -68,6 +68,9 @@ struct RowFwdParams {
     int tma_store;  // 1: epilogue via TMA store (OC % 32 == 0)
 };
 
+#ifndef CKS_ROW_EPI_BUFS
+#define CKS_ROW_EPI_BUFS 2  // TMA-store staging buffers per epilogue warp (2 or 4)
+#endif
 template <int ROWB, int BN, bool TF>
 struct RowFwdShape {
     static constexpr int EB = TF ? 4 : 2;
@@ -75,7 +78,7 @@ struct RowFwdShape {
     static constexpr int STAGE = 128 * ROWB;       // one X row of 128 images
     // 4 epilogue warps x 2 x (32 rows x 128 B): two TMA stores in flight per warp
     // (four measured no faster on the stem: the stores are not what bounds it)
-    static constexpr int EPI_BUFS = 2;
+    static constexpr int EPI_BUFS = CKS_ROW_EPI_BUFS;
     static constexpr int STAGING = 4 * EPI_BUFS * 4096;
     static constexpr int RMAX = 256 / BN < 8 ? 256 / BN : 8;  // 2 x R x BN TMEM columns <= 512
 };
@@ -307,7 +310,12 @@ __global__ void __launch_bounds__(256, 1)
                     ptx::tmem_ld_wait();
                     if (p.tma_store) {
                         uint8_t* buf = my + (q++ & uint32_t(S::EPI_BUFS - 1)) * 4096;
-                        if (ptx::elect_one()) ptx::bulk_wait_read1();  // buffer of chunk q-2 drained
+                        if (ptx::elect_one()) {  // buffer of chunk q - EPI_BUFS drained
+                            if constexpr (S::EPI_BUFS == 4)
+                                ptx::bulk_wait_read3();
+                            else
+                                ptx::bulk_wait_read1();
+                        }
                         __syncwarp();
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
