@@ -169,7 +169,7 @@ struct Knobs {
     bool ov = false;
     int bn = 0, pbw = 0, z = 0, apos = 0, bst = 0;
     int kb = 0, epi = 1, unified = 1, mcast = 0, kimg128 = 1, zc = 1, epi8 = 0, wmt = 1, pair = 1, smem_cap = 0,
-        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1, wrow_q = 0, acc1 = 0;
+        gz_max = 64, wzc = 2, epi_bufs = 1, wa1 = 1, wmt_tf32 = 1, wa1_tf32 = 1, wtc = 1, pair_tf32 = 1, tf32_wide = 1, wpp = 1, pair_waves_tf32 = 25, bf16_wide = 1, wmt128 = 1, ks_mp = 1, rg = 1, wrow_q = 0, acc1 = 0, wmt_lmin = -1;
     Knobs() {
         if (const char* e = cks_knob("CKS_IGEMM_CFG")) ov = sscanf(e, "%d,%d,%d,%d,%d", &bn, &pbw, &z, &apos, &bst) >= 3;
         if (const char* e = cks_knob("CKS_IGEMM_KB")) kb = atoi(e);
@@ -202,6 +202,7 @@ struct Knobs {
         if (const char* e = cks_knob("CKS_RG")) rg = atoi(e) != 0;  // 0: batch-as-M tiles at any N
         if (const char* e = cks_knob("CKS_WROW_Q")) wrow_q = atoi(e);  // narrow Sk-dilated: output rows per k-block
         if (const char* e = cks_knob("CKS_ACC1")) acc1 = atoi(e) != 0;  // single TMEM accumulator buffer (experiments)
+        if (const char* e = cks_knob("CKS_WMT_LMIN")) wmt_lmin = atoi(e);  // Sk-dilated row tiles: min k-blocks per tap
     }
 };
 static const Knobs& knobs() {
@@ -916,7 +917,14 @@ static WgradCfg wgrad_cfg_plan(const cks_geom& g, cks_dtype dt, int gz_req, int 
         if (ntaps == 0) lmin = 1;
     };
     compute_lmin();
-    if (c.mt > 1 && lmin < 2048) {  // small maps: row tiles cost parallelism (C2 sweep slower); one tap per tile
+    // small maps: row tiles cost parallelism (C2 sweep slower); one tap per tile.  Measured
+    // (tools/time_op.py, CKS_WMT_LMIN): 64-channel row tiles win from ~1e5 (positions x images)
+    // per filter row up (C2 vgg32 64->64 s1: TF32 74 -> 39 us, BF16 51 -> 29 us; C5 l2a TF32
+    // 104 -> 88 us) and lose on smaller maps (vgg16 64->128 s2: +44-68 %); 128-channel row tiles
+    // (one accumulator buffer) keep the former rule (>= 2048 k-blocks)
+    const bool small = knobs().wmt_lmin >= 0 ? lmin < knobs().wmt_lmin
+                                             : (c.BN == 64 ? lmin * c.kimg < 100000 : lmin < 2048);
+    if (c.mt > 1 && small) {
         c.mt = 1;
         compute_lmin();
     }
