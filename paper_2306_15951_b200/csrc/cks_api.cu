@@ -570,34 +570,56 @@ void fill_row_classes(RowClass* dst, const std::vector<RowClassH>& src) {
 }
 
 template <int ROWB, int BN, bool TF>
-cks_status launch_fwd_row_t(const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem, int grid,
-                            cudaStream_t st) {
-    auto kern = fwd_row_kernel<ROWB, BN, TF>;
+cks_status launch_fwd_row_t(const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, const RowXMaps& xm,
+                            int smem, int grid, cudaStream_t st) {
+    // row groups are a separate instantiation (the 128-image path keeps its exact code)
+    auto kern = p.rg ? fwd_row_kernel<ROWB, BN, TF, true> : fwd_row_kernel<ROWB, BN, TF, false>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
-    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, ty, p);
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, ty, p, xm);
 }
 
 template <int ROWB, bool TF>
-cks_status launch_fwd_row_rb(int BN, const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p, int smem,
-                             int grid, cudaStream_t st) {
+cks_status launch_fwd_row_rb(int BN, const CUtensorMap& tx, const CUtensorMap& ty, const RowFwdParams& p,
+                             const RowXMaps& xm, int smem, int grid, cudaStream_t st) {
     switch (BN) {
-        case 32: return launch_fwd_row_t<ROWB, 32, TF>(tx, ty, p, smem, grid, st);
-        case 64: return launch_fwd_row_t<ROWB, 64, TF>(tx, ty, p, smem, grid, st);
-        case 128: return launch_fwd_row_t<ROWB, 128, TF>(tx, ty, p, smem, grid, st);
+        case 32: return launch_fwd_row_t<ROWB, 32, TF>(tx, ty, p, xm, smem, grid, st);
+        case 64: return launch_fwd_row_t<ROWB, 64, TF>(tx, ty, p, xm, smem, grid, st);
+        case 128: return launch_fwd_row_t<ROWB, 128, TF>(tx, ty, p, xm, smem, grid, st);
         case 256:
-            if constexpr (!TF) return launch_fwd_row_t<ROWB, 256, TF>(tx, ty, p, smem, grid, st);
+            if constexpr (!TF) return launch_fwd_row_t<ROWB, 256, TF>(tx, ty, p, xm, smem, grid, st);
             break;
     }
     return CKS_ERR_UNSUPPORTED;
 }
 
-cks_status run_fwd_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, const void* x, const void* w, float* y,
+cks_status run_fwd_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc_in, const void* x, const void* w, float* y,
                        cudaStream_t st) {
+    RowCfg rc = rc_in;
     CUtensorMap tx, ty;
     memset(&ty, 0, sizeof(ty));
     if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 128, 1, false)) return CKS_ERR_CUDA;
+    static thread_local RowXMaps xm;  // per-class maps of the row-group plan (unused otherwise)
+    if (rc.rg) {
+        // per class: (W*C elements, N, class column, H), column stride cstep*sw*C, box JB x rg x rg_pc
+        const uint64_t eb = uint64_t(elem_bytes(dt));
+        bool ok = rc.cls.size() <= size_t(kRowClasses);
+        for (size_t k = 0; ok && k < rc.cls.size(); ++k) {
+            const RowClassH& c = rc.cls[k];
+            const uint64_t cs = c.ncols > 1 ? uint64_t(c.cstep) * g.sw * g.C * eb : 16;
+            uint64_t d[4] = {uint64_t(g.W * g.C), uint64_t(g.N), uint64_t(c.ncols), uint64_t(g.H)};
+            uint64_t sb[3] = {uint64_t(g.H * g.W * g.C) * eb, cs, uint64_t(g.W * g.C) * eb};
+            uint32_t box[4] = {uint32_t(rc.JB), uint32_t(rc.rg), uint32_t(rc.rg_pc), 1};
+            ok = cs % 16 == 0 && make_tmap4(&xm.m[k], dt, x, d, sb, box, int(rc.JB * eb), false);
+        }
+        if (!ok) rc = row_cfg_fwd(g, dt, false);  // a class the row-group boxes cannot address: 128-image tiles
+    }
     RowFwdParams p;
     memset(&p, 0, sizeof(p));
+    if (rc.rg) {
+        p.rg = rc.rg;
+        p.rg_shift = rc.rg == 32 ? 5 : 6;
+        p.rg_pc = rc.rg_pc;
+    }
     p.w = w;
     p.y = y;
     p.N = int(g.N), p.H = int(g.H), p.W = int(g.W), p.C = int(g.C), p.OC = int(g.OC);
@@ -616,12 +638,12 @@ cks_status run_fwd_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, const 
     }
     const bool tf = dt == CKS_TF32;
     switch (rc.ROWB) {
-        case 32: return tf ? launch_fwd_row_rb<32, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
-                           : launch_fwd_row_rb<32, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
-        case 64: return tf ? launch_fwd_row_rb<64, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
-                           : launch_fwd_row_rb<64, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
-        case 128: return tf ? launch_fwd_row_rb<128, true>(rc.BN, tx, ty, p, rc.smem, rc.grid, st)
-                            : launch_fwd_row_rb<128, false>(rc.BN, tx, ty, p, rc.smem, rc.grid, st);
+        case 32: return tf ? launch_fwd_row_rb<32, true>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st)
+                           : launch_fwd_row_rb<32, false>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st);
+        case 64: return tf ? launch_fwd_row_rb<64, true>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st)
+                           : launch_fwd_row_rb<64, false>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st);
+        case 128: return tf ? launch_fwd_row_rb<128, true>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st)
+                            : launch_fwd_row_rb<128, false>(rc.BN, tx, ty, p, xm, rc.smem, rc.grid, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }

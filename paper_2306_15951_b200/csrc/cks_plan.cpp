@@ -653,7 +653,7 @@ static void row_spread(std::vector<RowClassH>& cls, int64_t total, const std::ve
 
 // Narrow ConvV2: tile = R output rows x one column x 128 images x all OC,
 // the class's filter rows resident in shared memory.
-static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
+static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt, bool allow_rg) {
     RowCfg c;
     if (!row_setup(g, dt, c) || g.OC > (dt == CKS_TF32 ? 128 : 256)) return c;  // instantiated BN range
     c.BN = 32;
@@ -666,13 +666,21 @@ static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
     if (c.stages < 3) return c;
     c.smem = 1024 + wbytes + c.stages * stage + staging + 512;
     c.nblk = int((g.N + 127) / 128);
+    // row groups (small batches): an M tile is rg_pc columns of one class x rg images, each
+    // column group one TMA box of a per-class tensor map (column stride cstep * sw * C)
+    if (allow_rg && rg_images(g.N) > 0) {
+        c.rg = rg_images(g.N);
+        c.rg_pc = 128 / c.rg;
+        c.nblk = 1;
+    }
     const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
+    auto col_units = [&](const RowClassH& k) { return c.rg ? (k.ncols + c.rg_pc - 1) / c.rg_pc : k.ncols; };
     // output rows per tile: X rows are loaded once per tile (h reuse), as many as
     // TMEM holds while the grid keeps >= 2 tiles per SM
     const int rmax = std::min(8, 256 / c.BN);
     auto tiles_for = [&](int r) {
         int64_t t = 0;
-        for (auto& k : c.cls) t += cdiv(OH, r) * k.ncols * c.nblk;
+        for (auto& k : c.cls) t += cdiv(OH, r) * col_units(k) * c.nblk;
         return t;
     };
     c.R = 1;
@@ -681,7 +689,7 @@ static RowCfg row_cfg_fwd_plan(const cks_geom& g, cks_dtype dt) {
     c.tiles = tiles_for(c.R);
     std::vector<int64_t> cap;
     for (auto& k : c.cls) {
-        k.work = cdiv(OH, c.R) * k.ncols * c.nblk;
+        k.work = cdiv(OH, c.R) * col_units(k) * c.nblk;
         cap.push_back(k.work);
     }
     row_spread(c.cls, std::max<int64_t>(int64_t(c.cls.size()), 148), cap);
@@ -822,8 +830,8 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
         if (op == CKS_OP_FWD) {
             const RowCfg r = row_cfg_fwd(g, dt);
             if (r.ok) {
-                snprintf(b, sizeof b, "row_fwd ROWB=%d JB=%d BN=%d R=%d stages=%d grid=%d tiles=%lld classes=%d cls=",
-                         r.ROWB, r.JB, r.BN, r.R, r.stages, r.grid, (long long)r.tiles, int(r.cls.size()));
+                snprintf(b, sizeof b, "row_fwd ROWB=%d JB=%d BN=%d R=%d stages=%d grid=%d tiles=%lld rg=%d classes=%d cls=",
+                         r.ROWB, r.JB, r.BN, r.R, r.stages, r.grid, (long long)r.tiles, r.rg, int(r.cls.size()));
                 return std::string(b) + row_classes_str(r.cls);
             }
         }
@@ -1115,9 +1123,9 @@ IgemmCfg igemm_cfg_deconv(const cks_geom& g, cks_dtype dt, int num_sms) {
     static PlanMemo<IgemmCfg> memo;
     return memo.get(plan_key(g, dt, 1, 0, num_sms), [&] { return igemm_cfg_deconv_plan(g, dt, num_sms); });
 }
-RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt) {
+RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt, bool allow_rg) {
     static PlanMemo<RowCfg> memo;
-    return memo.get(plan_key(g, dt, 0, 0, 0), [&] { return row_cfg_fwd_plan(g, dt); });
+    return memo.get(plan_key(g, dt, 0, allow_rg ? 1 : 0, 0), [&] { return row_cfg_fwd_plan(g, dt, allow_rg); });
 }
 RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
     static PlanMemo<RowCfg> memo;

@@ -66,6 +66,16 @@ struct RowFwdParams {
     RowClass cls[kRowClasses];
     int stages;     // A ring depth (one X row per stage)
     int tma_store;  // 1: epilogue via TMA store (OC % 32 == 0)
+    // Row groups (small batches, N <= 64; kernel template RG): the M = 128 rows of a tile are
+    // rg_pc columns of ONE class x rg images (row r = column r / rg, image r % rg), loaded by one
+    // box of the class's own tensor map (RowXMaps: dims (W*C, N, class column, H), column stride
+    // cstep * sw * C) -- every column of a class shares the box origin alignment and K chunks
+    int rg, rg_shift, rg_pc;
+};
+
+// Per-class X tensor maps of the row-group ConvV2 (kernel parameter space, < 4 KB in total).
+struct RowXMaps {
+    CUtensorMap m[kRowClasses];
 };
 
 #ifndef CKS_ROW_EPI_BUFS
@@ -93,17 +103,33 @@ __device__ __forceinline__ int row_class_of(const RowClass* cls, int ncls, int b
     return k;
 }
 
-// Tile t of class k: (row block ob, column i, image block nb), nb fastest.
+// Tile t of class k: (row block ob, column i, image block nb), nb fastest.  Row groups: (row
+// block, column group g of rg_pc class columns starting at class column ci0), g fastest.
+template <bool RG>
 struct RowFwdTile {
     int nb, ow, oh0, rn;  // rn: rows in this block
+    int ci0;              // row groups: first class column of the group
     __device__ RowFwdTile(int t, const RowClass& c, const RowFwdParams& p) {
-        nb = t % p.nblk;
-        const int r = t / p.nblk;
-        ow = c.col0 + c.cstep * (r % c.ncols);
-        oh0 = (r / c.ncols) * p.R;
+        if (RG) {
+            const int ng = (c.ncols + p.rg_pc - 1) / p.rg_pc;
+            nb = 0;
+            ci0 = (t % ng) * p.rg_pc;
+            ow = c.col0 + c.cstep * ci0;
+            oh0 = (t / ng) * p.R;
+        } else {
+            nb = t % p.nblk;
+            const int r = t / p.nblk;
+            ci0 = r % c.ncols;
+            ow = c.col0 + c.cstep * ci0;
+            oh0 = (r / c.ncols) * p.R;
+        }
         rn = min(p.R, p.OH - oh0);
     }
 };
+template <bool RG>
+__device__ __forceinline__ int row_fwd_ntiles(const RowClass& c, const RowFwdParams& p) {
+    return ((p.OH + p.R - 1) / p.R) * (RG ? (c.ncols + p.rg_pc - 1) / p.rg_pc : c.ncols * p.nblk);
+}
 
 // Shared-memory row slot of filter row fh in KB-CONV-ROW's B operand: filter rows are grouped by
 // fh mod sh, each group in DECREASING fh, so the filter rows fh, fh - sh, fh - 2 sh, ... that one X
@@ -117,10 +143,10 @@ __host__ __device__ __forceinline__ int row_fwd_slot(int fh, int FH, int sh) {
 }
 
 
-template <int ROWB, int BN, bool TF>
+template <int ROWB, int BN, bool TF, bool RG = false>
 __global__ void __launch_bounds__(256, 1)
     fwd_row_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
-                   const __grid_constant__ RowFwdParams p) {
+                   const __grid_constant__ RowFwdParams p, const __grid_constant__ RowXMaps xm) {
     using S = RowFwdShape<ROWB, BN, TF>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -146,6 +172,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmX);
         if (p.tma_store) ptx::prefetch_tmap(&tmY);
+        if (RG) ptx::prefetch_tmap(&xm.m[k]);
     }
     if (warp == 1 && lane == 0) {
         for (int i = 0; i < p.stages; ++i) {
@@ -204,16 +231,18 @@ __global__ void __launch_bounds__(256, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const int ci = int(blockIdx.x) - cl.base;
-    const int ntiles = ((p.OH + p.R - 1) / p.R) * cl.ncols * p.nblk;
+    const int ntiles = row_fwd_ntiles<RG>(cl, p);
 
     if (warp == 0) {
         // ---------------- TMA producer: one box per VALID X row of the tile (T1 trimming)
         uint32_t s = 0, ph = 0;
         for (int t = ci; t < ntiles; t += cl.cnt) {
-            const RowFwdTile tl(t, cl, p);
+            const RowFwdTile<RG> tl(t, cl, p);
             const int ih0 = tl.oh0 * p.sh - p.ph;
             const int rl = max(ih0, 0), rh = min(p.H, ih0 + p.sh * (tl.rn - 1) + p.FH);
-            const int origin = (tl.ow * p.sw - p.pw) * p.C + cl.off;
+            // box origin in the flattened (W*C) row; row groups: of class column 0 (the class map's
+            // column coordinate adds ci0 * cstep * sw * C)
+            const int origin = ((RG ? cl.col0 : tl.ow) * p.sw - p.pw) * p.C + cl.off;
             for (int ih = rl; ih < rh; ++ih) {
                 const int ru = rut[ih - ih0];
                 const int r0 = ru >> 4, r1 = min(tl.rn, ru & 15);
@@ -221,7 +250,10 @@ __global__ void __launch_bounds__(256, 1)
                 ptx::mbar_wait(&empty[s], ph ^ 1u);
                 if (ptx::elect_one()) {
                     ptx::mbar_arrive_expect_tx(&full[s], uint32_t(S::STAGE));
-                    ptx::tma_load_4d(abuf + s * S::STAGE, &tmX, &full[s], origin, tl.nb * 128, ih, 0);
+                    if (RG)  // rg_pc columns x rg images of the class (column stride in the class map)
+                        ptx::tma_load_4d(abuf + s * S::STAGE, &xm.m[k], &full[s], origin, 0, tl.ci0, ih);
+                    else
+                        ptx::tma_load_4d(abuf + s * S::STAGE, &tmX, &full[s], origin, tl.nb * 128, ih, 0);
                 }
                 __syncwarp();
                 if (++s == uint32_t(p.stages)) {
@@ -240,7 +272,7 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t bdesc0 = ptx::smem_desc_kmajor(w0 + 32u * uint32_t(cl.kc0), ROWB);
         uint32_t s = 0, ph = 0, i = 0;
         for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
-            const RowFwdTile tl(t, cl, p);
+            const RowFwdTile<RG> tl(t, cl, p);
             const int ih0 = tl.oh0 * p.sh - p.ph;
             const int rl = max(ih0, 0), rh = min(p.H, ih0 + p.sh * (tl.rn - 1) + p.FH);
             const uint32_t acc = i & 1u, aph = (i >> 1) & 1u;
@@ -295,11 +327,17 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* my = stg + sub * S::EPI_BUFS * 4096;
         uint32_t i = 0, q = 0;
         for (int t = ci; t < ntiles; t += cl.cnt, ++i) {
-            const RowFwdTile tl(t, cl, p);
+            const RowFwdTile<RG> tl(t, cl, p);
             const uint32_t acc = i & 1u, aph = (i >> 1) & 1u;
             ptx::mbar_wait(&tfull[acc], aph);
             ptx::tc_fence_after();
-            const int n = tl.nb * 128 + int(sub * 32 + lane);
+            // M row -> (column, image).  Row groups (rg >= 32): the warp's 32 rows are 32 images of
+            // one class column; columns past the class's last are computed but never stored
+            const int wci = RG ? tl.ci0 + (int(sub * 32) >> p.rg_shift) : tl.ci0;
+            const bool wlive = !RG || wci < cl.ncols;
+            const int wow = cl.col0 + cl.cstep * wci;
+            const int n0 = RG ? (int(sub * 32) & (p.rg - 1)) : tl.nb * 128 + int(sub * 32);
+            const int n = n0 + int(lane);
             for (int r = 0; r < tl.rn; ++r) {
                 const int oh = tl.oh0 + r;
 #pragma unroll 1
@@ -308,6 +346,7 @@ __global__ void __launch_bounds__(256, 1)
                     uint32_t v[32];
                     ptx::tmem_ld32(tmem_base + ((sub * 32u) << 16) + acc * uint32_t(S::RMAX * BN) + uint32_t(r * BN + c0), v);
                     ptx::tmem_ld_wait();
+                    if (!wlive) continue;  // warp-uniform
                     if (p.tma_store) {
                         uint8_t* buf = my + (q++ & uint32_t(S::EPI_BUFS - 1)) * 4096;
                         if (ptx::elect_one()) {  // buffer of chunk q - EPI_BUFS drained
@@ -324,12 +363,12 @@ __global__ void __launch_bounds__(256, 1)
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (ptx::elect_one()) {
-                            ptx::tma_store_4d(&tmY, buf, c0, tl.ow, oh, tl.nb * 128 + int(sub * 32));
+                            ptx::tma_store_4d(&tmY, buf, c0, wow, oh, n0);
                             ptx::bulk_commit();
                         }
                         __syncwarp();
                     } else if (n < p.N) {
-                        float* dst = p.y + ((static_cast<long long>(n) * p.OH + oh) * p.OW + tl.ow) * p.OC;
+                        float* dst = p.y + ((static_cast<long long>(n) * p.OH + oh) * p.OW + wow) * p.OC;
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (c0 + j < p.OC) dst[c0 + j] = __uint_as_float(v[j]);

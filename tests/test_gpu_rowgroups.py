@@ -155,3 +155,52 @@ def test_row_group_wgrad(torch_cuda, lay, gz, dtype):
     """Sk-dilated with position chunks: every tap multiplies only the K rows of its valid positions
     (chunks cut by the T3 ranges at both ends), G_Z segments split the chunk sequence."""
     check_full(torch_cuda, lay, dtype, config=15, idx=int(lay.name[3:]), ops=("wgrad",), gz=gz)
+
+
+def _narrow_rg_layers(n, seed, dtype):
+    """Narrow-channel ConvV2 (filter-row kernel) at small batches: row groups of rg_pc class
+    columns x rg images, one box of the class's own tensor map (column stride cstep*sw*C)."""
+    from test_gpu_parity import _narrow_layers
+    out = []
+    rng = np.random.default_rng(seed + 7)
+    for lay in _narrow_layers(3 * n, seed, dtype):
+        N = int(rng.choice([1, 5, 20, 32, 33, 47, 64]))
+        out.append(Layer(lay.name.replace("narrow", "nrg"), N, lay.C, lay.H, lay.W + 8 * int(rng.integers(0, 3)),
+                         lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw))
+        if len(out) == n:
+            break
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("k", range(14))
+def test_row_group_narrow_fwd(torch_cuda, k, dtype):
+    lay = _narrow_rg_layers(14, 41 if dtype == "bf16" else 43, dtype)[k]
+    check_full(torch_cuda, lay, dtype, config=17, idx=k, ops=("fwd",))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("lay", [Layer("nrs0", 32, 3, 61, 64, 64, 7, 7, 2, 2, 3, 3),    # ResNet stem at 32 images
+                                 Layer("nrs1", 48, 3, 33, 40, 64, 3, 3, 1, 1, 1, 1),    # 3x3 s1, ragged groups
+                                 Layer("nrs2", 7, 3, 32, 32, 64, 5, 5, 2, 2, 2, 2)],    # 5x5 s2, 7 images
+                         ids=lambda l: l.name)
+def test_row_group_narrow_fwd_plans(torch_cuda, lay, dtype):
+    """The plan takes row groups for the filter-row ConvV2 and the output matches the oracle;
+    a NaN-prefilled output proves every valid (image, pixel) is written and nothing else."""
+    from paper_2306_15951_b200 import _lib as L
+    from paper_2306_15951_b200 import ops as K
+    torch = torch_cuda
+    g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+    d = L.plan_dict(g, L.CKS_BF16 if dtype == "bf16" else L.CKS_TF32, L.CKS_OP_FWD)
+    assert d["kind"] == "row_fwd" and int(d["rg"]) == (32 if lay.N <= 32 else 64), d
+    a = make_layer_inputs(lay, 18, int(lay.name[3:]), dtype)
+    X, W = dev(torch, a["X"], dtype), dev(torch, a["W"], dtype)
+    OH, OW = lay.out_hw()
+    n = lay.N * OH * OW * lay.OC
+    buf = torch.full((n + 4096,), float("nan"), device="cuda")
+    y = buf[:n].view(lay.N, OH, OW, lay.OC)
+    K.conv2d_fwd(X, W, (lay.sh, lay.sw), (lay.ph, lay.pw), out=y)
+    torch.cuda.synchronize()
+    assert not torch.isnan(y).any() and torch.isnan(buf[n:]).all()
+    check(y.cpu().numpy(), O.conv_ref(a["X"], a["W"], lay.sh, lay.sw, lay.ph, lay.pw), dtype, f"{lay} fwd",
+          red_len(lay, "fwd"))
