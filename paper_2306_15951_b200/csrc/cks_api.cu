@@ -649,33 +649,64 @@ cks_status run_fwd_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc_in, con
 }
 
 template <int ROWB, int BN, bool TF>
-cks_status launch_wgrad_row_t(const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p, int smem,
-                              cudaStream_t st) {
-    auto kern = wgrad_row_kernel<ROWB, BN, TF>;
+cks_status launch_wgrad_row_t(const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p,
+                              const RowWXMaps& xm, int smem, cudaStream_t st) {
+    // row groups: a separate instantiation (the 64-image path keeps its exact code)
+    auto kern = p.rg ? wgrad_row_kernel<ROWB, BN, TF, true> : wgrad_row_kernel<ROWB, BN, TF, false>;
     if (set_smem(kern, smem) != CKS_OK) return CKS_ERR_CUDA;
     long long grid = std::max<long long>(1, std::min<long long>(p.num_tiles, device_sms()));
-    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, tdy, p);
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(256), smem, st, tx, tdy, p, xm);
 }
 
 template <int ROWB, bool TF>
 cks_status launch_wgrad_row_rb(int BN, const CUtensorMap& tx, const CUtensorMap& tdy, const RowWgradParams& p,
-                               int smem, cudaStream_t st) {
+                               const RowWXMaps& xm, int smem, cudaStream_t st) {
     switch (BN) {
-        case 64: return launch_wgrad_row_t<ROWB, 64, TF>(tx, tdy, p, smem, st);
-        case 128: return launch_wgrad_row_t<ROWB, 128, TF>(tx, tdy, p, smem, st);
-        case 256: return launch_wgrad_row_t<ROWB, 256, TF>(tx, tdy, p, smem, st);
+        case 64: return launch_wgrad_row_t<ROWB, 64, TF>(tx, tdy, p, xm, smem, st);
+        case 128: return launch_wgrad_row_t<ROWB, 128, TF>(tx, tdy, p, xm, smem, st);
+        case 256: return launch_wgrad_row_t<ROWB, 256, TF>(tx, tdy, p, xm, smem, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
 
-cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, const void* x, const CUtensorMap& tdy,
-                         float* wout, long long part_stride, cudaStream_t st) {
+cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc_in, const void* x, const void* dys,
+                         int64_t OCp, const CUtensorMap& tdy, float* wout, long long part_stride, cudaStream_t st) {
     const bool tf = dt == CKS_TF32;
+    RowCfg rc = rc_in;
+    static thread_local RowWXMaps xm;  // per-class maps of the row-group plan (unused otherwise)
+    if (rc.rg) {
+        // per class: X (W*C, N, class column, H) and dY (OCp, N, class column, OH), column strides
+        // cstep*sw*C / cstep*OCp elements; boxes of rg images x rg_pc columns
+        const uint64_t eb = uint64_t(elem_bytes(dt));
+        const int xr = int(g.FH) + g.sh * (rc.q - 1);
+        const int64_t OH = axis_h(g).O, OW = axis_w(g).O;
+        bool ok = rc.cls.size() <= size_t(kRowWgradRgClasses);
+        for (size_t k = 0; ok && k < rc.cls.size(); ++k) {
+            const RowClassH& c = rc.cls[k];
+            const uint64_t xs = c.ncols > 1 ? uint64_t(c.cstep) * g.sw * g.C * eb : 16;
+            const uint64_t ys = c.ncols > 1 ? uint64_t(c.cstep) * OCp * eb : 16;
+            uint64_t dx[4] = {uint64_t(g.W * g.C), uint64_t(g.N), uint64_t(c.ncols), uint64_t(g.H)};
+            uint64_t sx[3] = {uint64_t(g.H * g.W * g.C) * eb, xs, uint64_t(g.W * g.C) * eb};
+            uint32_t bx[4] = {uint32_t(rc.JB), uint32_t(rc.rg), uint32_t(rc.rg_pc), uint32_t(xr)};
+            // dY columns of class k start at output column col0 (the class map's base is shifted there)
+            const void* ybase = static_cast<const uint8_t*>(dys) + int64_t(c.col0) * OCp * int64_t(eb);
+            uint64_t dy[4] = {uint64_t(OCp), uint64_t(g.N), uint64_t(c.ncols), uint64_t(OH)};
+            uint64_t sy[3] = {uint64_t(OH * OW * OCp) * eb, ys, uint64_t(OW * OCp) * eb};
+            uint32_t by[4] = {uint32_t(128 / eb), uint32_t(rc.rg), uint32_t(rc.rg_pc), 1};
+            ok = xs % 16 == 0 && ys % 16 == 0 && make_tmap4(&xm.x[k], dt, x, dx, sx, bx, int(rc.JB * eb), tf) &&
+                 make_tmap4(&xm.dy[k], dt, ybase, dy, sy, by, 128, tf);
+        }
+        if (!ok) rc = row_cfg_wgrad(g, dt, rc.gz, kPlanSMs, false);  // same partial count: 64-image k-blocks
+    }
     CUtensorMap tx;
     const int xrows = int(g.FH) + g.sh * (rc.q - 1);  // one X box serves q output rows
     if (!make_row_xmap(&tx, x, g, dt, uint32_t(rc.JB), 64, uint32_t(xrows), tf)) return CKS_ERR_CUDA;
     RowWgradParams q;
     memset(&q, 0, sizeof(q));
+    if (rc.rg) {
+        q.rg = rc.rg;
+        q.rg_pk = rc.rg_pc;
+    }
     q.out = wout;
     q.part_stride = part_stride;
     q.N = int(g.N), q.H = int(g.H), q.W = int(g.W), q.C = int(g.C), q.OC = int(g.OC);
@@ -692,11 +723,11 @@ cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc, cons
     q.q = rc.q;
     q.xrows = xrows;
     q.a_bytes = ((rc.q - 1) * g.sh + rc.mb * (128 / rc.JB)) * 64 * rc.ROWB;
-    if (tf) return rc.ROWB == 128 ? launch_wgrad_row_rb<128, true>(rc.BN, tx, tdy, q, rc.smem, st) : CKS_ERR_UNSUPPORTED;
+    if (tf) return rc.ROWB == 128 ? launch_wgrad_row_rb<128, true>(rc.BN, tx, tdy, q, xm, rc.smem, st) : CKS_ERR_UNSUPPORTED;
     switch (rc.ROWB) {
-        case 32: return launch_wgrad_row_rb<32, false>(rc.BN, tx, tdy, q, rc.smem, st);
-        case 64: return launch_wgrad_row_rb<64, false>(rc.BN, tx, tdy, q, rc.smem, st);
-        case 128: return launch_wgrad_row_rb<128, false>(rc.BN, tx, tdy, q, rc.smem, st);
+        case 32: return launch_wgrad_row_rb<32, false>(rc.BN, tx, tdy, q, xm, rc.smem, st);
+        case 64: return launch_wgrad_row_rb<64, false>(rc.BN, tx, tdy, q, xm, rc.smem, st);
+        case 128: return launch_wgrad_row_rb<128, false>(rc.BN, tx, tdy, q, xm, rc.smem, st);
     }
     return CKS_ERR_UNSUPPORTED;
 }
@@ -1214,7 +1245,7 @@ static cks_status wgrad_impl(const cks_geom* g, cks_dtype dt, const void* x, con
                            : (ar ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ar_local_offset(L)) : dw);
     const long long part_stride = g->OC * g->FH * g->FW * g->C;
     if (cfg.row) {  // narrow channels: (fh, fw, c) rows as the GEMM M dimension
-        s = run_wgrad_row(*g, dt, row_cfg_wgrad(*g, dt, gz, kPlanSMs), x, ta, wout, part_stride, st);
+        s = run_wgrad_row(*g, dt, row_cfg_wgrad(*g, dt, gz, kPlanSMs), x, dys, OCp, ta, wout, part_stride, st);
     } else {
         CUtensorMap tb;  // X viewed as (C, W, H, N): leaping rows ih = oh*sh + fh - ph
         if (cfg.rg) {  // row groups: (C, N, W, H), rg images x rg_pk leaping columns (element stride s_w)

@@ -751,7 +751,7 @@ int64_t row_wgrad_padding_macs(const cks_geom& g, cks_dtype dt) {
 // Narrow Sk-dilated: M = (fh, e) rows, 128/JB filter rows per M-block; N = OC
 // block; K = (oh, column, 64 images) of one column class, split into
 // segments; every segment of every class is one G_Z map-reduce partial.
-static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms, bool allow_rg) {
     RowCfg c;
     if (!row_setup(g, dt, c)) return c;
     if (dt == CKS_TF32) {  // MN-major tf32 needs the 128-byte (BASE32B) swizzle
@@ -768,6 +768,14 @@ static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, in
     if (c.BN > cap) return c;
     c.nbs = int((pad_ch(g.OC, dt) + c.BN - 1) / c.BN);
     c.nblk = int((g.N + 63) / 64);
+    // row groups (N <= 32): a 64-row k-block = rg_pc class columns x rg images (per-class maps,
+    // kernels/narrow.cuh RowWXMaps: at most kRowWgradRgClasses = 12 classes)
+    if (allow_rg && knobs().rg && 2 * g.N <= 64 && c.cls.size() <= 12) {
+        c.rg = g.N <= 16 ? 16 : 32;
+        c.rg_pc = 64 / c.rg;
+        c.nblk = 1;
+    }
+    auto col_units = [&](const RowClassH& k) -> int64_t { return c.rg ? (k.ncols + c.rg_pc - 1) / c.rg_pc : k.ncols; };
     const int64_t OH = out_extent(g.H, g.FH, g.sh, g.ph);
     // Output rows per k-block q: one X box of FH + sh*(q-1) rows serves q output rows.  Measured
     // (tools/time_op.py, CKS_WROW_Q): ResNet stem TF32 407 -> 329 us (q = 2), BF16 252 -> 206 (2)
@@ -784,7 +792,7 @@ static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, in
                 break;
             }
             const int64_t stage = ((q - 1) * g.sh + int64_t(c.mb) * R) * atom + int64_t(q) * c.BN * 64 * eb;
-            const int64_t kblocks = ((OH + q - 1) / q) * ow_cols * c.nblk;
+            const int64_t kblocks = ((OH + q - 1) / q) * (c.rg ? (ow_cols + c.rg_pc - 1) / c.rg_pc : ow_cols) * c.nblk;
             const bool forced = knobs().wrow_q > 0;
             const bool saves = 5 * (g.FH + g.sh * (q - 1)) <= 4 * q * g.FH;  // <= 80 % of the rows
             const bool enough = kblocks >= int64_t(q == 2 ? 4 : 16) * num_sms;
@@ -796,7 +804,7 @@ static RowCfg row_cfg_wgrad_plan(const cks_geom& g, cks_dtype dt, int gz_req, in
     }
     std::vector<int64_t> segcap;
     for (auto& k : c.cls) {
-        k.work = ((OH + c.q - 1) / c.q) * k.ncols * c.nblk;
+        k.work = ((OH + c.q - 1) / c.q) * col_units(k) * c.nblk;
         segcap.push_back(gz_req > 0 ? k.work : std::max<int64_t>(1, k.work / 8));  // >= 8 k-blocks per segment
     }
     const int64_t want = gz_req > 0 ? gz_req : std::max<int64_t>(1, num_sms / c.nbs);
@@ -849,8 +857,9 @@ std::string describe_plan(const cks_geom& g, cks_dtype dt, cks_op op, int gz, in
     const WgradCfg w = wgrad_cfg(g, dt, gz, num_sms);
     if (w.row) {
         const RowCfg r = row_cfg_wgrad(g, dt, gz, num_sms);
-        snprintf(b, sizeof b, "row_wgrad ROWB=%d JB=%d BN=%d mb=%d nbs=%d gz=%d stages=%d q=%d tiles=%lld classes=%d cls=",
-                 r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, r.q, (long long)r.tiles, int(r.cls.size()));
+        snprintf(b, sizeof b,
+                 "row_wgrad ROWB=%d JB=%d BN=%d mb=%d nbs=%d gz=%d stages=%d q=%d tiles=%lld rg=%d classes=%d cls=",
+                 r.ROWB, r.JB, r.BN, r.mb, r.nbs, r.gz, r.stages, r.q, (long long)r.tiles, r.rg, int(r.cls.size()));
         return std::string(b) + row_classes_str(r.cls);
     }
     snprintf(b, sizeof b,
@@ -1127,9 +1136,10 @@ RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt, bool allow_rg) {
     static PlanMemo<RowCfg> memo;
     return memo.get(plan_key(g, dt, 0, allow_rg ? 1 : 0, 0), [&] { return row_cfg_fwd_plan(g, dt, allow_rg); });
 }
-RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms) {
+RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms, bool allow_rg) {
     static PlanMemo<RowCfg> memo;
-    return memo.get(plan_key(g, dt, 2, gz_req, num_sms), [&] { return row_cfg_wgrad_plan(g, dt, gz_req, num_sms); });
+    return memo.get(plan_key(g, dt, allow_rg ? 2 : 4, gz_req, num_sms),
+                    [&] { return row_cfg_wgrad_plan(g, dt, gz_req, num_sms, allow_rg); });
 }
 IgemmCfg igemm_cfg_deconv_w(const cks_geom& g, cks_dtype dt, int num_sms) {
     static PlanMemo<IgemmCfg> memo;

@@ -180,13 +180,13 @@ struct RowCfg {
     int mb = 1, nbs = 1, gz = 1, nblk = 1;  // wgrad: M-blocks, OC blocks, G_Z (total partials), 64-image blocks
     int q = 1;           // wgrad: output rows per k-block (one X box of FH + sh * (q - 1) rows)
     int rg = 0;          // ConvV2 row groups (N <= 64): images per M tile (32 / 64), 0 = 128-image M tiles
-    int rg_pc = 1;       // ConvV2 row groups: columns of one class per M tile (128 / rg)
+    int rg_pc = 1;       // row groups: class columns per M tile (ConvV2: 128 / rg) / per k-block (wgrad: 64 / rg)
     std::vector<RowClassH> cls;
     int grid = 1;        // CTAs
     int64_t tiles = 0;
 };
 RowCfg row_cfg_fwd(const cks_geom& g, cks_dtype dt, bool allow_rg = true);
-RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms);
+RowCfg row_cfg_wgrad(const cks_geom& g, cks_dtype dt, int gz_req, int num_sms, bool allow_rg = true);
 // Products of the row kernels with spatial-padding zeros (host model, per
 // image): ConvV2 (the partial last K chunk of right-border columns) and
 // Sk-dilated (zero-fill rows inside an issued M-block, box elements beyond

@@ -406,10 +406,24 @@ struct RowWgradParams {
     // q rows' M-blocks (row oh0 + i starts at atom i * sh), so the X rows shared by neighbouring
     // output rows cross L2 -> SM once per k-block instead of once per output row
     int q, xrows;
+    // Row groups (small batches, kernel template RG): a k-block is rg_pk class columns x rg images
+    // (64 K rows, column-major), both operands from per-class maps (RowWXMaps) with a column dim
+    int rg, rg_pk;
 };
 
+// Per-class X and dY tensor maps of the row-group Sk-dilated (kernel parameter space).
+constexpr int kRowWgradRgClasses = 12;
+struct RowWXMaps {
+    CUtensorMap x[kRowWgradRgClasses], dy[kRowWgradRgClasses];
+};
+template <bool RG>
+__device__ __forceinline__ int row_wgrad_cols(const RowClass& c, const RowWgradParams& p) {
+    return RG ? (c.ncols + p.rg_pk - 1) / p.rg_pk : c.ncols;  // k-block column units of a class
+}
+
 // Tile t -> OC block nb, segment (partial) part of class k, its k-block range
-// [kb0, kb1) over the class's (oh, column, 64-image) positions.
+// [kb0, kb1) over the class's (oh, column, 64-image) positions (row groups: column chunks).
+template <bool RG>
 struct RowWTile {
     int nb, k, part;
     uint32_t kb0, kb1;
@@ -418,7 +432,8 @@ struct RowWTile {
         part = t / p.nbs;
         k = row_class_of(p.cls, p.ncls, part);
         const int z = part - p.cls[k].base, gzc = p.cls[k].cnt;
-        const uint32_t L = uint32_t((p.OH + p.q - 1) / p.q) * uint32_t(p.cls[k].ncols) * uint32_t(p.nblk64);
+        const uint32_t L =
+            uint32_t((p.OH + p.q - 1) / p.q) * uint32_t(row_wgrad_cols<RG>(p.cls[k], p)) * uint32_t(p.nblk64);
         kb0 = uint32_t(uint64_t(L) * uint32_t(z) / uint32_t(gzc));
         kb1 = uint32_t(uint64_t(L) * uint32_t(z + 1) / uint32_t(gzc));
     }
@@ -434,10 +449,10 @@ __device__ __forceinline__ uint32_t row_wgrad_mmask(int oh, int R, const RowWgra
     return m;
 }
 
-template <int ROWB, int BN, bool TF>
+template <int ROWB, int BN, bool TF, bool RG = false>
 __global__ void __launch_bounds__(256, 1)
     wgrad_row_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDY,
-                     const __grid_constant__ RowWgradParams p) {
+                     const __grid_constant__ RowWgradParams p, const __grid_constant__ RowWXMaps xm) {
     constexpr int EB = TF ? 4 : 2;
     constexpr int JB = ROWB / EB;       // MN elements per filter row of A
     constexpr int R = 128 / JB;         // filter rows per M-block
@@ -484,12 +499,14 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t pol = is_b ? ptx::l2_policy_evict_first() : ptx::l2_policy_evict_last();
         uint32_t stage = 0, phase = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const RowWTile c(t, p);
+            const RowWTile<RG> c(t, p);
             const RowClass cl = p.cls[c.k];
             for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
                 const int n64 = int(kb % uint32_t(p.nblk64));
                 const int pos = int(kb / uint32_t(p.nblk64));
-                const int oh0 = (pos / cl.ncols) * p.q, ow = cl.col0 + cl.cstep * (pos % cl.ncols);
+                const int cu = row_wgrad_cols<RG>(cl, p);
+                const int ci0 = (pos % cu) * (RG ? p.rg_pk : 1);  // first class column of the k-block
+                const int oh0 = (pos / cu) * p.q, ow = cl.col0 + cl.cstep * ci0;
                 const int nq = min(p.q, p.OH - oh0);
                 ptx::mbar_wait(&empty[stage], phase ^ 1u);
                 uint8_t* st = smem + stage * stage_bytes;
@@ -499,15 +516,24 @@ __global__ void __launch_bounds__(256, 1)
                     // dY, which is read once (L2 eviction priorities)
                     if (!is_b) {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(p.xrows * 64 * ROWB));
-                        ptx::tma_load_4d_hint(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
-                                              oh0 * p.sh - p.ph, 0, pol);
+                        if (RG)  // rg_pk class columns x rg images (origin of class column 0 + column dim)
+                            ptx::tma_load_4d_hint(st, &xm.x[c.k], &full[stage], (cl.col0 * p.sw - p.pw) * p.C + cl.off,
+                                                  0, ci0, oh0 * p.sh - p.ph, pol);
+                        else
+                            ptx::tma_load_4d_hint(st, &tmX, &full[stage], (ow * p.sw - p.pw) * p.C + cl.off, n64 * 64,
+                                                  oh0 * p.sh - p.ph, 0, pol);
                     } else {
                         ptx::mbar_arrive_expect_tx(&full[stage], uint32_t(nq * B_BYTES));
                         for (int i = 0; i < nq; ++i)
 #pragma unroll
-                            for (int j = 0; j < BN / CH; ++j)
-                                ptx::tma_load_4d_hint(st + p.a_bytes + i * B_BYTES + j * 8192, &tmDY, &full[stage],
-                                                      c.nb * BN + j * CH, ow, oh0 + i, n64 * 64, pol);
+                            for (int j = 0; j < BN / CH; ++j) {
+                                if (RG)
+                                    ptx::tma_load_4d_hint(st + p.a_bytes + i * B_BYTES + j * 8192, &xm.dy[c.k],
+                                                          &full[stage], c.nb * BN + j * CH, 0, ci0, oh0 + i, pol);
+                                else
+                                    ptx::tma_load_4d_hint(st + p.a_bytes + i * B_BYTES + j * 8192, &tmDY, &full[stage],
+                                                          c.nb * BN + j * CH, ow, oh0 + i, n64 * 64, pol);
+                            }
                     }
                 }
                 __syncwarp();
@@ -525,13 +551,13 @@ __global__ void __launch_bounds__(256, 1)
         const uint64_t bdesc0 = TF ? ptx::smem_desc_mn_b32(s0, 8192, 512) : ptx::smem_desc_sw128(s0, 8192, 1024);
         uint32_t stage = 0, phase = 0, tph = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const RowWTile c(t, p);
+            const RowWTile<RG> c(t, p);
             const RowClass cl = p.cls[c.k];
             ptx::mbar_wait(tempty, tph ^ 1u);
             ptx::tc_fence_after();
             uint32_t started = 0;
             for (uint32_t kb = c.kb0; kb < c.kb1; ++kb) {
-                const int oh0 = (int(kb / uint32_t(p.nblk64)) / cl.ncols) * p.q;
+                const int oh0 = (int(kb / uint32_t(p.nblk64)) / row_wgrad_cols<RG>(cl, p)) * p.q;
                 const int nq = min(p.q, p.OH - oh0);
                 uint32_t mmq = 0;  // M-blocks issued in this k-block (any of its output rows)
                 for (int i = 0; i < nq; ++i) mmq |= row_wgrad_mmask(oh0 + i, R, p);
@@ -577,13 +603,13 @@ __global__ void __launch_bounds__(256, 1)
         const int jn = p.FW * p.C;
         uint32_t tph = 0;
         for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            const RowWTile c(t, p);
+            const RowWTile<RG> c(t, p);
             const RowClass cl = p.cls[c.k];
             const int nb = c.nb;
             uint32_t started = 0;  // M-blocks that received an MMA (the same walk as the issuer)
             for (uint32_t kb = c.kb0; kb < c.kb1;) {
                 const int pos = int(kb / uint32_t(p.nblk64));
-                const int oh0 = (pos / cl.ncols) * p.q;
+                const int oh0 = (pos / row_wgrad_cols<RG>(cl, p)) * p.q;
                 for (int i = 0; i < p.q && oh0 + i < p.OH; ++i) started |= row_wgrad_mmask(oh0 + i, R, p);
                 kb = uint32_t(pos + 1) * uint32_t(p.nblk64);  // next position
             }

@@ -204,3 +204,25 @@ def test_row_group_narrow_fwd_plans(torch_cuda, lay, dtype):
     assert not torch.isnan(y).any() and torch.isnan(buf[n:]).all()
     check(y.cpu().numpy(), O.conv_ref(a["X"], a["W"], lay.sh, lay.sw, lay.ph, lay.pw), dtype, f"{lay} fwd",
           red_len(lay, "fwd"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("gz", [0, 3])
+@pytest.mark.parametrize("k", range(10))
+def test_row_group_narrow_wgrad(torch_cuda, k, gz, dtype):
+    """Narrow-channel Sk-dilated (filter-row kernel) at N <= 32: k-blocks of rg_pc class columns x
+    rg images through per-class X / dY maps; columns past a class end are zero fill."""
+    lay = _narrow_rg_layers(10, 51 if dtype == "bf16" else 53, dtype)[k]
+    lay = Layer(lay.name, min(lay.N, 1 + (k * 7) % 32), lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh,
+                lay.sw, lay.ph, lay.pw)
+    check_full(torch_cuda, lay, dtype, config=19, idx=k, ops=("wgrad",), gz=gz)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_row_group_narrow_wgrad_stem(torch_cuda, dtype):
+    from paper_2306_15951_b200 import _lib as L
+    lay = Layer("nws0", 24, 3, 61, 64, 64, 7, 7, 2, 2, 3, 3)
+    g = L.make_geom(lay.N, lay.C, lay.H, lay.W, lay.OC, lay.FH, lay.FW, lay.sh, lay.sw, lay.ph, lay.pw)
+    d = L.plan_dict(g, L.CKS_BF16 if dtype == "bf16" else L.CKS_TF32, L.CKS_OP_WGRAD)
+    assert d["kind"] == "row_wgrad" and int(d["rg"]) == 32, d
+    check_full(torch_cuda, lay, dtype, config=19, idx=99, ops=("wgrad",))
