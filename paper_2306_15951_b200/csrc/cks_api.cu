@@ -732,6 +732,15 @@ cks_status run_wgrad_row(const cks_geom& g, cks_dtype dt, const RowCfg& rc_in, c
     return CKS_ERR_UNSUPPORTED;
 }
 
+// Staggered filter-row groups (experiments: CKS_WGRAD_STAGGER=0/1)
+bool wgrad_stagger() {
+    static const bool on = [] {
+        const char* e = cks_knob("CKS_WGRAD_STAGGER");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return on;
+}
+
 // per-tap Sk-dilated-V2 kernel (KB-WGRAD)
 cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, const Axis& ah, const Axis& aw,
                           const CUtensorMap& ta, const CUtensorMap& tb, float* wout, long long part_stride,
@@ -789,6 +798,7 @@ cks_status run_wgrad_taps(const cks_geom& g, cks_dtype dt, const WgradCfg& cfg, 
     p.pp = cfg.pp;
     p.rg = cfg.rg;
     p.rg_pk = cfg.rg ? cfg.rg_pk : 1;
+    p.stag = (cfg.tc > 1 && g.sh == 1 && !ad && wgrad_stagger()) ? 1 : 0;
     p.Wx = int(g.W);
     p.ouh_s = 1 << 20;
     p.ouh_e = -(1 << 20);

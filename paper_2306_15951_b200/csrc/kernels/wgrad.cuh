@@ -77,6 +77,7 @@ struct WgradParams {
     // (position-major K rows; boxes over (C, N, W, H) maps); a tap multiplies only the K rows of
     // its valid positions.  rg = 0: k-blocks of KIMG images at one position (rg_pk = 1).
     int rg, rg_pk;
+    int stag;  // filter-row groups, s_h = 1: staggered walk (the group shares X rows instead of dY rows)
 };
 
 // One TMA box = 128 B of channels x 64 images (64 bf16 / 32 fp32 channels):
@@ -142,10 +143,13 @@ __device__ __forceinline__ WTile wdecode(long long t64, const WgradParams& p) {
     c.fd = fdh / p.FH;
     c.fh = fdh - c.fd * p.FH;
     c.fw = MT > 1 ? 0 : tap % p.FW;
-    c.ohs = p.tc > 1 ? p.ouh_s : p.oh_s[c.fh];
+    // filter-row groups walk the union oh range in lockstep; staggered (s_h = 1): filter row fh
+    // runs oh = t - fh at step t, so the group's CTAs read the SAME X row (ih = t - ph) together
+    c.ohs = p.tc > 1 ? p.ouh_s - (p.stag ? c.fh : 0) : p.oh_s[c.fh];
     c.ods = p.od_s[c.fd];
     c.ows = MT > 1 ? p.ouw_s : p.ow_s[c.fw];
-    const int hn = (p.tc > 1 ? p.ouh_e : p.oh_e[c.fh]) - c.ohs, wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
+    const int hn = p.tc > 1 ? p.ouh_e - p.ouh_s + (p.stag ? p.tc - 1 : 0) : p.oh_e[c.fh] - c.ohs;
+    const int wn = (MT > 1 ? p.ouw_e : p.ow_e[c.fw]) - c.ows;
     const int dn = p.od_e[c.fd] - c.ods;
     c.wn = p.pp ? wn / 2 : (RG ? (wn + p.rg_pk - 1) / p.rg_pk : wn);  // pairs (host: wn even) / chunks
     c.wr = wn;
