@@ -199,9 +199,11 @@ cks_status launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, int
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = size_t(smem);
     cfg.stream = st;
+    // experiments: CKS_NO_PDL=1 launches without programmatic dependent launch (ncu graph probes)
+    static const bool no_pdl = cks_knob("CKS_NO_PDL") != nullptr;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = unsigned(cluster);
     attr[1].val.clusterDim.y = 1;
