@@ -1384,13 +1384,20 @@ cks_status cks_conv3d_fwd(const cks_geom3* g, cks_dtype dt, const void* x, const
         wsrc = wp;
     }
     IgemmCfg cfg = igemm_cfg_fwd3(*g, dt, kPlanSMs);
+    if (cfg.rg_ni > 0) rh = igemm_rows_fwd(g2, cfg.rg_ni);  // row groups (N <= 64) inside a depth slice
     const uint32_t BK = uint32_t(cfg.KB / eb);
     CUtensorMap ta, tb;
-    {   // X viewed as (C, N, W, D*H): depth and row flattened (a row step never crosses a depth slice)
+    {   // X viewed as (C, N, W, D*H): depth and row flattened (a row step never crosses a depth slice;
+        // row groups: rg_ph rows of one slice at element stride s_h, trailing box rows never stored)
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->N), uint64_t(g->W), uint64_t(g->D * g->H)};
         uint64_t sb[3] = {uint64_t(g->D * g->H * g->W * Cp * eb), uint64_t(Cp * eb), uint64_t(g->W * Cp * eb)};
         uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
-        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
+        uint32_t es[4] = {1, 1, 1, uint32_t(cfg.rg_es)};
+        if (cfg.rg_ni > 0) {
+            box[1] = uint32_t(cfg.rg_ni);
+            box[3] = uint32_t(cfg.rg_ph * cfg.rg_es);
+        }
+        if (!make_tmap4(&ta, dt, xs, d, sb, box, cfg.KB, false, cfg.rg_ni > 0 ? es : nullptr)) return CKS_ERR_CUDA;
     }
     {   // W viewed as (C, OC, FD*FH*FW, 1): one box = the FW taps of filter row (fd, fh)
         uint64_t d[4] = {uint64_t(Cp), uint64_t(g->OC), uint64_t(g->FD * g->FH * g->FW), 1};
@@ -1431,13 +1438,18 @@ cks_status cks_deconv3d(const cks_geom3* g, cks_dtype dt, const void* dy, const 
         dys = p;
     }
     IgemmCfg cfg = igemm_cfg_deconv3(*g, dt, kPlanSMs);
+    if (cfg.rg_ni > 0) rh = igemm_rows_deconv(g2, cfg.rg_ni);  // row groups (N <= 64) inside a depth slice
     const uint32_t BK = uint32_t(cfg.KB / eb);
     const int64_t CWm0 = cdiv(g->FW, g->sw), atomw = 128 / eb;
     CUtensorMap ta, tb;
-    {   // dY viewed as (OC, N, OW, OD*OH)
+    {   // dY viewed as (OC, N, OW, OD*OH) (row groups: rg_ph consecutive dY rows of one slice)
         uint64_t d[4] = {uint64_t(OCp), uint64_t(g->N), uint64_t(OW), uint64_t(OD * OH)};
         uint64_t sb[3] = {uint64_t(OD * OH * OW * OCp * eb), uint64_t(OCp * eb), uint64_t(OW * OCp * eb)};
         uint32_t box[4] = {BK, 128u, uint32_t(cfg.apos), 1};
+        if (cfg.rg_ni > 0) {
+            box[1] = uint32_t(cfg.rg_ni);
+            box[3] = uint32_t(cfg.rg_ph);
+        }
         if (!make_tmap4(&ta, dt, dys, d, sb, box, cfg.KB)) return CKS_ERR_CUDA;
     }
     // W (OHWI) read directly: filter rows (fd, fh) flattened to FD*FH

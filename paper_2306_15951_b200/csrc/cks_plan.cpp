@@ -1190,9 +1190,14 @@ IgemmCfg igemm_cfg_fwd3(const cks_geom3& g, cks_dtype dt, int num_sms) {
     static PlanMemo<IgemmCfg> memo;
     return memo.get(plan_key3(g, dt, 0, 0, num_sms), [&] {
         const cks_geom g2 = plane_geom(g);
-        const Axis ad = axis_d(g), ah = axis_h(g2), aw = axis_w(g2);
-        return igemm_cfg(ad.O * ah.O, {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt),
-                         max_window(krows_fwd(ah)) * max_window(krows_fwd(ad)), g.FW, g.sw, num_sms);
+        const Axis ad = axis_d(g), aw = axis_w(g2);
+        const int rg = rg_plan(g2, false);  // row groups inside a depth slice (h rows of one window)
+        const auto rh = igemm_rows_fwd(g2, rg);
+        IgemmCfg c = igemm_cfg(ad.O * int64_t(rh.size()), {aw.O}, g.N, g.OC, pad_ch(g.C, dt), elem_bytes(dt),
+                               max_window(rh) * max_window(krows_fwd(ad)), g.FW, g.sw, num_sms, 0, 0, rg);
+        c.rg_es = int(g.sh);
+        c.rg_ostep = 1;
+        return c;
     });
 }
 
@@ -1200,14 +1205,19 @@ IgemmCfg igemm_cfg_deconv3(const cks_geom3& g, cks_dtype dt, int num_sms) {
     static PlanMemo<IgemmCfg> memo;
     return memo.get(plan_key3(g, dt, 1, 0, num_sms), [&] {
         const cks_geom g2 = plane_geom(g);
-        const Axis ad = axis_d(g), ah = axis_h(g2), aw = axis_w(g2);
+        const Axis ad = axis_d(g), aw = axis_w(g2);
         std::vector<int64_t> cnt;
         for (auto& ph : table_t2(aw)) cnt.push_back(ph.U);
         const int atomw = int(128 / elem_bytes(dt));
         const int fb = g.C % atomw == 0 ? -atomw : atomw;  // Stage1-free: whole 128-byte MN atoms of W
-        return igemm_cfg(ad.I * ah.I, cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt),
-                         max_window(krows_deconv(ah)) * max_window(krows_deconv(ad)), cdiv(g.FW, g.sw), 1, num_sms,
-                         0, fb);
+        const int rg = rg_plan(g2, true);
+        const auto rh = igemm_rows_deconv(g2, rg);
+        IgemmCfg c = igemm_cfg(ad.I * int64_t(rh.size()), cnt, g.N, g.C, pad_ch(g.OC, dt), elem_bytes(dt),
+                               max_window(rh) * max_window(krows_deconv(ad)), cdiv(g.FW, g.sw), 1, num_sms, 0, fb,
+                               rg);
+        c.rg_es = 1;
+        c.rg_ostep = int(g.sh);
+        return c;
     });
 }
 

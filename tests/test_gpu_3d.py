@@ -131,3 +131,25 @@ def test_3d_deconv_unsupported_narrow_rows(torch_cuda):
     G = torch.zeros((2, 4, 4, 4, 8), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(L.CksError):
         K.deconv3d(G, W, (8, 8, 8), 2, 1)
+
+
+RG_CASES = {
+    # small clip batches (row groups of 4 / 2 h rows x 32 / 64 clips inside each depth slice)
+    "rg_r3d_s1": (8, 64, 64, (8, 14, 14), (3, 3, 3), (1, 1, 1), (1, 1, 1)),
+    "rg_r3d_s2": (24, 64, 128, (8, 15, 13), (3, 3, 3), (2, 2, 2), (1, 1, 1)),
+    "rg_gen3d": (33, 64, 32, (6, 8, 8), (4, 4, 4), (2, 2, 2), (1, 1, 1)),
+    "rg_hw_s3": (64, 32, 48, (5, 19, 11), (1, 3, 3), (1, 3, 2), (0, 1, 1)),
+}
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("name", list(RG_CASES))
+def test_3d_row_groups(torch_cuda, name, dtype):
+    """3-D ConvV2 / KS-deconv at N <= 64: row groups of h rows inside each depth slice (the same
+    grouping as the 2-D plane, whose plan reports rg = 32 / 64 for these batches)."""
+    from paper_2306_15951_b200 import _lib as L
+    case = RG_CASES[name]
+    N, C, OC, dhw, f, s, p = case
+    plane = L.make_geom(N, C, dhw[1], dhw[2], OC, f[1], f[2], s[1], s[2], p[1], p[2])
+    assert int(L.plan_dict(plane, L.CKS_BF16, L.CKS_OP_FWD)["rg"]) == (32 if N <= 32 else 64)
+    _run3(torch_cuda, case, dtype, ops=("fwd", "deconv"), seed=11)
