@@ -226,3 +226,15 @@ def test_row_group_narrow_wgrad_stem(torch_cuda, dtype):
     d = L.plan_dict(g, L.CKS_BF16 if dtype == "bf16" else L.CKS_TF32, L.CKS_OP_WGRAD)
     assert d["kind"] == "row_wgrad" and int(d["rg"]) == 32, d
     check_full(torch_cuda, lay, dtype, config=19, idx=99, ops=("wgrad",))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("lay", [Layer("rgz0", 16, 512, 4, 4, 256, 3, 3, 2, 2, 1, 1),    # cluster split-K (Z = 8)
+                                 Layer("rgz1", 32, 512, 4, 4, 512, 3, 3, 1, 1, 1, 1),
+                                 Layer("rgz2", 8, 256, 8, 8, 256, 3, 3, 1, 1, 1, 1),     # TF32: Z = 2 clusters
+                                 Layer("rgz3", 64, 512, 7, 7, 512, 3, 3, 1, 1, 1, 1)],   # 2-row groups, l4-like
+                         ids=lambda l: l.name)
+def test_row_group_split_k(torch_cuda, lay, dtype):
+    """Row groups with the in-cluster split-K reduce (DSMEM): the reducing CTA maps its column
+    slice's rows back to (image, output row) of the group."""
+    check_full(torch_cuda, lay, dtype, config=20, idx=int(lay.name[3:]))
