@@ -337,3 +337,16 @@ def test_row_group_wgrad_plans():
                 assert int(d["rg"]) == want, (geo, dt, d)
                 if want:
                     assert int(d["rg_pk"]) * want == int(d["kimg"]) and d["pp"] == "0", d
+
+
+def test_row_group_narrow_plans():
+    """Narrow-channel (filter-row) kernels at small batches: ConvV2 row groups for N <= 64,
+    Sk-dilated class-column k-blocks for N <= 32; batch-as-M / 64-image k-blocks above."""
+    for N, want_f, want_w in [(1, 32, 16), (16, 32, 16), (32, 32, 32), (33, 64, 0), (64, 64, 0), (65, 0, 0),
+                              (256, 0, 0)]:
+        g = L.make_geom(N, 3, 224, 224, 64, 7, 7, 2, 2, 3, 3)
+        for dt in (L.CKS_BF16, L.CKS_TF32):
+            f = L.plan_dict(g, dt, L.CKS_OP_FWD)
+            w = L.plan_dict(g, dt, L.CKS_OP_WGRAD)
+            assert f["kind"] == "row_fwd" and int(f["rg"]) == want_f, (N, dt, f)
+            assert w["kind"] == "row_wgrad" and int(w["rg"]) == want_w, (N, dt, w)
