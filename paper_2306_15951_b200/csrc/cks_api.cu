@@ -1591,8 +1591,7 @@ cks_status cks_dilated_wgrad_allreduce_emulated(int32_t world, const cks_geom* g
         return last_cuda();
     const long long resident = (long long)per_sm * device_sms();
     blocks = std::max<long long>(1, std::min<long long>(blocks, resident / world));
-    cudaLaunchConfig_t cfg;
-    memset(&cfg, 0, sizeof(cfg));
+    cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(blocks), unsigned(world));
     cfg.blockDim = dim3(256);
     cfg.stream = static_cast<cudaStream_t>(stream);
