@@ -351,10 +351,10 @@ def test_config_layers_reduced_batch_tf32(torch_cuda, cfg, i, lay):
 
 # ------------------------------------------ full size, sampled outputs
 def _full_tf32():
-    """TF32 at full size: the headline workload's distinct shapes (C3 stem, l1,
-    l2a, l2ds, l3, l4 -- the plans at N = 256: G_Z, clusters, row kernels) and
-    the C4 generator layers."""
-    keep = {"stem", "l1_0", "l2a", "l2ds", "l3_0", "l4a", "l4_0"}
+    """TF32 at full size: EVERY distinct shape of the headline workload (C3 = C5 layers at
+    N = 256: stem, l1, l2a / l2ds / l2, l3a / l3ds / l3, l4a / l4ds / l4 -- the plans the bench
+    times: G_Z, clusters, CTA pairs, row tiles, row kernels) and the C4 generator layers."""
+    keep = {"stem", "l1_0", "l2a", "l2ds", "l2_0", "l3a", "l3ds", "l3_0", "l4a", "l4ds", "l4_0"}
     return [c for c in _config_layers() if (c[0] == 2 and c[2].name in keep) or c[0] == 3]
 
 
